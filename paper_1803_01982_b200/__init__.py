@@ -1,0 +1,20 @@
+"""B200-native Flip-Flop SRQR engine (arXiv:1803.01982 hot path, sm_100a).
+
+Drop-in for the reference ``ffsrqr`` hot path: ``flip_flop_srqr``, ``srqr``,
+``trqrcp`` and their result types, plus caller seams for HOSVD and the SVT
+(IALM) solvers.  Compute runs in hand-written CUDA (libffb200.so, C ABI in
+include/ffb200.h); this package is host glue only and has no CPU fallback.
+"""
+from .errors import (CertificationError, DimensionError, EngineUnavailable, NumericalError,
+                     SingularTrailingBlockError)
+from .results import (ApproxSvd, PartialFactorization, SketchParams, SrqrCertificate, SrqrResult,
+                      WYFactor, flip_flop_flop_formula)
+from .engine import flip_flop_srqr, srqr, trqrcp
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "ApproxSvd", "CertificationError", "DimensionError", "EngineUnavailable", "NumericalError",
+    "PartialFactorization", "SingularTrailingBlockError", "SketchParams", "SrqrCertificate",
+    "SrqrResult", "WYFactor", "flip_flop_flop_formula", "flip_flop_srqr", "srqr", "trqrcp",
+]

@@ -1,0 +1,657 @@
+// Orchestrator and C ABI of the B200 Flip-Flop SRQR engine.
+//
+// One call = one factorization, enqueued on the caller's stream with no host
+// synchronisation until the end: TRQRCP (sketch GEMM, per-block cooperative
+// pivot kernel, CholeskyQR3 + Householder-reconstruction panels, compact-WY
+// GEMMs), SRQR (extension, g2 estimate, pack) and — speculatively, assuming
+// the first g2 test certifies — the flip-flop tail (partial LQ, A*Qhat,
+// small SVD, back-mapping).  A single sync at the end reads the certificate;
+// only if a swap is needed (g2 > g, rare: 0 swaps on every BASELINE config)
+// does the host drive the reference's swap loop and redo the tail.
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ffb200.h"
+#include "ffb_gemm.h"
+#include "ffb_kernels.cuh"
+
+using namespace ffb;
+
+struct ffb_ctx {
+  int device = 0;
+  int sms = 148;
+  int max_coop_blocks_smem = 0;
+  cusolverDnHandle_t solver = nullptr;
+  std::string err;
+  double* pinned = nullptr;        // host staging for g2 Gaussians
+  size_t pinned_cap = 0;
+  SrqrScalars* sc_host = nullptr;  // pinned
+  int svd_kind = 0;                // 0 = gesvd, 1 = gesvdj
+};
+
+namespace {
+
+constexpr int kPanelW = 64;
+constexpr size_t kAlign = 256;
+
+struct Bump {
+  char* base;
+  size_t off = 0;
+  size_t cap;
+  bool ok = true;
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + kAlign - 1) / kAlign * kAlign;
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += std::max<size_t>(count, 1) * sizeof(T);
+    if (off > cap) ok = false;
+    return p;
+  }
+};
+
+struct Dims {
+  int64_t m, n, k, l, b, p, s, d;
+  double g;
+  uint64_t seed;
+  int mode;
+};
+
+struct Work {
+  // TRQRCP
+  double *B, *colsq, *Y, *T, *WT, *R, *Q;
+  int64_t *arr, *pos;
+  double *P, *Xa, *Xb, *G1, *WTg, *S1, *S2, *Racc, *Rinv, *Ut, *Dv, *Rb, *Bp, *Z;
+  double *hhW, *hhW2;
+  // pivots
+  PivSlot* slots;
+  double *slotdata, *pwork, *gap;
+  uint32_t* flags;
+  int64_t* hist;
+  int G, cpc;
+  bool piv_smem;
+  size_t piv_smem_bytes;
+  // SRQR
+  double *r, *rinit, *u, *ct, *part, *rot, *g2om, *g2z;
+  SrqrScalars* sc;
+  uint32_t* status;
+  // flip-flop
+  double *X, *Yl, *Tl, *Rl, *TYt, *Qh, *Yh, *tmp, *Yt, *Tt, *Rt, *Us, *VsT, *sig, *W1, *W2;
+  double* svdwork;
+  int* svdinfo;
+  int lwork;
+  double* gpart;
+  size_t gpart_cap;
+};
+
+int64_t max_i(int64_t a, int64_t b) { return a > b ? a : b; }
+
+// Pivot-kernel geometry: G CTAs (<= #SMs, >= 32 columns each), columns in
+// shared memory when they fit.
+void pivot_geometry(const ffb_ctx* ctx, int64_t n, int64_t s, Work& w) {
+  int G = (int)std::min<int64_t>(ctx ? ctx->sms : 148, std::max<int64_t>(1, (n + 31) / 32));
+  int cpc = (int)((n + G - 1) / G);
+  const size_t smem_all = pivots_smem_bytes((int)s, cpc, true);
+  w.piv_smem = smem_all <= 200 * 1024;
+  w.G = G;
+  w.cpc = cpc;
+  w.piv_smem_bytes = pivots_smem_bytes((int)s, cpc, w.piv_smem);
+}
+
+size_t carve(const ffb_ctx* ctx, const Dims& D, void* base, size_t cap, Work& w, int lwork) {
+  Bump b{static_cast<char*>(base), 0, cap};
+  const int64_t m = D.m, n = D.n, l = D.l, s = D.s, bmax = std::min<int64_t>(D.b, l);
+  const int64_t L1 = l + 1;
+  const int64_t mn = max_i(m, n);
+  w.B = b.take<double>(s * n);
+  w.colsq = b.take<double>(n);
+  w.arr = b.take<int64_t>(n);
+  w.pos = b.take<int64_t>(n);
+  w.Y = b.take<double>(m * l);
+  w.T = b.take<double>(l * l);
+  w.WT = b.take<double>(l * n);
+  w.R = b.take<double>(L1 * n);
+  w.Q = b.take<double>(m * L1);
+  w.P = b.take<double>(m * bmax);
+  w.Xa = b.take<double>(mn * kPanelW);
+  w.Xb = b.take<double>(mn * kPanelW);
+  w.G1 = b.take<double>(bmax * n);
+  w.WTg = b.take<double>(l * bmax);
+  w.S1 = b.take<double>(max_i(l, 1) * max_i(bmax, kPanelW));
+  w.S2 = b.take<double>(max_i(l, 1) * max_i(bmax, kPanelW));
+  w.Racc = b.take<double>(kPanelW * kPanelW);
+  w.Rinv = b.take<double>(kPanelW * kPanelW);
+  w.Ut = b.take<double>(kPanelW * kPanelW);
+  w.Dv = b.take<double>(kPanelW);
+  w.Rb = b.take<double>(bmax * bmax);
+  w.Bp = b.take<double>(s * bmax);
+  w.Z = b.take<double>(s * bmax);
+  w.hhW = b.take<double>(kPanelW * max_i(l, 1));
+  w.hhW2 = b.take<double>(kPanelW * max_i(l, 1));
+  pivot_geometry(ctx, n, s, w);
+  w.slots = b.take<PivSlot>(4 * (size_t)w.G);
+  w.slotdata = b.take<double>(2 * (size_t)w.G * s);
+  w.flags = b.take<uint32_t>(w.G);
+  w.hist = b.take<int64_t>(max_i(D.b, 1));
+  w.gap = b.take<double>(max_i(l, 1));
+  w.pwork = w.piv_smem ? nullptr : b.take<double>((size_t)w.G * s * w.cpc);
+  w.r = b.take<double>(n);
+  w.rinit = b.take<double>(n);
+  w.u = b.take<double>(m);
+  w.ct = b.take<double>(L1);
+  w.part = b.take<double>(max_i(4096, (m + 255) / 256 + 1));
+  w.rot = b.take<double>(4 * L1 + 8);
+  w.g2om = b.take<double>(D.d * L1);
+  w.g2z = b.take<double>(D.d * L1);
+  w.sc = b.take<SrqrScalars>(1);
+  w.status = b.take<uint32_t>(1);
+  w.TYt = b.take<double>(l * l);
+  if (D.mode == FFB_MODE_FLIPFLOP) {
+    w.X = b.take<double>(n * l);
+    w.Yl = b.take<double>(n * l);
+    w.Tl = b.take<double>(l * l);
+    w.Rl = b.take<double>(l * l);
+    w.Qh = b.take<double>(n * l);
+    w.Yh = b.take<double>(n * l);
+    w.tmp = b.take<double>(m * l);
+    w.Yt = b.take<double>(m * l);
+    w.Tt = b.take<double>(l * l);
+    w.Rt = b.take<double>(l * l);
+    w.Us = b.take<double>(l * l);
+    w.VsT = b.take<double>(l * l);
+    w.sig = b.take<double>(l);
+    w.W1 = b.take<double>(l * D.k);
+    w.W2 = b.take<double>(l * D.k);
+    w.svdwork = b.take<double>(std::max(lwork, 1));
+    w.svdinfo = b.take<int>(4);
+    w.lwork = lwork;
+  }
+  // split-K scratch: the rest, at least 4 Mi doubles
+  w.gpart_cap = std::max<size_t>(4u << 20, (size_t)64 * kPanelW * kPanelW);
+  w.gpart = b.take<double>(w.gpart_cap);
+  return b.off + kAlign;
+}
+
+struct Eng {
+  ffb_ctx* ctx;
+  cudaStream_t st;
+  Dims D;
+  Work w;
+  GemmCtx gc;
+  int64_t launches = 0;
+  cudaError_t cerr = cudaSuccess;
+
+  bool ok(cudaError_t e) {
+    if (e != cudaSuccess && cerr == cudaSuccess) cerr = e;
+    ++launches;
+    return e == cudaSuccess;
+  }
+  void gemm(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda, bool akc,
+            const double* B, int64_t ldb, bool bkc, double beta, double* C, int64_t ldc) {
+    if (cerr != cudaSuccess) return;
+    cudaError_t e = gemm_f64(gc, st, M, N, K, alpha, A, lda, akc, B, ldb, bkc, beta, C, ldc);
+    if (e != cudaSuccess) cerr = e;
+  }
+  // Gram partials of X (rows x w, ld ldx): returns splits, partials in gc.partial
+  int gram(const double* X, int64_t rows, int w_, int64_t ldx) {
+    GemmPartialOut po{64, nullptr, 0};
+    if (cerr != cudaSuccess) return 1;
+    cudaError_t e = gemm_f64(gc, st, w_, w_, rows, 1.0, X, ldx, true, X, ldx, true, 0.0, nullptr,
+                             w_, &po);
+    if (e != cudaSuccess) cerr = e;
+    return po.splits;
+  }
+  void memset2d(double* p, int64_t ld, int64_t rows, int64_t cols) {
+    if (rows <= 0 || cols <= 0) return;
+    ok(cudaMemset2DAsync(p, ld * sizeof(double), 0, rows * sizeof(double), cols, st));
+  }
+
+  // Householder panel (Mp x wb, wb <= 64) by shifted CholeskyQR3 + reconstruction.
+  void recon(const double* Xp, int64_t Mp, int wb, int64_t ldx, double* Yp, int64_t ldy,
+             double* Tp, int64_t ldt, double* Rp, int64_t ldr) {
+    // pass 1 (shifted)
+    int sp = gram(Xp, Mp, wb, ldx);
+    ok(launch_cholinv(st, gc.partial, sp, wb, Mp, true, true, w.Racc, w.Rinv, w.status));
+    gemm(Mp, wb, wb, 1.0, Xp, ldx, false, w.Rinv, wb, true, 0.0, w.Xa, Mp);
+    // pass 2
+    sp = gram(w.Xa, Mp, wb, Mp);
+    ok(launch_cholinv(st, gc.partial, sp, wb, Mp, false, false, w.Racc, w.Rinv, w.status));
+    gemm(Mp, wb, wb, 1.0, w.Xa, Mp, false, w.Rinv, wb, true, 0.0, w.Xb, Mp);
+    // pass 3
+    sp = gram(w.Xb, Mp, wb, Mp);
+    ok(launch_cholinv(st, gc.partial, sp, wb, Mp, false, false, w.Racc, w.Rinv, w.status));
+    gemm(Mp, wb, wb, 1.0, w.Xb, Mp, false, w.Rinv, wb, true, 0.0, w.Xa, Mp);
+    // signs + reflectors
+    ok(launch_signlu(st, w.Xa, Mp, wb, w.Racc, Yp, ldy, Tp, ldt, Rp, ldr, w.Ut, w.Dv));
+    if (Mp > wb) gemm(Mp - wb, wb, wb, 1.0, w.Xa + wb, Mp, false, w.Ut, wb, true, 0.0, Yp + wb, ldy);
+  }
+
+  // Blocked Householder QR of X (Mx x Nx, ld ldx), panels of <= 64 columns.
+  // Y (ld ldy), T (ld ldt), R (ld ldr): R gets the diagonal blocks, and the full
+  // upper triangle when full_r.  X is overwritten by the trailing updates.
+  void hh_qr(double* X, int64_t Mx, int64_t Nx, int64_t ldx, double* Y, int64_t ldy, double* T,
+             int64_t ldt, double* R, int64_t ldr, bool full_r) {
+    memset2d(Y, ldy, Mx, Nx);
+    memset2d(T, ldt, Nx, Nx);
+    memset2d(R, ldr, Nx, Nx);
+    for (int64_t c0 = 0; c0 < Nx; c0 += kPanelW) {
+      const int64_t c1 = std::min<int64_t>(Nx, c0 + kPanelW);
+      const int wb = (int)(c1 - c0);
+      const int64_t Mp = Mx - c0;
+      double* Yp = Y + c0 + c0 * ldy;
+      double* Tp = T + c0 + c0 * ldt;
+      recon(X + c0 + c0 * ldx, Mp, wb, ldx, Yp, ldy, Tp, ldt, R + c0 + c0 * ldr, ldr);
+      if (c1 < Nx) {
+        const int64_t Nt = Nx - c1;
+        gemm(wb, Nt, Mp, 1.0, Yp, ldy, true, X + c0 + c1 * ldx, ldx, true, 0.0, w.hhW, wb);
+        gemm(wb, Nt, wb, 1.0, Tp, ldt, true, w.hhW, wb, true, 0.0, w.hhW2, wb);
+        gemm(Mp, Nt, wb, -1.0, Yp, ldy, false, w.hhW2, wb, true, 1.0, X + c0 + c1 * ldx, ldx);
+        if (full_r) ok(launch_copy_rows(st, X + c0 + c1 * ldx, ldx, wb, Nt, R + c0 + c1 * ldr, ldr));
+      }
+      if (c0 > 0) {
+        // T12 = -T11 (Y1^T Y2) T22 ; Y2 is zero above row c0
+        gemm(c0, wb, Mx - c0, 1.0, Y + c0, ldy, true, Yp, ldy, true, 0.0, w.S1, c0);
+        gemm(c0, wb, wb, 1.0, w.S1, c0, false, Tp, ldt, true, 0.0, w.S2, c0);
+        gemm(c0, wb, c0, -1.0, T, ldt, false, w.S2, c0, true, 0.0, T + c0 * ldt, ldt);
+      }
+    }
+  }
+};
+
+int fail(ffb_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+int cuda_fail(ffb_ctx* ctx, cudaError_t e, const char* where) {
+  return fail(ctx, FFB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+int svd_lwork(ffb_ctx* ctx, int64_t l) {
+  int lw = 0;
+  if (!ctx || !ctx->solver) return 0;
+  cusolverDnDgesvd_bufferSize(ctx->solver, (int)l, (int)l, &lw);
+  return lw;
+}
+
+bool validate(const Dims& D) {
+  if (D.m < 1 || D.n < 1) return false;
+  if (!(1 <= D.k && D.k <= D.l && D.l <= std::min(D.m, D.n))) return false;
+  if (D.b < 1 || D.p < 0 || D.s > D.m) return false;
+  if (D.d < 1 || D.d > D.l) return false;
+  if (D.mode != FFB_MODE_TRQRCP && D.l + 1 > std::min(D.m, D.n)) return false;
+  if (D.b > 64) return false;  // panel kernels are sized for b <= 64
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ffb_version(void) { return "ffb200 0.1.0 (sm_100a, FP64 DMMA)"; }
+
+int ffb_ctx_create(int device, ffb_ctx** out) {
+  if (!out) return FFB_ERR_ARGUMENT;
+  ffb_ctx* c = new ffb_ctx();
+  c->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    delete c;
+    return FFB_ERR_CUDA;
+  }
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) c->solver = nullptr;
+  cudaMallocHost(&c->sc_host, sizeof(SrqrScalars));
+  const char* sv = getenv("FFB_SVD");
+  c->svd_kind = (sv && std::string(sv) == "gesvdj") ? 1 : 0;
+  *out = c;
+  return FFB_OK;
+}
+
+int ffb_ctx_destroy(ffb_ctx* c) {
+  if (!c) return FFB_OK;
+  if (c->solver) cusolverDnDestroy(c->solver);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->sc_host) cudaFreeHost(c->sc_host);
+  delete c;
+  return FFB_OK;
+}
+
+const char* ffb_last_error(const ffb_ctx* c) { return c ? c->err.c_str() : "no context"; }
+
+int ffb_workspace_query(int64_t m, int64_t n, const ffb_params* prm, int mode, size_t* bytes) {
+  if (!prm || !bytes) return FFB_ERR_ARGUMENT;
+  Dims D{m, n, prm->k, prm->l, prm->b, prm->p, prm->b + prm->p, prm->d, prm->g, prm->seed, mode};
+  if (!validate(D)) return FFB_ERR_DIMENSION;
+  Work w;
+  // SVD workspace: exact cuSOLVER query when a device is present, else a bound.
+  static cusolverDnHandle_t qh = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    if (cusolverDnCreate(&qh) != CUSOLVER_STATUS_SUCCESS) qh = nullptr;
+  }
+  int lw = (int)(4 * D.l * D.l + 4096);
+  if (qh && mode == FFB_MODE_FLIPFLOP) {
+    int q = 0;
+    if (cusolverDnDgesvd_bufferSize(qh, (int)D.l, (int)D.l, &q) == CUSOLVER_STATUS_SUCCESS)
+      lw = std::max(lw, q);
+  }
+  *bytes = carve(nullptr, D, nullptr, (size_t)-1, w, lw) + (8u << 20);
+  return FFB_OK;
+}
+
+int ffb_gemm(ffb_ctx* ctx, void* stream, int64_t M, int64_t N, int64_t K, double alpha,
+             const double* A, int64_t lda, int a_kc, const double* B, int64_t ldb, int b_kc,
+             double beta, double* C, int64_t ldc, void* workspace, size_t workspace_bytes) {
+  if (!ctx) return FFB_ERR_ARGUMENT;
+  GemmCtx gc;
+  gc.sms = ctx->sms;
+  gc.partial = static_cast<double*>(workspace);
+  gc.partial_cap = workspace ? workspace_bytes / sizeof(double) : 0;
+  cudaError_t e = gemm_f64(gc, (cudaStream_t)stream, M, N, K, alpha, A, lda, a_kc != 0, B, ldb,
+                           b_kc != 0, beta, C, ldc);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "ffb_gemm");
+  return FFB_OK;
+}
+
+int ffb_block_pivots(ffb_ctx* ctx, void* stream, const double* B, int64_t s, int64_t n,
+                     int64_t ldb, int64_t j0, int64_t bb, int64_t* arr, int64_t* pos, double* gap,
+                     void* workspace, size_t workspace_bytes) {
+  if (!ctx) return FFB_ERR_ARGUMENT;
+  if (bb < 1 || j0 < 0 || j0 + bb > n) return fail(ctx, FFB_ERR_DIMENSION, "bad pivot block");
+  Work w;
+  pivot_geometry(ctx, n, s, w);
+  Bump b{static_cast<char*>(workspace), 0, workspace_bytes};
+  w.slots = b.take<PivSlot>(4 * (size_t)w.G);
+  w.slotdata = b.take<double>(2 * (size_t)w.G * s);
+  w.flags = b.take<uint32_t>(w.G);
+  w.hist = b.take<int64_t>(bb);
+  w.pwork = w.piv_smem ? nullptr : b.take<double>((size_t)w.G * s * w.cpc);
+  if (!b.ok) return fail(ctx, FFB_ERR_ARGUMENT, "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(w.flags, 0, sizeof(uint32_t) * w.G, st);
+  PivotArgs a{B, ldb, (int)s, n, j0, (int)bb, arr, pos, w.G, w.cpc, w.pwork, w.slots, w.slotdata,
+              w.flags, w.hist, gap};
+  if (e == cudaSuccess) {
+    static bool attr[2] = {false, false};
+    if (!attr[w.piv_smem]) {
+      cudaFuncSetAttribute(pivots_kernel_ptr(w.piv_smem), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           210 * 1024);
+      attr[w.piv_smem] = true;
+    }
+    e = launch_pivots(st, a, w.piv_smem, w.piv_smem_bytes);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "ffb_block_pivots");
+  return FFB_OK;
+}
+
+int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, int64_t n,
+            int64_t lda, const ffb_params* prm, const double* omega, ffb_gauss_cb gauss,
+            void* gauss_user, void* workspace, size_t workspace_bytes, ffb_result* out) {
+  if (!ctx || !prm || !out || !A || !omega || !workspace) return FFB_ERR_ARGUMENT;
+  Eng e;
+  e.ctx = ctx;
+  e.st = (cudaStream_t)stream;
+  Dims& D = e.D;
+  D = Dims{m, n, prm->k, prm->l, prm->b, prm->p, prm->b + prm->p, prm->d, prm->g, prm->seed, mode};
+  if (!validate(D) || lda < m) return fail(ctx, FFB_ERR_DIMENSION, "invalid dimensions/parameters");
+  if (mode == FFB_MODE_FLIPFLOP && (!out->u || !out->s || !out->v))
+    return fail(ctx, FFB_ERR_ARGUMENT, "u, s, v outputs are required");
+  const int lw = (mode == FFB_MODE_FLIPFLOP) ? std::max(svd_lwork(ctx, D.l), 1) : 1;
+  Work& w = e.w;
+  const size_t need = carve(ctx, D, workspace, workspace_bytes, w, lw);
+  if (need > workspace_bytes) return fail(ctx, FFB_ERR_ARGUMENT, "workspace too small");
+  e.gc.sms = ctx->sms;
+  e.gc.partial = w.gpart;
+  e.gc.partial_cap = w.gpart_cap;
+  cudaStream_t st = e.st;
+  const int64_t l = D.l, s = D.s, L1 = l + 1;
+  if (ctx->solver) cusolverDnSetStream(ctx->solver, st);
+
+  // g2 test matrix for swaps == 0 (stream 1000), generated on the host by the
+  // reference's RNG and staged now so the pipeline never waits for the host.
+  auto stage_gauss = [&](int64_t swaps) -> int {
+    const size_t cnt = (size_t)D.d * L1;
+    if (ctx->pinned_cap < cnt) {
+      if (ctx->pinned) cudaFreeHost(ctx->pinned);
+      cudaMallocHost(&ctx->pinned, cnt * sizeof(double));
+      ctx->pinned_cap = cnt;
+    }
+    cudaStreamSynchronize(st);  // previous staging copy may still read the buffer
+    if (!gauss || gauss(gauss_user, D.seed, 1000 + (uint64_t)swaps, D.d, L1, ctx->pinned) != 0)
+      return fail(ctx, FFB_ERR_ARGUMENT, "gauss callback failed");
+    e.ok(cudaMemcpyAsync(w.g2om, ctx->pinned, cnt * sizeof(double), cudaMemcpyHostToDevice, st));
+    return FFB_OK;
+  };
+  if (mode != FFB_MODE_TRQRCP) {
+    int rc = stage_gauss(0);
+    if (rc) return rc;
+  }
+
+  // ---------------------------------------------------------------- TRQRCP
+  e.ok(cudaMemsetAsync(w.status, 0, sizeof(uint32_t), st));
+  // B = Omega * A (Omega row-major s x m: A-operand with contiguous k)
+  e.gemm(s, n, m, 1.0, omega, m, true, A, lda, true, 0.0, w.B, s);
+  e.ok(launch_colsq(st, A, lda, m, n, w.colsq));
+  e.ok(launch_iota2(st, w.arr, w.pos, n));
+  e.memset2d(w.Y, m, m, l);
+  e.memset2d(w.T, l, l, l);
+  e.memset2d(w.WT, l, l, n);
+  e.memset2d(w.R, L1, L1, n);
+  {
+    static bool attr[2] = {false, false};
+    if (!attr[w.piv_smem]) {
+      cudaFuncSetAttribute(pivots_kernel_ptr(w.piv_smem), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           210 * 1024);
+      attr[w.piv_smem] = true;
+    }
+  }
+  for (int64_t j0 = 0; j0 < l && e.cerr == cudaSuccess; j0 += D.b) {
+    const int64_t bb = std::min<int64_t>(D.b, l - j0), e1 = j0 + bb;
+    // (K2) pivots on the sketch
+    e.ok(cudaMemsetAsync(w.flags, 0, sizeof(uint32_t) * w.G, st));
+    PivotArgs pa{w.B, s, (int)s, n, j0, (int)bb, w.arr, w.pos, w.G, w.cpc, w.pwork, w.slots,
+                 w.slotdata, w.flags, w.hist, w.gap + j0};
+    e.ok(launch_pivots(st, pa, w.piv_smem, w.piv_smem_bytes));
+    // (K4) panel P = A[:, piv] - Y[:, :j0] WT[:j0, piv]
+    e.ok(launch_gather_cols(st, A, lda, m, w.arr + j0, bb, w.P, m));
+    if (j0 > 0) {
+      e.ok(launch_gather_cols(st, w.WT, l, j0, w.arr + j0, bb, w.WTg, j0));
+      e.gemm(m, bb, j0, -1.0, w.Y, m, false, w.WTg, j0, true, 1.0, w.P, m);
+    }
+    // Householder QR of P[j0:, :] -> Y block, T block, Rb
+    e.hh_qr(w.P + j0, m - j0, bb, m, w.Y + j0 + j0 * m, m, w.T + j0 + j0 * l, l, w.Rb, bb, true);
+    // T12 = -T11 (Y1^T Y2) T22
+    if (j0 > 0) {
+      e.gemm(j0, bb, m - j0, 1.0, w.Y + j0, m, true, w.Y + j0 + j0 * m, m, true, 0.0, w.S1, j0);
+      e.gemm(j0, bb, bb, 1.0, w.S1, j0, false, w.T + j0 + j0 * l, l, true, 0.0, w.S2, j0);
+      e.gemm(j0, bb, j0, -1.0, w.T, l, false, w.S2, j0, true, 0.0, w.T + j0 * l, l);
+    }
+    // (K5) WT[j0:e, :] = T22^T (Y2^T A - (Y2^T Y1) WT[:j0, :])
+    e.gemm(bb, n, m - j0, 1.0, w.Y + j0 + j0 * m, m, true, A + j0, lda, true, 0.0, w.G1, bb);
+    if (j0 > 0) e.gemm(bb, n, j0, -1.0, w.S1, j0, true, w.WT, l, true, 1.0, w.G1, bb);
+    e.gemm(bb, n, bb, 1.0, w.T + j0 + j0 * l, l, true, w.G1, bb, true, 0.0, w.WT + j0, l);
+    // (K6) R[j0:e, :] = A[j0:e, :] - Y[j0:e, :e] WT[:e, :]
+    e.ok(launch_copy_rows(st, A + j0, lda, bb, n, w.R + j0, L1));
+    e.gemm(bb, n, e1, -1.0, w.Y + j0, m, false, w.WT, l, true, 1.0, w.R + j0, L1);
+    e.ok(launch_fix_rrows(st, w.R, L1, j0, (int)bb, w.arr, w.Rb, bb));
+    // sketch update B[:, trailing] -= (B_piv R11^{-1}) R12
+    if (e1 < n) {
+      e.ok(launch_gather_cols(st, w.B, s, s, w.arr + j0, bb, w.Bp, s));
+      e.ok(launch_trsm_rows_upper(st, w.Bp, s, (int)s, w.Rb, bb, (int)bb, w.Z, s, w.status));
+      e.gemm(s, n, bb, -1.0, w.Z, s, false, w.R + j0, L1, true, 1.0, w.B, s);
+    }
+  }
+
+  auto outputs_common = [&]() {
+    if (out->perm)
+      e.ok(cudaMemcpyAsync(out->perm, w.arr, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, st));
+    if (out->R) e.ok(launch_r_arranged(st, w.R, L1, w.arr, l, n, out->R, out->ldr, l));
+    if (out->B) e.ok(launch_gather_cols(st, w.B, s, s, w.arr, n, out->B, out->ldb));
+    if (out->pivot_gap)
+      e.ok(cudaMemcpyAsync(out->pivot_gap, w.gap, sizeof(double) * l, cudaMemcpyDeviceToDevice, st));
+  };
+
+  if (mode == FFB_MODE_TRQRCP) {
+    outputs_common();
+    if (out->Y) e.ok(cudaMemcpy2DAsync(out->Y, out->ldy * 8, w.Y, m * 8, m * 8, l, cudaMemcpyDeviceToDevice, st));
+    if (out->T) e.ok(cudaMemcpy2DAsync(out->T, out->ldt * 8, w.T, l * 8, l * 8, l, cudaMemcpyDeviceToDevice, st));
+    cudaError_t se = cudaStreamSynchronize(st);
+    if (e.cerr != cudaSuccess) return cuda_fail(ctx, e.cerr, "trqrcp launch");
+    if (se != cudaSuccess) return cuda_fail(ctx, se, "trqrcp");
+    uint32_t stw = 0;
+    cudaMemcpy(&stw, w.status, sizeof(stw), cudaMemcpyDeviceToHost);
+    out->status_bits = stw;
+    out->flops = e.gc.flops;
+    out->kernels = e.gc.launches + e.launches;
+    if (stw & (kStNonFinite | kStCholFail)) return fail(ctx, FFB_ERR_NUMERICAL, "numerical failure in TRQRCP");
+    return FFB_OK;
+  }
+
+  // ------------------------------------------------------------------ SRQR
+  // dense Q[:, :l] = E - Y (T Y[:l, :]^T)   (srqr.py:91-93)
+  e.gemm(l, l, l, 1.0, w.T, l, false, w.Y, m, false, 0.0, w.TYt, l);
+  e.gemm(m, l, l, -1.0, w.Y, m, false, w.TYt, l, true, 0.0, w.Q, m);
+  e.ok(launch_add_identity(st, w.Q, m, m, l, 1.0));
+  e.ok(cudaMemsetAsync(w.Q + m * l, 0, sizeof(double) * m, st));
+  e.ok(launch_rinit(st, w.B, s, (int)s, w.arr, n, l, w.r, w.rinit));
+  e.ok(launch_anorm(st, w.colsq, n, w.sc));
+  auto extend = [&]() {
+    e.ok(launch_ext_pick(st, l, n, w.arr, w.pos, w.r, w.rinit, w.sc));
+    e.ok(launch_ext_project(st, A, lda, m, l, w.Q, m, w.R, L1, w.arr, w.u, w.ct, w.part, w.sc, w.r, w.R));
+    const int nparts = (int)((m + 255) / 256);
+    e.ok(launch_ext_finish(st, w.part, nparts, l, n, w.arr, w.R, L1, w.r, w.sc, w.u, m, w.Q + m * l));
+  };
+  extend();
+  e.ok(launch_g2(st, w.R, L1, w.arr, l, w.g2om, (int)D.d, D.g, w.g2z, w.sc));
+
+  auto pack_and_outputs = [&]() {
+    e.ok(launch_pack(st, w.R, L1, w.arr, w.colsq, l, n, w.part, 0, w.sc));
+    outputs_common();
+    if (out->Q) e.ok(cudaMemcpy2DAsync(out->Q, out->ldq * 8, w.Q, m * 8, m * 8, L1, cudaMemcpyDeviceToDevice, st));
+    if (out->rtilde) e.ok(launch_r_arranged(st, w.R, L1, w.arr, L1, L1, out->rtilde, L1, L1));
+  };
+
+  // ------------------------------------------------------------ flip-flop
+  auto flipflop = [&]() {
+    const int64_t k = D.k;
+    e.ok(launch_build_rt(st, w.R, L1, w.arr, l, n, w.X, n));
+    e.hh_qr(w.X, n, l, n, w.Yl, n, w.Tl, l, w.Rl, l, false);
+    if (out->diag_L) e.ok(launch_diag(st, w.Rl, l, l, out->diag_L));
+    // Qhat1 = E - Yl (Tl Yl[:l,:]^T) ; Yh = Pi Qhat1 (rows scattered to original order)
+    e.gemm(l, l, l, 1.0, w.Tl, l, false, w.Yl, n, false, 0.0, w.TYt, l);
+    e.gemm(n, l, l, -1.0, w.Yl, n, false, w.TYt, l, true, 0.0, w.Qh, n);
+    e.ok(launch_add_identity(st, w.Qh, n, n, l, 1.0));
+    e.ok(launch_scatter_rows(st, w.Qh, n, n, l, w.arr, w.Yh, n));
+    // (K13) tmp = A * Yh
+    e.gemm(m, l, n, 1.0, A, lda, false, w.Yh, n, true, 0.0, w.tmp, m);
+    // (K14) tmp = Qt Rt, SVD(Rt)
+    e.hh_qr(w.tmp, m, l, m, w.Yt, m, w.Tt, l, w.Rt, l, true);
+    if (ctx->solver && e.cerr == cudaSuccess) {
+      cusolverStatus_t cs = cusolverDnDgesvd(ctx->solver, 'A', 'A', (int)l, (int)l, w.Rt, (int)l,
+                                             w.sig, w.Us, (int)l, w.VsT, (int)l, w.svdwork,
+                                             w.lwork, nullptr, w.svdinfo);
+      if (cs != CUSOLVER_STATUS_SUCCESS) e.cerr = cudaErrorUnknown;
+      ++e.launches;
+    }
+    // (K15) u = Qt[:, :l] Us[:, :k] ; v = Yh Vs[:, :k]
+    e.gemm(l, k, l, 1.0, w.Yt, m, true, w.Us, l, true, 0.0, w.W1, l);
+    e.gemm(l, k, l, 1.0, w.Tt, l, false, w.W1, l, true, 0.0, w.W2, l);
+    e.gemm(m, k, l, -1.0, w.Yt, m, false, w.W2, l, true, 0.0, out->u, out->ldu);
+    e.ok(launch_add_top(st, out->u, out->ldu, w.Us, l, l, k));
+    e.gemm(n, k, l, 1.0, w.Yh, n, false, w.VsT, l, false, 0.0, out->v, out->ldv);
+    e.ok(cudaMemcpyAsync(out->s, w.sig, sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
+    if (out->sv_all) e.ok(cudaMemcpyAsync(out->sv_all, w.sig, sizeof(double) * l, cudaMemcpyDeviceToDevice, st));
+  };
+
+  pack_and_outputs();
+  if (mode == FFB_MODE_FLIPFLOP) flipflop();
+
+  auto read_sc = [&]() -> cudaError_t {
+    e.ok(cudaMemcpyAsync(ctx->sc_host, w.sc, sizeof(SrqrScalars), cudaMemcpyDeviceToHost, st));
+    return cudaStreamSynchronize(st);
+  };
+  cudaError_t se = read_sc();
+  if (e.cerr != cudaSuccess) return cuda_fail(ctx, e.cerr, "launch");
+  if (se != cudaSuccess) return cuda_fail(ctx, se, "srqr");
+  SrqrScalars sc = *ctx->sc_host;
+  uint32_t stw = 0;
+  cudaMemcpy(&stw, w.status, sizeof(stw), cudaMemcpyDeviceToHost);
+  stw |= sc.status;
+  out->status_bits = stw;
+  if (stw & kStNonFinite) return fail(ctx, FFB_ERR_NUMERICAL, "non-finite values in input or factors");
+  if (stw & kStCholFail) return fail(ctx, FFB_ERR_NUMERICAL, "panel CholeskyQR breakdown (rank-deficient panel)");
+  if (stw & kStSingular) return fail(ctx, FFB_ERR_SINGULAR_TRAILING, "zero diagonal in leading triangular block");
+
+  int64_t swaps = 0;
+  if (sc.need_swap) {
+    // ---- the reference's swap loop (srqr.py:192-206), host-driven
+    while (true) {
+      if (swaps >= 50 * l) {
+        pack_and_outputs();
+        se = read_sc();
+        sc = *ctx->sc_host;
+        out->alpha = sc.alpha; out->g1 = sc.g1; out->g2 = sc.g2; out->r22 = sc.r22;
+        out->tau_bound = sc.tau; out->tau_hat_bound = sc.tau_hat; out->swaps = swaps;
+        return fail(ctx, FFB_ERR_CERTIFICATION, "swap cap reached");
+      }
+      e.ok(launch_ext_row(st, A, lda, m, n, l, w.Q, m, w.R, L1, w.arr, w.colsq, w.r, w.rinit, w.sc));
+      if (swaps < 64) out->i_off_trace[swaps] = sc.i_off;
+      ++swaps;
+      e.ok(launch_rotate_out(st, w.R, L1, w.Q, m, m, n, l, w.arr, w.pos, w.r, w.rinit, w.sc, w.rot));
+      e.ok(launch_revert(st, w.R, L1, w.arr, l, n, w.r));
+      extend();
+      se = read_sc();
+      if (e.cerr != cudaSuccess || se != cudaSuccess) return cuda_fail(ctx, e.cerr ? e.cerr : se, "swap");
+      sc = *ctx->sc_host;
+      if (!(sc.alpha > 0.0)) break;
+      int rc = stage_gauss(swaps);
+      if (rc) return rc;
+      e.ok(launch_g2(st, w.R, L1, w.arr, l, w.g2om, (int)D.d, D.g, w.g2z, w.sc));
+      se = read_sc();
+      if (e.cerr != cudaSuccess || se != cudaSuccess) return cuda_fail(ctx, e.cerr ? e.cerr : se, "swap g2");
+      sc = *ctx->sc_host;
+      if (sc.status & kStSingular) return fail(ctx, FFB_ERR_SINGULAR_TRAILING, "zero diagonal in leading triangular block");
+      if (!sc.need_swap) break;
+    }
+    pack_and_outputs();
+    if (mode == FFB_MODE_FLIPFLOP) flipflop();
+    se = read_sc();
+    if (e.cerr != cudaSuccess) return cuda_fail(ctx, e.cerr, "launch");
+    if (se != cudaSuccess) return cuda_fail(ctx, se, "flipflop");
+    sc = *ctx->sc_host;
+  }
+  if (mode == FFB_MODE_FLIPFLOP) {
+    int info = 0;
+    cudaMemcpy(&info, w.svdinfo, sizeof(int), cudaMemcpyDeviceToHost);
+    if (info != 0) return fail(ctx, FFB_ERR_NUMERICAL, "small SVD did not converge");
+  }
+  out->alpha = sc.alpha;
+  out->g1 = sc.g1;
+  out->g2 = sc.alpha > 0.0 ? sc.g2 : 0.0;
+  out->r22 = sc.r22;
+  out->tau_bound = sc.tau;
+  out->tau_hat_bound = sc.tau_hat;
+  out->swaps = swaps;
+  out->flops = e.gc.flops;
+  out->kernels = e.gc.launches + e.launches;
+  return FFB_OK;
+}
+
+int ffb_flipflop(ffb_ctx* ctx, void* stream, const double* A, int64_t m, int64_t n, int64_t lda,
+                 const ffb_params* prm, const double* omega, ffb_gauss_cb gauss, void* gauss_user,
+                 void* workspace, size_t workspace_bytes, ffb_result* out) {
+  return ffb_run(ctx, stream, FFB_MODE_FLIPFLOP, A, m, n, lda, prm, omega, gauss, gauss_user,
+                 workspace, workspace_bytes, out);
+}
+
+}  // extern "C"

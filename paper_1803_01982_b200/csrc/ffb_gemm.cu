@@ -1,0 +1,124 @@
+// Host dispatcher for the FP64 DMMA GEMM engine (tile configs x operand layouts).
+#include <algorithm>
+
+#include "ffb_gemm.h"
+#include "gemm_f64.cuh"
+
+namespace ffb {
+
+namespace {
+
+template <int BM, int BN, int BK, int WM, int WN, bool AK, bool BKC, int ST>
+cudaError_t launch_cfg(cudaStream_t st, const GemmArgs& g, dim3 grid) {
+  using Cfg = GemmCfg<BM, BN, BK, WM, WN, AK, BKC, ST>;
+  auto kern = gemm_f64_kernel<BM, BN, BK, WM, WN, AK, BKC, ST>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
+    attr = true;
+  }
+  kern<<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(g);
+  return cudaGetLastError();
+}
+
+struct Shape {
+  int bm, bn, bk;
+};
+
+// Tile selection by M (the output rows): sketch / WT rows have M = s or b <= 96,
+// the tall products (A*Yhat, panel updates) have M = m.
+int pick_cfg(int64_t M) {
+  if (M <= 48) return 0;
+  if (M <= 64) return 1;
+  if (M <= 96) return 2;
+  if (M >= 1024) return 3;
+  return 1;
+}
+
+const Shape kShapes[4] = {{48, 64, 16}, {64, 64, 16}, {96, 64, 16}, {128, 64, 16}};
+
+template <bool AK, bool BKC>
+cudaError_t launch_layout(int cfg, cudaStream_t st, const GemmArgs& g, dim3 grid) {
+  switch (cfg) {
+    case 0: return launch_cfg<48, 64, 16, 24, 32, AK, BKC, 4>(st, g, grid);
+    case 1: return launch_cfg<64, 64, 16, 32, 32, AK, BKC, 4>(st, g, grid);
+    case 2: return launch_cfg<96, 64, 16, 48, 32, AK, BKC, 4>(st, g, grid);
+    default: return launch_cfg<128, 64, 16, 32, 32, AK, BKC, 4>(st, g, grid);
+  }
+}
+
+}  // namespace
+
+cudaError_t gemm_f64(GemmCtx& c, cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha,
+                     const double* A, int64_t lda, bool akc, const double* B, int64_t ldb, bool bkc,
+                     double beta, double* C, int64_t ldc, GemmPartialOut* pout) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  const int cfg = pick_cfg(M);
+  const Shape sh = kShapes[cfg];
+  const int64_t gx = (N + sh.bn - 1) / sh.bn, gy = (M + sh.bm - 1) / sh.bm;
+  const int64_t tiles = gx * gy;
+  const int64_t target = 2LL * c.sms;
+  int64_t splits = 1;
+  if (K <= 0) {
+    splits = 1;
+  } else if (pout) {
+    splits = std::max<int64_t>(1, std::min<int64_t>(pout->max_splits, K / 256));
+    while (splits > 1 && (size_t)splits * M * N > c.partial_cap) --splits;
+  } else if (tiles < target) {
+    splits = (target + tiles - 1) / tiles;
+    splits = std::min<int64_t>(splits, std::max<int64_t>(1, K / (sh.bk * 8)));
+    splits = std::min<int64_t>(splits, 64);
+    while (splits > 1 && (size_t)splits * M * N > c.partial_cap) --splits;
+  }
+  GemmArgs g;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.alpha = alpha;
+  g.beta = beta;
+  g.A = A;
+  g.lda = lda;
+  g.B = B;
+  g.ldb = ldb;
+  g.C = C;
+  g.ldc = ldc;
+  g.partial = c.partial;
+  g.splits = (int)splits;
+  g.force_partial = pout ? 1 : 0;
+  int64_t kper = (K + splits - 1) / splits;
+  kper = ((kper + sh.bk - 1) / sh.bk) * sh.bk;
+  g.k_per = std::max<int64_t>(kper, sh.bk);
+  if (K > 0) {
+    // recompute the effective split count after rounding k_per up
+    splits = (K + g.k_per - 1) / g.k_per;
+    g.splits = (int)splits;
+  }
+  if (pout) {
+    pout->part = c.partial;
+    pout->splits = (int)splits;
+  }
+  if (K <= 0) {
+    // C = beta * C (alpha * 0): handled by a tile pass with empty K.
+    g.splits = 1;
+    g.force_partial = pout ? 1 : 0;
+  }
+  dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)g.splits);
+  cudaError_t e;
+  if (akc && bkc) e = launch_layout<true, true>(cfg, st, g, grid);
+  else if (akc && !bkc) e = launch_layout<true, false>(cfg, st, g, grid);
+  else if (!akc && bkc) e = launch_layout<false, true>(cfg, st, g, grid);
+  else e = launch_layout<false, false>(cfg, st, g, grid);
+  if (e != cudaSuccess) return e;
+  c.launches += 1;
+  c.flops += 2 * M * N * std::max<int64_t>(K, 0);
+  if (g.splits > 1 && !pout) {
+    const int64_t total = M * N;
+    unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 4096);
+    gemm_splitk_reduce<<<blocks, 256, 0, st>>>(c.partial, g.splits, M, N, alpha, beta, C, ldc);
+    c.launches += 1;
+    e = cudaGetLastError();
+  }
+  return e;
+}
+
+}  // namespace ffb

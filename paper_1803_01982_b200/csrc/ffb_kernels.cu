@@ -1,0 +1,1230 @@
+// Non-GEMM kernels of the Flip-Flop SRQR engine (sm_100a).
+//
+// Reference semantics cited per kernel; see DESIGN.md for the data layout:
+// A, B (sketch), R, WT are kept in ORIGINAL column order and an arrangement
+// array arr[pos] = column (with its inverse pos[column]) replaces the
+// reference's physical reorders (ffsrqr/sketch.py:70-72,120-121).
+#include <math.h>
+
+#include "ffb_common.cuh"
+#include "ffb_kernels.cuh"
+
+namespace ffb {
+
+#define FFB_LAUNCH_CHECK() return cudaGetLastError()
+
+FFB_DEV void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+FFB_DEV uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+static inline unsigned nblk(int64_t work, int per) {
+  int64_t b = (work + per - 1) / per;
+  if (b < 1) b = 1;
+  if (b > 2147483647LL) b = 2147483647LL;
+  return (unsigned)b;
+}
+
+// ----------------------------------------------------------------- basics
+
+__global__ void colsq_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n,
+                             double* __restrict__ colsq) {
+  const int lane = threadIdx.x & 31;
+  const int64_t col = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (col >= n) return;
+  const double* a = A + col * lda;
+  double s0 = 0.0, s1 = 0.0;
+  int64_t i = lane;
+  for (; i + 32 < m; i += 64) {
+    const double x = a[i], y = a[i + 32];
+    s0 = fma(x, x, s0);
+    s1 = fma(y, y, s1);
+  }
+  if (i < m) s0 = fma(a[i], a[i], s0);
+  const double s = warp_sum(s0 + s1);
+  if (lane == 0) colsq[col] = s;
+}
+
+cudaError_t launch_colsq(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n,
+                         double* colsq) {
+  colsq_kernel<<<nblk(n, 8), 256, 0, st>>>(A, lda, m, n, colsq);
+  FFB_LAUNCH_CHECK();
+}
+
+__global__ void iota2_kernel(int64_t* arr, int64_t* pos, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    arr[i] = i;
+    pos[i] = i;
+  }
+}
+
+cudaError_t launch_iota2(cudaStream_t st, int64_t* arr, int64_t* pos, int64_t n) {
+  iota2_kernel<<<nblk(n, 256) > 1024 ? 1024 : nblk(n, 256), 256, 0, st>>>(arr, pos, n);
+  FFB_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------ sketch QRCP pivots (K2)
+//
+// bb steps of Householder QRCP on a working copy of the sketch's trailing
+// columns (positions >= j0), returning only the swap-history arrangement —
+// ffsrqr/sketch.py:62-67 -> ffsrqr/_kernels_numba.py:15-94.  Cooperative
+// persistent kernel: CTA g owns original columns [g*cpc, (g+1)*cpc) in shared
+// memory (or an L2-resident global slab when they do not fit).  Each step:
+// local candidate -> publish (r, position, column data) -> one all-to-all flag
+// wait -> every CTA picks the same global winner (largest r, ties to the lowest
+// position) and computes the same reflector -> local update + norm downdate
+// with the 1e-8 guard recompute.
+
+template <bool SMEM>
+__global__ void __launch_bounds__(1024) pivots_kernel(PivotArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const int s = a.s, cpc = a.cpc, tid = threadIdx.x, nt = blockDim.x;
+  const int64_t c0 = (int64_t)blockIdx.x * cpc;
+  int64_t ncl = a.n - c0;
+  if (ncl > cpc) ncl = cpc;
+  if (ncl < 0) ncl = 0;
+  const int nc = (int)ncl;
+  double* W = SMEM ? sm : a.work + (size_t)blockIdx.x * s * cpc;   // [s][cpc]
+  double* base = SMEM ? sm + (size_t)s * cpc : sm;
+  double* r = base;
+  double* r0 = r + cpc;
+  int64_t* pp = reinterpret_cast<int64_t*>(r0 + cpc);
+  double* xv = reinterpret_cast<double*>(pp + cpc);    // winner column, then reflector v
+  double* red_v = xv + s + 1;
+  int64_t* red_i = reinterpret_cast<int64_t*>(red_v + 32);
+  __shared__ int s_wcta, s_wc;
+  __shared__ double s_tau, s_div, s_gap;
+
+  for (int idx = tid; idx < s * nc; idx += nt) {
+    const int c = idx / s, i = idx % s;
+    W[i * cpc + c] = a.B[i + (c0 + c) * a.ldb];
+  }
+  for (int c = tid; c < nc; c += nt) pp[c] = a.pos[c0 + c];
+  __syncthreads();
+  // r = squared column norms of the working copy (numba 22-29).
+  for (int c = tid; c < nc; c += nt) {
+    double t0 = 0.0, t1 = 0.0;
+    int i = 0;
+    for (; i + 1 < s; i += 2) {
+      const double x = W[i * cpc + c], y = W[(i + 1) * cpc + c];
+      t0 = fma(x, x, t0);
+      t1 = fma(y, y, t1);
+    }
+    if (i < s) t0 = fma(W[i * cpc + c], W[i * cpc + c], t0);
+    r[c] = t0 + t1;
+    r0[c] = r[c];
+  }
+  __syncthreads();
+
+  for (int j = 0; j < a.bb; ++j) {
+    const int64_t P = a.j0 + j;
+    const int par = j & 1;
+    // (1) local best (largest r, ties -> lowest position) and local runner-up.
+    ArgMax best{-1.0, -1};
+    for (int c = tid; c < nc; c += nt)
+      if (pp[c] >= P) best = argmax_better(best, ArgMax{r[c], pp[c]});
+    best = block_argmax(best, red_v, red_i);
+    ArgMax sec{-1.0, -1};
+    for (int c = tid; c < nc; c += nt)
+      if (pp[c] >= P && pp[c] != best.i) sec = argmax_better(sec, ArgMax{r[c], pp[c]});
+    sec = block_argmax(sec, red_v, red_i);
+    if (tid == 0) s_wc = -1;
+    __syncthreads();
+    if (best.i >= 0)
+      for (int c = tid; c < nc; c += nt)
+        if (pp[c] == best.i) s_wc = c;
+    __syncthreads();
+    // (2) publish candidate + its column data, then release this CTA's flag.
+    PivSlot* slot = a.slots + (size_t)par * a.G * 2;
+    double* sdata = a.slotdata + ((size_t)par * a.G + blockIdx.x) * s;
+    const int wc = s_wc;
+    if (wc >= 0)
+      for (int i = tid; i < s; i += nt) sdata[i] = W[i * cpc + wc];
+    if (tid == 0) {
+      slot[2 * blockIdx.x] = PivSlot{best.v, best.i};
+      slot[2 * blockIdx.x + 1] = PivSlot{sec.v, sec.i};
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release_u32(a.flags + blockIdx.x, (uint32_t)(j + 1));
+    // (3) all-to-all wait; every CTA derives the same global winner.
+    ArgMax g{-1.0, -1};
+    for (int t = tid; t < a.G; t += nt) {
+      while (ld_acquire_u32(a.flags + t) < (uint32_t)(j + 1)) {
+      }
+      const PivSlot ps = slot[2 * t];
+      if (ps.pos >= 0) g = argmax_better(g, ArgMax{ps.r, ps.pos});
+    }
+    const ArgMax gw = block_argmax(g, red_v, red_i);
+    // runner-up = max over (other CTAs' bests, winner CTA's second) -> gap trace.
+    ArgMax g2{-1.0, -1};
+    if (tid == 0) s_wcta = -1;
+    __syncthreads();
+    for (int t = tid; t < a.G; t += nt) {
+      const PivSlot b0 = slot[2 * t], b1 = slot[2 * t + 1];
+      if (b0.pos == gw.i) {
+        s_wcta = t;
+        if (b1.pos >= 0) g2 = argmax_better(g2, ArgMax{b1.r, b1.pos});
+      } else if (b0.pos >= 0) {
+        g2 = argmax_better(g2, ArgMax{b0.r, b0.pos});
+      }
+    }
+    g2 = block_argmax(g2, red_v, red_i);
+    const int wcta = s_wcta;
+    const int64_t wpos = gw.i;
+    {
+      const double* wd = a.slotdata + ((size_t)par * a.G + wcta) * s;
+      for (int i = tid; i < s; i += nt) xv[i] = wd[i];
+    }
+    // (4) swap positions P <-> wpos (swap-history semantics, numba 38-51).
+    for (int c = tid; c < nc; c += nt) {
+      if (pp[c] == wpos) pp[c] = P;
+      else if (pp[c] == P) pp[c] = wpos;
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+      const int64_t t = a.arr[P];
+      a.arr[P] = a.arr[wpos];
+      a.arr[wpos] = t;
+      a.hist[j] = wpos;
+      if (a.gap) a.gap[j] = (gw.v > 0.0 && g2.i >= 0) ? (gw.v - g2.v) / gw.v : 1.0;
+    }
+    __syncthreads();
+    // (5) reflector from the winner column, rows j..s-1 (ffsrqr/qr.py:21-43 and
+    // _kernels_numba.py:53-71): tail == 0 -> identity (tau = 0); otherwise
+    // alpha = -sign(x0)||x|| (+||x|| when x0 == 0), v = tail / (x0 - alpha).
+    if (tid < 32) {
+      double t = 0.0;
+      for (int i = j + 1 + tid; i < s; i += 32) t = fma(xv[i], xv[i], t);
+      t = warp_sum(t);
+      if (tid == 0) {
+        const double x0 = xv[j];
+        double tau = 0.0, div = 1.0;
+        if (t != 0.0) {
+          const double nrm = sqrt(x0 * x0 + t);
+          const double alpha = x0 == 0.0 ? nrm : -copysign(nrm, x0);
+          div = x0 - alpha;
+          tau = (alpha - x0) / alpha;
+        }
+        s_tau = tau;
+        s_div = div;
+      }
+    }
+    __syncthreads();
+    const double tau = s_tau;
+    if (tau != 0.0) {
+      const double div = s_div;
+      for (int i = j + 1 + tid; i < s; i += nt) xv[i] = xv[i] / div;
+    }
+    __syncthreads();
+    // (6) apply H = I - tau v v^T to the active local columns, then downdate
+    // r -= R[j,c]^2 with the guard recompute (numba 72-92).
+    for (int c = tid; c < nc; c += nt) {
+      if (pp[c] <= P) continue;
+      double* col = W + c;
+      if (tau != 0.0) {
+        double w0 = col[j * cpc], w1 = 0.0;
+        int i = j + 1;
+        for (; i + 1 < s; i += 2) {
+          w0 = fma(xv[i], col[i * cpc], w0);
+          w1 = fma(xv[i + 1], col[(i + 1) * cpc], w1);
+        }
+        if (i < s) w0 = fma(xv[i], col[i * cpc], w0);
+        const double w = (w0 + w1) * tau;
+        col[j * cpc] -= w;
+        for (int q = j + 1; q < s; ++q) col[q * cpc] = fma(-xv[q], w, col[q * cpc]);
+      }
+      const double rj = col[j * cpc];
+      double rr = r[c] - rj * rj;
+      if (rr < 1e-8 * r0[c] || rr < 0.0) {
+        double t0 = 0.0, t1 = 0.0;
+        int i = j + 1;
+        for (; i + 1 < s; i += 2) {
+          t0 = fma(col[i * cpc], col[i * cpc], t0);
+          t1 = fma(col[(i + 1) * cpc], col[(i + 1) * cpc], t1);
+        }
+        if (i < s) t0 = fma(col[i * cpc], col[i * cpc], t0);
+        const double f = t0 + t1;
+        rr = f > 0.0 ? f : 0.0;
+      }
+      r[c] = rr;
+    }
+    __syncthreads();
+  }
+  for (int c = tid; c < nc; c += nt) a.pos[c0 + c] = pp[c];
+}
+
+size_t pivots_smem_bytes(int s, int cpc, bool smem_mode) {
+  size_t b = (smem_mode ? (size_t)s * cpc : 0) * sizeof(double);
+  b += (size_t)cpc * (2 * sizeof(double) + sizeof(int64_t));
+  b += (size_t)(s + 1) * sizeof(double) + 32 * sizeof(double) + 32 * sizeof(int64_t);
+  return b;
+}
+
+void* pivots_kernel_ptr(bool smem_mode) {
+  return smem_mode ? (void*)pivots_kernel<true> : (void*)pivots_kernel<false>;
+}
+
+cudaError_t launch_pivots(cudaStream_t st, const PivotArgs& a, bool smem_mode, size_t smem) {
+  int threads = ((a.cpc + 31) / 32) * 32;
+  if (threads < 64) threads = 64;
+  if (threads > 1024) threads = 1024;
+  PivotArgs args = a;
+  void* kargs[] = {&args};
+  return cudaLaunchCooperativeKernel(pivots_kernel_ptr(smem_mode), dim3(a.G), dim3(threads), kargs,
+                                     smem, st);
+}
+
+
+// ------------------------------------------------------- gathers / copies
+
+__global__ void gather_cols_kernel(const double* __restrict__ src, int64_t ld_src, int64_t rows,
+                                   const int64_t* __restrict__ idx, int64_t ncols,
+                                   double* __restrict__ dst, int64_t ld_dst) {
+  const int64_t j = blockIdx.y;
+  const int64_t c = idx[j];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i + j * ld_dst] = src[i + c * ld_src];
+}
+
+cudaError_t launch_gather_cols(cudaStream_t st, const double* src, int64_t ld_src, int64_t rows,
+                               const int64_t* idx, int64_t ncols, double* dst, int64_t ld_dst) {
+  if (rows <= 0 || ncols <= 0) return cudaSuccess;
+  unsigned gx = nblk(rows, 256);
+  if (gx > 64) gx = 64;
+  gather_cols_kernel<<<dim3(gx, (unsigned)ncols), 256, 0, st>>>(src, ld_src, rows, idx, ncols, dst,
+                                                                 ld_dst);
+  FFB_LAUNCH_CHECK();
+}
+
+// dst[idx[c], j] = src[c, j]
+__global__ void scatter_rows_kernel(const double* __restrict__ src, int64_t ld_src, int64_t nrows,
+                                    int64_t ncols, const int64_t* __restrict__ idx,
+                                    double* __restrict__ dst, int64_t ld_dst) {
+  const int64_t total = nrows * ncols;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t % nrows, j = t / nrows;
+    dst[idx[c] + j * ld_dst] = src[c + j * ld_src];
+  }
+}
+
+cudaError_t launch_scatter_rows(cudaStream_t st, const double* src, int64_t ld_src, int64_t nrows,
+                                int64_t ncols, const int64_t* idx, double* dst, int64_t ld_dst) {
+  const int64_t total = nrows * ncols;
+  if (total <= 0) return cudaSuccess;
+  unsigned g = nblk(total, 256);
+  if (g > 4096) g = 4096;
+  scatter_rows_kernel<<<g, 256, 0, st>>>(src, ld_src, nrows, ncols, idx, dst, ld_dst);
+  FFB_LAUNCH_CHECK();
+}
+
+__global__ void copy2d_kernel(const double* __restrict__ src, int64_t ld_src, int64_t rows,
+                              int64_t cols, double* __restrict__ dst, int64_t ld_dst) {
+  const int64_t total = rows * cols;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t % rows, j = t / rows;
+    dst[i + j * ld_dst] = src[i + j * ld_src];
+  }
+}
+
+cudaError_t launch_copy_rows(cudaStream_t st, const double* src, int64_t ld_src, int64_t rows,
+                             int64_t cols, double* dst, int64_t ld_dst) {
+  const int64_t total = rows * cols;
+  if (total <= 0) return cudaSuccess;
+  unsigned g = nblk(total, 256);
+  if (g > 8192) g = 8192;
+  copy2d_kernel<<<g, 256, 0, st>>>(src, ld_src, rows, cols, dst, ld_dst);
+  FFB_LAUNCH_CHECK();
+}
+
+__global__ void fill_kernel(double* p, size_t count, double v) {
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < count;
+       t += (size_t)gridDim.x * blockDim.x)
+    p[t] = v;
+}
+
+cudaError_t launch_fill(cudaStream_t st, double* p, size_t count, double v) {
+  if (!count) return cudaSuccess;
+  unsigned g = nblk((int64_t)count, 256);
+  if (g > 8192) g = 8192;
+  fill_kernel<<<g, 256, 0, st>>>(p, count, v);
+  FFB_LAUNCH_CHECK();
+}
+
+__global__ void add_identity_kernel(double* X, int64_t ld, int64_t nd, double scale) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd;
+       i += (int64_t)gridDim.x * blockDim.x)
+    X[i + i * ld] += scale;
+}
+
+cudaError_t launch_add_identity(cudaStream_t st, double* X, int64_t ld, int64_t rows,
+                                int64_t cols, double scale) {
+  const int64_t nd = rows < cols ? rows : cols;
+  if (nd <= 0) return cudaSuccess;
+  add_identity_kernel<<<nblk(nd, 256) > 256 ? 256 : nblk(nd, 256), 256, 0, st>>>(X, ld, nd, scale);
+  FFB_LAUNCH_CHECK();
+}
+
+__global__ void add_top_kernel(double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t rows,
+                               int64_t cols) {
+  const int64_t total = rows * cols;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t % rows, j = t / rows;
+    X[i + j * ldx] += Y[i + j * ldy];
+  }
+}
+
+cudaError_t launch_add_top(cudaStream_t st, double* X, int64_t ldx, const double* Y, int64_t ldy,
+                           int64_t rows, int64_t cols) {
+  const int64_t total = rows * cols;
+  if (total <= 0) return cudaSuccess;
+  unsigned g = nblk(total, 256);
+  if (g > 4096) g = 4096;
+  add_top_kernel<<<g, 256, 0, st>>>(X, ldx, Y, ldy, rows, cols);
+  FFB_LAUNCH_CHECK();
+}
+
+__global__ void finite_check_kernel(const double* x, size_t count, uint32_t* status) {
+  bool bad = false;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < count;
+       t += (size_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(x[t]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(status, kStNonFinite);
+}
+
+cudaError_t launch_finite_check(cudaStream_t st, const double* x, size_t count, uint32_t* status) {
+  if (!count) return cudaSuccess;
+  unsigned g = nblk((int64_t)count, 256);
+  if (g > 1184) g = 1184;
+  finite_check_kernel<<<g, 256, 0, st>>>(x, count, status);
+  FFB_LAUNCH_CHECK();
+}
+
+// ------------------------------------- panel reconstruction (K4 / K12)
+//
+// A Householder panel (rows x w, w <= 64) is factored as shifted CholeskyQR3
+// (Gram -> Cholesky -> X R^-1, three passes; first pass shifted by
+// 11(Mw + w(w+1)) u tr(G), Fukaya et al. 2020) followed by the Householder
+// reconstruction of Ballard et al.: LU without pivoting of Q_top*D - I where
+// the sign D_c is chosen so that every pivot is <= -1.  This reproduces the
+// reflectors of LAPACK-style Householder QR with the reference's sign rule
+// alpha = -sign(x0)||x|| (ffsrqr/qr.py:21-43, _kernels_numpy.py:84-109):
+// Q - E = Y (-T Y1^T) is exactly that LU, with pivot -tau_c in [-2,-1].  A
+// pivot of exactly 0 (|z| == 1) is the reference's identity-reflector branch.
+
+constexpr int kMaxW = 64;
+constexpr int kSLD = kMaxW + 1;
+
+// Sum split-K partial Grams, optional shift, Cholesky (upper R, R^T R = G),
+// R^-1, and Racc <- R * Racc (Racc := R when `first`).  One CTA.
+__global__ void __launch_bounds__(256) cholinv_kernel(const double* __restrict__ part, int splits,
+                                                      int w, int64_t rows_m, int shift, int first,
+                                                      double* Racc, double* Rinv,
+                                                      uint32_t* status) {
+  extern __shared__ __align__(16) double dsm[];
+  double* G = dsm;
+  double* R = G + kMaxW * kSLD;
+  double* X = R + kMaxW * kSLD;
+  __shared__ double red[8];
+  __shared__ int bad;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int ww = w * w;
+  if (tid == 0) bad = 0;
+  for (int t = tid; t < ww; t += nt) {
+    double acc = 0.0;
+    for (int q = 0; q < splits; ++q) acc += part[(size_t)q * ww + t];
+    const int i = t % w, j = t / w;
+    G[i * kSLD + j] = acc;
+    R[i * kSLD + j] = 0.0;
+  }
+  __syncthreads();
+  double tr = 0.0;
+  for (int i = tid; i < w; i += nt) tr += G[i * kSLD + i];
+  tr = block_sum(tr, red);
+  if (tr == 0.0) {
+    // all-zero panel: R = I, R^-1 = I, Racc := 0 (first) / unchanged.  signlu
+    // then emits identity reflectors (reference's tail == 0 branch).
+    for (int t = tid; t < ww; t += nt) {
+      const int i = t % w, j = t / w;
+      Rinv[i + j * w] = (i == j) ? 1.0 : 0.0;
+      if (first) Racc[i + j * w] = 0.0;
+    }
+    return;
+  }
+  if (shift) {
+    const double sh = 11.0 * ((double)rows_m * w + (double)w * (w + 1)) * 1.1102230246251565e-16 * tr;
+    for (int i = tid; i < w; i += nt) G[i * kSLD + i] += sh;
+    __syncthreads();
+  }
+  // right-looking Cholesky on the upper triangle
+  for (int j = 0; j < w; ++j) {
+    if (tid == 0) {
+      double d = G[j * kSLD + j];
+      if (!(d > 0.0) || !isfinite(d)) {
+        bad = 1;
+        d = d > 0.0 ? d : 1e-300;
+      }
+      R[j * kSLD + j] = sqrt(d);
+    }
+    __syncthreads();
+    const double rjj = R[j * kSLD + j];
+    for (int k = j + 1 + tid; k < w; k += nt) R[j * kSLD + k] = G[j * kSLD + k] / rjj;
+    __syncthreads();
+    const int rem = w - j - 1;
+    for (int t = tid; t < rem * rem; t += nt) {
+      const int k = j + 1 + t / rem, q = j + 1 + t % rem;
+      if (q >= k) G[k * kSLD + q] -= R[j * kSLD + k] * R[j * kSLD + q];
+    }
+    __syncthreads();
+  }
+  // inverse of upper-triangular R, one column per thread (back substitution)
+  for (int c = tid; c < w; c += nt) {
+    for (int i = 0; i < w; ++i) X[i * kSLD + c] = 0.0;
+    X[c * kSLD + c] = 1.0 / R[c * kSLD + c];
+    for (int i = c - 1; i >= 0; --i) {
+      double acc = 0.0;
+      for (int k = i + 1; k <= c; ++k) acc = fma(R[i * kSLD + k], X[k * kSLD + c], acc);
+      X[i * kSLD + c] = -acc / R[i * kSLD + i];
+    }
+  }
+  __syncthreads();
+  for (int t = tid; t < ww; t += nt) {
+    const int i = t % w, j = t / w;
+    Rinv[i + j * w] = X[i * kSLD + j];
+    double acc;
+    if (first) {
+      acc = R[i * kSLD + j];
+    } else {
+      acc = 0.0;
+      for (int k = i; k <= j; ++k) acc = fma(R[i * kSLD + k], Racc[k + j * w], acc);
+    }
+    G[i * kSLD + j] = acc;  // reuse G as staging for the new Racc
+  }
+  __syncthreads();
+  for (int t = tid; t < ww; t += nt) {
+    const int i = t % w, j = t / w;
+    Racc[i + j * w] = G[i * kSLD + j];
+  }
+  if (tid == 0 && bad) atomicOr(status, kStCholFail);
+}
+
+cudaError_t launch_cholinv(cudaStream_t st, const double* part, int splits, int w, int64_t rows_m,
+                           bool shift, bool first, double* Racc, double* Rinv, uint32_t* status) {
+  static bool init = false;
+  constexpr int kSm = 3 * kMaxW * kSLD * sizeof(double);
+  if (!init) {
+    cudaFuncSetAttribute(cholinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSm);
+    init = true;
+  }
+  cholinv_kernel<<<1, 256, kSm, st>>>(part, splits, w, rows_m, shift ? 1 : 0, first ? 1 : 0, Racc,
+                                     Rinv, status);
+  FFB_LAUNCH_CHECK();
+}
+
+// LU of Q_top*D - I with per-column sign choice; emits L (into Y's top w rows),
+// T = -U L^{-T}, R = D*Racc (upper), D, and Ut = D * U^{-1} (zero-pivot columns
+// zeroed) so that the lower reflector rows are Y2 = Q_bottom * Ut.  One CTA.
+__global__ void __launch_bounds__(256) signlu_kernel(const double* __restrict__ Qtop, int64_t ldq,
+                                                     int w, const double* __restrict__ Racc,
+                                                     double* Y, int64_t ldy, double* T,
+                                                     int64_t ldt, double* Rout, int64_t ldr,
+                                                     double* Ut, double* Dout) {
+  extern __shared__ __align__(16) double dsm[];
+  double* q = dsm;
+  double* L = q + kMaxW * kSLD;
+  double* U = L + kMaxW * kSLD;
+  __shared__ double Dd[kMaxW];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  bool zero_panel = true;
+  for (int i = 0; i < w; ++i) zero_panel &= (Racc[i + i * w] == 0.0);
+  if (zero_panel) {
+    for (int t = tid; t < w * w; t += nt) {
+      const int i = t % w, j = t / w;
+      Y[i + j * ldy] = (i == j) ? 1.0 : 0.0;
+      T[i + j * ldt] = 0.0;
+      Rout[i + j * ldr] = 0.0;
+      Ut[i + j * w] = 0.0;
+    }
+    for (int i = tid; i < w; i += nt) Dout[i] = 1.0;
+    return;
+  }
+  for (int t = tid; t < w * w; t += nt) {
+    const int i = t % w, j = t / w;
+    q[i * kSLD + j] = Qtop[i + j * ldq];
+    L[i * kSLD + j] = (i == j) ? 1.0 : 0.0;
+    U[i * kSLD + j] = 0.0;
+  }
+  __syncthreads();
+  for (int c = 0; c < w; ++c) {
+    if (tid == 0) {
+      const double z = q[c * kSLD + c];
+      double d;
+      if (fabs(z) == 1.0) d = z > 0.0 ? 1.0 : -1.0;    // identity reflector (tail == 0)
+      else d = z > 0.0 ? -1.0 : 1.0;                   // pivot -(1+|z|) = -tau
+      Dd[c] = d;
+      U[c * kSLD + c] = d * z - 1.0;
+    }
+    __syncthreads();
+    const double d = Dd[c], ucc = U[c * kSLD + c];
+    for (int i = c + 1 + tid; i < w; i += nt) L[i * kSLD + c] = ucc != 0.0 ? d * q[i * kSLD + c] / ucc : 0.0;
+    for (int k = tid; k < c; k += nt) U[k * kSLD + c] = d * q[k * kSLD + c];
+    __syncthreads();
+    const int rem = w - c - 1;
+    for (int t = tid; t < rem * rem; t += nt) {
+      const int i = c + 1 + t % rem, jj = c + 1 + t / rem;
+      q[i * kSLD + jj] -= L[i * kSLD + c] * q[c * kSLD + jj];
+    }
+    __syncthreads();
+  }
+  // Ut = D * U^{-1} with zero pivots -> zero columns; row i solves e_i = y U.
+  // T = -U L^{-T}: row i solves t L^T = -U[i,:].
+  for (int i = tid; i < w; i += nt) {
+    double y[kMaxW];
+    for (int c = 0; c < w; ++c) {
+      double acc = (c == i) ? 1.0 : 0.0;
+      for (int k = 0; k < c; ++k) acc = fma(-y[k], U[k * kSLD + c], acc);
+      const double ucc = U[c * kSLD + c];
+      y[c] = ucc != 0.0 ? acc / ucc : 0.0;
+    }
+    for (int c = 0; c < w; ++c) Ut[i + c * w] = Dd[i] * y[c];
+    for (int jj = 0; jj < w; ++jj) {
+      double acc = -U[i * kSLD + jj];
+      for (int k = 0; k < jj; ++k) acc = fma(-y[k], L[jj * kSLD + k], acc);
+      y[jj] = acc;  // overwrite is safe: y[k<jj] now holds t_k
+    }
+    for (int jj = 0; jj < w; ++jj) T[i + jj * ldt] = y[jj];
+  }
+  for (int t = tid; t < w * w; t += nt) {
+    const int i = t % w, j = t / w;
+    Y[i + j * ldy] = L[i * kSLD + j];
+    Rout[i + j * ldr] = (i <= j) ? Dd[i] * Racc[i + j * w] : 0.0;
+  }
+  for (int i = tid; i < w; i += nt) Dout[i] = Dd[i];
+}
+
+cudaError_t launch_signlu(cudaStream_t st, const double* Qtop, int64_t ldq, int w,
+                          const double* Racc, double* Y, int64_t ldy, double* T, int64_t ldt,
+                          double* R, int64_t ldr, double* Ut, double* D) {
+  static bool init = false;
+  constexpr int kSm = 3 * kMaxW * kSLD * sizeof(double);
+  if (!init) {
+    cudaFuncSetAttribute(signlu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSm);
+    init = true;
+  }
+  signlu_kernel<<<1, 256, kSm, st>>>(Qtop, ldq, w, Racc, Y, ldy, T, ldt, R, ldr, Ut, D);
+  FFB_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------ TRQRCP helpers
+
+// R rows j0..j0+bb: entries at arrangement positions < j0 are exact zeros and the
+// block's own columns take the panel's upper-triangular R (alpha on the
+// diagonal, ffsrqr/sketch.py:137-139).
+__global__ void fix_rrows_kernel(double* R, int64_t ldr, int64_t j0, int bb,
+                                 const int64_t* __restrict__ arr, const double* __restrict__ Rb,
+                                 int64_t ldrb) {
+  const int64_t e = j0 + bb;
+  const int64_t total = (int64_t)bb * e;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t % bb);
+    const int64_t p = t / bb;
+    const int64_t col = arr[p];
+    double v = 0.0;
+    if (p >= j0 && p - j0 >= i) v = Rb[i + (p - j0) * ldrb];
+    R[(j0 + i) + col * ldr] = v;
+  }
+}
+
+cudaError_t launch_fix_rrows(cudaStream_t st, double* R, int64_t ldr, int64_t j0, int bb,
+                             const int64_t* arr, const double* Rb, int64_t ldrb) {
+  const int64_t total = (int64_t)bb * (j0 + bb);
+  fix_rrows_kernel<<<nblk(total, 256) > 1024 ? 1024 : nblk(total, 256), 256, 0, st>>>(
+      R, ldr, j0, bb, arr, Rb, ldrb);
+  FFB_LAUNCH_CHECK();
+}
+
+// Z = Bp * Rb^{-1} row by row (Rb upper w x w).  Exact zero pivots give zero
+// columns and raise kStZeroPivot (the reference falls back to lstsq,
+// ffsrqr/sketch.py:75-83).
+__global__ void trsm_rows_upper_kernel(const double* __restrict__ Bp, int64_t ldb, int rows,
+                                       const double* __restrict__ Rb, int64_t ldrb, int w,
+                                       double* Z, int64_t ldz, uint32_t* status) {
+  __shared__ double Rs[kMaxW * kSLD];
+  for (int t = threadIdx.x; t < w * w; t += blockDim.x) {
+    const int i = t % w, j = t / w;
+    Rs[i * kSLD + j] = Rb[i + j * ldrb];
+  }
+  __syncthreads();
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  double y[kMaxW];
+  bool zp = false;
+  for (int c = 0; c < w; ++c) {
+    double acc = Bp[row + c * (int64_t)ldb];
+    for (int k = 0; k < c; ++k) acc = fma(-y[k], Rs[k * kSLD + c], acc);
+    const double d = Rs[c * kSLD + c];
+    if (d != 0.0) {
+      y[c] = acc / d;
+    } else {
+      y[c] = 0.0;
+      zp = true;
+    }
+    Z[row + c * ldz] = y[c];
+  }
+  if (zp) atomicOr(status, kStZeroPivot);
+}
+
+cudaError_t launch_trsm_rows_upper(cudaStream_t st, const double* Bp, int64_t ldb, int rows,
+                                   const double* Rb, int64_t ldrb, int w, double* Z, int64_t ldz,
+                                   uint32_t* status) {
+  trsm_rows_upper_kernel<<<nblk(rows, 64), 64, 0, st>>>(Bp, ldb, rows, Rb, ldrb, w, Z, ldz, status);
+  FFB_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------ SRQR (K7-K11)
+
+// r[p] = ||B[:, arr[p]]||^2 / s for p >= l (sketch-based initialisation,
+// ffsrqr/srqr.py:98-101); zero for p < l.
+__global__ void rinit_kernel(const double* __restrict__ B, int64_t ldb, int s,
+                             const int64_t* __restrict__ arr, int64_t n, int64_t l, double* r,
+                             double* rinit) {
+  const int lane = threadIdx.x & 31;
+  const int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (p >= n) return;
+  double v = 0.0;
+  if (p >= l) {
+    const double* b = B + arr[p] * ldb;
+    double acc = 0.0;
+    for (int i = lane; i < s; i += 32) acc = fma(b[i], b[i], acc);
+    v = warp_sum(acc) / (double)s;
+  }
+  if (lane == 0) {
+    r[p] = v;
+    rinit[p] = v;
+  }
+}
+
+cudaError_t launch_rinit(cudaStream_t st, const double* B, int64_t ldb, int s, const int64_t* arr,
+                         int64_t n, int64_t l, double* r, double* rinit) {
+  rinit_kernel<<<nblk(n, 8), 256, 0, st>>>(B, ldb, s, arr, n, l, r, rinit);
+  FFB_LAUNCH_CHECK();
+}
+
+__global__ void anorm_kernel(const double* __restrict__ colsq, int64_t n, SrqrScalars* sc) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += colsq[i];
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) {
+    sc->anorm = sqrt(acc);
+    sc->status = isfinite(acc) ? 0u : kStNonFinite;
+    sc->need_swap = 0;
+    sc->alpha = 0.0;
+    sc->g2 = 0.0;
+  }
+}
+
+cudaError_t launch_anorm(cudaStream_t st, const double* colsq, int64_t n, SrqrScalars* sc) {
+  anorm_kernel<<<1, 1024, 0, st>>>(colsq, n, sc);
+  FFB_LAUNCH_CHECK();
+}
+
+// piv = l + argmax r[l:] (ties -> lowest position); swap into position l
+// (ffsrqr/srqr.py:121-123, swap_cols 109-115).
+__global__ void __launch_bounds__(1024) ext_pick_kernel(int64_t l, int64_t n, int64_t* arr,
+                                                        int64_t* pos, double* r, double* rinit,
+                                                        SrqrScalars* sc) {
+  __shared__ double red_v[32];
+  __shared__ int64_t red_i[32];
+  ArgMax best{-1.0, -1};
+  for (int64_t p = l + threadIdx.x; p < n; p += blockDim.x) best = argmax_better(best, ArgMax{r[p], p});
+  best = block_argmax(best, red_v, red_i);
+  if (threadIdx.x == 0) {
+    const int64_t q = best.i < 0 ? l : best.i;
+    sc->piv = q;
+    if (q != l) {
+      const int64_t a = arr[l], b = arr[q];
+      arr[l] = b;
+      arr[q] = a;
+      pos[b] = l;
+      pos[a] = q;
+      double t = r[l];
+      r[l] = r[q];
+      r[q] = t;
+      t = rinit[l];
+      rinit[l] = rinit[q];
+      rinit[q] = t;
+    }
+  }
+}
+
+cudaError_t launch_ext_pick(cudaStream_t st, int64_t l, int64_t n, int64_t* arr, int64_t* pos,
+                            double* r, double* rinit, SrqrScalars* sc) {
+  ext_pick_kernel<<<1, 1024, 0, st>>>(l, n, arr, pos, r, rinit, sc);
+  FFB_LAUNCH_CHECK();
+}
+
+// u = A[:, c] - Q1 R[:l, c]   (c = arr[l])
+__global__ void ext_u_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t l,
+                             const double* __restrict__ Q, int64_t ldq, const double* __restrict__ R,
+                             int64_t ldr, const int64_t* __restrict__ arr, double* u) {
+  extern __shared__ double rc[];
+  const int64_t c = arr[l];
+  for (int64_t j = threadIdx.x; j < l; j += blockDim.x) rc[j] = R[j + c * ldr];
+  __syncthreads();
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double a0 = 0.0, a1 = 0.0;
+  int64_t j = 0;
+  for (; j + 1 < l; j += 2) {
+    a0 = fma(Q[i + j * ldq], rc[j], a0);
+    a1 = fma(Q[i + (j + 1) * ldq], rc[j + 1], a1);
+  }
+  if (j < l) a0 = fma(Q[i + j * ldq], rc[j], a0);
+  u[i] = A[i + c * lda] - (a0 + a1);
+}
+
+// ct[j] = Q[:, j]^T u  (one CTA per j, deterministic)
+__global__ void ext_ct_kernel(const double* __restrict__ Q, int64_t ldq, int64_t m,
+                              const double* __restrict__ u, double* ct) {
+  __shared__ double red[32];
+  const int64_t j = blockIdx.x;
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) acc = fma(Q[i + j * ldq], u[i], acc);
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) ct[j] = acc;
+}
+
+// u -= Q1 ct  (second CGS pass, srqr.py:125); per-block partial ||u||^2
+__global__ void ext_u2_kernel(const double* __restrict__ Q, int64_t ldq, int64_t m, int64_t l,
+                              const double* __restrict__ ct, double* u, double* part) {
+  extern __shared__ double cs[];
+  __shared__ double red[32];
+  for (int64_t j = threadIdx.x; j < l; j += blockDim.x) cs[j] = ct[j];
+  __syncthreads();
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double sq = 0.0;
+  if (i < m) {
+    double a0 = 0.0, a1 = 0.0;
+    int64_t j = 0;
+    for (; j + 1 < l; j += 2) {
+      a0 = fma(Q[i + j * ldq], cs[j], a0);
+      a1 = fma(Q[i + (j + 1) * ldq], cs[j + 1], a1);
+    }
+    if (j < l) a0 = fma(Q[i + j * ldq], cs[j], a0);
+    const double v = u[i] - (a0 + a1);
+    u[i] = v;
+    sq = v * v;
+  }
+  sq = block_sum(sq, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = sq;
+}
+
+// alpha = ||u||; rank test alpha <= 1e-14 max(||A||_F, 1e-300) (srqr.py:127-133);
+// R row l := alpha e_l (srqr.py:128,135), r[l] = alpha^2.
+__global__ void ext_fin_kernel(const double* __restrict__ part, int nparts, int64_t l, int64_t n,
+                               const int64_t* __restrict__ arr, double* R, int64_t ldr, double* r,
+                               SrqrScalars* sc) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int t = threadIdx.x; t < nparts; t += blockDim.x) acc += part[t];
+  acc = block_sum(acc, red);
+  double alpha = sqrt(acc);
+  const double an = sc->anorm;
+  if (alpha <= 1e-14 * fmax(an, 1e-300)) alpha = 0.0;
+  for (int64_t c = threadIdx.x; c < n; c += blockDim.x) R[l + c * ldr] = 0.0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    sc->alpha = alpha;
+    if (!isfinite(acc)) sc->status |= kStNonFinite;
+    R[l + arr[l] * ldr] = alpha;
+    if (alpha > 0.0) r[l] = alpha * alpha;
+  }
+}
+
+__global__ void ext_q_kernel(const double* __restrict__ u, int64_t m, double* Ql,
+                             const SrqrScalars* sc) {
+  const double alpha = sc->alpha;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < m) Ql[i] = alpha > 0.0 ? u[i] / alpha : 0.0;
+}
+
+cudaError_t launch_ext_project(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t l,
+                               const double* Q, int64_t ldq, const double* R, int64_t ldr,
+                               const int64_t* arr, double* u, double* ct, double* part,
+                               SrqrScalars* sc, double* r, double* Rfull) {
+  (void)R;
+  const unsigned g = nblk(m, 256);
+  const size_t sh = sizeof(double) * (size_t)(l > 0 ? l : 1);
+  ext_u_kernel<<<g, 256, sh, st>>>(A, lda, m, l, Q, ldq, Rfull, ldr, arr, u);
+  if (l > 0) {
+    ext_ct_kernel<<<(unsigned)l, 256, 0, st>>>(Q, ldq, m, u, ct);
+  }
+  ext_u2_kernel<<<g, 256, sh, st>>>(Q, ldq, m, l, ct, u, part);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ext_finish(cudaStream_t st, const double* part, int nparts, int64_t l, int64_t n,
+                              const int64_t* arr, double* R, int64_t ldr, double* r,
+                              SrqrScalars* sc, const double* u, int64_t m, double* Ql) {
+  ext_fin_kernel<<<1, 1024, 0, st>>>(part, nparts, l, n, arr, R, ldr, r, sc);
+  ext_q_kernel<<<nblk(m, 256), 256, 0, st>>>(u, m, Ql, sc);
+  FFB_LAUNCH_CHECK();
+}
+
+// Extension row R[l, arr[p]] = q^T A[:, arr[p]] for p > l, downdate r and the
+// guard recompute against exact_trailing_sq(i, l+1) (srqr.py:136-149).  Only
+// materialised on the swap path (the row is dead when g2 <= g).
+__global__ void ext_row_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n,
+                               int64_t l, const double* __restrict__ q, double* R, int64_t ldr,
+                               const int64_t* __restrict__ arr, const double* __restrict__ colsq,
+                               double* r, const double* __restrict__ rinit,
+                               const SrqrScalars* sc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t p = l + 1 + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (p >= n || !(sc->alpha > 0.0)) return;
+  const int64_t col = arr[p];
+  const double* a = A + col * lda;
+  double acc = 0.0;
+  for (int64_t i = lane; i < m; i += 32) acc = fma(q[i], a[i], acc);
+  acc = warp_sum(acc);
+  // exact trailing norm below l+1 rows, needed only by the guard
+  double rs = 0.0;
+  for (int64_t i = lane; i < l; i += 32) {
+    const double v = R[i + col * ldr];
+    rs = fma(v, v, rs);
+  }
+  rs = warp_sum(rs);
+  if (lane == 0) {
+    R[l + col * ldr] = acc;
+    double rr = r[p] - acc * acc;
+    if (rr < 1e-8 * rinit[p] || rr < 0.0) rr = fmax(colsq[col] - (rs + acc * acc), 0.0);
+    r[p] = rr;
+  }
+}
+
+cudaError_t launch_ext_row(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n,
+                           int64_t l, const double* Q, int64_t ldq, double* R, int64_t ldr,
+                           const int64_t* arr, const double* colsq, double* r,
+                           const double* rinit, const SrqrScalars* sc) {
+  if (n <= l + 1) return cudaSuccess;
+  ext_row_kernel<<<nblk(n - l - 1, 8), 256, 0, st>>>(A, lda, m, n, l, Q + l * ldq, R, ldr, arr,
+                                                       colsq, r, rinit, sc);
+  FFB_LAUNCH_CHECK();
+}
+
+// g2 estimate (ffsrqr/srqr.py:49-64): Z = Rtilde^{-1} Omega^T by back
+// substitution, one warp per right-hand side; row norms; first argmax;
+// g2 = |alpha|/sqrt(d) * max.  Omega is d x (l+1) row-major (numpy C order).
+__global__ void __launch_bounds__(1024) g2_kernel(const double* __restrict__ R, int64_t ldr,
+                                                  const int64_t* __restrict__ arr, int64_t l,
+                                                  const double* __restrict__ omega, int d, double g,
+                                                  double* Z, SrqrScalars* sc) {
+  __shared__ double red_v[32];
+  __shared__ int64_t red_i[32];
+  __shared__ int sing;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t L1 = l + 1;
+  const double alpha = sc->alpha;
+  if (threadIdx.x == 0) sing = 0;
+  __syncthreads();
+  if (!(alpha > 0.0)) {
+    if (threadIdx.x == 0) {
+      sc->g2 = 0.0;
+      sc->i_off = 0;
+      sc->need_swap = 0;
+    }
+    return;
+  }
+  for (int64_t i = threadIdx.x; i < L1; i += blockDim.x) {
+    const double dv = (i == l) ? alpha : R[i + arr[i] * ldr];
+    if (dv == 0.0) sing = 1;
+  }
+  __syncthreads();
+  if (sing) {
+    if (threadIdx.x == 0) {
+      sc->status |= kStSingular;
+      sc->need_swap = 0;
+    }
+    return;
+  }
+  for (int rhs = wid; rhs < d; rhs += nw) {
+    double* z = Z + (int64_t)rhs * L1;
+    for (int64_t i = l; i >= 0; --i) {
+      double acc = 0.0;
+      for (int64_t j = i + 1 + lane; j <= l; j += 32) {
+        const double rij = (j == l && i == l) ? alpha : R[i + arr[j] * ldr];
+        acc = fma(rij, z[j], acc);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        const double dii = (i == l) ? alpha : R[i + arr[i] * ldr];
+        z[i] = (omega[(int64_t)rhs * L1 + i] - acc) / dii;
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  ArgMax best{-1.0, -1};
+  for (int64_t i = threadIdx.x; i < L1; i += blockDim.x) {
+    double acc = 0.0;
+    for (int rhs = 0; rhs < d; ++rhs) {
+      const double v = Z[(int64_t)rhs * L1 + i];
+      acc = fma(v, v, acc);
+    }
+    best = argmax_better(best, ArgMax{sqrt(acc), i});
+  }
+  best = block_argmax(best, red_v, red_i);
+  if (threadIdx.x == 0) {
+    const double g2 = fabs(alpha) / sqrt((double)d) * best.v;
+    sc->g2 = g2;
+    sc->i_off = best.i;
+    sc->need_swap = g2 > g ? 1u : 0u;
+  }
+}
+
+cudaError_t launch_g2(cudaStream_t st, const double* R, int64_t ldr, const int64_t* arr, int64_t l,
+                      const double* omega, int d, double g, double* Z, SrqrScalars* sc) {
+  g2_kernel<<<1, 32 * (d < 32 ? (d < 1 ? 1 : d) : 32), 0, st>>>(R, ldr, arr, l, omega, d, g, Z, sc);
+  FFB_LAUNCH_CHECK();
+}
+
+// _pack (srqr.py:213-235): trail_sq = max(colsq - ||R[:l, c]||^2, 0) over
+// positions >= l; r22 = sqrt(max); g1 = r22/alpha; tau bounds.
+__global__ void pack_part_kernel(const double* __restrict__ R, int64_t ldr,
+                                 const int64_t* __restrict__ arr, const double* __restrict__ colsq,
+                                 int64_t l, int64_t n, double* part) {
+  __shared__ double wmax[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double mx = 0.0;
+  for (int64_t p = l + (int64_t)blockIdx.x * nw + wid; p < n; p += (int64_t)gridDim.x * nw) {
+    const int64_t col = arr[p];
+    const double* rc = R + col * ldr;
+    double acc = 0.0;
+    for (int64_t i = lane; i < l; i += 32) acc = fma(rc[i], rc[i], acc);
+    acc = warp_sum(acc);
+    mx = fmax(mx, fmax(colsq[col] - acc, 0.0));
+  }
+  if (lane == 0) wmax[wid] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t = fmax(t, wmax[w]);
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void pack_fin_kernel(const double* __restrict__ part, int nparts, int64_t l, int64_t n,
+                                SrqrScalars* sc) {
+  if (threadIdx.x != 0) return;
+  double t = 0.0;
+  for (int q = 0; q < nparts; ++q) t = fmax(t, part[q]);
+  const double r22 = (n > l) ? sqrt(t) : 0.0;
+  const double alpha = sc->alpha;
+  const double g1 = alpha > 0.0 ? r22 / alpha : 0.0;
+  const double g2 = alpha > 0.0 ? sc->g2 : 0.0;
+  sc->r22 = r22;
+  sc->g1 = g1;
+  sc->tau = g1 * g2 * sqrt((double)(l + 1) * (double)(n - l));
+  sc->tau_hat = g1 * g2 * sqrt((double)l * (double)(n - l));
+}
+
+cudaError_t launch_pack(cudaStream_t st, const double* R, int64_t ldr, const int64_t* arr,
+                        const double* colsq, int64_t l, int64_t n, double* part, int64_t swaps,
+                        SrqrScalars* sc) {
+  (void)swaps;
+  const int nparts = 148;
+  pack_part_kernel<<<nparts, 256, 0, st>>>(R, ldr, arr, colsq, l, n, part);
+  pack_fin_kernel<<<1, 32, 0, st>>>(part, nparts, l, n, sc);
+  FFB_LAUNCH_CHECK();
+}
+
+// rotate_out (srqr.py:152-164): cyclic left shift of positions i_off..l, then
+// the Givens chase of qr.py:182-209 (rotations computed sequentially from the
+// diagonal columns, identical arithmetic to row-wise application), applied to
+// every column of R and to the columns of Q (qr.py:212-219).
+__global__ void rot_compute_kernel(double* R, int64_t ldr, int64_t l, int64_t* arr, int64_t* pos,
+                                   double* r, double* rinit, const SrqrScalars* sc, double* rot,
+                                   double* scratch) {
+  if (threadIdx.x != 0) return;
+  const int64_t i_off = sc->i_off;
+  if (i_off < l) {
+    const int64_t a0 = arr[i_off];
+    const double r0 = r[i_off], q0 = rinit[i_off];
+    for (int64_t p = i_off; p < l; ++p) {
+      arr[p] = arr[p + 1];
+      r[p] = r[p + 1];
+      rinit[p] = rinit[p + 1];
+      pos[arr[p]] = p;
+    }
+    arr[l] = a0;
+    r[l] = r0;
+    rinit[l] = q0;
+    pos[a0] = l;
+  }
+  // rotations: for i = i_off..l-1 on rows (i, i+1), from column arr[i]
+  for (int64_t i = i_off; i < l; ++i) {
+    const int64_t col = arr[i];
+    // column entries rows i_off..i+1 after rotations i_off..i-1
+    double* x = scratch;
+    for (int64_t k = i_off; k <= i + 1; ++k) x[k - i_off] = R[k + col * ldr];
+    for (int64_t k = i_off; k < i; ++k) {
+      const double c = rot[3 * k], s = rot[3 * k + 1];
+      if (rot[3 * k + 2] != 0.0) continue;
+      const double up = c * x[k - i_off] + s * x[k + 1 - i_off];
+      const double lo = -s * x[k - i_off] + c * x[k + 1 - i_off];
+      x[k - i_off] = up;
+      x[k + 1 - i_off] = lo;
+    }
+    const double a = x[i - i_off], b = x[i + 1 - i_off];
+    if (b == 0.0) {
+      rot[3 * i] = 1.0;
+      rot[3 * i + 1] = 0.0;
+      rot[3 * i + 2] = 1.0;  // skipped
+    } else {
+      const double h = hypot(a, b);
+      rot[3 * i] = a / h;
+      rot[3 * i + 1] = b / h;
+      rot[3 * i + 2] = 0.0;
+    }
+  }
+}
+
+__global__ void rot_apply_R_kernel(double* R, int64_t ldr, int64_t n, int64_t l,
+                                   const int64_t* __restrict__ arr, const double* __restrict__ rot,
+                                   const SrqrScalars* sc) {
+  const int64_t i_off = sc->i_off;
+  for (int64_t col = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; col < n;
+       col += (int64_t)gridDim.x * blockDim.x) {
+    double* rc = R + col * ldr;
+    for (int64_t i = i_off; i < l; ++i) {
+      if (rot[3 * i + 2] != 0.0) continue;
+      const double c = rot[3 * i], s = rot[3 * i + 1];
+      const double a = rc[i], b = rc[i + 1];
+      rc[i] = c * a + s * b;
+      rc[i + 1] = -s * a + c * b;
+    }
+  }
+}
+
+__global__ void rot_zero_kernel(double* R, int64_t ldr, int64_t l, const int64_t* __restrict__ arr,
+                                const double* __restrict__ rot, const SrqrScalars* sc) {
+  const int64_t i_off = sc->i_off;
+  for (int64_t i = i_off + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (rot[3 * i + 2] == 0.0) R[(i + 1) + arr[i] * ldr] = 0.0;
+}
+
+__global__ void rot_apply_Q_kernel(double* Q, int64_t ldq, int64_t m, int64_t l,
+                                   const double* __restrict__ rot, const SrqrScalars* sc) {
+  const int64_t i_off = sc->i_off;
+  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < m;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t i = i_off; i < l; ++i) {
+      if (rot[3 * i + 2] != 0.0) continue;
+      const double c = rot[3 * i], s = rot[3 * i + 1];
+      const double q0 = Q[row + i * ldq], q1 = Q[row + (i + 1) * ldq];
+      Q[row + i * ldq] = c * q0 + s * q1;
+      Q[row + (i + 1) * ldq] = -s * q0 + c * q1;
+    }
+  }
+}
+
+cudaError_t launch_rotate_out(cudaStream_t st, double* R, int64_t ldr, double* Q, int64_t ldq,
+                              int64_t m, int64_t n, int64_t l, int64_t* arr, int64_t* pos,
+                              double* r, double* rinit, const SrqrScalars* sc, double* rot) {
+  double* scratch = rot + 3 * (l + 1);
+  rot_compute_kernel<<<1, 32, 0, st>>>(R, ldr, l, arr, pos, r, rinit, sc, rot, scratch);
+  rot_apply_R_kernel<<<nblk(n, 256) > 1184 ? 1184 : nblk(n, 256), 256, 0, st>>>(R, ldr, n, l, arr,
+                                                                                  rot, sc);
+  rot_zero_kernel<<<nblk(l + 1, 256), 256, 0, st>>>(R, ldr, l, arr, rot, sc);
+  rot_apply_Q_kernel<<<nblk(m, 256) > 1184 ? 1184 : nblk(m, 256), 256, 0, st>>>(Q, ldq, m, l, rot,
+                                                                                  sc);
+  FFB_LAUNCH_CHECK();
+}
+
+// revert_extension (srqr.py:166-171)
+__global__ void revert_kernel(const double* __restrict__ R, int64_t ldr,
+                              const int64_t* __restrict__ arr, int64_t l, int64_t n, double* r) {
+  for (int64_t p = l + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const double v = R[l + arr[p] * ldr];
+    if (p == l) r[p] = v * v;
+    else r[p] += v * v;
+  }
+}
+
+cudaError_t launch_revert(cudaStream_t st, const double* R, int64_t ldr, const int64_t* arr,
+                          int64_t l, int64_t n, double* r) {
+  revert_kernel<<<nblk(n - l, 256) > 1184 ? 1184 : nblk(n - l, 256), 256, 0, st>>>(R, ldr, arr, l,
+                                                                                    n, r);
+  FFB_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------- outputs
+
+// out[i, c] = R[i, arr[c]] for i < rows, zero below the diagonal for i < tri_rows
+__global__ void r_arranged_kernel(const double* __restrict__ R, int64_t ldr,
+                                  const int64_t* __restrict__ arr, int64_t rows, int64_t n,
+                                  double* out, int64_t ldo, int64_t tri_rows) {
+  const int64_t total = rows * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t % rows, c = t / rows;
+    out[i + c * ldo] = (i > c && i < tri_rows) ? 0.0 : R[i + arr[c] * ldr];
+  }
+}
+
+cudaError_t launch_r_arranged(cudaStream_t st, const double* R, int64_t ldr, const int64_t* arr,
+                              int64_t rows, int64_t n, double* out, int64_t ldo,
+                              int64_t tri_rows) {
+  const int64_t total = rows * n;
+  if (total <= 0) return cudaSuccess;
+  unsigned g = nblk(total, 256);
+  if (g > 8192) g = 8192;
+  r_arranged_kernel<<<g, 256, 0, st>>>(R, ldr, arr, rows, n, out, ldo, tri_rows);
+  FFB_LAUNCH_CHECK();
+}
+
+// X = (R arranged, upper trapezoidal)^T : X[c, i] = R[i, arr[c]] for i <= c
+__global__ void build_rt_kernel(const double* __restrict__ R, int64_t ldr,
+                                const int64_t* __restrict__ arr, int64_t l, int64_t n, double* X,
+                                int64_t ldx) {
+  const int64_t total = l * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t % n, i = t / n;
+    X[c + i * ldx] = (i <= c) ? R[i + arr[c] * ldr] : 0.0;
+  }
+}
+
+cudaError_t launch_build_rt(cudaStream_t st, const double* R, int64_t ldr, const int64_t* arr,
+                            int64_t l, int64_t n, double* X, int64_t ldx) {
+  const int64_t total = l * n;
+  unsigned g = nblk(total, 256);
+  if (g > 8192) g = 8192;
+  build_rt_kernel<<<g, 256, 0, st>>>(R, ldr, arr, l, n, X, ldx);
+  FFB_LAUNCH_CHECK();
+}
+
+__global__ void diag_kernel(const double* R, int64_t ldr, int64_t nd, double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = R[i + i * ldr];
+}
+
+cudaError_t launch_diag(cudaStream_t st, const double* R, int64_t ldr, int64_t nd, double* out) {
+  diag_kernel<<<nblk(nd, 256), 256, 0, st>>>(R, ldr, nd, out);
+  FFB_LAUNCH_CHECK();
+}
+
+}  // namespace ffb

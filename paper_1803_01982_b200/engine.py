@@ -1,0 +1,238 @@
+"""Drop-in host entry points over the sm_100a engine (C ABI, include/ffb200.h).
+
+Mirrors the reference's Python API for the hot path:
+
+* ``flip_flop_srqr(A, k, l=None, b=32, p=5, epsilon=0.5, g=2.0, d=None, seed=0)``
+  — ffsrqr/svd.py:43-98 (same clamp of b, p for small m, same defaults, same
+  result type ``ApproxSvd`` with ``meta["srqr"]``/``["params"]``/``["method"]``)
+* ``srqr(A, params)`` — ffsrqr/srqr.py:174-210 (``SrqrResult``)
+* ``trqrcp(A, params)`` — ffsrqr/sketch.py:150-161 (``PartialFactorization``)
+
+Inputs may be numpy arrays (results come back as numpy, like the reference)
+or CUDA float64 torch tensors (results stay on the device).  Errors are the
+reference's exception classes.  Differences, all documented in DESIGN.md:
+``meta["srqr"].fact.R`` is the true SRQR R (the reference overwrites it
+through a NumPy view, svd.py:67-68) and ``meta["diag_L"]`` exposes the
+partial-LQ diagonal explicitly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+
+import numpy as np
+
+from . import _capi, rng
+from .errors import (CertificationError, DimensionError, EngineUnavailable, NumericalError,
+                     SingularTrailingBlockError)
+from .results import (ApproxSvd, PartialFactorization, SketchParams, SrqrCertificate, SrqrResult,
+                      WYFactor)
+
+_tls = threading.local()
+
+
+def _torch():
+    try:
+        import torch
+    except ImportError as e:  # pragma: no cover
+        raise EngineUnavailable("torch is required for device memory") from e
+    if not torch.cuda.is_available():
+        raise EngineUnavailable("no CUDA device: the B200 engine has no CPU fallback")
+    return torch
+
+
+def _device(device):
+    torch = _torch()
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    d = torch.device(device)
+    if d.type != "cuda":
+        raise EngineUnavailable("the B200 engine runs on CUDA devices only")
+    return torch.device("cuda", d.index if d.index is not None else torch.cuda.current_device())
+
+
+def _colmajor(torch, rows, cols, device, dtype=None):
+    dtype = dtype or torch.float64
+    return torch.empty((cols, rows), dtype=dtype, device=device).t()
+
+
+def _to_device_colmajor(A, device):
+    """(col-major float64 CUDA tensor, is_numpy_input)."""
+    torch = _torch()
+    if isinstance(A, torch.Tensor):
+        if A.dim() != 2:
+            raise DimensionError("expected a 2-D matrix")
+        A = A.to(device=device, dtype=torch.float64)
+        m, n = A.shape
+        if not (A.stride(0) == 1 and A.stride(1) >= max(m, 1)):
+            A = A.t().contiguous().t()
+        return A, False
+    a = np.asarray(A, dtype=float)
+    if a.ndim != 2:
+        raise DimensionError("expected a 2-D matrix")
+    if a.flags.f_contiguous:
+        t = torch.from_numpy(a.T).to(device)         # (n, m) row-major == A column-major
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(a)).to(device).t().contiguous()
+    return t.t(), True
+
+
+def _workspace(torch, device, nbytes):
+    key = (device.index,)
+    cache = getattr(_tls, "ws", None)
+    if cache is None:
+        cache = _tls.ws = {}
+    buf = cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(int(nbytes * 1.1) + 4096, dtype=torch.uint8, device=device)
+        cache[key] = buf
+    return buf
+
+
+@_capi.GAUSS_CB
+def _gauss_cb(user, seed, stream, rows, cols, out):
+    try:
+        arr = np.ctypeslib.as_array(out, shape=(int(rows) * int(cols),))
+        arr[:] = rng.gaussian(int(rows), int(cols), int(seed), int(stream)).ravel()
+        return 0
+    except Exception:  # pragma: no cover - surfaced as FFB_ERR_ARGUMENT
+        return 1
+
+
+def run(A, params: SketchParams, mode, device=None, want=("R", "Q", "rtilde", "perm")):
+    """Run one factorization mode through the C ABI; returns a dict of outputs."""
+    torch = _torch()
+    dev = _device(device if device is not None else (A.device if isinstance(A, torch.Tensor) and A.is_cuda else None))
+    with torch.cuda.device(dev):
+        Ad, is_np = _to_device_colmajor(A, dev)
+        m, n = Ad.shape
+        prm = params.resolve(m, n)
+        if mode != _capi.FFB_MODE_TRQRCP and prm.l + 1 > min(m, n):
+            raise DimensionError(f"srqr needs l+1 <= min(m,n); got l={prm.l}, min={min(m, n)}")
+        if prm.b > 64:
+            raise DimensionError("the B200 engine supports block sizes b <= 64")
+        lib = _capi.load()
+        ctx = _capi.context(dev.index)
+        cp = _capi.Params(prm.k, prm.l, prm.b, prm.p, prm.d, prm.epsilon, prm.g,
+                          int(prm.seed) & 0xFFFFFFFFFFFFFFFF)
+        nbytes = C.c_size_t()
+        rc = lib.ffb_workspace_query(m, n, C.byref(cp), mode, C.byref(nbytes))
+        if rc != _capi.FFB_OK:
+            raise DimensionError("invalid dimensions for the engine")
+        ws = _workspace(torch, dev, nbytes.value)
+        s = prm.b + prm.p
+        omega = torch.from_numpy(rng.gaussian(s, m, prm.seed, rng.STREAM_SKETCH)).to(dev)
+        l, k = prm.l, prm.k
+        out = {}
+        res = _capi.Result()
+        if mode == _capi.FFB_MODE_FLIPFLOP:
+            out["u"] = _colmajor(torch, m, k, dev)
+            out["s"] = torch.empty(k, dtype=torch.float64, device=dev)
+            out["v"] = _colmajor(torch, n, k, dev)
+            out["diag_L"] = torch.empty(l, dtype=torch.float64, device=dev)
+            out["sv_all"] = torch.empty(l, dtype=torch.float64, device=dev)
+            res.u, res.ldu = out["u"].data_ptr(), m
+            res.s = out["s"].data_ptr()
+            res.v, res.ldv = out["v"].data_ptr(), n
+            res.diag_L = out["diag_L"].data_ptr()
+            res.sv_all = out["sv_all"].data_ptr()
+        out["perm"] = torch.empty(n, dtype=torch.int64, device=dev)
+        res.perm = out["perm"].data_ptr()
+        out["R"] = _colmajor(torch, l, n, dev)
+        res.R, res.ldr = out["R"].data_ptr(), l
+        out["pivot_gap"] = torch.empty(l, dtype=torch.float64, device=dev)
+        res.pivot_gap = out["pivot_gap"].data_ptr()
+        if mode == _capi.FFB_MODE_TRQRCP:
+            out["Y"] = _colmajor(torch, m, l, dev)
+            out["T"] = _colmajor(torch, l, l, dev)
+            out["B"] = _colmajor(torch, s, n, dev)
+            res.Y, res.ldy = out["Y"].data_ptr(), m
+            res.T, res.ldt = out["T"].data_ptr(), l
+            res.B, res.ldb = out["B"].data_ptr(), s
+        else:
+            out["Q"] = _colmajor(torch, m, l + 1, dev)
+            out["rtilde"] = _colmajor(torch, l + 1, l + 1, dev)
+            res.Q, res.ldq = out["Q"].data_ptr(), m
+            res.rtilde = out["rtilde"].data_ptr()
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        rc = lib.ffb_run(ctx, C.c_void_p(stream), mode, C.c_void_p(Ad.data_ptr()), m, n,
+                         Ad.stride(1), C.byref(cp), C.c_void_p(omega.data_ptr()), _gauss_cb, None,
+                         C.c_void_p(ws.data_ptr()), ws.numel(), C.byref(res))
+        out.update(alpha=res.alpha, g1=res.g1, g2=res.g2, tau=res.tau_bound,
+                   tau_hat=res.tau_hat_bound, r22=res.r22, swaps=int(res.swaps),
+                   flops=int(res.flops), kernels=int(res.kernels),
+                   status_bits=int(res.status_bits),
+                   i_offs=[int(res.i_off_trace[i]) for i in range(min(int(res.swaps), 64))],
+                   is_numpy=is_np, params=prm, m=m, n=n)
+        if rc == _capi.FFB_OK:
+            return out
+        msg = _capi.last_error(ctx)
+        if rc == _capi.FFB_ERR_DIMENSION:
+            raise DimensionError(msg)
+        if rc == _capi.FFB_ERR_SINGULAR_TRAILING:
+            raise SingularTrailingBlockError(msg)
+        if rc == _capi.FFB_ERR_CERTIFICATION:
+            raise CertificationError(msg, result=_srqr_result(out))
+        if rc == _capi.FFB_ERR_NUMERICAL:
+            raise NumericalError(msg)
+        raise RuntimeError(f"ffb_run failed ({rc}): {msg}")
+
+
+def _conv(x, as_np):
+    if not as_np:
+        return x
+    return x.detach().cpu().numpy()
+
+
+def _srqr_result(out):
+    np_ = out["is_numpy"]
+    prm = out["params"]
+    l = prm.l
+    Q = _conv(out["Q"], np_)
+    fact = PartialFactorization(R=_conv(out["R"], np_), perm=_conv(out["perm"], np_), k=l,
+                                q_dense=Q[:, :l])
+    cert = SrqrCertificate(alpha=abs(out["alpha"]), g1=out["g1"], g2=out["g2"],
+                           swaps=out["swaps"], tau_bound=out["tau"],
+                           tau_hat_bound=out["tau_hat"])
+    return SrqrResult(fact=fact, cert=cert, r22_norm_estimate=out["r22"],
+                      rtilde=_conv(out["rtilde"], np_), q_ext=Q)
+
+
+def flip_flop_srqr(A, k, l=None, b=32, p=5, epsilon=0.5, g=2.0, d=None, seed=0, device=None):
+    """Rank-k approximate SVD via spectrum-revealing QR plus a flipped QR
+    (ffsrqr/svd.py:43-98), on the B200 engine."""
+    shape = tuple(A.shape)
+    if len(shape) != 2:
+        raise DimensionError("expected a 2-D matrix")
+    m, n = shape
+    if b + p > m:                       # svd.py:53-55
+        b = max(1, m - p)
+        p = m - b
+    params = SketchParams(k=k, l=l, b=b, p=p, epsilon=epsilon, g=g, d=d, seed=seed)
+    out = run(A, params, _capi.FFB_MODE_FLIPFLOP, device=device)
+    np_ = out["is_numpy"]
+    res = _srqr_result(out)
+    meta = {"srqr": res, "params": out["params"], "method": "flip_flop_srqr",
+            "diag_L": _conv(out["diag_L"], np_), "sv_all": _conv(out["sv_all"], np_),
+            "pivot_gap": _conv(out["pivot_gap"], np_), "engine": "ffb200-sm100a",
+            "kernels": out["kernels"], "i_offs": out["i_offs"]}
+    return ApproxSvd(u=_conv(out["u"], np_), s=_conv(out["s"], np_), v=_conv(out["v"], np_),
+                     flop_count=out["flops"], meta=meta)
+
+
+def srqr(A, params: SketchParams, device=None):
+    """Spectrum-revealing QR to params.l steps (ffsrqr/srqr.py:174-210)."""
+    out = run(A, params, _capi.FFB_MODE_SRQR, device=device)
+    return _srqr_result(out)
+
+
+def trqrcp(A, params: SketchParams, device=None):
+    """Truncated randomized QRCP (ffsrqr/sketch.py:150-161)."""
+    out = run(A, params, _capi.FFB_MODE_TRQRCP, device=device)
+    np_ = out["is_numpy"]
+    prm = out["params"]
+    fact = PartialFactorization(R=_conv(out["R"], np_), perm=_conv(out["perm"], np_), k=prm.l,
+                                wy=WYFactor(_conv(out["Y"], np_), _conv(out["T"], np_)))
+    fact.sketch = _conv(out["B"], np_)
+    fact.pivot_gap = _conv(out["pivot_gap"], np_)
+    return fact
