@@ -53,6 +53,7 @@ class Result(C.Structure):
         ("flops", C.c_int64),
         ("kernels", C.c_int64),
         ("status_bits", C.c_uint32),
+        ("svd_sweeps", C.c_int32),
         ("i_off_trace", C.c_int64 * 64),
     ]
 

@@ -13,7 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libffb200.so")
-SOURCES = ["ffb_engine.cu", "ffb_gemm.cu", "ffb_kernels.cu"]
+SOURCES = ["ffb_engine.cu", "ffb_gemm.cu", "ffb_kernels.cu", "ffb_jacobi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-diag-suppress", "177"]
@@ -57,7 +57,7 @@ def build(force=False, verbose=False):
             sys.stderr.write(out.decode())
             raise RuntimeError(f"nvcc failed on {src}")
     tmp = LIB + ".tmp"
-    cmd = [cc, *ARCH, "-shared", "-o", tmp, *objs, "-L/usr/local/cuda/lib64", "-lcusolver",
+    cmd = [cc, *ARCH, "-shared", "-o", tmp, *objs, "-L/usr/local/cuda/lib64",
            "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

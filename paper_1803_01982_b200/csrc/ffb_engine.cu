@@ -9,7 +9,6 @@
 // only if a swap is needed (g2 > g, rare: 0 swaps on every BASELINE config)
 // does the host drive the reference's swap loop and redo the tail.
 #include <cuda_runtime.h>
-#include <cusolverDn.h>
 
 #include <algorithm>
 #include <cmath>
@@ -21,6 +20,7 @@
 
 #include "../../include/ffb200.h"
 #include "ffb_gemm.h"
+#include "ffb_jacobi.cuh"
 #include "ffb_kernels.cuh"
 
 using namespace ffb;
@@ -29,12 +29,10 @@ struct ffb_ctx {
   int device = 0;
   int sms = 148;
   int max_coop_blocks_smem = 0;
-  cusolverDnHandle_t solver = nullptr;
   std::string err;
   double* pinned = nullptr;        // host staging for g2 Gaussians
   size_t pinned_cap = 0;
   SrqrScalars* sc_host = nullptr;  // pinned
-  int svd_kind = 0;                // 0 = gesvd, 1 = gesvdj
 };
 
 namespace {
@@ -68,7 +66,7 @@ struct Work {
   // TRQRCP
   double *B, *colsq, *Y, *T, *WT, *R, *Q;
   int64_t *arr, *pos;
-  double *P, *Xa, *Xb, *G1, *WTg, *S1, *S2, *Racc, *Rinv, *Ut, *Dv, *Rb, *Bp, *Z;
+  double *P, *Xa, *Xb, *G1, *WTg, *S1, *S2, *Racc, *Gm, *Rinv, *Ut, *Dv, *Rb, *Bp, *Z;
   double *hhW, *hhW2;
   // pivots
   PivSlot* slots;
@@ -83,10 +81,10 @@ struct Work {
   SrqrScalars* sc;
   uint32_t* status;
   // flip-flop
-  double *X, *Yl, *Tl, *Rl, *TYt, *Qh, *Yh, *tmp, *Yt, *Tt, *Rt, *Us, *VsT, *sig, *W1, *W2;
-  double* svdwork;
-  int* svdinfo;
-  int lwork;
+  double *X, *Yl, *Tl, *Rl, *TYt, *Qh, *Yh, *tmp, *Yt, *Tt, *Rt, *Us, *VsT, *Vo, *sig, *W1, *W2;
+  double* joff;
+  uint32_t* jbar;
+  int *jsweeps, *jorder;
   double* gpart;
   size_t gpart_cap;
 };
@@ -105,7 +103,9 @@ void pivot_geometry(const ffb_ctx* ctx, int64_t n, int64_t s, Work& w) {
   w.piv_smem_bytes = pivots_smem_bytes((int)s, cpc, w.piv_smem);
 }
 
-size_t carve(const ffb_ctx* ctx, const Dims& D, void* base, size_t cap, Work& w, int lwork) {
+constexpr int kMaxSweeps = 40;
+
+size_t carve(const ffb_ctx* ctx, const Dims& D, void* base, size_t cap, Work& w) {
   Bump b{static_cast<char*>(base), 0, cap};
   const int64_t m = D.m, n = D.n, l = D.l, s = D.s, bmax = std::min<int64_t>(D.b, l);
   const int64_t L1 = l + 1;
@@ -127,6 +127,7 @@ size_t carve(const ffb_ctx* ctx, const Dims& D, void* base, size_t cap, Work& w,
   w.S1 = b.take<double>(max_i(l, 1) * max_i(bmax, kPanelW));
   w.S2 = b.take<double>(max_i(l, 1) * max_i(bmax, kPanelW));
   w.Racc = b.take<double>(kPanelW * kPanelW);
+  w.Gm = b.take<double>(kPanelW * kPanelW);
   w.Rinv = b.take<double>(kPanelW * kPanelW);
   w.Ut = b.take<double>(kPanelW * kPanelW);
   w.Dv = b.take<double>(kPanelW);
@@ -166,12 +167,14 @@ size_t carve(const ffb_ctx* ctx, const Dims& D, void* base, size_t cap, Work& w,
     w.Rt = b.take<double>(l * l);
     w.Us = b.take<double>(l * l);
     w.VsT = b.take<double>(l * l);
+    w.Vo = b.take<double>(l * l);
     w.sig = b.take<double>(l);
     w.W1 = b.take<double>(l * D.k);
     w.W2 = b.take<double>(l * D.k);
-    w.svdwork = b.take<double>(std::max(lwork, 1));
-    w.svdinfo = b.take<int>(4);
-    w.lwork = lwork;
+    w.joff = b.take<double>(kMaxSweeps);
+    w.jbar = b.take<uint32_t>(4);
+    w.jsweeps = b.take<int>(4);
+    w.jorder = b.take<int>(l);
   }
   // split-K scratch: the rest, at least 4 Mi doubles
   w.gpart_cap = std::max<size_t>(4u << 20, (size_t)64 * kPanelW * kPanelW);
@@ -199,14 +202,9 @@ struct Eng {
     cudaError_t e = gemm_f64(gc, st, M, N, K, alpha, A, lda, akc, B, ldb, bkc, beta, C, ldc);
     if (e != cudaSuccess) cerr = e;
   }
-  // Gram partials of X (rows x w, ld ldx): returns splits, partials in gc.partial
-  int gram(const double* X, int64_t rows, int w_, int64_t ldx) {
-    GemmPartialOut po{64, nullptr, 0};
-    if (cerr != cudaSuccess) return 1;
-    cudaError_t e = gemm_f64(gc, st, w_, w_, rows, 1.0, X, ldx, true, X, ldx, true, 0.0, nullptr,
-                             w_, &po);
-    if (e != cudaSuccess) cerr = e;
-    return po.splits;
+  // Gram G = X^T X (w x w, reduced in fixed order) of X (rows x w, ld ldx)
+  void gram(const double* X, int64_t rows, int w_, int64_t ldx) {
+    gemm(w_, w_, rows, 1.0, X, ldx, true, X, ldx, true, 0.0, w.Gm, w_);
   }
   void memset2d(double* p, int64_t ld, int64_t rows, int64_t cols) {
     if (rows <= 0 || cols <= 0) return;
@@ -217,16 +215,16 @@ struct Eng {
   void recon(const double* Xp, int64_t Mp, int wb, int64_t ldx, double* Yp, int64_t ldy,
              double* Tp, int64_t ldt, double* Rp, int64_t ldr) {
     // pass 1 (shifted)
-    int sp = gram(Xp, Mp, wb, ldx);
-    ok(launch_cholinv(st, gc.partial, sp, wb, Mp, true, true, w.Racc, w.Rinv, w.status));
+    gram(Xp, Mp, wb, ldx);
+    ok(launch_cholinv(st, w.Gm, wb, Mp, true, true, w.Racc, w.Rinv, w.status));
     gemm(Mp, wb, wb, 1.0, Xp, ldx, false, w.Rinv, wb, true, 0.0, w.Xa, Mp);
     // pass 2
-    sp = gram(w.Xa, Mp, wb, Mp);
-    ok(launch_cholinv(st, gc.partial, sp, wb, Mp, false, false, w.Racc, w.Rinv, w.status));
+    gram(w.Xa, Mp, wb, Mp);
+    ok(launch_cholinv(st, w.Gm, wb, Mp, false, false, w.Racc, w.Rinv, w.status));
     gemm(Mp, wb, wb, 1.0, w.Xa, Mp, false, w.Rinv, wb, true, 0.0, w.Xb, Mp);
     // pass 3
-    sp = gram(w.Xb, Mp, wb, Mp);
-    ok(launch_cholinv(st, gc.partial, sp, wb, Mp, false, false, w.Racc, w.Rinv, w.status));
+    gram(w.Xb, Mp, wb, Mp);
+    ok(launch_cholinv(st, w.Gm, wb, Mp, false, false, w.Racc, w.Rinv, w.status));
     gemm(Mp, wb, wb, 1.0, w.Xb, Mp, false, w.Rinv, wb, true, 0.0, w.Xa, Mp);
     // signs + reflectors
     ok(launch_signlu(st, w.Xa, Mp, wb, w.Racc, Yp, ldy, Tp, ldt, Rp, ldr, w.Ut, w.Dv));
@@ -274,13 +272,6 @@ int cuda_fail(ffb_ctx* ctx, cudaError_t e, const char* where) {
   return fail(ctx, FFB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
-int svd_lwork(ffb_ctx* ctx, int64_t l) {
-  int lw = 0;
-  if (!ctx || !ctx->solver) return 0;
-  cusolverDnDgesvd_bufferSize(ctx->solver, (int)l, (int)l, &lw);
-  return lw;
-}
-
 bool validate(const Dims& D) {
   if (D.m < 1 || D.n < 1) return false;
   if (!(1 <= D.k && D.k <= D.l && D.l <= std::min(D.m, D.n))) return false;
@@ -307,17 +298,13 @@ int ffb_ctx_create(int device, ffb_ctx** out) {
     return FFB_ERR_CUDA;
   }
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
-  if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) c->solver = nullptr;
   cudaMallocHost(&c->sc_host, sizeof(SrqrScalars));
-  const char* sv = getenv("FFB_SVD");
-  c->svd_kind = (sv && std::string(sv) == "gesvdj") ? 1 : 0;
   *out = c;
   return FFB_OK;
 }
 
 int ffb_ctx_destroy(ffb_ctx* c) {
   if (!c) return FFB_OK;
-  if (c->solver) cusolverDnDestroy(c->solver);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->sc_host) cudaFreeHost(c->sc_host);
   delete c;
@@ -331,20 +318,7 @@ int ffb_workspace_query(int64_t m, int64_t n, const ffb_params* prm, int mode, s
   Dims D{m, n, prm->k, prm->l, prm->b, prm->p, prm->b + prm->p, prm->d, prm->g, prm->seed, mode};
   if (!validate(D)) return FFB_ERR_DIMENSION;
   Work w;
-  // SVD workspace: exact cuSOLVER query when a device is present, else a bound.
-  static cusolverDnHandle_t qh = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    if (cusolverDnCreate(&qh) != CUSOLVER_STATUS_SUCCESS) qh = nullptr;
-  }
-  int lw = (int)(4 * D.l * D.l + 4096);
-  if (qh && mode == FFB_MODE_FLIPFLOP) {
-    int q = 0;
-    if (cusolverDnDgesvd_bufferSize(qh, (int)D.l, (int)D.l, &q) == CUSOLVER_STATUS_SUCCESS)
-      lw = std::max(lw, q);
-  }
-  *bytes = carve(nullptr, D, nullptr, (size_t)-1, w, lw) + (8u << 20);
+  *bytes = carve(nullptr, D, nullptr, (size_t)-1, w) + (8u << 20);
   return FFB_OK;
 }
 
@@ -406,16 +380,14 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
   if (!validate(D) || lda < m) return fail(ctx, FFB_ERR_DIMENSION, "invalid dimensions/parameters");
   if (mode == FFB_MODE_FLIPFLOP && (!out->u || !out->s || !out->v))
     return fail(ctx, FFB_ERR_ARGUMENT, "u, s, v outputs are required");
-  const int lw = (mode == FFB_MODE_FLIPFLOP) ? std::max(svd_lwork(ctx, D.l), 1) : 1;
   Work& w = e.w;
-  const size_t need = carve(ctx, D, workspace, workspace_bytes, w, lw);
+  const size_t need = carve(ctx, D, workspace, workspace_bytes, w);
   if (need > workspace_bytes) return fail(ctx, FFB_ERR_ARGUMENT, "workspace too small");
   e.gc.sms = ctx->sms;
   e.gc.partial = w.gpart;
   e.gc.partial_cap = w.gpart_cap;
   cudaStream_t st = e.st;
   const int64_t l = D.l, s = D.s, L1 = l + 1;
-  if (ctx->solver) cusolverDnSetStream(ctx->solver, st);
 
   // g2 test matrix for swaps == 0 (stream 1000), generated on the host by the
   // reference's RNG and staged now so the pipeline never waits for the host.
@@ -556,19 +528,17 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
     e.gemm(m, l, n, 1.0, A, lda, false, w.Yh, n, true, 0.0, w.tmp, m);
     // (K14) tmp = Qt Rt, SVD(Rt)
     e.hh_qr(w.tmp, m, l, m, w.Yt, m, w.Tt, l, w.Rt, l, true);
-    if (ctx->solver && e.cerr == cudaSuccess) {
-      cusolverStatus_t cs = cusolverDnDgesvd(ctx->solver, 'A', 'A', (int)l, (int)l, w.Rt, (int)l,
-                                             w.sig, w.Us, (int)l, w.VsT, (int)l, w.svdwork,
-                                             w.lwork, nullptr, w.svdinfo);
-      if (cs != CUSOLVER_STATUS_SUCCESS) e.cerr = cudaErrorUnknown;
-      ++e.launches;
-    }
+    // one-sided block Jacobi SVD of Rt (ffb_jacobi.cu): Rt = Us diag(sig) Vo^T
+    e.memset2d(w.VsT, l, l, l);
+    e.ok(launch_add_identity(st, w.VsT, l, l, l, 1.0));
+    e.ok(launch_jacobi_svd(st, ctx->sms, w.Rt, l, w.VsT, l, (int)l, w.sig, w.Us, l, w.Vo, l, w.jbar,
+                           w.joff, w.jsweeps, w.jorder, kMaxSweeps));
     // (K15) u = Qt[:, :l] Us[:, :k] ; v = Yh Vs[:, :k]
     e.gemm(l, k, l, 1.0, w.Yt, m, true, w.Us, l, true, 0.0, w.W1, l);
     e.gemm(l, k, l, 1.0, w.Tt, l, false, w.W1, l, true, 0.0, w.W2, l);
     e.gemm(m, k, l, -1.0, w.Yt, m, false, w.W2, l, true, 0.0, out->u, out->ldu);
     e.ok(launch_add_top(st, out->u, out->ldu, w.Us, l, l, k));
-    e.gemm(n, k, l, 1.0, w.Yh, n, false, w.VsT, l, false, 0.0, out->v, out->ldv);
+    e.gemm(n, k, l, 1.0, w.Yh, n, false, w.Vo, l, true, 0.0, out->v, out->ldv);
     e.ok(cudaMemcpyAsync(out->s, w.sig, sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
     if (out->sv_all) e.ok(cudaMemcpyAsync(out->sv_all, w.sig, sizeof(double) * l, cudaMemcpyDeviceToDevice, st));
   };
@@ -631,9 +601,10 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
     sc = *ctx->sc_host;
   }
   if (mode == FFB_MODE_FLIPFLOP) {
-    int info = 0;
-    cudaMemcpy(&info, w.svdinfo, sizeof(int), cudaMemcpyDeviceToHost);
-    if (info != 0) return fail(ctx, FFB_ERR_NUMERICAL, "small SVD did not converge");
+    int sweeps = 0;
+    cudaMemcpy(&sweeps, w.jsweeps, sizeof(int), cudaMemcpyDeviceToHost);
+    out->svd_sweeps = sweeps;
+    if (sweeps >= kMaxSweeps) return fail(ctx, FFB_ERR_NUMERICAL, "small SVD did not converge");
   }
   out->alpha = sc.alpha;
   out->g1 = sc.g1;

@@ -423,10 +423,10 @@ cudaError_t launch_finite_check(cudaStream_t st, const double* x, size_t count, 
 constexpr int kMaxW = 64;
 constexpr int kSLD = kMaxW + 1;
 
-// Sum split-K partial Grams, optional shift, Cholesky (upper R, R^T R = G),
-// R^-1, and Racc <- R * Racc (Racc := R when `first`).  One CTA.
-__global__ void __launch_bounds__(256) cholinv_kernel(const double* __restrict__ part, int splits,
-                                                      int w, int64_t rows_m, int shift, int first,
+// Gram G (w x w, reduced), optional shift, Cholesky (upper R, R^T R = G),
+// R^-1, and Racc <- R * Racc (Racc := R when `first`).  One CTA, 256 threads.
+__global__ void __launch_bounds__(256) cholinv_kernel(const double* __restrict__ Gin, int w,
+                                                      int64_t rows_m, int shift, int first,
                                                       double* Racc, double* Rinv,
                                                       uint32_t* status) {
   extern __shared__ __align__(16) double dsm[];
@@ -439,11 +439,10 @@ __global__ void __launch_bounds__(256) cholinv_kernel(const double* __restrict__
   const int ww = w * w;
   if (tid == 0) bad = 0;
   for (int t = tid; t < ww; t += nt) {
-    double acc = 0.0;
-    for (int q = 0; q < splits; ++q) acc += part[(size_t)q * ww + t];
     const int i = t % w, j = t / w;
-    G[i * kSLD + j] = acc;
+    G[i * kSLD + j] = Gin[t];
     R[i * kSLD + j] = 0.0;
+    X[i * kSLD + j] = 0.0;
   }
   __syncthreads();
   double tr = 0.0;
@@ -464,19 +463,15 @@ __global__ void __launch_bounds__(256) cholinv_kernel(const double* __restrict__
     for (int i = tid; i < w; i += nt) G[i * kSLD + i] += sh;
     __syncthreads();
   }
-  // right-looking Cholesky on the upper triangle
+  // right-looking Cholesky on the upper triangle: 2 barriers per column
   for (int j = 0; j < w; ++j) {
-    if (tid == 0) {
-      double d = G[j * kSLD + j];
-      if (!(d > 0.0) || !isfinite(d)) {
-        bad = 1;
-        d = d > 0.0 ? d : 1e-300;
-      }
-      R[j * kSLD + j] = sqrt(d);
+    double d = G[j * kSLD + j];
+    if (!(d > 0.0) || !isfinite(d)) {
+      if (tid == 0) bad = 1;
+      d = d > 0.0 ? d : 1e-300;
     }
-    __syncthreads();
-    const double rjj = R[j * kSLD + j];
-    for (int k = j + 1 + tid; k < w; k += nt) R[j * kSLD + k] = G[j * kSLD + k] / rjj;
+    const double rjj = sqrt(d);
+    for (int k = j + tid; k < w; k += nt) R[j * kSLD + k] = (k == j) ? rjj : G[j * kSLD + k] / rjj;
     __syncthreads();
     const int rem = w - j - 1;
     for (int t = tid; t < rem * rem; t += nt) {
@@ -485,28 +480,30 @@ __global__ void __launch_bounds__(256) cholinv_kernel(const double* __restrict__
     }
     __syncthreads();
   }
-  // inverse of upper-triangular R, one column per thread (back substitution)
-  for (int c = tid; c < w; c += nt) {
-    for (int i = 0; i < w; ++i) X[i * kSLD + c] = 0.0;
-    X[c * kSLD + c] = 1.0 / R[c * kSLD + c];
-    for (int i = c - 1; i >= 0; --i) {
+  // X = R^-1 by rows from the bottom; 4 lanes per column share each dot.
+  {
+    const int c = tid >> 2, sub = tid & 3;
+    for (int i = w - 1; i >= 0; --i) {
       double acc = 0.0;
-      for (int k = i + 1; k <= c; ++k) acc = fma(R[i * kSLD + k], X[k * kSLD + c], acc);
-      X[i * kSLD + c] = -acc / R[i * kSLD + i];
+      if (c < w && c >= i)
+        for (int k = i + 1 + sub; k <= c; k += 4) acc = fma(R[i * kSLD + k], X[k * kSLD + c], acc);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if (c < w && c >= i && sub == 0) X[i * kSLD + c] = ((i == c ? 1.0 : 0.0) - acc) / R[i * kSLD + i];
+      __syncthreads();
     }
   }
-  __syncthreads();
+  // new Racc = R * Racc (upper x upper), staged in G
   for (int t = tid; t < ww; t += nt) {
     const int i = t % w, j = t / w;
     Rinv[i + j * w] = X[i * kSLD + j];
-    double acc;
+    double acc = 0.0;
     if (first) {
       acc = R[i * kSLD + j];
-    } else {
-      acc = 0.0;
+    } else if (i <= j) {
       for (int k = i; k <= j; ++k) acc = fma(R[i * kSLD + k], Racc[k + j * w], acc);
     }
-    G[i * kSLD + j] = acc;  // reuse G as staging for the new Racc
+    G[i * kSLD + j] = acc;
   }
   __syncthreads();
   for (int t = tid; t < ww; t += nt) {
@@ -516,16 +513,16 @@ __global__ void __launch_bounds__(256) cholinv_kernel(const double* __restrict__
   if (tid == 0 && bad) atomicOr(status, kStCholFail);
 }
 
-cudaError_t launch_cholinv(cudaStream_t st, const double* part, int splits, int w, int64_t rows_m,
-                           bool shift, bool first, double* Racc, double* Rinv, uint32_t* status) {
+cudaError_t launch_cholinv(cudaStream_t st, const double* G, int w, int64_t rows_m, bool shift,
+                           bool first, double* Racc, double* Rinv, uint32_t* status) {
   static bool init = false;
   constexpr int kSm = 3 * kMaxW * kSLD * sizeof(double);
   if (!init) {
     cudaFuncSetAttribute(cholinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSm);
     init = true;
   }
-  cholinv_kernel<<<1, 256, kSm, st>>>(part, splits, w, rows_m, shift ? 1 : 0, first ? 1 : 0, Racc,
-                                     Rinv, status);
+  cholinv_kernel<<<1, 256, kSm, st>>>(G, w, rows_m, shift ? 1 : 0, first ? 1 : 0, Racc, Rinv,
+                                       status);
   FFB_LAUNCH_CHECK();
 }
 
@@ -541,6 +538,8 @@ __global__ void __launch_bounds__(256) signlu_kernel(const double* __restrict__ 
   double* q = dsm;
   double* L = q + kMaxW * kSLD;
   double* U = L + kMaxW * kSLD;
+  double* Ui = U + kMaxW * kSLD;      // D * U^{-1}
+  double* Ts = Ui + kMaxW * kSLD;     // T
   __shared__ double Dd[kMaxW];
   const int tid = threadIdx.x, nt = blockDim.x;
   bool zero_panel = true;
@@ -564,16 +563,16 @@ __global__ void __launch_bounds__(256) signlu_kernel(const double* __restrict__ 
   }
   __syncthreads();
   for (int c = 0; c < w; ++c) {
+    // every thread derives the same sign from q[c][c] (no extra barrier)
+    const double z = q[c * kSLD + c];
+    double d;
+    if (fabs(z) == 1.0) d = z > 0.0 ? 1.0 : -1.0;    // identity reflector (tail == 0)
+    else d = z > 0.0 ? -1.0 : 1.0;                   // pivot -(1+|z|) = -tau
+    const double ucc = d * z - 1.0;
     if (tid == 0) {
-      const double z = q[c * kSLD + c];
-      double d;
-      if (fabs(z) == 1.0) d = z > 0.0 ? 1.0 : -1.0;    // identity reflector (tail == 0)
-      else d = z > 0.0 ? -1.0 : 1.0;                   // pivot -(1+|z|) = -tau
       Dd[c] = d;
-      U[c * kSLD + c] = d * z - 1.0;
+      U[c * kSLD + c] = ucc;
     }
-    __syncthreads();
-    const double d = Dd[c], ucc = U[c * kSLD + c];
     for (int i = c + 1 + tid; i < w; i += nt) L[i * kSLD + c] = ucc != 0.0 ? d * q[i * kSLD + c] / ucc : 0.0;
     for (int k = tid; k < c; k += nt) U[k * kSLD + c] = d * q[k * kSLD + c];
     __syncthreads();
@@ -584,27 +583,35 @@ __global__ void __launch_bounds__(256) signlu_kernel(const double* __restrict__ 
     }
     __syncthreads();
   }
-  // Ut = D * U^{-1} with zero pivots -> zero columns; row i solves e_i = y U.
-  // T = -U L^{-T}: row i solves t L^T = -U[i,:].
-  for (int i = tid; i < w; i += nt) {
-    double y[kMaxW];
+  // Column-sequential solves, all rows in parallel (4 lanes per row):
+  //   Ui row i: y U = e_i  -> y_c = (delta_ic - sum_{k<c} y_k U[k][c]) / U[c][c]
+  //   T  row i: t L^T = -U[i,:] -> t_c = -U[i][c] - sum_{k<c} t_k L[c][k]
+  {
+    const int i = tid >> 2, sub = tid & 3;
     for (int c = 0; c < w; ++c) {
-      double acc = (c == i) ? 1.0 : 0.0;
-      for (int k = 0; k < c; ++k) acc = fma(-y[k], U[k * kSLD + c], acc);
-      const double ucc = U[c * kSLD + c];
-      y[c] = ucc != 0.0 ? acc / ucc : 0.0;
+      double a0 = 0.0, a1 = 0.0;
+      if (i < w)
+        for (int k = sub; k < c; k += 4) {
+          a0 = fma(Ui[i * kSLD + k], U[k * kSLD + c], a0);
+          a1 = fma(Ts[i * kSLD + k], L[c * kSLD + k], a1);
+        }
+      a0 += __shfl_xor_sync(0xffffffffu, a0, 1);
+      a0 += __shfl_xor_sync(0xffffffffu, a0, 2);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, 1);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, 2);
+      if (i < w && sub == 0) {
+        const double ucc = U[c * kSLD + c];
+        Ui[i * kSLD + c] = ucc != 0.0 ? ((i == c ? 1.0 : 0.0) - a0) / ucc : 0.0;
+        Ts[i * kSLD + c] = -U[i * kSLD + c] - a1;
+      }
+      __syncthreads();
     }
-    for (int c = 0; c < w; ++c) Ut[i + c * w] = Dd[i] * y[c];
-    for (int jj = 0; jj < w; ++jj) {
-      double acc = -U[i * kSLD + jj];
-      for (int k = 0; k < jj; ++k) acc = fma(-y[k], L[jj * kSLD + k], acc);
-      y[jj] = acc;  // overwrite is safe: y[k<jj] now holds t_k
-    }
-    for (int jj = 0; jj < w; ++jj) T[i + jj * ldt] = y[jj];
   }
   for (int t = tid; t < w * w; t += nt) {
     const int i = t % w, j = t / w;
     Y[i + j * ldy] = L[i * kSLD + j];
+    T[i + j * ldt] = Ts[i * kSLD + j];
+    Ut[i + j * w] = Dd[i] * Ui[i * kSLD + j];
     Rout[i + j * ldr] = (i <= j) ? Dd[i] * Racc[i + j * w] : 0.0;
   }
   for (int i = tid; i < w; i += nt) Dout[i] = Dd[i];
@@ -614,7 +621,7 @@ cudaError_t launch_signlu(cudaStream_t st, const double* Qtop, int64_t ldq, int 
                           const double* Racc, double* Y, int64_t ldy, double* T, int64_t ldt,
                           double* R, int64_t ldr, double* Ut, double* D) {
   static bool init = false;
-  constexpr int kSm = 3 * kMaxW * kSLD * sizeof(double);
+  constexpr int kSm = 5 * kMaxW * kSLD * sizeof(double);
   if (!init) {
     cudaFuncSetAttribute(signlu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSm);
     init = true;

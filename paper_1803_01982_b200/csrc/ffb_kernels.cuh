@@ -73,8 +73,8 @@ cudaError_t launch_add_top(cudaStream_t st, double* X, int64_t ldx, const double
                            int64_t rows, int64_t cols);
 
 // Panel reconstruction pieces.
-cudaError_t launch_cholinv(cudaStream_t st, const double* part, int splits, int w, int64_t rows_m,
-                           bool shift, bool first, double* Racc, double* Rinv, uint32_t* status);
+cudaError_t launch_cholinv(cudaStream_t st, const double* G, int w, int64_t rows_m, bool shift,
+                           bool first, double* Racc, double* Rinv, uint32_t* status);
 cudaError_t launch_signlu(cudaStream_t st, const double* Qtop, int64_t ldq, int w,
                           const double* Racc, double* Y, int64_t ldy, double* T, int64_t ldt,
                           double* R, int64_t ldr, double* Ut, double* D);

@@ -161,7 +161,7 @@ def run(A, params: SketchParams, mode, device=None, want=("R", "Q", "rtilde", "p
         out.update(alpha=res.alpha, g1=res.g1, g2=res.g2, tau=res.tau_bound,
                    tau_hat=res.tau_hat_bound, r22=res.r22, swaps=int(res.swaps),
                    flops=int(res.flops), kernels=int(res.kernels),
-                   status_bits=int(res.status_bits),
+                   status_bits=int(res.status_bits), svd_sweeps=int(res.svd_sweeps),
                    i_offs=[int(res.i_off_trace[i]) for i in range(min(int(res.swaps), 64))],
                    is_numpy=is_np, params=prm, m=m, n=n)
         if rc == _capi.FFB_OK:
@@ -215,7 +215,8 @@ def flip_flop_srqr(A, k, l=None, b=32, p=5, epsilon=0.5, g=2.0, d=None, seed=0, 
     meta = {"srqr": res, "params": out["params"], "method": "flip_flop_srqr",
             "diag_L": _conv(out["diag_L"], np_), "sv_all": _conv(out["sv_all"], np_),
             "pivot_gap": _conv(out["pivot_gap"], np_), "engine": "ffb200-sm100a",
-            "kernels": out["kernels"], "i_offs": out["i_offs"]}
+            "kernels": out["kernels"], "i_offs": out["i_offs"],
+            "svd_sweeps": out["svd_sweeps"]}
     return ApproxSvd(u=_conv(out["u"], np_), s=_conv(out["s"], np_), v=_conv(out["v"], np_),
                      flop_count=out["flops"], meta=meta)
 
