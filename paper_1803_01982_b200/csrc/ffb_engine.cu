@@ -22,6 +22,7 @@
 #include "ffb_gemm.h"
 #include "ffb_jacobi.cuh"
 #include "ffb_kernels.cuh"
+#include "ffb_panel.cuh"
 
 using namespace ffb;
 
@@ -66,7 +67,8 @@ struct Work {
   // TRQRCP
   double *B, *colsq, *Y, *T, *WT, *R, *Q;
   int64_t *arr, *pos;
-  double *P, *Xa, *Xb, *G1, *WTg, *S1, *S2, *Racc, *Gm, *Rinv, *Ut, *Dv, *Rb, *Bp, *Z;
+  double *P, *Xa, *Xb, *G1, *WTg, *S1, *S2, *Racc, *Gm, *ppart, *Rinv, *Ut, *Dv, *Rb, *Bp, *Z;
+  uint32_t* pbar;
   double *hhW, *hhW2;
   // pivots
   PivSlot* slots;
@@ -128,6 +130,8 @@ size_t carve(const ffb_ctx* ctx, const Dims& D, void* base, size_t cap, Work& w)
   w.S2 = b.take<double>(max_i(l, 1) * max_i(bmax, kPanelW));
   w.Racc = b.take<double>(kPanelW * kPanelW);
   w.Gm = b.take<double>(kPanelW * kPanelW);
+  w.ppart = b.take<double>((size_t)(ctx ? ctx->sms : 160) * kPanelW * kPanelW);
+  w.pbar = b.take<uint32_t>(4);
   w.Rinv = b.take<double>(kPanelW * kPanelW);
   w.Ut = b.take<double>(kPanelW * kPanelW);
   w.Dv = b.take<double>(kPanelW);
@@ -211,24 +215,14 @@ struct Eng {
     ok(cudaMemset2DAsync(p, ld * sizeof(double), 0, rows * sizeof(double), cols, st));
   }
 
-  // Householder panel (Mp x wb, wb <= 64) by shifted CholeskyQR3 + reconstruction.
+  // Householder panel (Mp x wb, wb <= 64): one fused cooperative kernel
+  // (shifted CholeskyQR3 + Householder reconstruction, ffb_panel.cu).
   void recon(const double* Xp, int64_t Mp, int wb, int64_t ldx, double* Yp, int64_t ldy,
              double* Tp, int64_t ldt, double* Rp, int64_t ldr) {
-    // pass 1 (shifted)
-    gram(Xp, Mp, wb, ldx);
-    ok(launch_cholinv(st, w.Gm, wb, Mp, true, true, w.Racc, w.Rinv, w.status));
-    gemm(Mp, wb, wb, 1.0, Xp, ldx, false, w.Rinv, wb, true, 0.0, w.Xa, Mp);
-    // pass 2
-    gram(w.Xa, Mp, wb, Mp);
-    ok(launch_cholinv(st, w.Gm, wb, Mp, false, false, w.Racc, w.Rinv, w.status));
-    gemm(Mp, wb, wb, 1.0, w.Xa, Mp, false, w.Rinv, wb, true, 0.0, w.Xb, Mp);
-    // pass 3
-    gram(w.Xb, Mp, wb, Mp);
-    ok(launch_cholinv(st, w.Gm, wb, Mp, false, false, w.Racc, w.Rinv, w.status));
-    gemm(Mp, wb, wb, 1.0, w.Xb, Mp, false, w.Rinv, wb, true, 0.0, w.Xa, Mp);
-    // signs + reflectors
-    ok(launch_signlu(st, w.Xa, Mp, wb, w.Racc, Yp, ldy, Tp, ldt, Rp, ldr, w.Ut, w.Dv));
-    if (Mp > wb) gemm(Mp - wb, wb, wb, 1.0, w.Xa + wb, Mp, false, w.Ut, wb, true, 0.0, Yp + wb, ldy);
+    if (cerr != cudaSuccess) return;
+    ok(launch_panel_qr(st, ctx->sms, Xp, ldx, Mp, wb, Yp, ldy, Tp, ldt, Rp, ldr, w.Xa, w.Xb,
+                       w.ppart, w.Gm, w.pbar, w.status));
+    gc.flops += 3 * 4 * Mp * (int64_t)wb * wb + 2 * Mp * (int64_t)wb * wb;
   }
 
   // Blocked Householder QR of X (Mx x Nx, ld ldx), panels of <= 64 columns.
@@ -459,7 +453,8 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
     // sketch update B[:, trailing] -= (B_piv R11^{-1}) R12
     if (e1 < n) {
       e.ok(launch_gather_cols(st, w.B, s, s, w.arr + j0, bb, w.Bp, s));
-      e.ok(launch_trsm_rows_upper(st, w.Bp, s, (int)s, w.Rb, bb, (int)bb, w.Z, s, w.status));
+      e.ok(launch_triinv_upper(st, w.Rb, bb, (int)bb, w.Rinv, w.status));
+      e.gemm(s, bb, bb, 1.0, w.Bp, s, false, w.Rinv, bb, true, 0.0, w.Z, s);
       e.gemm(s, n, bb, -1.0, w.Z, s, false, w.R + j0, L1, true, 1.0, w.B, s);
     }
   }

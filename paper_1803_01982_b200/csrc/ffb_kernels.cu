@@ -463,22 +463,25 @@ __global__ void __launch_bounds__(256) cholinv_kernel(const double* __restrict__
     for (int i = tid; i < w; i += nt) G[i * kSLD + i] += sh;
     __syncthreads();
   }
-  // right-looking Cholesky on the upper triangle: 2 barriers per column
-  for (int j = 0; j < w; ++j) {
-    double d = G[j * kSLD + j];
-    if (!(d > 0.0) || !isfinite(d)) {
-      if (tid == 0) bad = 1;
-      d = d > 0.0 ? d : 1e-300;
+  // right-looking Cholesky on the upper triangle: 2 barriers per column; thread
+  // (tx = column q, ty = row phase) layout, no integer division in the loop
+  {
+    const int tx = tid & 63, ty = tid >> 6, nty = nt >> 6;
+    for (int j = 0; j < w; ++j) {
+      double d = G[j * kSLD + j];
+      if (!(d > 0.0) || !isfinite(d)) {
+        if (tid == 0) bad = 1;
+        d = d > 0.0 ? d : 1e-300;
+      }
+      const double rjj = sqrt(d);
+      if (ty == 0 && tx >= j && tx < w) R[j * kSLD + tx] = (tx == j) ? rjj : G[j * kSLD + tx] / rjj;
+      __syncthreads();
+      if (tx > j && tx < w) {
+        const double rq = R[j * kSLD + tx];
+        for (int k = j + 1 + ty; k <= tx; k += nty) G[k * kSLD + tx] -= R[j * kSLD + k] * rq;
+      }
+      __syncthreads();
     }
-    const double rjj = sqrt(d);
-    for (int k = j + tid; k < w; k += nt) R[j * kSLD + k] = (k == j) ? rjj : G[j * kSLD + k] / rjj;
-    __syncthreads();
-    const int rem = w - j - 1;
-    for (int t = tid; t < rem * rem; t += nt) {
-      const int k = j + 1 + t / rem, q = j + 1 + t % rem;
-      if (q >= k) G[k * kSLD + q] -= R[j * kSLD + k] * R[j * kSLD + q];
-    }
-    __syncthreads();
   }
   // X = R^-1 by rows from the bottom; 4 lanes per column share each dot.
   {
@@ -576,10 +579,12 @@ __global__ void __launch_bounds__(256) signlu_kernel(const double* __restrict__ 
     for (int i = c + 1 + tid; i < w; i += nt) L[i * kSLD + c] = ucc != 0.0 ? d * q[i * kSLD + c] / ucc : 0.0;
     for (int k = tid; k < c; k += nt) U[k * kSLD + c] = d * q[k * kSLD + c];
     __syncthreads();
-    const int rem = w - c - 1;
-    for (int t = tid; t < rem * rem; t += nt) {
-      const int i = c + 1 + t % rem, jj = c + 1 + t / rem;
-      q[i * kSLD + jj] -= L[i * kSLD + c] * q[c * kSLD + jj];
+    {
+      const int tx = tid & 63, ty = tid >> 6, nty = nt >> 6;
+      if (tx > c && tx < w) {
+        const double qc = q[c * kSLD + tx];
+        for (int i = c + 1 + ty; i < w; i += nty) q[i * kSLD + tx] -= L[i * kSLD + c] * qc;
+      }
     }
     __syncthreads();
   }
@@ -659,41 +664,54 @@ cudaError_t launch_fix_rrows(cudaStream_t st, double* R, int64_t ldr, int64_t j0
   FFB_LAUNCH_CHECK();
 }
 
-// Z = Bp * Rb^{-1} row by row (Rb upper w x w).  Exact zero pivots give zero
-// columns and raise kStZeroPivot (the reference falls back to lstsq,
-// ffsrqr/sketch.py:75-83).
-__global__ void trsm_rows_upper_kernel(const double* __restrict__ Bp, int64_t ldb, int rows,
-                                       const double* __restrict__ Rb, int64_t ldrb, int w,
-                                       double* Z, int64_t ldz, uint32_t* status) {
-  __shared__ double Rs[kMaxW * kSLD];
-  for (int t = threadIdx.x; t < w * w; t += blockDim.x) {
+// Rinv = Rb^{-1} for an upper-triangular w x w Rb (w <= 64), so that the sketch
+// update Z = B_piv Rb^{-1} runs as one DMMA GEMM.  Exact zero pivots (only an
+// all-zero panel produces them) give zero rows and raise kStZeroPivot; the
+// reference would fall back to lstsq there (ffsrqr/sketch.py:75-83).
+__global__ void __launch_bounds__(256) triinv_upper_kernel(const double* __restrict__ Rb,
+                                                           int64_t ldrb, int w, double* Rinv,
+                                                           uint32_t* status) {
+  extern __shared__ __align__(16) double dsm[];
+  double* R = dsm;
+  double* X = R + kMaxW * kSLD;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  bool zp = false;
+  for (int t = tid; t < w * w; t += nt) {
     const int i = t % w, j = t / w;
-    Rs[i * kSLD + j] = Rb[i + j * ldrb];
+    R[i * kSLD + j] = Rb[i + j * ldrb];
+    X[i * kSLD + j] = 0.0;
   }
   __syncthreads();
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= rows) return;
-  double y[kMaxW];
-  bool zp = false;
-  for (int c = 0; c < w; ++c) {
-    double acc = Bp[row + c * (int64_t)ldb];
-    for (int k = 0; k < c; ++k) acc = fma(-y[k], Rs[k * kSLD + c], acc);
-    const double d = Rs[c * kSLD + c];
-    if (d != 0.0) {
-      y[c] = acc / d;
-    } else {
-      y[c] = 0.0;
-      zp = true;
+  const int c = tid >> 2, sub = tid & 3;
+  for (int i = w - 1; i >= 0; --i) {
+    double acc = 0.0;
+    if (c < w && c >= i)
+      for (int k = i + 1 + sub; k <= c; k += 4) acc = fma(R[i * kSLD + k], X[k * kSLD + c], acc);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (c < w && c >= i && sub == 0) {
+      const double d = R[i * kSLD + i];
+      if (d != 0.0) X[i * kSLD + c] = ((i == c ? 1.0 : 0.0) - acc) / d;
+      else zp = true;
     }
-    Z[row + c * ldz] = y[c];
+    __syncthreads();
+  }
+  for (int t = tid; t < w * w; t += nt) {
+    const int i = t % w, j = t / w;
+    Rinv[i + j * w] = X[i * kSLD + j];
   }
   if (zp) atomicOr(status, kStZeroPivot);
 }
 
-cudaError_t launch_trsm_rows_upper(cudaStream_t st, const double* Bp, int64_t ldb, int rows,
-                                   const double* Rb, int64_t ldrb, int w, double* Z, int64_t ldz,
-                                   uint32_t* status) {
-  trsm_rows_upper_kernel<<<nblk(rows, 64), 64, 0, st>>>(Bp, ldb, rows, Rb, ldrb, w, Z, ldz, status);
+cudaError_t launch_triinv_upper(cudaStream_t st, const double* Rb, int64_t ldrb, int w,
+                                double* Rinv, uint32_t* status) {
+  static bool init = false;
+  constexpr int kSm = 2 * kMaxW * kSLD * sizeof(double);
+  if (!init) {
+    cudaFuncSetAttribute(triinv_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSm);
+    init = true;
+  }
+  triinv_upper_kernel<<<1, 256, kSm, st>>>(Rb, ldrb, w, Rinv, status);
   FFB_LAUNCH_CHECK();
 }
 

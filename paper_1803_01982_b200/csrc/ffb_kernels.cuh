@@ -82,9 +82,8 @@ cudaError_t launch_signlu(cudaStream_t st, const double* Qtop, int64_t ldq, int 
 // TRQRCP helpers.
 cudaError_t launch_fix_rrows(cudaStream_t st, double* R, int64_t ldr, int64_t j0, int bb,
                              const int64_t* arr, const double* Rb, int64_t ldrb);
-cudaError_t launch_trsm_rows_upper(cudaStream_t st, const double* Bp, int64_t ldb, int rows,
-                                   const double* Rb, int64_t ldrb, int w, double* Z, int64_t ldz,
-                                   uint32_t* status);
+cudaError_t launch_triinv_upper(cudaStream_t st, const double* Rb, int64_t ldrb, int w,
+                                double* Rinv, uint32_t* status);
 
 // SRQR.
 cudaError_t launch_rinit(cudaStream_t st, const double* B, int64_t ldb, int s, const int64_t* arr,

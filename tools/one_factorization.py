@@ -26,4 +26,4 @@ for _ in range(a.reps):
     r = ffb.flip_flop_srqr(A, cfg.k, l=cfg.l, b=cfg.b, p=cfg.p, seed=0)
 torch.cuda.synchronize()
 torch.cuda.nvtx.range_pop()
-print("kernels per factorization:", r.meta["kernels"], "swaps:", r.meta["srqr"].cert.swaps)
+print("kernels per factorization:", r.meta["kernels"], "swaps:", r.meta["srqr"].cert.swaps, "svd_sweeps:", r.meta.get("svd_sweeps"))
