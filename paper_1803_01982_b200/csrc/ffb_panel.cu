@@ -16,6 +16,7 @@
 
 #include "ffb_common.cuh"
 #include "ffb_panel.cuh"
+#include "ffb_tile64.cuh"
 
 namespace ffb {
 
@@ -53,64 +54,6 @@ FFB_DEV void grid_sync(uint32_t* bar, uint32_t nblocks) {
   __syncthreads();
 }
 
-// Cholesky (upper, R^T R = G) of the w x w Gram in Gs (destroyed), R into Rs,
-// X = R^-1 into Xs.  256 threads.  Returns false on breakdown.
-FFB_DEV bool chol_inv(double* Gs, double* Rs, double* Xs, int w, double shift_coef, bool& zero) {
-  __shared__ double red[8];
-  __shared__ int bad;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  if (tid == 0) bad = 0;
-  double tr = 0.0;
-  for (int i = tid; i < w; i += nt) tr += Gs[i * kL + i];
-  tr = block_sum(tr, red);
-  for (int t = tid; t < kW * kW; t += nt) {
-    Rs[(t >> 6) * kL + (t & 63)] = 0.0;
-    Xs[(t >> 6) * kL + (t & 63)] = 0.0;
-  }
-  zero = (tr == 0.0);
-  if (zero) {
-    __syncthreads();
-    for (int i = tid; i < w; i += nt) {
-      Rs[i * kL + i] = 1.0;
-      Xs[i * kL + i] = 1.0;
-    }
-    __syncthreads();
-    return true;
-  }
-  if (shift_coef > 0.0) {
-    for (int i = tid; i < w; i += nt) Gs[i * kL + i] += shift_coef * tr;
-  }
-  __syncthreads();
-  const int tx = tid & 63, ty = tid >> 6, nty = nt >> 6;
-  for (int j = 0; j < w; ++j) {
-    double d = Gs[j * kL + j];
-    if (!(d > 0.0) || !isfinite(d)) {
-      if (tid == 0) bad = 1;
-      d = d > 0.0 ? d : 1e-300;
-    }
-    const double rjj = sqrt(d);
-    if (ty == 0 && tx >= j && tx < w) Rs[j * kL + tx] = (tx == j) ? rjj : Gs[j * kL + tx] / rjj;
-    __syncthreads();
-    if (tx > j && tx < w) {
-      const double rq = Rs[j * kL + tx];
-      for (int k = j + 1 + ty; k <= tx; k += nty) Gs[k * kL + tx] -= Rs[j * kL + k] * rq;
-    }
-    __syncthreads();
-  }
-  // X = R^-1, rows from the bottom, 4 lanes per column
-  const int c = tid >> 2, sub = tid & 3;
-  for (int i = w - 1; i >= 0; --i) {
-    double acc = 0.0;
-    if (c < w && c >= i)
-      for (int k = i + 1 + sub; k <= c; k += 4) acc = fma(Rs[i * kL + k], Xs[k * kL + c], acc);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    if (c < w && c >= i && sub == 0) Xs[i * kL + c] = ((i == c ? 1.0 : 0.0) - acc) / Rs[i * kL + i];
-    __syncthreads();
-  }
-  return bad == 0;
-}
-
 // out(rows x w) = in(rows x w) * Xs (upper triangular), chunk in smem (Cs),
 // result written to global dst (ld ldd).  256 threads: thread -> (row, 16 cols).
 FFB_DEV void apply_upper(const double* Cs, int rows, int w, const double* Xs, double* dst,
@@ -135,21 +78,22 @@ FFB_DEV void apply_upper(const double* Cs, int rows, int w, const double* Xs, do
 }  // namespace
 
 __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
+  using namespace tile64;
   extern __shared__ __align__(16) double sm[];
-  double* Gs = sm;                    // w x w Gram / LU workspace
-  double* Rs = Gs + kW * kL;          // Cholesky factor / L
-  double* Xs = Rs + kW * kL;          // R^-1 / U
-  double* Ra = Xs + kW * kL;          // Racc (every CTA keeps it; cheap)
-  double* Cs = Ra + kW * kL;          // staged chunk of rows (kCH x w)
-  double* Ws = Cs + kCH * kL;         // Ut / T staging
+  double* Rs = sm;                    // Cholesky factor / L of the sign LU
+  double* Xs = Rs + kW * kL;          // R^-1 / U of the sign LU
+  double* Ra = Xs + kW * kL;          // Racc (accumulated R of the three passes)
+  double* Cs = Ra + kW * kL;          // staged chunk of rows (kCH x w) / Ui
+  double* Ws = Cs + kCH * kL;         // Linv / row stage
+  double* buf = Ws + kW * kL;         // 256 doubles of broadcast scratch
   __shared__ double Dd[kW];
-  __shared__ int s_zero;
+  __shared__ double red[8];
   const int tid = threadIdx.x, nt = blockDim.x, G = gridDim.x, w = a.w;
   const int64_t Mp = a.Mp;
   const int64_t r0 = (int64_t)blockIdx.x * a.rpc;
   const int64_t r1 = r0 + a.rpc < Mp ? r0 + a.rpc : Mp;
   const int ww = w * w;
-  const int bi = (tid & 15) * 4, bj = (tid >> 4) * 4;
+  const int bi = bi_of(tid), bj = bj_of(tid);
   bool zero = false;
 
   for (int pass = 0; pass < 3; ++pass) {
@@ -157,11 +101,11 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
     const int64_t lds = pass == 0 ? a.ldx : Mp;
     double* dst = pass == 1 ? a.Qb : a.Qa;
     // (a) local Gram of rows [r0, r1)
-    double acc[4][4];
+    Tile acc;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+      for (int j = 0; j < 4; ++j) acc.v[i][j] = 0.0;
     for (int64_t c0 = r0; c0 < r1; c0 += kCH) {
       const int rows = (int)(r1 - c0 < kCH ? r1 - c0 : kCH);
       __syncthreads();
@@ -180,7 +124,7 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fma(x[i], y[j], acc[i][j]);
+          for (int j = 0; j < 4; ++j) acc.v[i][j] = fma(x[i], y[j], acc.v[i][j]);
       }
     }
     double* mypart = a.part + (size_t)blockIdx.x * ww;
@@ -188,7 +132,7 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (bi + i < w && bj + j < w) mypart[(bi + i) + (bj + j) * w] = acc[i][j];
+        if (bi + i < w && bj + j < w) mypart[(bi + i) + (bj + j) * w] = acc.v[i][j];
     grid_sync(a.bar, G);
     // (b) distributed fixed-order reduction
     {
@@ -201,34 +145,60 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
       }
     }
     grid_sync(a.bar, G);
-    // (c) Cholesky + inverse (redundant in every CTA), Racc update
-    for (int t = tid; t < ww; t += nt) {
-      const int i = t % w, j = t / w;
-      Gs[i * kL + j] = a.Gg[t];
-    }
-    __syncthreads();
-    const double shift = pass == 0 ? 11.0 * ((double)Mp * w + (double)w * (w + 1)) * 1.1102230246251565e-16 : 0.0;
-    bool zp = false;
-    const bool ok = chol_inv(Gs, Rs, Xs, w, shift, zp);
+    // (c) every CTA: shifted Cholesky + inverse (redundant, no broadcast step)
+    Tile g;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        g.v[i][j] = (bi + i < w && bj + j < w) ? a.Gg[(bi + i) + (bj + j) * w] : 0.0;
+    double tr = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (bi + i == bj + j) tr += g.v[i][j];
+    tr = block_sum(tr, red);
+    const bool zp = (tr == 0.0);
     if (pass == 0) zero = zp;
-    if (!ok && blockIdx.x == 0 && tid == 0) atomicOr(a.status, 2u /* kStCholFail */);
-    // Racc <- R * Racc (pass 0: Racc = R; zero panel: Racc = 0)
-    for (int t = tid; t < ww; t += nt) {
-      const int i = t % w, j = t / w;
-      double v = 0.0;
-      if (zero) {
-        v = 0.0;
-      } else if (pass == 0) {
-        v = Rs[i * kL + j];
-      } else if (i <= j) {
-        for (int k = i; k <= j; ++k) v = fma(Rs[i * kL + k], Ra[k * kL + j], v);
+    if (zp) {
+      for (int t = tid; t < kW * kW; t += nt) {
+        const int r = t >> 6, c = t & 63;
+        Rs[r * kL + c] = (r == c) ? 1.0 : 0.0;
+        Xs[r * kL + c] = (r == c) ? 1.0 : 0.0;
       }
-      Gs[i * kL + j] = v;
+      __syncthreads();
+    } else {
+      if (pass == 0) {
+        const double sh = 11.0 * ((double)Mp * w + (double)w * (w + 1)) * 1.1102230246251565e-16 * tr;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (bi + i == bj + j && bi + i < w) g.v[i][j] += sh;
+      }
+      const bool ok = chol_upper(g, w, Rs, buf);
+      if (!ok && blockIdx.x == 0 && tid == 0) atomicOr(a.status, 2u /* kStCholFail */);
+      Tile x;
+      inv_upper(Rs, w, x, buf);
+      store(x, Xs);
+      __syncthreads();
     }
-    __syncthreads();
-    for (int t = tid; t < ww; t += nt) {
-      const int i = t % w, j = t / w;
-      Ra[i * kL + j] = Gs[i * kL + j];
+    // Racc <- R * Racc (pass 0: Racc = R; zero panel: Racc = 0)
+    {
+      Tile ra;
+      if (zero) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) ra.v[i][j] = 0.0;
+      } else if (pass == 0) {
+        load(ra, Rs, kW);
+      } else {
+        mm(Rs, Ra, w, ra);
+      }
+      __syncthreads();
+      store(ra, Ra);
     }
     // (d) own rows <- rows * R^-1
     for (int64_t c0 = r0; c0 < r1; c0 += kCH) {
@@ -244,86 +214,59 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
   }
   grid_sync(a.bar, G);   // Q = Qa complete (top w rows visible to every CTA)
 
-  // (e) sign-fixing LU of Q_top * D - I (redundant in every CTA)
-  if (tid == 0) s_zero = zero ? 1 : 0;
-  double* q = Gs;   // w x w working copy of Q_top
-  double* L = Rs;
-  double* U = Xs;
-  for (int t = tid; t < kW * kW; t += nt) {
-    const int i = t >> 6, j = t & 63;
-    q[i * kL + j] = (i < w && j < w) ? a.Qa[i + (int64_t)j * Mp] : 0.0;
-    L[i * kL + j] = (i == j) ? 1.0 : 0.0;
-    U[i * kL + j] = 0.0;
-  }
-  __syncthreads();
-  if (!s_zero) {
-    for (int c = 0; c < w; ++c) {
-      const double z = q[c * kL + c];
-      double d;
-      if (fabs(z) == 1.0) d = z > 0.0 ? 1.0 : -1.0;   // identity reflector (tail == 0)
-      else d = z > 0.0 ? -1.0 : 1.0;                  // pivot -(1+|z|) = -tau
-      const double ucc = d * z - 1.0;
-      if (tid == 0) {
-        Dd[c] = d;
-        U[c * kL + c] = ucc;
-      }
-      for (int i = c + 1 + tid; i < w; i += nt) L[i * kL + c] = ucc != 0.0 ? d * q[i * kL + c] / ucc : 0.0;
-      for (int k = tid; k < c; k += nt) U[k * kL + c] = d * q[k * kL + c];
-      __syncthreads();
-      const int tx = tid & 63, ty = tid >> 6, nty = nt >> 6;
-      if (tx > c && tx < w) {
-        const double qc = q[c * kL + tx];
-        for (int i = c + 1 + ty; i < w; i += nty) q[i * kL + tx] -= L[i * kL + c] * qc;
-      }
-      __syncthreads();
-    }
+  // (e) Householder reconstruction (redundant in every CTA)
+  double* Ls = Rs;
+  double* Us = Xs;
+  double* Ui = Cs;
+  double* Li = Ws;
+  if (!zero) {
+    Tile q;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        q.v[i][j] = (bi + i < w && bj + j < w) ? a.Qa[(bi + i) + (int64_t)(bj + j) * Mp] : 0.0;
+    sign_lu(q, w, Ls, Us, Dd, buf);
+    Tile x;
+    inv_upper(Us, w, x, buf);        // zero pivots -> zero row and column
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) x.v[i][j] *= (bi + i < w) ? Dd[bi + i] : 0.0;
+    store(x, Ui);                    // Ui = D * U^-1
+    inv_unit_lower(Ls, w, x, buf);
+    store(x, Li);
+    __syncthreads();
   } else {
-    for (int i = tid; i < w; i += nt) Dd[i] = 1.0;
+    for (int t = tid; t < kW * kW; t += nt) {
+      const int r = t >> 6, c = t & 63;
+      Ls[r * kL + c] = (r == c) ? 1.0 : 0.0;
+      Us[r * kL + c] = 0.0;
+      Ui[r * kL + c] = 0.0;
+      Li[r * kL + c] = (r == c) ? 1.0 : 0.0;
+    }
+    for (int i = tid; i < kW; i += nt) Dd[i] = 1.0;
     __syncthreads();
   }
-  // Ui = D * U^{-1} (into Cs, zero-pivot rule) and T = -U L^{-T} (into Ws)
-  double* Ui = Cs;
-  double* Ts = Ws;
-  {
-    const int i = tid >> 2, sub = tid & 3;
-    for (int c = 0; c < w; ++c) {
-      double a0 = 0.0, a1 = 0.0;
-      if (i < w)
-        for (int k = sub; k < c; k += 4) {
-          a0 = fma(Ui[i * kL + k], U[k * kL + c], a0);
-          a1 = fma(Ts[i * kL + k], L[c * kL + k], a1);
+  if (blockIdx.x == 0) {
+    Tile tt;
+    mm(Us, Li, w, tt, false, true);  // U * L^{-T}; T = -that
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = bi + i, c = bj + j;
+        if (r < w && c < w) {
+          a.T[r + (int64_t)c * a.ldt] = -tt.v[i][j];
+          a.Y[r + (int64_t)c * a.ldy] = Ls[r * kL + c];
+          a.R[r + (int64_t)c * a.ldr] = (r <= c) ? Dd[r] * Ra[r * kL + c] : 0.0;
         }
-      a0 += __shfl_xor_sync(0xffffffffu, a0, 1);
-      a0 += __shfl_xor_sync(0xffffffffu, a0, 2);
-      a1 += __shfl_xor_sync(0xffffffffu, a1, 1);
-      a1 += __shfl_xor_sync(0xffffffffu, a1, 2);
-      if (i < w && sub == 0) {
-        const double ucc = U[c * kL + c];
-        Ui[i * kL + c] = (ucc != 0.0 && !s_zero) ? ((i == c ? 1.0 : 0.0) - a0) / ucc : 0.0;
-        Ts[i * kL + c] = s_zero ? 0.0 : -U[i * kL + c] - a1;
       }
-      __syncthreads();
-    }
-  }
-  // scale rows of Ui by D (Y2 = Q_bottom * D * U^-1)
-  for (int t = tid; t < ww; t += nt) {
-    const int i = t % w, j = t / w;
-    Ui[i * kL + j] *= Dd[i];
   }
   __syncthreads();
-  if (blockIdx.x == 0) {
-    for (int t = tid; t < ww; t += nt) {
-      const int i = t % w, j = t / w;
-      a.Y[i + (int64_t)j * a.ldy] = L[i * kL + j];
-      a.T[i + (int64_t)j * a.ldt] = Ts[i * kL + j];
-      a.R[i + (int64_t)j * a.ldr] = (i <= j) ? Dd[i] * Ra[i * kL + j] : 0.0;
-    }
-  }
   // (f) Y rows >= w: Y = Q * (D U^-1)  (Ui is upper triangular)
   {
     const int64_t y0 = r0 > w ? r0 : w;
-    // Ws is reused as the row stage (Ts no longer needed after CTA 0 wrote it)
-    __syncthreads();
     double* Ys = Ws;
     for (int64_t c0 = y0; c0 < r1; c0 += kCH) {
       const int rows = (int)(r1 - c0 < kCH ? r1 - c0 : kCH);
@@ -338,7 +281,7 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
   }
 }
 
-size_t panel_smem_bytes() { return sizeof(double) * (size_t)(5 * kW * kL + kCH * kL); }
+size_t panel_smem_bytes() { return sizeof(double) * (size_t)(4 * kW * kL + kCH * kL + 256); }
 
 int panel_grid(int sms, int64_t Mp) {
   int64_t g = (Mp + 63) / 64;

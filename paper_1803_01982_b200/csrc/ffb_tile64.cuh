@@ -1,0 +1,247 @@
+// Register-tiled dense kernels for w x w (w <= 64) matrices on one CTA of 256
+// threads: thread t owns the 4x4 tile at rows bi = (t%16)*4, cols bj = (t/16)*4.
+// Each elimination step publishes one row/column through shared memory and
+// synchronises once or twice, so a 64-step factorization costs ~64 barriers and
+// ~16 FMAs per thread per step instead of dependent shared-memory chains.
+//
+// Shared-memory matrices use a padded leading dimension kTL (65 doubles).
+#pragma once
+#include "ffb_common.cuh"
+
+namespace ffb {
+namespace tile64 {
+
+constexpr int kTL = 65;
+
+struct Tile {
+  double v[4][4];
+};
+
+FFB_DEV int bi_of(int tid) { return (tid & 15) * 4; }
+FFB_DEV int bj_of(int tid) { return (tid >> 4) * 4; }
+
+FFB_DEV void load(Tile& t, const double* M, int w, bool ident_pad = false) {
+  const int bi = bi_of(threadIdx.x), bj = bj_of(threadIdx.x);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = bi + i, c = bj + j;
+      t.v[i][j] = (r < w && c < w) ? M[r * kTL + c] : ((ident_pad && r == c) ? 1.0 : 0.0);
+    }
+}
+
+FFB_DEV void store(const Tile& t, double* M) {
+  const int bi = bi_of(threadIdx.x), bj = bj_of(threadIdx.x);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) M[(bi + i) * kTL + bj + j] = t.v[i][j];
+}
+
+FFB_DEV void set_identity(Tile& t) {
+  const int bi = bi_of(threadIdx.x), bj = bj_of(threadIdx.x);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) t.v[i][j] = (bi + i == bj + j) ? 1.0 : 0.0;
+}
+
+// Upper Cholesky R^T R = G (G given as a tile, upper triangle used).  Writes R
+// (full 64x64, zeros elsewhere) to Rs.  buf: >= 2*64 + 2 doubles of scratch.
+// Non-positive pivots are clamped (returns false).
+FFB_DEV bool chol_upper(Tile& g, int w, double* Rs, double* buf) {
+  const int tid = threadIdx.x, bi = bi_of(tid), bj = bj_of(tid);
+  double* row = buf;        // [64] current row of R
+  double* dgl = buf + 64;   // [1] pivot
+  bool ok = true;
+  // zero R outside what we write
+  for (int t = tid; t < 64 * 64; t += blockDim.x) Rs[(t >> 6) * kTL + (t & 63)] = 0.0;
+  for (int j = 0; j < w; ++j) {
+    // publish pivot
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+      if (j == bi + ii) {
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+          if (j == bj + jj) dgl[0] = g.v[ii][jj];
+      }
+    __syncthreads();
+    double d = dgl[0];
+    if (!(d > 0.0) || !isfinite(d)) {
+      ok = false;
+      d = d > 0.0 ? d : 1e-300;
+    }
+    const double rjj = sqrt(d), inv = 1.0 / rjj;
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) {
+      if (j == bi + ii) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int col = bj + c;
+          if (col >= j && col < w) {
+            const double r = (col == j) ? rjj : g.v[ii][c] * inv;
+            row[col] = r;
+            Rs[j * kTL + col] = r;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    double rr[4], rc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      rr[q] = (bi + q > j && bi + q < w) ? row[bi + q] : 0.0;
+      rc[q] = (bj + q > j && bj + q < w) ? row[bj + q] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) g.v[i][c] = fma(-rr[i], rc[c], g.v[i][c]);
+  }
+  __syncthreads();
+  return ok;
+}
+
+// X = R^{-1} for upper-triangular R in Rs (Gauss-Jordan from the bottom, one
+// barrier per step, double-buffered row broadcast).  Zero pivots give zero rows
+// (the reference's identity-reflector / lstsq fallbacks never divide by them).
+FFB_DEV void inv_upper(const double* Rs, int w, Tile& x, double* buf) {
+  const int tid = threadIdx.x, bi = bi_of(tid), bj = bj_of(tid);
+  set_identity(x);
+  for (int i = w - 1; i >= 0; --i) {
+    double* row = buf + (i & 1) * 64;
+    {
+      const double d = Rs[i * kTL + i];
+      const double inv = d != 0.0 ? 1.0 / d : 0.0;
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii)
+        if (i == bi + ii) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            x.v[ii][c] *= inv;
+            row[bj + c] = x.v[ii][c];
+          }
+        }
+    }
+    __syncthreads();
+    double rk[4], xr[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      rk[q] = (bi + q < i) ? Rs[(bi + q) * kTL + i] : 0.0;
+      xr[q] = row[bj + q];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) x.v[k][c] = fma(-rk[k], xr[c], x.v[k][c]);
+  }
+  __syncthreads();
+}
+
+// X = L^{-1} for unit-lower-triangular L in Ls (forward Gauss-Jordan).
+FFB_DEV void inv_unit_lower(const double* Ls, int w, Tile& x, double* buf) {
+  const int tid = threadIdx.x, bi = bi_of(tid), bj = bj_of(tid);
+  set_identity(x);
+  for (int i = 0; i < w; ++i) {
+    double* row = buf + (i & 1) * 64;
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+      if (i == bi + ii) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) row[bj + c] = x.v[ii][c];
+      }
+    __syncthreads();
+    double lk[4], xr[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      lk[q] = (bi + q > i && bi + q < w) ? Ls[(bi + q) * kTL + i] : 0.0;
+      xr[q] = row[bj + q];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) x.v[k][c] = fma(-lk[k], xr[c], x.v[k][c]);
+  }
+  __syncthreads();
+}
+
+// C = op(A) * op(B) (op = transpose when ta / tb) with A, B in shared memory (kTL).
+FFB_DEV void mm(const double* A, const double* B, int w, Tile& c, bool ta = false, bool tb = false) {
+  const int tid = threadIdx.x, bi = bi_of(tid), bj = bj_of(tid);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) c.v[i][j] = 0.0;
+  for (int k = 0; k < w; ++k) {
+    double a[4], b[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      a[q] = ta ? A[k * kTL + bi + q] : A[(bi + q) * kTL + k];
+      b[q] = tb ? B[(bj + q) * kTL + k] : B[k * kTL + bj + q];
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c.v[i][j] = fma(a[i], b[j], c.v[i][j]);
+  }
+}
+
+// LU without pivoting of Q_top * D - I with the Householder sign rule (see
+// ffb_panel.cu): q tile in, L (unit lower) and U (upper) to Ls/Us, D to Dd.
+FFB_DEV void sign_lu(Tile& q, int w, double* Ls, double* Us, double* Dd, double* buf) {
+  const int tid = threadIdx.x, bi = bi_of(tid), bj = bj_of(tid);
+  for (int t = tid; t < 64 * 64; t += blockDim.x) {
+    const int r = t >> 6, c = t & 63;
+    Ls[r * kTL + c] = (r == c) ? 1.0 : 0.0;
+    Us[r * kTL + c] = 0.0;
+  }
+  __syncthreads();
+  for (int c = 0; c < w; ++c) {
+    double* col = buf + (c & 1) * 128;      // column c of the working matrix
+    double* rowc = col + 64;                // row c of the working matrix
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj)
+      if (c == bj + jj) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) col[bi + i] = q.v[i][jj];
+      }
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+      if (c == bi + ii) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) rowc[bj + j] = q.v[ii][j];
+      }
+    __syncthreads();
+    const double z = col[c];
+    double d;
+    if (fabs(z) == 1.0) d = z > 0.0 ? 1.0 : -1.0;   // identity reflector (tail == 0)
+    else d = z > 0.0 ? -1.0 : 1.0;                  // pivot -(1+|z|) = -tau
+    const double ucc = d * z - 1.0;
+    const double sc = ucc != 0.0 ? d / ucc : 0.0;
+    if (tid < 64) {
+      const int r = tid;
+      if (r < c) Us[r * kTL + c] = d * col[r];
+      else if (r == c) {
+        Us[c * kTL + c] = ucc;
+        Dd[c] = d;
+      } else if (r < w) {
+        Ls[r * kTL + c] = sc * col[r];
+      }
+    }
+    double li[4], rj[4];
+#pragma unroll
+    for (int q2 = 0; q2 < 4; ++q2) {
+      li[q2] = (bi + q2 > c && bi + q2 < w) ? sc * col[bi + q2] : 0.0;
+      rj[q2] = (bj + q2 > c && bj + q2 < w) ? rowc[bj + q2] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) q.v[i][j] = fma(-li[i], rj[j], q.v[i][j]);
+  }
+  __syncthreads();
+}
+
+}  // namespace tile64
+}  // namespace ffb
