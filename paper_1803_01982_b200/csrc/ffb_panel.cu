@@ -54,25 +54,72 @@ FFB_DEV void grid_sync(uint32_t* bar, uint32_t nblocks) {
   __syncthreads();
 }
 
-// out(rows x w) = in(rows x w) * Xs (upper triangular), chunk in smem (Cs),
-// result written to global dst (ld ldd).  256 threads: thread -> (row, 16 cols).
-FFB_DEV void apply_upper(const double* Cs, int rows, int w, const double* Xs, double* dst,
-                         int64_t ldd, int64_t row0) {
-  const int tid = threadIdx.x;
-  for (int t = tid; t < rows * 4; t += blockDim.x) {
-    const int r = t >> 2, cg = (t & 3) * 16;
-    double acc[16];
+// Stage rows [c0, c0+rows) of src (ld lds) into Cs (kCH x kL), zero padding for
+// rows >= rows (to a multiple of 4) and columns >= w, so DMMA tiles see zeros.
+FFB_DEV void load_chunk(double* Cs, const double* src, int64_t lds, int64_t c0, int rows, int w) {
+  const int rows4 = (rows + 3) & ~3;
+  for (int t = threadIdx.x; t < rows4 * kW; t += blockDim.x) {
+    const int rr = t % rows4, cc = t / rows4;
+    Cs[rr * kL + cc] = (rr < rows && cc < w) ? src[(c0 + rr) + (int64_t)cc * lds] : 0.0;
+  }
+}
+
+// Warp tile of a 64 x 64 product: warp -> rows 16*(warp/2)..+16, cols 32*(warp%2)..+32.
+struct Acc64 {
+  double c[2][4][2];
+};
+
+FFB_DEV void acc_zero(Acc64& a) {
 #pragma unroll
-    for (int q = 0; q < 16; ++q) acc[q] = 0.0;
-    for (int k = 0; k < w; ++k) {
-      const double x = Cs[r * kL + k];
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int q = 0; q < 16; ++q) acc[q] = fma(x, Xs[k * kL + cg + q], acc[q]);
+    for (int j = 0; j < 4; ++j) a.c[i][j][0] = a.c[i][j][1] = 0.0;
+}
+
+// acc += A(64 x K) * B(K x 64); A(i,k) = at ? A[k*kL + i] : A[i*kL + k]; B(k,j) = B[k*kL + j].
+FFB_DEV void dmma64(Acc64& acc, const double* A, bool at, const double* B, int K) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;
+  const int fr = lane >> 2, fk = lane & 3;
+  for (int k0 = 0; k0 < K; k0 += 4) {
+    double af[2], bf[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int r = r0 + 8 * i + fr, k = k0 + fk;
+      af[i] = at ? A[k * kL + r] : A[r * kL + k];
     }
 #pragma unroll
-    for (int q = 0; q < 16; ++q)
-      if (cg + q < w) dst[(row0 + r) + (int64_t)(cg + q) * ldd] = acc[q];
+    for (int j = 0; j < 4; ++j) bf[j] = B[(k0 + fk) * kL + c0 + 8 * j + fr];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_884(acc.c[i][j][0], acc.c[i][j][1], af[i], bf[j]);
   }
+}
+
+// Write rows < rows, cols < w of the accumulator to global dst (row offset row0).
+FFB_DEV void acc_store_global(const Acc64& acc, double* dst, int64_t ldd, int64_t row0, int rows,
+                              int w) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = r0 + 8 * i + (lane >> 2), c = c0 + 8 * j + 2 * (lane & 3) + h;
+        if (r < rows && c < w) dst[(row0 + r) + (int64_t)c * ldd] = acc.c[i][j][h];
+      }
+}
+
+// rows x w chunk in Cs times upper-triangular Xs (w x w) -> global dst
+FFB_DEV void apply_upper(const double* Cs, int rows, int w, const double* Xs, double* dst,
+                         int64_t ldd, int64_t row0) {
+  Acc64 acc;
+  acc_zero(acc);
+  dmma64(acc, Cs, false, Xs, (w + 3) & ~3);
+  acc_store_global(acc, dst, ldd, row0, rows, w);
 }
 
 }  // namespace
@@ -100,39 +147,17 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
     const double* src = pass == 0 ? a.X : (pass == 1 ? a.Qa : a.Qb);
     const int64_t lds = pass == 0 ? a.ldx : Mp;
     double* dst = pass == 1 ? a.Qb : a.Qa;
-    // (a) local Gram of rows [r0, r1)
-    Tile acc;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc.v[i][j] = 0.0;
+    // (a) local Gram of rows [r0, r1) on DMMA (Cs^T Cs per staged chunk)
+    Acc64 gacc;
+    acc_zero(gacc);
     for (int64_t c0 = r0; c0 < r1; c0 += kCH) {
       const int rows = (int)(r1 - c0 < kCH ? r1 - c0 : kCH);
       __syncthreads();
-      for (int t = tid; t < rows * w; t += nt) {
-        const int r = t % rows, c = t / rows;
-        Cs[r * kL + c] = src[(c0 + r) + (int64_t)c * lds];
-      }
+      load_chunk(Cs, src, lds, c0, rows, w);
       __syncthreads();
-      for (int r = 0; r < rows; ++r) {
-        double x[4], y[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          x[i] = Cs[r * kL + bi + i];
-          y[i] = Cs[r * kL + bj + i];
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc.v[i][j] = fma(x[i], y[j], acc.v[i][j]);
-      }
+      dmma64(gacc, Cs, true, Cs, (rows + 3) & ~3);
     }
-    double* mypart = a.part + (size_t)blockIdx.x * ww;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (bi + i < w && bj + j < w) mypart[(bi + i) + (bj + j) * w] = acc.v[i][j];
+    acc_store_global(gacc, a.part + (size_t)blockIdx.x * ww, w, 0, w, w);
     grid_sync(a.bar, G);
     // (b) distributed fixed-order reduction
     {
@@ -161,12 +186,62 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
     tr = block_sum(tr, red);
     const bool zp = (tr == 0.0);
     if (pass == 0) zero = zp;
+    // passes 1, 2: G = I + E; when |E| is small use R = I + triu(E,1) + diag(E)/2
+    // (error O(|E|^2)) and R^-1 = I - F + F^2 - F^3 (Neumann, F = R - I): no
+    // sequential factorization.  R stays upper triangular and X = Q R holds exactly.
+    bool first_order = false;
+    if (pass > 0 && !zp) {
+      double em = 0.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (bi + i < w && bj + j < w) em = fmax(em, fabs(g.v[i][j] - (bi + i == bj + j ? 1.0 : 0.0)));
+      em = warp_max(em);
+      __syncthreads();
+      if ((tid & 31) == 0) red[tid >> 5] = em;
+      __syncthreads();
+      em = 0.0;
+      for (int q = 0; q < (nt >> 5); ++q) em = fmax(em, red[q]);
+      __syncthreads();
+      first_order = em <= 1e-5;
+    }
     if (zp) {
       for (int t = tid; t < kW * kW; t += nt) {
         const int r = t >> 6, c = t & 63;
         Rs[r * kL + c] = (r == c) ? 1.0 : 0.0;
         Xs[r * kL + c] = (r == c) ? 1.0 : 0.0;
       }
+      __syncthreads();
+    } else if (first_order) {
+      // F into Rs (strict upper of E, half diagonal), then R^-1 = I - F + F^2 - F^3
+      Tile f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = bi + i, c = bj + j;
+          f.v[i][j] = (r < w && c < w) ? (r < c ? g.v[i][j] : (r == c ? 0.5 * (g.v[i][j] - 1.0) : 0.0)) : 0.0;
+        }
+      store(f, Rs);
+      __syncthreads();
+      Tile f2, f3;
+      mm(Rs, Rs, w, f2);
+      store(f2, Xs);
+      __syncthreads();
+      mm(Xs, Rs, w, f3);
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = bi + i, c = bj + j;
+          const double id = (r == c && r < w) ? 1.0 : 0.0;
+          f2.v[i][j] = id - f.v[i][j] + f2.v[i][j] - f3.v[i][j];   // R^-1
+          f.v[i][j] = id + f.v[i][j];                              // R
+        }
+      store(f2, Xs);
+      store(f, Rs);
       __syncthreads();
     } else {
       if (pass == 0) {
@@ -204,10 +279,7 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
     for (int64_t c0 = r0; c0 < r1; c0 += kCH) {
       const int rows = (int)(r1 - c0 < kCH ? r1 - c0 : kCH);
       __syncthreads();
-      for (int t = tid; t < rows * w; t += nt) {
-        const int r = t % rows, c = t / rows;
-        Cs[r * kL + c] = src[(c0 + r) + (int64_t)c * lds];
-      }
+      load_chunk(Cs, src, lds, c0, rows, w);
       __syncthreads();
       apply_upper(Cs, rows, w, Xs, dst, Mp, c0);
     }
@@ -271,10 +343,7 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
     for (int64_t c0 = y0; c0 < r1; c0 += kCH) {
       const int rows = (int)(r1 - c0 < kCH ? r1 - c0 : kCH);
       __syncthreads();
-      for (int t = tid; t < rows * w; t += nt) {
-        const int r = t % rows, c = t / rows;
-        Ys[r * kL + c] = a.Qa[(c0 + r) + (int64_t)c * Mp];
-      }
+      load_chunk(Ys, a.Qa, Mp, c0, rows, w);
       __syncthreads();
       apply_upper(Ys, rows, w, Ui, a.Y, a.ldy, c0);
     }
