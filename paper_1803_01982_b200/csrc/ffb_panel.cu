@@ -57,9 +57,10 @@ FFB_DEV void grid_sync(uint32_t* bar, uint32_t nblocks) {
 // Stage rows [c0, c0+rows) of src (ld lds) into Cs (kCH x kL), zero padding for
 // rows >= rows (to a multiple of 4) and columns >= w, so DMMA tiles see zeros.
 FFB_DEV void load_chunk(double* Cs, const double* src, int64_t lds, int64_t c0, int rows, int w) {
-  const int rows4 = (rows + 3) & ~3;
-  for (int t = threadIdx.x; t < rows4 * kW; t += blockDim.x) {
-    const int rr = t % rows4, cc = t / rows4;
+  // kCH == 64: thread -> (row = t & 63, col = t >> 6); consecutive threads read
+  // consecutive rows of one column (coalesced), no integer division
+  for (int t = threadIdx.x; t < kCH * kW; t += blockDim.x) {
+    const int rr = t & 63, cc = t >> 6;
     Cs[rr * kL + cc] = (rr < rows && cc < w) ? src[(c0 + rr) + (int64_t)cc * lds] : 0.0;
   }
 }
@@ -76,8 +77,9 @@ FFB_DEV void acc_zero(Acc64& a) {
     for (int j = 0; j < 4; ++j) a.c[i][j][0] = a.c[i][j][1] = 0.0;
 }
 
-// acc += A(64 x K) * B(K x 64); A(i,k) = at ? A[k*kL + i] : A[i*kL + k]; B(k,j) = B[k*kL + j].
-FFB_DEV void dmma64(Acc64& acc, const double* A, bool at, const double* B, int K) {
+// acc += A(64 x K) * B(K x 64); A(i,k) = at ? A[k*kL + i] : A[i*kL + k];
+// B(k,j) = bt ? B[j*kL + k] : B[k*kL + j].
+FFB_DEV void dmma64(Acc64& acc, const double* A, bool at, const double* B, int K, bool bt = false) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;
   const int fr = lane >> 2, fk = lane & 3;
@@ -89,7 +91,8 @@ FFB_DEV void dmma64(Acc64& acc, const double* A, bool at, const double* B, int K
       af[i] = at ? A[k * kL + r] : A[r * kL + k];
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) bf[j] = B[(k0 + fk) * kL + c0 + 8 * j + fr];
+    for (int j = 0; j < 4; ++j)
+      bf[j] = bt ? B[(c0 + 8 * j + fr) * kL + k0 + fk] : B[(k0 + fk) * kL + c0 + 8 * j + fr];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -111,6 +114,30 @@ FFB_DEV void acc_store_global(const Acc64& acc, double* dst, int64_t ldd, int64_
         const int r = r0 + 8 * i + (lane >> 2), c = c0 + 8 * j + 2 * (lane & 3) + h;
         if (r < rows && c < w) dst[(row0 + r) + (int64_t)c * ldd] = acc.c[i][j][h];
       }
+}
+
+// C (smem, 64 x 64 padded) = scale * accumulator
+FFB_DEV void acc_store_smem(const Acc64& acc, double* C, double scale) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = r0 + 8 * i + (lane >> 2), c = c0 + 8 * j + 2 * (lane & 3) + h;
+        C[r * kL + c] = scale * acc.c[i][j][h];
+      }
+}
+
+// C = scale * op(A) op(B) for 64 x 64 shared-memory matrices (DMMA)
+FFB_DEV void mm_smem(const double* A, bool at, const double* B, bool bt, int K, double* C,
+                     double scale) {
+  Acc64 acc;
+  acc_zero(acc);
+  dmma64(acc, A, at, B, (K + 3) & ~3, bt);
+  acc_store_smem(acc, C, scale);
 }
 
 // rows x w chunk in Cs times upper-triangular Xs (w x w) -> global dst
@@ -225,23 +252,27 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
         }
       store(f, Rs);
       __syncthreads();
-      Tile f2, f3;
-      mm(Rs, Rs, w, f2);
-      store(f2, Xs);
+      mm_smem(Rs, false, Rs, false, w, Ws, 1.0);     // F^2
       __syncthreads();
-      mm(Xs, Rs, w, f3);
+      mm_smem(Ws, false, Rs, false, w, Xs, 1.0);     // F^3
       __syncthreads();
+      {
+        Tile f2, f3;
+        load(f2, Ws, kW);
+        load(f3, Xs, kW);
+        __syncthreads();
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int r = bi + i, c = bj + j;
-          const double id = (r == c && r < w) ? 1.0 : 0.0;
-          f2.v[i][j] = id - f.v[i][j] + f2.v[i][j] - f3.v[i][j];   // R^-1
-          f.v[i][j] = id + f.v[i][j];                              // R
-        }
-      store(f2, Xs);
-      store(f, Rs);
+          for (int j = 0; j < 4; ++j) {
+            const int r = bi + i, c = bj + j;
+            const double id = (r == c && r < w) ? 1.0 : 0.0;
+            f2.v[i][j] = id - f.v[i][j] + f2.v[i][j] - f3.v[i][j];   // R^-1
+            f.v[i][j] = id + f.v[i][j];                              // R
+          }
+        store(f2, Xs);
+        store(f, Rs);
+      }
       __syncthreads();
     } else {
       if (pass == 0) {
@@ -259,21 +290,15 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
       store(x, Xs);
       __syncthreads();
     }
-    // Racc <- R * Racc (pass 0: Racc = R; zero panel: Racc = 0)
-    {
-      Tile ra;
-      if (zero) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) ra.v[i][j] = 0.0;
-      } else if (pass == 0) {
-        load(ra, Rs, kW);
-      } else {
-        mm(Rs, Ra, w, ra);
-      }
+    // Racc <- R * Racc (pass 0: Racc = R; zero panel: Racc = 0), DMMA via Ws
+    if (zero) {
+      for (int t = tid; t < kW * kW; t += nt) Ra[(t >> 6) * kL + (t & 63)] = 0.0;
+    } else if (pass == 0) {
+      for (int t = tid; t < kW * kW; t += nt) Ra[(t >> 6) * kL + (t & 63)] = Rs[(t >> 6) * kL + (t & 63)];
+    } else {
+      mm_smem(Rs, false, Ra, false, w, Ws, 1.0);
       __syncthreads();
-      store(ra, Ra);
+      for (int t = tid; t < kW * kW; t += nt) Ra[(t >> 6) * kL + (t & 63)] = Ws[(t >> 6) * kL + (t & 63)];
     }
     // (d) own rows <- rows * R^-1
     for (int64_t c0 = r0; c0 < r1; c0 += kCH) {
@@ -321,19 +346,22 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
     __syncthreads();
   }
   if (blockIdx.x == 0) {
-    Tile tt;
-    mm(Us, Li, w, tt, false, true);  // U * L^{-T}; T = -that
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int r = bi + i, c = bj + j;
-        if (r < w && c < w) {
-          a.T[r + (int64_t)c * a.ldt] = -tt.v[i][j];
-          a.Y[r + (int64_t)c * a.ldy] = Ls[r * kL + c];
-          a.R[r + (int64_t)c * a.ldr] = (r <= c) ? Dd[r] * Ra[r * kL + c] : 0.0;
-        }
-      }
+    // T = -U L^{-T}  (DMMA, into Ws is not possible: Ws holds Li) -> use Ra's
+    // neighbour?  Ra is still needed for R; compute into registers per warp tile.
+    Acc64 tacc;
+    acc_zero(tacc);
+    dmma64(tacc, Us, false, Li, (w + 3) & ~3, true);
+    acc_store_global(tacc, a.T, a.ldt, 0, w, w);
+    // T = -(U L^{-T}): negate in place below after a barrier
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) {
+    for (int t = tid; t < ww; t += nt) {
+      const int r = t % w, c = t / w;
+      a.T[r + (int64_t)c * a.ldt] = -a.T[r + (int64_t)c * a.ldt];
+      a.Y[r + (int64_t)c * a.ldy] = Ls[r * kL + c];
+      a.R[r + (int64_t)c * a.ldr] = (r <= c) ? Dd[r] * Ra[r * kL + c] : 0.0;
+    }
   }
   __syncthreads();
   // (f) Y rows >= w: Y = Q * (D U^-1)  (Ui is upper triangular)
