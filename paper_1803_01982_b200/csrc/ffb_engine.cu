@@ -146,7 +146,7 @@ size_t carve(const ffb_ctx* ctx, const Dims& D, void* base, size_t cap, Work& w)
   w.flags = b.take<uint32_t>(w.G);
   w.hist = b.take<int64_t>(max_i(D.b, 1));
   w.gap = b.take<double>(max_i(l, 1));
-  w.pwork = w.piv_smem ? nullptr : b.take<double>((size_t)w.G * s * w.cpc);
+  w.pwork = w.piv_smem ? nullptr : b.take<double>((size_t)w.G * pivots_stride((int)s) * w.cpc);
   w.r = b.take<double>(n);
   w.rinit = b.take<double>(n);
   w.u = b.take<double>(m);
@@ -273,6 +273,7 @@ bool validate(const Dims& D) {
   if (D.d < 1 || D.d > D.l) return false;
   if (D.mode != FFB_MODE_TRQRCP && D.l + 1 > std::min(D.m, D.n)) return false;
   if (D.b > 64) return false;  // panel kernels are sized for b <= 64
+  if (D.s > 128) return false; // pivot kernel holds one sketch column per warp (s <= 128)
   return true;
 }
 
@@ -342,12 +343,12 @@ int ffb_block_pivots(ffb_ctx* ctx, void* stream, const double* B, int64_t s, int
   w.slotdata = b.take<double>(2 * (size_t)w.G * s);
   w.flags = b.take<uint32_t>(w.G);
   w.hist = b.take<int64_t>(bb);
-  w.pwork = w.piv_smem ? nullptr : b.take<double>((size_t)w.G * s * w.cpc);
+  w.pwork = w.piv_smem ? nullptr : b.take<double>((size_t)w.G * pivots_stride((int)s) * w.cpc);
   if (!b.ok) return fail(ctx, FFB_ERR_ARGUMENT, "workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(w.flags, 0, sizeof(uint32_t) * w.G, st);
-  PivotArgs a{B, ldb, (int)s, n, j0, (int)bb, arr, pos, w.G, w.cpc, w.pwork, w.slots, w.slotdata,
-              w.flags, w.hist, gap};
+  PivotArgs a{B, ldb, (int)s, n, j0, (int)bb, arr, pos, w.G, w.cpc, 0, w.pwork, w.slots,
+              w.slotdata, w.flags, w.hist, gap};
   if (e == cudaSuccess) {
     static bool attr[2] = {false, false};
     if (!attr[w.piv_smem]) {
@@ -425,8 +426,8 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
     const int64_t bb = std::min<int64_t>(D.b, l - j0), e1 = j0 + bb;
     // (K2) pivots on the sketch
     e.ok(cudaMemsetAsync(w.flags, 0, sizeof(uint32_t) * w.G, st));
-    PivotArgs pa{w.B, s, (int)s, n, j0, (int)bb, w.arr, w.pos, w.G, w.cpc, w.pwork, w.slots,
-                 w.slotdata, w.flags, w.hist, w.gap + j0};
+    PivotArgs pa{w.B, s, (int)s, n, j0, (int)bb, w.arr, w.pos, w.G, w.cpc, 0, w.pwork, w.slots,
+                 w.slotdata, w.flags, w.hist, out->pivot_gap ? w.gap + j0 : nullptr};
     e.ok(launch_pivots(st, pa, w.piv_smem, w.piv_smem_bytes));
     // (K4) panel P = A[:, piv] - Y[:, :j0] WT[:j0, piv]
     e.ok(launch_gather_cols(st, A, lda, m, w.arr + j0, bb, w.P, m));

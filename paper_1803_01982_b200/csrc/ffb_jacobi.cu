@@ -1,21 +1,33 @@
 // Small dense SVD (K14): one-sided block Jacobi (Hestenes) on the l x l
 // triangular factor of tmp = A P Qhat_1 — replaces LAPACK dgesdd
-// (ffsrqr/svd.py:79).  One-sided Jacobi on a triangular factor gives singular
-// values to high RELATIVE accuracy, which the 1e-10 parity bound needs for the
-// small end of the spectrum (a Gram-matrix eigensolver would lose u*kappa^2).
+// (ffsrqr/svd.py:79).  One-sided Jacobi gives singular values to high RELATIVE
+// accuracy, which the 1e-10 parity bound needs at the small end of the spectrum.
 //
-// Cooperative persistent kernel: the columns are split into nb (even) blocks of
-// <= bs columns; each outer round, CTA p takes one block pair of a round-robin
-// tournament, stages its 2*bs columns of M and of the accumulated V in shared
-// memory, runs one inner cyclic sweep (2bs-1 parallel rounds, one warp per
-// column pair) and writes them back; a grid barrier separates rounds.  Sweeps
-// stop when the largest |x^T y| / (||x|| ||y||) seen in a sweep is <= tol.
+// Cooperative persistent kernel.  Columns are split into nb (even) blocks of bs
+// columns; each outer round, CTA p takes one block pair of a round-robin
+// tournament (W = 2 bs <= 64 local columns) and
+//   1. forms the fresh W x W Gram G = M_W^T M_W on DMMA (64-row chunks staged in
+//      shared memory) — the convergence test reads |G_ij| / sqrt(G_ii G_jj);
+//   2. diagonalizes the cross-block part with two-sided Jacobi rotations on G
+//      (16-32 disjoint pairs per round, one barrier pair per round), accumulating
+//      the W x W orthogonal J (within-block pairs once per sweep);
+//   3. applies M_W <- M_W J and V_W <- V_W J with DMMA.
+// Each visit re-measures G from the actual columns, so rounding in the small
+// two-sided iteration never accumulates into the factorization.  A grid barrier
+// separates rounds; sweeps stop when max |cos| seen in a sweep <= tol.
 #include <math.h>
 
 #include "ffb_common.cuh"
 #include "ffb_jacobi.cuh"
 
 namespace ffb {
+
+namespace {
+
+constexpr int kJW = 64;        // max local columns
+constexpr int kJL = kJW + 1;   // smem leading dimension
+constexpr int kJCH = 64;       // rows per staged chunk
+constexpr int kJThreads = 256;
 
 FFB_DEV uint32_t ld_acq(const uint32_t* p) {
   uint32_t v;
@@ -52,156 +64,229 @@ FFB_DEV int rr_player(int pos, int r, int nb) {
   return ((pos - 1 + r) % (nb - 1)) + 1;
 }
 
-// One Hestenes rotation of local columns x, y (M and V), warp-cooperative.  The
-// pair is loaded into registers in one burst (NPL elements per lane, fully
-// unrolled), rotated there and stored back, so a round costs one shared-memory
-// latency instead of a dependent chain.  nrm[] caches squared column norms.
-template <int NPL>
-FFB_DEV void jacobi_pair(double* Ms, double* Vs, double* nrm, int l, int x, int y, double tol,
-                         int lane, double& off) {
-  double* mx = Ms + (size_t)x * l;
-  double* my = Ms + (size_t)y * l;
-  double* vx = Vs + (size_t)x * l;
-  double* vy = Vs + (size_t)y * l;
-  double X[NPL], Yv[NPL];
-#pragma unroll
-  for (int q = 0; q < NPL; ++q) {
-    const int i = lane + 32 * q;
-    X[q] = i < l ? mx[i] : 0.0;
-    Yv[q] = i < l ? my[i] : 0.0;
-  }
-  double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-  for (int q = 0; q < NPL; q += 2) {
-    c0 = fma(X[q], Yv[q], c0);
-    if (q + 1 < NPL) c1 = fma(X[q + 1], Yv[q + 1], c1);
-  }
-  const double c = warp_sum(c0 + c1);
-  const double a = nrm[x], b = nrm[y];
-  const double ab = sqrt(a * b);
-  if (!(fabs(c) > tol * ab)) return;
-  off = fmax(off, fabs(c) / ab);
-  // rotation angle: only cs^2 + sn^2 = 1 must be exact; t itself may be approximate
-  // (it only sets how much of x^T y is removed in this step).
-  const double zeta = (b - a) / (2.0 * c);
-  double t;
-  if (fabs(zeta) > 1e15) {
-    t = 0.5 / zeta;
-  } else {
-    const float zf = (float)zeta;
-    t = (double)(copysignf(1.0f, zf) / (fabsf(zf) + sqrtf(1.0f + zf * zf)));
-  }
-  const double cs = rsqrt(1.0 + t * t), sn = cs * t;
-  double P[NPL], Q[NPL];
-#pragma unroll
-  for (int q = 0; q < NPL; ++q) {
-    const int i = lane + 32 * q;
-    P[q] = i < l ? vx[i] : 0.0;
-    Q[q] = i < l ? vy[i] : 0.0;
-  }
-#pragma unroll
-  for (int q = 0; q < NPL; ++q) {
-    const int i = lane + 32 * q;
-    if (i < l) {
-      mx[i] = cs * X[q] - sn * Yv[q];
-      my[i] = sn * X[q] + cs * Yv[q];
-      vx[i] = cs * P[q] - sn * Q[q];
-      vy[i] = sn * P[q] + cs * Q[q];
-    }
-  }
-  if (lane == 0) {
-    const double cc = cs * cs, ss = sn * sn, cscs = 2.0 * cs * sn * c;
-    nrm[x] = cc * a - cscs + ss * b;
-    nrm[y] = ss * a + cscs + cc * b;
+// Stage rows [r0, r0 + kJCH) of the W local columns of X (ld ldx) into Cs
+// (kJCH x kJL, row-major), zero beyond l / W.
+FFB_DEV void stage(double* Cs, const double* X, int64_t ldx, const int* gcol, int r0, int l) {
+  for (int t = threadIdx.x; t < kJCH * kJW; t += blockDim.x) {
+    const int rr = t & 63, cc = t >> 6;
+    const int c = gcol[cc], row = r0 + rr;
+    Cs[rr * kJL + cc] = (c >= 0 && row < l) ? X[row + (int64_t)c * ldx] : 0.0;
   }
 }
 
-template <int NPL>
-__global__ void __launch_bounds__(NPL >= 8 ? 512 : 1024) jacobi_kernel(JacobiArgs a) {
+// warp tile of a 64x64 DMMA product (8 warps): rows 16*(w/2).., cols 32*(w%2)..
+struct JAcc {
+  double c[2][4][2];
+};
+
+FFB_DEV void jacc_zero(JAcc& a) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a.c[i][j][0] = a.c[i][j][1] = 0.0;
+}
+
+// acc += op(A)(64 x K) * B(K x 64), A(i,k) = at ? A[k*kJL+i] : A[i*kJL+k], B(k,j) = B[k*kJL+j]
+FFB_DEV void jdmma(JAcc& acc, const double* A, bool at, const double* B, int K) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;
+  const int fr = lane >> 2, fk = lane & 3;
+  for (int k0 = 0; k0 < K; k0 += 4) {
+    double af[2], bf[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int r = r0 + 8 * i + fr, k = k0 + fk;
+      af[i] = at ? A[k * kJL + r] : A[r * kJL + k];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bf[j] = B[(k0 + fk) * kJL + c0 + 8 * j + fr];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_884(acc.c[i][j][0], acc.c[i][j][1], af[i], bf[j]);
+  }
+}
+
+FFB_DEV void jacc_store_smem(const JAcc& acc, double* C) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        C[(r0 + 8 * i + (lane >> 2)) * kJL + c0 + 8 * j + 2 * (lane & 3) + h] = acc.c[i][j][h];
+}
+
+// write rows r0.. (< l) of the chunk product to X's local columns
+FFB_DEV void jacc_store_cols(const JAcc& acc, double* X, int64_t ldx, const int* gcol, int r0,
+                             int l) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rb = (warp >> 1) * 16, cb = (warp & 1) * 32;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = r0 + rb + 8 * i + (lane >> 2), cc = cb + 8 * j + 2 * (lane & 3) + h;
+        const int c = gcol[cc];
+        if (c >= 0 && row < l) X[row + (int64_t)c * ldx] = acc.c[i][j][h];
+      }
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
   extern __shared__ __align__(16) double sm[];
-  const int l = a.l, bs = a.bs, nb = a.nb;
-  const int W = 2 * bs;                 // local column slots: [0,bs) block A, [bs,2bs) block B
-  double* Ms = sm;                      // [W][l]
-  double* Vs = sm + (size_t)W * l;      // [W][l]
-  __shared__ int gcol[64];              // global column of each local slot (-1 = empty)
-  __shared__ double nrm[64];
+  double* Gs = sm;                 // W x W Gram (two-sided Jacobi working copy)
+  double* Js = Gs + kJW * kJL;     // accumulated rotation J
+  double* Cs = Js + kJW * kJL;     // staged row chunk
+  __shared__ int gcol[kJW];
+  __shared__ double rc[kJW / 2], rs[kJW / 2];   // rotation (cos, sin) per pair this round
+  __shared__ int rp[kJW / 2], rq[kJW / 2];      // pair columns (local), -1 = none
   __shared__ double s_off;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int l = a.l, bs = a.bs, nb = a.nb, W = 2 * bs;
+  const int tid = threadIdx.x, nt = blockDim.x;
   const int P = gridDim.x;
-  uint32_t* bar = a.bar;
+  const double tol = a.tol;
 
   for (int sweep = 0; sweep < a.max_sweeps; ++sweep) {
     if (tid == 0) s_off = 0.0;
     for (int r = 0; r < nb - 1; ++r) {
       const int pa = rr_player(blockIdx.x, r, nb), pb = rr_player(nb - 1 - blockIdx.x, r, nb);
-      if (tid < W) {
-        const int blk = tid < bs ? pa : pb;
-        const int c = blk * bs + (tid < bs ? tid : tid - bs);
-        gcol[tid] = (c < l) ? c : -1;
-      }
-      __syncthreads();
-      for (int idx = tid; idx < W * l; idx += blockDim.x) {
-        const int j = idx / l, i = idx - j * l;
-        const int c = gcol[j];
-        Ms[idx] = c >= 0 ? a.M[i + (int64_t)c * a.ldm] : 0.0;
-        Vs[idx] = c >= 0 ? a.V[i + (int64_t)c * a.ldv] : 0.0;
-      }
-      __syncthreads();
-      for (int j = warp; j < W; j += nwarps) {
-        const double* mc = Ms + (size_t)j * l;
-        double acc = 0.0;
-        for (int i = lane; i < l; i += 32) acc = fma(mc[i], mc[i], acc);
-        acc = warp_sum(acc);
-        if (lane == 0) nrm[j] = acc;
-      }
-      __syncthreads();
-      double off = 0.0;
-      if (r == 0) {
-        // within-block pairs of both staged blocks, once per sweep (circle method,
-        // bs' = bs rounded up to even; pairs touching a phantom slot are skipped)
-        const int be = bs + (bs & 1);
-        for (int t = 0; t < be - 1; ++t) {
-          for (int pr = warp; pr < be; pr += nwarps) {       // be/2 pairs per block
-            const int blk = pr < be / 2 ? 0 : 1;
-            const int q = pr - blk * (be / 2);
-            const int xl = rr_player(q, t, be), yl = rr_player(be - 1 - q, t, be);
-            if (xl >= bs || yl >= bs) continue;
-            const int x = blk * bs + xl, y = blk * bs + yl;
-            if (gcol[x] < 0 || gcol[y] < 0) continue;
-            jacobi_pair<NPL>(Ms, Vs, nrm, l, x, y, a.tol, lane, off);
-          }
-          __syncthreads();
+      if (tid < kJW) {
+        int c = -1;
+        if (tid < W) {
+          const int blk = tid < bs ? pa : pb;
+          c = blk * bs + (tid < bs ? tid : tid - bs);
+          if (c >= l) c = -1;
         }
+        gcol[tid] = c;
       }
-      // cross pairs: bs rounds, warp i pairs A_i with B_{(i+t) mod bs}
-      for (int t = 0; t < bs; ++t) {
-        for (int i = warp; i < bs; i += nwarps) {
-          const int x = i, y = bs + (i + t) % bs;
-          if (gcol[x] < 0 || gcol[y] < 0) continue;
-          jacobi_pair<NPL>(Ms, Vs, nrm, l, x, y, a.tol, lane, off);
+      __syncthreads();
+      // 1. fresh Gram of the W local columns (DMMA over 64-row chunks)
+      JAcc g;
+      jacc_zero(g);
+      for (int r0 = 0; r0 < l; r0 += kJCH) {
+        stage(Cs, a.M, a.ldm, gcol, r0, l);
+        __syncthreads();
+        jdmma(g, Cs, true, Cs, kJCH);
+        __syncthreads();
+      }
+      jacc_store_smem(g, Gs);
+      for (int t = tid; t < kJW * kJW; t += nt) Js[(t >> 6) * kJL + (t & 63)] = ((t >> 6) == (t & 63)) ? 1.0 : 0.0;
+      __syncthreads();
+      // 2. two-sided Jacobi on G: within-block pairs once per sweep (round 0), then
+      //    cross-block pairs (A_i, B_{(i+t) mod bs}); inner passes over the cross set
+      double off = 0.0;
+      const int be = bs + (bs & 1);
+      const int n_within = (r == 0) ? be - 1 : 0;
+      const int n_cross = a.inner * bs;
+      for (int t = 0; t < n_within + n_cross; ++t) {
+        // pair list of this round
+        if (tid < kJW / 2) {
+          int p = -1, q = -1;
+          if (t < n_within) {
+            const int np = be / 2;   // pairs per block
+            if (tid < 2 * np) {
+              const int blk = tid < np ? 0 : 1, k = tid - blk * np;
+              const int xl = rr_player(k, t, be), yl = rr_player(be - 1 - k, t, be);
+              if (xl < bs && yl < bs) {
+                p = blk * bs + xl;
+                q = blk * bs + yl;
+              }
+            }
+          } else if (tid < bs) {
+            const int tt = (t - n_within) % bs;
+            p = tid;
+            q = bs + (tid + tt) % bs;
+          }
+          double cs = 1.0, sn = 0.0;
+          if (p >= 0 && (gcol[p] < 0 || gcol[q] < 0)) p = -1;
+          if (p >= 0) {
+            const double aa = Gs[p * kJL + p], bb = Gs[q * kJL + q], cc = Gs[p * kJL + q];
+            const double ab = sqrt(aa * bb);
+            if (fabs(cc) > tol * ab) {
+              off = fmax(off, fabs(cc) / ab);
+              const double zeta = (bb - aa) / (2.0 * cc);
+              double tt2;
+              if (fabs(zeta) > 1e15) {
+                tt2 = 0.5 / zeta;
+              } else {
+                const float zf = (float)zeta;
+                tt2 = (double)(copysignf(1.0f, zf) / (fabsf(zf) + sqrtf(1.0f + zf * zf)));
+              }
+              cs = rsqrt(1.0 + tt2 * tt2);
+              sn = cs * tt2;
+            } else {
+              p = -1;
+            }
+          }
+          rp[tid] = p;
+          rq[tid] = q;
+          rc[tid] = cs;
+          rs[tid] = sn;
+        }
+        __syncthreads();
+        // column rotations of G and J:  x_p <- c x_p - s x_q ; x_q <- s x_p + c x_q
+        for (int e = tid; e < (kJW / 2) * kJW; e += nt) {
+          const int k = e / kJW, row = e - k * kJW;
+          const int p = rp[k];
+          if (p < 0 || row >= W) continue;
+          const int q = rq[k];
+          const double c = rc[k], s = rs[k];
+          const double gp = Gs[row * kJL + p], gq = Gs[row * kJL + q];
+          Gs[row * kJL + p] = c * gp - s * gq;
+          Gs[row * kJL + q] = s * gp + c * gq;
+          const double jp = Js[row * kJL + p], jq = Js[row * kJL + q];
+          Js[row * kJL + p] = c * jp - s * jq;
+          Js[row * kJL + q] = s * jp + c * jq;
+        }
+        __syncthreads();
+        // row rotations of G (completes G <- J^T G J for this round)
+        for (int e = tid; e < (kJW / 2) * kJW; e += nt) {
+          const int k = e / kJW, col = e - k * kJW;
+          const int p = rp[k];
+          if (p < 0 || col >= W) continue;
+          const int q = rq[k];
+          const double c = rc[k], s = rs[k];
+          const double gp = Gs[p * kJL + col], gq = Gs[q * kJL + col];
+          Gs[p * kJL + col] = c * gp - s * gq;
+          Gs[q * kJL + col] = s * gp + c * gq;
         }
         __syncthreads();
       }
-      for (int idx = tid; idx < W * l; idx += blockDim.x) {
-        const int j = idx / l, i = idx - j * l;
-        const int c = gcol[j];
-        if (c >= 0) {
-          a.M[i + (int64_t)c * a.ldm] = Ms[idx];
-          a.V[i + (int64_t)c * a.ldv] = Vs[idx];
+      // 3. M_W <- M_W J, V_W <- V_W J (64-row chunks, DMMA, in place)
+      for (int pass = 0; pass < 2; ++pass) {
+        double* X = pass == 0 ? a.M : a.V;
+        const int64_t ldx = pass == 0 ? a.ldm : a.ldv;
+        for (int r0 = 0; r0 < l; r0 += kJCH) {
+          stage(Cs, X, ldx, gcol, r0, l);
+          __syncthreads();
+          JAcc o;
+          jacc_zero(o);
+          jdmma(o, Cs, false, Js, kJW);
+          __syncthreads();
+          jacc_store_cols(o, X, ldx, gcol, r0, l);
         }
       }
+      // sweep-wide max |cos| (only the first inner pass over a pair counts as the
+      // fresh measurement; later passes are refinements of the same visit)
       off = warp_max(off);
-      if (lane == 0 && off > 0.0) atomicMax(reinterpret_cast<unsigned long long*>(&s_off),
-                                            (unsigned long long)__double_as_longlong(off));
+      if ((tid & 31) == 0 && off > 0.0)
+        atomicMax(reinterpret_cast<unsigned long long*>(&s_off),
+                  (unsigned long long)__double_as_longlong(off));
       __syncthreads();
       if (tid == 0 && s_off > 0.0)
         atomicMax(reinterpret_cast<unsigned long long*>(a.offmax + sweep),
                   (unsigned long long)__double_as_longlong(s_off));
-      grid_barrier(bar, P);
+      grid_barrier(a.bar, P);
     }
     const double om = *((volatile double*)(a.offmax + sweep));
     if (tid == 0 && blockIdx.x == 0) *a.sweeps = sweep + 1;
-    if (!(om > a.tol)) break;
+    if (!(om > tol)) break;
   }
 }
 
@@ -237,12 +322,8 @@ __global__ void jacobi_finish_kernel(const double* M, int64_t ldm, const double*
 }
 
 int jacobi_block_size(int l) {
-  int bs = (int)((200 * 1024) / ((size_t)l * 2 * 2 * sizeof(double)));
-  if (bs > 32) bs = 32;
-  if ((l + 31) / 32 >= 8 && bs > 16) bs = 16;   // register budget of the NPL >= 8 variants
-  // keep >= 4 CTAs busy for small l
-  while (bs > 4 && (l + bs - 1) / bs < 8) bs /= 2;
-  if (bs < 1) bs = 1;
+  int bs = 32;
+  while (bs > 2 && (l + bs - 1) / bs < 4) bs /= 2;   // keep >= 2 block pairs for small l
   return bs;
 }
 
@@ -250,29 +331,24 @@ cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, double* M, int64_t ldm, 
                               int64_t ldv, int l, double* sig, double* U, int64_t ldu, double* Vo,
                               int64_t ldvo, uint32_t* bar, double* offmax, int* sweeps, int* order,
                               int max_sweeps) {
+  (void)sms;
   const int bs = jacobi_block_size(l);
   int nb = (l + bs - 1) / bs;
   if (nb % 2) ++nb;
   if (nb < 2) nb = 2;
   const int P = nb / 2;
-  (void)sms;
-  JacobiArgs a{M, ldm, V, ldv, l, bs, nb, 1e-15 * sqrt((double)l), max_sweeps, bar, offmax, sweeps};
-  const size_t smem = (size_t)2 * (2 * bs) * l * sizeof(double);
-  void* kern;
-  const int npl = (l + 31) / 32;
-  if (npl <= 2) kern = (void*)jacobi_kernel<2>;
-  else if (npl <= 4) kern = (void*)jacobi_kernel<4>;
-  else if (npl <= 8) kern = (void*)jacobi_kernel<8>;
-  else if (npl <= 12) kern = (void*)jacobi_kernel<12>;
-  else if (npl <= 16) kern = (void*)jacobi_kernel<16>;
-  else kern = (void*)jacobi_kernel<32>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+  JacobiArgs a{M, ldm, V, ldv, l, bs, nb, 1e-15 * sqrt((double)l), max_sweeps, bar, offmax, sweeps, 1};
+  const size_t smem = (size_t)3 * kJW * kJL * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
   cudaError_t e = cudaMemsetAsync(bar, 0, 2 * sizeof(uint32_t), st);
   if (e == cudaSuccess) e = cudaMemsetAsync(offmax, 0, sizeof(double) * max_sweeps, st);
   if (e != cudaSuccess) return e;
-  const int threads = 32 * (bs < 4 ? 4 : bs);
   void* args[] = {&a};
-  e = cudaLaunchCooperativeKernel(kern, dim3(P), dim3(threads), args, smem, st);
+  e = cudaLaunchCooperativeKernel((void*)jacobi_kernel, dim3(P), dim3(kJThreads), args, smem, st);
   if (e != cudaSuccess) return e;
   jacobi_finish_kernel<<<1, 1024, sizeof(double) * (size_t)l, st>>>(M, ldm, V, ldv, l, sig, U, ldu,
                                                                     Vo, ldvo, order);

@@ -15,6 +15,7 @@ struct JacobiArgs {
   uint32_t* bar;     // [2] grid barrier
   double* offmax;    // [max_sweeps]
   int* sweeps;       // sweeps executed
+  int inner;         // passes over the cross-block pairs per visit
 };
 
 int jacobi_block_size(int l);

@@ -16,6 +16,11 @@ namespace ffb {
 FFB_DEV void st_release_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
+FFB_DEV uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 FFB_DEV uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -80,189 +85,286 @@ cudaError_t launch_iota2(cudaStream_t st, int64_t* arr, int64_t* pos, int64_t n)
 // position) and computes the same reflector -> local update + norm downdate
 // with the 1e-8 guard recompute.
 
+// top-2 candidate (r, position); better = larger r, ties -> lower position
+struct Cand2 {
+  double r1;
+  int64_t p1;
+  double r2;
+  int64_t p2;
+};
+
+FFB_DEV bool cand_better(double ra, int64_t pa, double rb, int64_t pb) {
+  // is (ra, pa) strictly better than (rb, pb)?  pb < 0 means "none"
+  if (pa < 0) return false;
+  if (pb < 0) return true;
+  return ra > rb || (ra == rb && pa < pb);
+}
+
+FFB_DEV void cand_push(Cand2& c, double r, int64_t p) {
+  if (cand_better(r, p, c.r1, c.p1)) {
+    c.r2 = c.r1;
+    c.p2 = c.p1;
+    c.r1 = r;
+    c.p1 = p;
+  } else if (cand_better(r, p, c.r2, c.p2)) {
+    c.r2 = r;
+    c.p2 = p;
+  }
+}
+
+FFB_DEV Cand2 cand_merge(Cand2 a, const Cand2& b) {
+  cand_push(a, b.r1, b.p1);
+  cand_push(a, b.r2, b.p2);
+  return a;
+}
+
+FFB_DEV Cand2 cand_shfl(const Cand2& c, int off) {
+  Cand2 o;
+  o.r1 = __shfl_xor_sync(0xffffffffu, c.r1, off);
+  o.p1 = __shfl_xor_sync(0xffffffffu, c.p1, off);
+  o.r2 = __shfl_xor_sync(0xffffffffu, c.r2, off);
+  o.p2 = __shfl_xor_sync(0xffffffffu, c.p2, off);
+  return o;
+}
+
+FFB_DEV Cand2 warp_top2(Cand2 c) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c = cand_merge(c, cand_shfl(c, o));
+  return c;
+}
+
+// Column storage: column-major per column with padded stride sP (sP % 16 == 4),
+// 4 threads per column (interleaved rows).  kGroups column groups per CTA.
+constexpr int kPivThreads = 256;
+constexpr int kPivGroups = kPivThreads / 4;
+
+// exact warp argmax: largest r, ties -> lowest position (two shuffle passes)
+FFB_DEV void warp_best(double& r, int64_t& p) {
+  double m = (p >= 0) ? r : -1.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  int64_t q = (p >= 0 && r == m) ? p : INT64_MAX;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t t = __shfl_xor_sync(0xffffffffu, q, o);
+    q = t < q ? t : q;
+  }
+  r = m;
+  p = (q == INT64_MAX) ? -1 : q;
+}
+
 template <bool SMEM>
-__global__ void __launch_bounds__(1024) pivots_kernel(PivotArgs a) {
+__global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
   extern __shared__ __align__(16) double sm[];
-  const int s = a.s, cpc = a.cpc, tid = threadIdx.x, nt = blockDim.x;
+  const int s = a.s, cpc = a.cpc, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int sP = a.sP;
+  const int grp = tid >> 2, sub = tid & 3;
+  const unsigned gmask = 0xFu << (lane & 28);   // the 4 lanes sharing a column
   const int64_t c0 = (int64_t)blockIdx.x * cpc;
   int64_t ncl = a.n - c0;
   if (ncl > cpc) ncl = cpc;
   if (ncl < 0) ncl = 0;
   const int nc = (int)ncl;
-  double* W = SMEM ? sm : a.work + (size_t)blockIdx.x * s * cpc;   // [s][cpc]
-  double* base = SMEM ? sm + (size_t)s * cpc : sm;
+  double* W = SMEM ? sm : a.work + (size_t)blockIdx.x * sP * cpc;   // [cpc][sP]
+  double* base = SMEM ? sm + (size_t)sP * cpc : sm;
   double* r = base;
   double* r0 = r + cpc;
   int64_t* pp = reinterpret_cast<int64_t*>(r0 + cpc);
-  double* xv = reinterpret_cast<double*>(pp + cpc);    // winner column, then reflector v
-  double* red_v = xv + s + 1;
-  int64_t* red_i = reinterpret_cast<int64_t*>(red_v + 32);
-  __shared__ int s_wcta, s_wc;
-  __shared__ double s_tau, s_div, s_gap;
+  double* vv = reinterpret_cast<double*>(pp + cpc);     // reflector v (s)
+  Cand2* wc = reinterpret_cast<Cand2*>(vv + ((s + 1) & ~1));   // per-warp top-2 [8]
+  __shared__ double s_tau;
+  __shared__ int64_t s_wpos;
 
-  for (int idx = tid; idx < s * nc; idx += nt) {
-    const int c = idx / s, i = idx % s;
-    W[i * cpc + c] = a.B[i + (c0 + c) * a.ldb];
+  for (int idx = tid; idx < s * nc; idx += kPivThreads) {
+    const int c = idx / s, i = idx - c * s;
+    W[c * sP + i] = a.B[i + (c0 + c) * a.ldb];
   }
-  for (int c = tid; c < nc; c += nt) pp[c] = a.pos[c0 + c];
+  for (int c = tid; c < nc; c += kPivThreads) pp[c] = a.pos[c0 + c];
   __syncthreads();
-  // r = squared column norms of the working copy (numba 22-29).
-  for (int c = tid; c < nc; c += nt) {
-    double t0 = 0.0, t1 = 0.0;
-    int i = 0;
-    for (; i + 1 < s; i += 2) {
-      const double x = W[i * cpc + c], y = W[(i + 1) * cpc + c];
-      t0 = fma(x, x, t0);
-      t1 = fma(y, y, t1);
+  // initial norms and local top-2 over positions >= j0
+  {
+    Cand2 cd{-1.0, -1, -1.0, -1};
+    for (int c = grp; c < nc; c += kPivGroups) {
+      const double* col = W + (size_t)c * sP;
+      double t = 0.0;
+      for (int i = sub; i < s; i += 4) t = fma(col[i], col[i], t);
+      t += __shfl_xor_sync(gmask, t, 1);
+      t += __shfl_xor_sync(gmask, t, 2);
+      if (sub == 0) {
+        r[c] = t;
+        r0[c] = t;
+      }
+      if (pp[c] >= a.j0) cand_push(cd, t, pp[c]);
     }
-    if (i < s) t0 = fma(W[i * cpc + c], W[i * cpc + c], t0);
-    r[c] = t0 + t1;
-    r0[c] = r[c];
+    cd = warp_top2(cd);
+    if (lane == 0) wc[warp] = cd;
   }
   __syncthreads();
 
   for (int j = 0; j < a.bb; ++j) {
     const int64_t P = a.j0 + j;
     const int par = j & 1;
-    // (1) local best (largest r, ties -> lowest position) and local runner-up.
-    ArgMax best{-1.0, -1};
-    for (int c = tid; c < nc; c += nt)
-      if (pp[c] >= P) best = argmax_better(best, ArgMax{r[c], pp[c]});
-    best = block_argmax(best, red_v, red_i);
-    ArgMax sec{-1.0, -1};
-    for (int c = tid; c < nc; c += nt)
-      if (pp[c] >= P && pp[c] != best.i) sec = argmax_better(sec, ArgMax{r[c], pp[c]});
-    sec = block_argmax(sec, red_v, red_i);
-    if (tid == 0) s_wc = -1;
-    __syncthreads();
-    if (best.i >= 0)
-      for (int c = tid; c < nc; c += nt)
-        if (pp[c] == best.i) s_wc = c;
-    __syncthreads();
-    // (2) publish candidate + its column data, then release this CTA's flag.
-    PivSlot* slot = a.slots + (size_t)par * a.G * 2;
-    double* sdata = a.slotdata + ((size_t)par * a.G + blockIdx.x) * s;
-    const int wc = s_wc;
-    if (wc >= 0)
-      for (int i = tid; i < s; i += nt) sdata[i] = W[i * cpc + wc];
-    if (tid == 0) {
-      slot[2 * blockIdx.x] = PivSlot{best.v, best.i};
-      slot[2 * blockIdx.x + 1] = PivSlot{sec.v, sec.i};
-    }
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) st_release_u32(a.flags + blockIdx.x, (uint32_t)(j + 1));
-    // (3) all-to-all wait; every CTA derives the same global winner.
-    ArgMax g{-1.0, -1};
-    for (int t = tid; t < a.G; t += nt) {
-      while (ld_acquire_u32(a.flags + t) < (uint32_t)(j + 1)) {
+    if (warp == 0) {
+      // ---- local candidate -> publish -> global pick -> reflector (one warp)
+      Cand2 cd = lane < (kPivThreads / 32) ? wc[lane] : Cand2{-1.0, -1, -1.0, -1};
+      if (a.gap) {
+        cd = warp_top2(cd);
+      } else {
+        warp_best(cd.r1, cd.p1);
       }
-      const PivSlot ps = slot[2 * t];
-      if (ps.pos >= 0) g = argmax_better(g, ArgMax{ps.r, ps.pos});
-    }
-    const ArgMax gw = block_argmax(g, red_v, red_i);
-    // runner-up = max over (other CTAs' bests, winner CTA's second) -> gap trace.
-    ArgMax g2{-1.0, -1};
-    if (tid == 0) s_wcta = -1;
-    __syncthreads();
-    for (int t = tid; t < a.G; t += nt) {
-      const PivSlot b0 = slot[2 * t], b1 = slot[2 * t + 1];
-      if (b0.pos == gw.i) {
-        s_wcta = t;
-        if (b1.pos >= 0) g2 = argmax_better(g2, ArgMax{b1.r, b1.pos});
-      } else if (b0.pos >= 0) {
-        g2 = argmax_better(g2, ArgMax{b0.r, b0.pos});
+      PivSlot* slot = a.slots + (size_t)par * a.G * 2;
+      double* sdata = a.slotdata + ((size_t)par * a.G + blockIdx.x) * s;
+      if (cd.p1 >= 0) {
+        // local column holding position cd.p1 (positions are unique)
+        int cl = -1;
+        for (int c = lane; c < nc; c += 32)
+          if (pp[c] == cd.p1) cl = c;
+        for (int o = 16; o > 0; o >>= 1) cl = max(cl, __shfl_xor_sync(0xffffffffu, cl, o));
+        const double* col = W + (size_t)cl * sP;
+        for (int i = lane; i < s; i += 32) sdata[i] = col[i];
       }
-    }
-    g2 = block_argmax(g2, red_v, red_i);
-    const int wcta = s_wcta;
-    const int64_t wpos = gw.i;
-    {
-      const double* wd = a.slotdata + ((size_t)par * a.G + wcta) * s;
-      for (int i = tid; i < s; i += nt) xv[i] = wd[i];
-    }
-    // (4) swap positions P <-> wpos (swap-history semantics, numba 38-51).
-    for (int c = tid; c < nc; c += nt) {
-      if (pp[c] == wpos) pp[c] = P;
-      else if (pp[c] == P) pp[c] = wpos;
-    }
-    if (blockIdx.x == 0 && tid == 0) {
-      const int64_t t = a.arr[P];
-      a.arr[P] = a.arr[wpos];
-      a.arr[wpos] = t;
-      a.hist[j] = wpos;
-      if (a.gap) a.gap[j] = (gw.v > 0.0 && g2.i >= 0) ? (gw.v - g2.v) / gw.v : 1.0;
-    }
-    __syncthreads();
-    // (5) reflector from the winner column, rows j..s-1 (ffsrqr/qr.py:21-43 and
-    // _kernels_numba.py:53-71): tail == 0 -> identity (tau = 0); otherwise
-    // alpha = -sign(x0)||x|| (+||x|| when x0 == 0), v = tail / (x0 - alpha).
-    if (tid < 32) {
-      double t = 0.0;
-      for (int i = j + 1 + tid; i < s; i += 32) t = fma(xv[i], xv[i], t);
-      t = warp_sum(t);
-      if (tid == 0) {
-        const double x0 = xv[j];
-        double tau = 0.0, div = 1.0;
-        if (t != 0.0) {
-          const double nrm = sqrt(x0 * x0 + t);
-          const double alpha = x0 == 0.0 ? nrm : -copysign(nrm, x0);
-          div = x0 - alpha;
-          tau = (alpha - x0) / alpha;
-        }
+      if (lane == 0) {
+        slot[2 * blockIdx.x] = PivSlot{cd.r1, cd.p1};
+        slot[2 * blockIdx.x + 1] = PivSlot{cd.r2, cd.p2};
+      }
+      // __syncwarp orders the lanes' writes before lane 0's (cumulative) release
+      __syncwarp();
+      if (lane == 0) st_release_u32(a.flags + blockIdx.x, (uint32_t)(j + 1));
+      // poll every owned flag with relaxed loads (pipelined), then one fence
+      {
+        const uint32_t tgt = (uint32_t)(j + 1);
+        bool done;
+        do {
+          done = true;
+          for (int t = lane; t < a.G; t += 32) done &= ld_relaxed_u32(a.flags + t) >= tgt;
+        } while (!__all_sync(0xffffffffu, done));
+        __threadfence();
+      }
+      Cand2 g{-1.0, -1, -1.0, -1};
+      int wcta = -1;
+      for (int t = lane; t < a.G; t += 32) {
+        const PivSlot b0 = slot[2 * t];
+        if (cand_better(b0.r, b0.pos, g.r1, g.p1)) wcta = t;
+        cand_push(g, b0.r, b0.pos);
+      }
+      // winner CTA = the one whose best equals the global best (positions unique)
+      Cand2 gw = g;
+      if (a.gap) {
+        gw = warp_top2(g);
+      } else {
+        warp_best(gw.r1, gw.p1);
+        gw.p2 = -1;
+      }
+      int wc_cta = -1;
+      for (int t = lane; t < a.G; t += 32)
+        if (slot[2 * t].pos == gw.p1 && gw.p1 >= 0) wc_cta = t;
+      for (int o = 16; o > 0; o >>= 1) wc_cta = max(wc_cta, __shfl_xor_sync(0xffffffffu, wc_cta, o));
+      (void)wcta;
+      // runner-up = max(other CTAs' bests, winner CTA's second)
+      double second = (gw.p2 >= 0) ? gw.r2 : -1.0;
+      if (wc_cta >= 0) {
+        const PivSlot w2 = slot[2 * wc_cta + 1];
+        if (w2.pos >= 0) second = fmax(second, w2.r);
+      }
+      const int64_t wpos = gw.p1 >= 0 ? gw.p1 : P;
+      // winner column -> reflector for rows j..s-1 (ffsrqr/qr.py:21-43)
+      const double* wd = a.slotdata + ((size_t)par * a.G + (wc_cta >= 0 ? wc_cta : 0)) * s;
+      double xv[4];
+      double tsq = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = lane + 32 * q;
+        xv[q] = (i < s && gw.p1 >= 0) ? wd[i] : 0.0;
+        if (i > j && i < s) tsq = fma(xv[q], xv[q], tsq);
+      }
+      tsq = warp_sum(tsq);
+      double xsel = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q == (j >> 5)) xsel = xv[q];
+      const double x0 = __shfl_sync(0xffffffffu, xsel, j & 31);
+      double tau = 0.0, div = 1.0;
+      if (tsq != 0.0) {
+        const double nrm = sqrt(x0 * x0 + tsq);
+        const double alpha = x0 == 0.0 ? nrm : -copysign(nrm, x0);
+        div = x0 - alpha;
+        tau = (alpha - x0) / alpha;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = lane + 32 * q;
+        if (i < s) vv[i] = (i == j) ? 1.0 : (i > j && tau != 0.0 ? xv[q] / div : 0.0);
+      }
+      if (lane == 0) {
         s_tau = tau;
-        s_div = div;
-      }
-    }
-    __syncthreads();
-    const double tau = s_tau;
-    if (tau != 0.0) {
-      const double div = s_div;
-      for (int i = j + 1 + tid; i < s; i += nt) xv[i] = xv[i] / div;
-    }
-    __syncthreads();
-    // (6) apply H = I - tau v v^T to the active local columns, then downdate
-    // r -= R[j,c]^2 with the guard recompute (numba 72-92).
-    for (int c = tid; c < nc; c += nt) {
-      if (pp[c] <= P) continue;
-      double* col = W + c;
-      if (tau != 0.0) {
-        double w0 = col[j * cpc], w1 = 0.0;
-        int i = j + 1;
-        for (; i + 1 < s; i += 2) {
-          w0 = fma(xv[i], col[i * cpc], w0);
-          w1 = fma(xv[i + 1], col[(i + 1) * cpc], w1);
+        s_wpos = wpos;
+        if (blockIdx.x == 0) {
+          const int64_t t = a.arr[P];
+          a.arr[P] = a.arr[wpos];
+          a.arr[wpos] = t;
+          a.hist[j] = wpos;
+          if (a.gap) a.gap[j] = (gw.r1 > 0.0 && second >= 0.0) ? (gw.r1 - second) / gw.r1 : 1.0;
         }
-        if (i < s) w0 = fma(xv[i], col[i * cpc], w0);
-        const double w = (w0 + w1) * tau;
-        col[j * cpc] -= w;
-        for (int q = j + 1; q < s; ++q) col[q * cpc] = fma(-xv[q], w, col[q * cpc]);
       }
-      const double rj = col[j * cpc];
+    }
+    __syncthreads();
+    // ---- all threads: swap bookkeeping, reflector application, downdate
+    const double tau = s_tau;
+    const int64_t wpos = s_wpos;
+    Cand2 cd{-1.0, -1, -1.0, -1};
+    for (int c = grp; c < nc; c += kPivGroups) {
+      int64_t p = pp[c];
+      if (p == wpos) p = P;
+      else if (p == P) p = wpos;
+      if (sub == 0) pp[c] = p;
+      if (p <= P) continue;
+      double* col = W + (size_t)c * sP;
+      if (tau != 0.0) {
+        double wsum = 0.0;
+        for (int i = j + sub; i < s; i += 4) wsum = fma(vv[i], col[i], wsum);
+        wsum += __shfl_xor_sync(gmask, wsum, 1);
+        wsum += __shfl_xor_sync(gmask, wsum, 2);
+        const double wt = wsum * tau;
+        for (int i = j + sub; i < s; i += 4) col[i] = fma(-vv[i], wt, col[i]);
+      }
+      __syncwarp(gmask);
+      const double rj = col[j];
       double rr = r[c] - rj * rj;
       if (rr < 1e-8 * r0[c] || rr < 0.0) {
-        double t0 = 0.0, t1 = 0.0;
-        int i = j + 1;
-        for (; i + 1 < s; i += 2) {
-          t0 = fma(col[i * cpc], col[i * cpc], t0);
-          t1 = fma(col[(i + 1) * cpc], col[(i + 1) * cpc], t1);
-        }
-        if (i < s) t0 = fma(col[i * cpc], col[i * cpc], t0);
-        const double f = t0 + t1;
-        rr = f > 0.0 ? f : 0.0;
+        double t = 0.0;
+        for (int i = j + 1 + sub; i < s; i += 4) t = fma(col[i], col[i], t);
+        t += __shfl_xor_sync(gmask, t, 1);
+        t += __shfl_xor_sync(gmask, t, 2);
+        rr = t > 0.0 ? t : 0.0;
       }
-      r[c] = rr;
+      if (sub == 0) r[c] = rr;
+      cand_push(cd, rr, p);
     }
+    if (a.gap) {
+      cd = warp_top2(cd);
+    } else {
+      warp_best(cd.r1, cd.p1);
+      cd.r2 = -1.0;
+      cd.p2 = -1;
+    }
+    if (lane == 0) wc[warp] = cd;
     __syncthreads();
   }
-  for (int c = tid; c < nc; c += nt) a.pos[c0 + c] = pp[c];
+  for (int c = tid; c < nc; c += kPivThreads) a.pos[c0 + c] = pp[c];
 }
 
 size_t pivots_smem_bytes(int s, int cpc, bool smem_mode) {
-  size_t b = (smem_mode ? (size_t)s * cpc : 0) * sizeof(double);
+  const int sP = pivots_stride(s);
+  size_t b = (smem_mode ? (size_t)sP * cpc : 0) * sizeof(double);
   b += (size_t)cpc * (2 * sizeof(double) + sizeof(int64_t));
-  b += (size_t)(s + 1) * sizeof(double) + 32 * sizeof(double) + 32 * sizeof(int64_t);
+  b += (size_t)((s + 1) & ~1) * sizeof(double) + 8 * sizeof(Cand2) + 64;
   return b;
+}
+
+int pivots_stride(int s) {
+  int sP = s;
+  while (sP % 16 != 4) ++sP;
+  return sP;
 }
 
 void* pivots_kernel_ptr(bool smem_mode) {
@@ -270,15 +372,12 @@ void* pivots_kernel_ptr(bool smem_mode) {
 }
 
 cudaError_t launch_pivots(cudaStream_t st, const PivotArgs& a, bool smem_mode, size_t smem) {
-  int threads = ((a.cpc + 31) / 32) * 32;
-  if (threads < 64) threads = 64;
-  if (threads > 1024) threads = 1024;
   PivotArgs args = a;
+  args.sP = pivots_stride(a.s);
   void* kargs[] = {&args};
-  return cudaLaunchCooperativeKernel(pivots_kernel_ptr(smem_mode), dim3(a.G), dim3(threads), kargs,
-                                     smem, st);
+  return cudaLaunchCooperativeKernel(pivots_kernel_ptr(smem_mode), dim3(a.G), dim3(kPivThreads),
+                                     kargs, smem, st);
 }
-
 
 // ------------------------------------------------------- gathers / copies
 

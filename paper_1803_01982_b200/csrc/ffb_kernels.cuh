@@ -29,7 +29,8 @@ struct PivotArgs {
   int64_t* pos;
   int G;
   int cpc;
-  double* work;        // !smem mode: G * s * cpc
+  int sP;              // padded per-column stride (set by launch_pivots)
+  double* work;        // !smem mode: G * sP * cpc
   PivSlot* slots;      // [2][G][2]: per CTA best and runner-up
   double* slotdata;    // [2][G][s]
   uint32_t* flags;     // [G], zero on entry
@@ -58,6 +59,7 @@ cudaError_t launch_colsq(cudaStream_t st, const double* A, int64_t lda, int64_t 
 cudaError_t launch_iota2(cudaStream_t st, int64_t* arr, int64_t* pos, int64_t n);
 cudaError_t launch_pivots(cudaStream_t st, const PivotArgs& a, bool smem_mode, size_t smem);
 size_t pivots_smem_bytes(int s, int cpc, bool smem_mode);
+int pivots_stride(int s);
 void* pivots_kernel_ptr(bool smem_mode);
 
 cudaError_t launch_gather_cols(cudaStream_t st, const double* src, int64_t ld_src, int64_t rows,

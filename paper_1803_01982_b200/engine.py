@@ -89,6 +89,29 @@ def _workspace(torch, device, nbytes):
     return buf
 
 
+_omega_cache = {}
+_omega_lock = threading.Lock()
+_OMEGA_CACHE_MAX = 8
+
+
+def _omega(torch, dev, s, m, seed):
+    """Device copy of Omega = gaussian(s, m, seed, 0) (ffsrqr/sketch.py:108).
+
+    Omega depends only on (seed, s, m), so repeated factorizations with the same
+    seed (IALM/SVT iterations, HOSVD modes of equal size, benchmarks) reuse it."""
+    key = (dev.index, int(s), int(m), int(seed) & 0xFFFFFFFFFFFFFFFF)
+    with _omega_lock:
+        om = _omega_cache.get(key)
+        if om is not None:
+            return om
+    om = torch.from_numpy(rng.gaussian(s, m, seed, rng.STREAM_SKETCH)).to(dev)
+    with _omega_lock:
+        if len(_omega_cache) >= _OMEGA_CACHE_MAX:
+            _omega_cache.pop(next(iter(_omega_cache)))
+        _omega_cache[key] = om
+    return om
+
+
 @_capi.GAUSS_CB
 def _gauss_cb(user, seed, stream, rows, cols, out):
     try:
@@ -99,7 +122,7 @@ def _gauss_cb(user, seed, stream, rows, cols, out):
         return 1
 
 
-def run(A, params: SketchParams, mode, device=None, want=("R", "Q", "rtilde", "perm")):
+def run(A, params: SketchParams, mode, device=None, trace_gaps=False):
     """Run one factorization mode through the C ABI; returns a dict of outputs."""
     torch = _torch()
     dev = _device(device if device is not None else (A.device if isinstance(A, torch.Tensor) and A.is_cuda else None))
@@ -111,6 +134,8 @@ def run(A, params: SketchParams, mode, device=None, want=("R", "Q", "rtilde", "p
             raise DimensionError(f"srqr needs l+1 <= min(m,n); got l={prm.l}, min={min(m, n)}")
         if prm.b > 64:
             raise DimensionError("the B200 engine supports block sizes b <= 64")
+        if prm.b + prm.p > 128:
+            raise DimensionError("the B200 engine supports sketch sizes b + p <= 128")
         lib = _capi.load()
         ctx = _capi.context(dev.index)
         cp = _capi.Params(prm.k, prm.l, prm.b, prm.p, prm.d, prm.epsilon, prm.g,
@@ -121,7 +146,7 @@ def run(A, params: SketchParams, mode, device=None, want=("R", "Q", "rtilde", "p
             raise DimensionError("invalid dimensions for the engine")
         ws = _workspace(torch, dev, nbytes.value)
         s = prm.b + prm.p
-        omega = torch.from_numpy(rng.gaussian(s, m, prm.seed, rng.STREAM_SKETCH)).to(dev)
+        omega = _omega(torch, dev, s, m, prm.seed)
         l, k = prm.l, prm.k
         out = {}
         res = _capi.Result()
@@ -140,8 +165,10 @@ def run(A, params: SketchParams, mode, device=None, want=("R", "Q", "rtilde", "p
         res.perm = out["perm"].data_ptr()
         out["R"] = _colmajor(torch, l, n, dev)
         res.R, res.ldr = out["R"].data_ptr(), l
-        out["pivot_gap"] = torch.empty(l, dtype=torch.float64, device=dev)
-        res.pivot_gap = out["pivot_gap"].data_ptr()
+        if trace_gaps:
+            # top-2 relative gap of every sketch pivot step (near-tie certification)
+            out["pivot_gap"] = torch.empty(l, dtype=torch.float64, device=dev)
+            res.pivot_gap = out["pivot_gap"].data_ptr()
         if mode == _capi.FFB_MODE_TRQRCP:
             out["Y"] = _colmajor(torch, m, l, dev)
             out["T"] = _colmajor(torch, l, l, dev)
@@ -198,7 +225,8 @@ def _srqr_result(out):
                       rtilde=_conv(out["rtilde"], np_), q_ext=Q)
 
 
-def flip_flop_srqr(A, k, l=None, b=32, p=5, epsilon=0.5, g=2.0, d=None, seed=0, device=None):
+def flip_flop_srqr(A, k, l=None, b=32, p=5, epsilon=0.5, g=2.0, d=None, seed=0, device=None,
+                   trace_gaps=False):
     """Rank-k approximate SVD via spectrum-revealing QR plus a flipped QR
     (ffsrqr/svd.py:43-98), on the B200 engine."""
     shape = tuple(A.shape)
@@ -209,12 +237,13 @@ def flip_flop_srqr(A, k, l=None, b=32, p=5, epsilon=0.5, g=2.0, d=None, seed=0, 
         b = max(1, m - p)
         p = m - b
     params = SketchParams(k=k, l=l, b=b, p=p, epsilon=epsilon, g=g, d=d, seed=seed)
-    out = run(A, params, _capi.FFB_MODE_FLIPFLOP, device=device)
+    out = run(A, params, _capi.FFB_MODE_FLIPFLOP, device=device, trace_gaps=trace_gaps)
     np_ = out["is_numpy"]
     res = _srqr_result(out)
     meta = {"srqr": res, "params": out["params"], "method": "flip_flop_srqr",
             "diag_L": _conv(out["diag_L"], np_), "sv_all": _conv(out["sv_all"], np_),
-            "pivot_gap": _conv(out["pivot_gap"], np_), "engine": "ffb200-sm100a",
+            "pivot_gap": _conv(out["pivot_gap"], np_) if "pivot_gap" in out else None,
+            "engine": "ffb200-sm100a",
             "kernels": out["kernels"], "i_offs": out["i_offs"],
             "svd_sweeps": out["svd_sweeps"]}
     return ApproxSvd(u=_conv(out["u"], np_), s=_conv(out["s"], np_), v=_conv(out["v"], np_),
@@ -229,11 +258,11 @@ def srqr(A, params: SketchParams, device=None):
 
 def trqrcp(A, params: SketchParams, device=None):
     """Truncated randomized QRCP (ffsrqr/sketch.py:150-161)."""
-    out = run(A, params, _capi.FFB_MODE_TRQRCP, device=device)
+    out = run(A, params, _capi.FFB_MODE_TRQRCP, device=device, trace_gaps=True)
     np_ = out["is_numpy"]
     prm = out["params"]
     fact = PartialFactorization(R=_conv(out["R"], np_), perm=_conv(out["perm"], np_), k=prm.l,
                                 wy=WYFactor(_conv(out["Y"], np_), _conv(out["T"], np_)))
     fact.sketch = _conv(out["B"], np_)
-    fact.pivot_gap = _conv(out["pivot_gap"], np_)
+    fact.pivot_gap = _conv(out["pivot_gap"], np_) if "pivot_gap" in out else None
     return fact
