@@ -16,17 +16,18 @@
 // two-sided iteration never accumulates into the factorization.  A grid barrier
 // separates rounds; sweeps stop when max |cos| seen in a sweep <= tol.
 #include <math.h>
+#include <stdlib.h>
 
 #include "ffb_common.cuh"
 #include "ffb_jacobi.cuh"
+
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace ffb {
 
 namespace {
 
-constexpr int kJW = 64;        // max local columns
-constexpr int kJL = kJW + 1;   // smem leading dimension
-constexpr int kJCH = 64;       // rows per staged chunk
 constexpr int kJThreads = 256;
 
 FFB_DEV uint32_t ld_acq(const uint32_t* p) {
@@ -64,99 +65,95 @@ FFB_DEV int rr_player(int pos, int r, int nb) {
   return ((pos - 1 + r) % (nb - 1)) + 1;
 }
 
-// Stage rows [r0, r0 + kJCH) of the W local columns of X (ld ldx) into Cs
-// (kJCH x kJL, row-major), zero beyond l / W.
-FFB_DEV void stage(double* Cs, const double* X, int64_t ldx, const int* gcol, int r0, int l) {
-  for (int t = threadIdx.x; t < kJCH * kJW; t += blockDim.x) {
-    const int rr = t & 63, cc = t >> 6;
-    const int c = gcol[cc], row = r0 + rr;
-    Cs[rr * kJL + cc] = (c >= 0 && row < l) ? X[row + (int64_t)c * ldx] : 0.0;
-  }
-}
-
-// warp tile of a 64x64 DMMA product (8 warps): rows 16*(w/2).., cols 32*(w%2)..
-struct JAcc {
-  double c[2][4][2];
-};
-
-FFB_DEV void jacc_zero(JAcc& a) {
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) a.c[i][j][0] = a.c[i][j][1] = 0.0;
-}
-
-// acc += op(A)(64 x K) * B(K x 64), A(i,k) = at ? A[k*kJL+i] : A[i*kJL+k], B(k,j) = B[k*kJL+j]
-FFB_DEV void jdmma(JAcc& acc, const double* A, bool at, const double* B, int K) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;
-  const int fr = lane >> 2, fk = lane & 3;
-  for (int k0 = 0; k0 < K; k0 += 4) {
-    double af[2], bf[4];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int r = r0 + 8 * i + fr, k = k0 + fk;
-      af[i] = at ? A[k * kJL + r] : A[r * kJL + k];
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) bf[j] = B[(k0 + fk) * kJL + c0 + 8 * j + fr];
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) dmma_884(acc.c[i][j][0], acc.c[i][j][1], af[i], bf[j]);
-  }
-}
-
-FFB_DEV void jacc_store_smem(const JAcc& acc, double* C) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-        C[(r0 + 8 * i + (lane >> 2)) * kJL + c0 + 8 * j + 2 * (lane & 3) + h] = acc.c[i][j][h];
-}
-
-// write rows r0.. (< l) of the chunk product to X's local columns
-FFB_DEV void jacc_store_cols(const JAcc& acc, double* X, int64_t ldx, const int* gcol, int r0,
-                             int l) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int rb = (warp >> 1) * 16, cb = (warp & 1) * 32;
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int row = r0 + rb + 8 * i + (lane >> 2), cc = cb + 8 * j + 2 * (lane & 3) + h;
-        const int c = gcol[cc];
-        if (c >= 0 && row < l) X[row + (int64_t)c * ldx] = acc.c[i][j][h];
-      }
-}
-
 }  // namespace
 
+// W (<= 32) local columns: M_W (and V_W when VRES) staged in shared memory
+// (l x W, row-major, ld kMW); G and J are W x W.  256 threads.  CLUSTER: the P
+// CTAs form one thread-block cluster and rounds are separated by the hardware
+// cluster barrier (release/acquire at cluster scope covers the global M, V).
+constexpr int kMW = 33;
+
+template <bool CLUSTER>
+FFB_DEV void round_barrier(uint32_t* bar, uint32_t P) {
+  if (CLUSTER) {
+    __syncthreads();
+    cg::this_cluster().sync();
+  } else {
+    grid_barrier(bar, P);
+  }
+}
+
+// stage the W local columns of X (rows < l) into S (lpad x kMW), loads in flight
+FFB_DEV void stage_cols(double* S, const double* X, int64_t ldx, const int* gcol, int l, int lpad) {
+  const int nt = blockDim.x;
+  const int total = lpad * 32;
+  for (int base = 0; base < total; base += nt * 16) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int t = base + threadIdx.x + u * nt;
+      const int rr = t % lpad, cc = t / lpad;
+      const int c = (t < total) ? gcol[cc] : -1;
+      v[u] = (c >= 0 && rr < l) ? X[rr + (int64_t)c * ldx] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int t = base + threadIdx.x + u * nt;
+      if (t < total) S[(t % lpad) * kMW + t / lpad] = v[u];
+    }
+  }
+}
+
+// X_W <- S_W J (64-row chunks of S in smem), written straight to global
+FFB_DEV void apply_cols(const double* S, const double* Js, double* X, int64_t ldx,
+                        const int* gcol, int l, int lpad) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int fr = lane >> 2, fk = lane & 3;
+  for (int ch = 0; ch < lpad; ch += 64) {
+    double acc[4][2];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+    const int rowt = ch + warp * 8;
+#pragma unroll
+    for (int k0 = 0; k0 < 32; k0 += 4) {
+      const double af = S[(rowt + fr) * kMW + k0 + fk];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_884(acc[j][0], acc[j][1], af, Js[(k0 + fk) * 33 + 8 * j + fr]);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int row = rowt + (lane >> 2), cc = 8 * j + 2 * (lane & 3) + hh;
+        const int c = gcol[cc];
+        if (c >= 0 && row < l) X[row + (int64_t)c * ldx] = acc[j][hh];
+      }
+  }
+}
+
+template <bool CLUSTER, bool VRES>
 __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
   extern __shared__ __align__(16) double sm[];
-  double* Gs = sm;                 // W x W Gram (two-sided Jacobi working copy)
-  double* Js = Gs + kJW * kJL;     // accumulated rotation J
-  double* Cs = Js + kJW * kJL;     // staged row chunk
-  __shared__ int gcol[kJW];
-  __shared__ double rc[kJW / 2], rs[kJW / 2];   // rotation (cos, sin) per pair this round
-  __shared__ int rp[kJW / 2], rq[kJW / 2];      // pair columns (local), -1 = none
+  const int l = a.l, bs = a.bs, nb = a.nb, W = 2 * bs;   // W <= 32
+  const int lpad = (l + 63) & ~63;
+  double* Ms = sm;                        // lpad x kMW : M_W (rows >= l zero)
+  double* Gs = Ms + (size_t)lpad * kMW;   // 32 x 33
+  double* Js = Gs + 32 * 33;              // 32 x 33
+  double* Vs = Js + 32 * 33;              // VRES: lpad x kMW ; else 64 x kMW chunk
+  __shared__ int gcol[32];
+  __shared__ double rc[16], rs[16];
+  __shared__ int rp[16], rq[16];
   __shared__ double s_off;
-  const int l = a.l, bs = a.bs, nb = a.nb, W = 2 * bs;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int P = gridDim.x;
   const double tol = a.tol;
+  const float tolf = (float)a.tol;
 
   for (int sweep = 0; sweep < a.max_sweeps; ++sweep) {
     if (tid == 0) s_off = 0.0;
     for (int r = 0; r < nb - 1; ++r) {
       const int pa = rr_player(blockIdx.x, r, nb), pb = rr_player(nb - 1 - blockIdx.x, r, nb);
-      if (tid < kJW) {
+      if (tid < 32) {
         int c = -1;
         if (tid < W) {
           const int blk = tid < bs ? pa : pb;
@@ -166,30 +163,50 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
         gcol[tid] = c;
       }
       __syncthreads();
-      // 1. fresh Gram of the W local columns (DMMA over 64-row chunks)
-      JAcc g;
-      jacc_zero(g);
-      for (int r0 = 0; r0 < l; r0 += kJCH) {
-        stage(Cs, a.M, a.ldm, gcol, r0, l);
-        __syncthreads();
-        jdmma(g, Cs, true, Cs, kJCH);
-        __syncthreads();
-      }
-      jacc_store_smem(g, Gs);
-      for (int t = tid; t < kJW * kJW; t += nt) Js[(t >> 6) * kJL + (t & 63)] = ((t >> 6) == (t & 63)) ? 1.0 : 0.0;
+      stage_cols(Ms, a.M, a.ldm, gcol, l, lpad);
+      if (VRES) stage_cols(Vs, a.V, a.ldv, gcol, l, lpad);
       __syncthreads();
-      // 2. two-sided Jacobi on G: within-block pairs once per sweep (round 0), then
-      //    cross-block pairs (A_i, B_{(i+t) mod bs}); inner passes over the cross set
+      // fresh Gram G = M_W^T M_W (32 x 32): warp w -> rows 8*(w/2).., cols 16*(w%2)..
+      {
+        const int r0 = (warp >> 1) * 8, c0 = (warp & 1) * 16;
+        const int fr = lane >> 2, fk = lane & 3;
+        double c00 = 0, c01 = 0, c10 = 0, c11 = 0, d00 = 0, d01 = 0, d10 = 0, d11 = 0;
+        int k0 = 0;
+        for (; k0 + 4 < lpad; k0 += 8) {
+          const double af = Ms[(k0 + fk) * kMW + r0 + fr];
+          const double b0 = Ms[(k0 + fk) * kMW + c0 + fr];
+          const double b1 = Ms[(k0 + fk) * kMW + c0 + 8 + fr];
+          const double ag = Ms[(k0 + 4 + fk) * kMW + r0 + fr];
+          const double e0 = Ms[(k0 + 4 + fk) * kMW + c0 + fr];
+          const double e1 = Ms[(k0 + 4 + fk) * kMW + c0 + 8 + fr];
+          dmma_884(c00, c01, af, b0);
+          dmma_884(c10, c11, af, b1);
+          dmma_884(d00, d01, ag, e0);
+          dmma_884(d10, d11, ag, e1);
+        }
+        for (; k0 < lpad; k0 += 4) {
+          const double af = Ms[(k0 + fk) * kMW + r0 + fr];
+          dmma_884(c00, c01, af, Ms[(k0 + fk) * kMW + c0 + fr]);
+          dmma_884(c10, c11, af, Ms[(k0 + fk) * kMW + c0 + 8 + fr]);
+        }
+        const int rr = r0 + (lane >> 2), cc = c0 + 2 * (lane & 3);
+        Gs[rr * 33 + cc] = c00 + d00;
+        Gs[rr * 33 + cc + 1] = c01 + d01;
+        Gs[rr * 33 + cc + 8] = c10 + d10;
+        Gs[rr * 33 + cc + 9] = c11 + d11;
+      }
+      for (int t = tid; t < 32 * 32; t += nt) Js[(t >> 5) * 33 + (t & 31)] = ((t >> 5) == (t & 31)) ? 1.0 : 0.0;
+      __syncthreads();
       double off = 0.0;
       const int be = bs + (bs & 1);
       const int n_within = (r == 0) ? be - 1 : 0;
       const int n_cross = a.inner * bs;
+      const int mrow = tid & 31, mpair = tid >> 5;          // pairs mpair, mpair+8
       for (int t = 0; t < n_within + n_cross; ++t) {
-        // pair list of this round
-        if (tid < kJW / 2) {
+        if (tid < 16) {
           int p = -1, q = -1;
           if (t < n_within) {
-            const int np = be / 2;   // pairs per block
+            const int np = be / 2;
             if (tid < 2 * np) {
               const int blk = tid < np ? 0 : 1, k = tid - blk * np;
               const int xl = rr_player(k, t, be), yl = rr_player(be - 1 - k, t, be);
@@ -206,10 +223,12 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
           double cs = 1.0, sn = 0.0;
           if (p >= 0 && (gcol[p] < 0 || gcol[q] < 0)) p = -1;
           if (p >= 0) {
-            const double aa = Gs[p * kJL + p], bb = Gs[q * kJL + q], cc = Gs[p * kJL + q];
-            const double ab = sqrt(aa * bb);
-            if (fabs(cc) > tol * ab) {
-              off = fmax(off, fabs(cc) / ab);
+            const double aa = Gs[p * 33 + p], bb = Gs[q * 33 + q], cc = Gs[p * 33 + q];
+            // threshold / angle in fp32 (only cs^2 + sn^2 = 1 must be exact)
+            const float abf = sqrtf((float)aa) * sqrtf((float)bb);
+            const float cf = fabsf((float)cc);
+            if (cf > tolf * abf) {
+              off = fmax(off, (double)(cf / abf));
               const double zeta = (bb - aa) / (2.0 * cc);
               double tt2;
               if (fabs(zeta) > 1e15) {
@@ -230,59 +249,78 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
           rs[tid] = sn;
         }
         __syncthreads();
-        // column rotations of G and J:  x_p <- c x_p - s x_q ; x_q <- s x_p + c x_q
-        for (int e = tid; e < (kJW / 2) * kJW; e += nt) {
-          const int k = e / kJW, row = e - k * kJW;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k = mpair + 8 * h;
           const int p = rp[k];
-          if (p < 0 || row >= W) continue;
-          const int q = rq[k];
-          const double c = rc[k], s = rs[k];
-          const double gp = Gs[row * kJL + p], gq = Gs[row * kJL + q];
-          Gs[row * kJL + p] = c * gp - s * gq;
-          Gs[row * kJL + q] = s * gp + c * gq;
-          const double jp = Js[row * kJL + p], jq = Js[row * kJL + q];
-          Js[row * kJL + p] = c * jp - s * jq;
-          Js[row * kJL + q] = s * jp + c * jq;
+          if (p >= 0) {
+            const int q = rq[k];
+            const double c = rc[k], s = rs[k];
+            const double gp = Gs[mrow * 33 + p], gq = Gs[mrow * 33 + q];
+            Gs[mrow * 33 + p] = c * gp - s * gq;
+            Gs[mrow * 33 + q] = s * gp + c * gq;
+            const double jp = Js[mrow * 33 + p], jq = Js[mrow * 33 + q];
+            Js[mrow * 33 + p] = c * jp - s * jq;
+            Js[mrow * 33 + q] = s * jp + c * jq;
+          }
         }
         __syncthreads();
-        // row rotations of G (completes G <- J^T G J for this round)
-        for (int e = tid; e < (kJW / 2) * kJW; e += nt) {
-          const int k = e / kJW, col = e - k * kJW;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k = mpair + 8 * h;
           const int p = rp[k];
-          if (p < 0 || col >= W) continue;
-          const int q = rq[k];
-          const double c = rc[k], s = rs[k];
-          const double gp = Gs[p * kJL + col], gq = Gs[q * kJL + col];
-          Gs[p * kJL + col] = c * gp - s * gq;
-          Gs[q * kJL + col] = s * gp + c * gq;
+          if (p >= 0) {
+            const int q = rq[k];
+            const double c = rc[k], s = rs[k];
+            const double gp = Gs[p * 33 + mrow], gq = Gs[q * 33 + mrow];
+            Gs[p * 33 + mrow] = c * gp - s * gq;
+            Gs[q * 33 + mrow] = s * gp + c * gq;
+          }
         }
         __syncthreads();
       }
-      // 3. M_W <- M_W J, V_W <- V_W J (64-row chunks, DMMA, in place)
-      for (int pass = 0; pass < 2; ++pass) {
-        double* X = pass == 0 ? a.M : a.V;
-        const int64_t ldx = pass == 0 ? a.ldm : a.ldv;
-        for (int r0 = 0; r0 < l; r0 += kJCH) {
-          stage(Cs, X, ldx, gcol, r0, l);
+      apply_cols(Ms, Js, a.M, a.ldm, gcol, l, lpad);
+      if (VRES) {
+        apply_cols(Vs, Js, a.V, a.ldv, gcol, l, lpad);
+      } else {
+        for (int ch = 0; ch < lpad; ch += 64) {
           __syncthreads();
-          JAcc o;
-          jacc_zero(o);
-          jdmma(o, Cs, false, Js, kJW);
+          for (int t = tid; t < 64 * 32; t += nt) {
+            const int rr = t & 63, cc = t >> 6;
+            const int c = gcol[cc];
+            Vs[rr * kMW + cc] = (c >= 0 && ch + rr < l) ? a.V[(ch + rr) + (int64_t)c * a.ldv] : 0.0;
+          }
           __syncthreads();
-          jacc_store_cols(o, X, ldx, gcol, r0, l);
+          // reuse apply_cols on one 64-row chunk (rows offset ch)
+          const int fr = lane >> 2, fk = lane & 3;
+          double acc[4][2];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+          for (int k0 = 0; k0 < 32; k0 += 4) {
+            const double af = Vs[(warp * 8 + fr) * kMW + k0 + fk];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma_884(acc[j][0], acc[j][1], af, Js[(k0 + fk) * 33 + 8 * j + fr]);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const int row = ch + warp * 8 + (lane >> 2), cc = 8 * j + 2 * (lane & 3) + hh;
+              const int c = gcol[cc];
+              if (c >= 0 && row < l) a.V[row + (int64_t)c * a.ldv] = acc[j][hh];
+            }
         }
       }
-      // sweep-wide max |cos| (only the first inner pass over a pair counts as the
-      // fresh measurement; later passes are refinements of the same visit)
       off = warp_max(off);
-      if ((tid & 31) == 0 && off > 0.0)
+      if (lane == 0 && off > 0.0)
         atomicMax(reinterpret_cast<unsigned long long*>(&s_off),
                   (unsigned long long)__double_as_longlong(off));
       __syncthreads();
       if (tid == 0 && s_off > 0.0)
         atomicMax(reinterpret_cast<unsigned long long*>(a.offmax + sweep),
                   (unsigned long long)__double_as_longlong(s_off));
-      grid_barrier(a.bar, P);
+      round_barrier<CLUSTER>(a.bar, P);
     }
     const double om = *((volatile double*)(a.offmax + sweep));
     if (tid == 0 && blockIdx.x == 0) *a.sweeps = sweep + 1;
@@ -322,7 +360,10 @@ __global__ void jacobi_finish_kernel(const double* M, int64_t ldm, const double*
 }
 
 int jacobi_block_size(int l) {
-  int bs = 32;
+  int bs = 16;
+  if (const char* e = getenv("FFB_JACOBI_BS")) bs = atoi(e);
+  if (bs > 16) bs = 16;
+  if (bs < 2) bs = 2;
   while (bs > 2 && (l + bs - 1) / bs < 4) bs /= 2;   // keep >= 2 block pairs for small l
   return bs;
 }
@@ -337,18 +378,41 @@ cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, double* M, int64_t ldm, 
   if (nb % 2) ++nb;
   if (nb < 2) nb = 2;
   const int P = nb / 2;
-  JacobiArgs a{M, ldm, V, ldv, l, bs, nb, 1e-15 * sqrt((double)l), max_sweeps, bar, offmax, sweeps, 1};
-  const size_t smem = (size_t)3 * kJW * kJL * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  int inner = 1;
+  if (const char* e = getenv("FFB_JACOBI_INNER")) inner = atoi(e);
+  if (inner < 1) inner = 1;
+  JacobiArgs a{M, ldm, V, ldv, l, bs, nb, 1e-15 * sqrt((double)l), max_sweeps, bar, offmax, sweeps, inner};
+  const size_t lpad = (size_t)((l + 63) & ~63);
+  const size_t fixed = sizeof(double) * (lpad * kMW + 2 * 32 * 33);
+  const bool vres = fixed + sizeof(double) * lpad * kMW <= 220 * 1024;
+  const size_t smem = vres ? fixed + sizeof(double) * lpad * kMW : fixed + sizeof(double) * 64 * kMW;
+  if (smem > 220 * 1024) return cudaErrorInvalidValue;   // l > ~800 not supported
+  const bool cluster = P <= 16 && getenv("FFB_JACOBI_NOCLUSTER") == nullptr;
+  void* kern = cluster ? (vres ? (void*)jacobi_kernel<true, true> : (void*)jacobi_kernel<true, false>)
+                       : (vres ? (void*)jacobi_kernel<false, true> : (void*)jacobi_kernel<false, false>);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   cudaError_t e = cudaMemsetAsync(bar, 0, 2 * sizeof(uint32_t), st);
   if (e == cudaSuccess) e = cudaMemsetAsync(offmax, 0, sizeof(double) * max_sweeps, st);
   if (e != cudaSuccess) return e;
   void* args[] = {&a};
-  e = cudaLaunchCooperativeKernel((void*)jacobi_kernel, dim3(P), dim3(kJThreads), args, smem, st);
+  if (cluster) {
+    if (P > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P);
+    cfg.blockDim = dim3(kJThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = P;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelExC(&cfg, kern, args);
+  } else {
+    e = cudaLaunchCooperativeKernel(kern, dim3(P), dim3(kJThreads), args, smem, st);
+  }
   if (e != cudaSuccess) return e;
   jacobi_finish_kernel<<<1, 1024, sizeof(double) * (size_t)l, st>>>(M, ldm, V, ldv, l, sig, U, ldu,
                                                                     Vo, ldvo, order);
