@@ -16,6 +16,7 @@
 // two-sided iteration never accumulates into the factorization.  A grid barrier
 // separates rounds; sweeps stop when max |cos| seen in a sweep <= tol.
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "ffb_common.cuh"
@@ -83,51 +84,65 @@ FFB_DEV void round_barrier(uint32_t* bar, uint32_t P) {
   }
 }
 
-// stage the W local columns of X (rows < l) into S (lpad x kMW), loads in flight
-FFB_DEV void stage_cols(double* S, const double* X, int64_t ldx, const int* gcol, int l, int lpad) {
-  const int nt = blockDim.x;
-  const int total = lpad * 32;
-  for (int base = 0; base < total; base += nt * 16) {
-    double v[16];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int t = base + threadIdx.x + u * nt;
-      const int rr = t % lpad, cc = t / lpad;
-      const int c = (t < total) ? gcol[cc] : -1;
-      v[u] = (c >= 0 && rr < l) ? X[rr + (int64_t)c * ldx] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int t = base + threadIdx.x + u * nt;
-      if (t < total) S[(t % lpad) * kMW + t / lpad] = v[u];
+// stage the W (=32) local columns of X (rows < l) into S (lpad x kMW) with
+// cp.async (zero-fill beyond l / empty slots): every copy of the CTA is in flight
+// at once; the caller commits and waits.  Warp w: columns w, w+8, ..; lanes: rows.
+FFB_DEV void stage_cols_async(double* S, const double* X, int64_t ldx, const int* gcol, int l,
+                              int lpad) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int cc = warp; cc < 32; cc += 8) {
+    const int c = gcol[cc];
+    const double* src = X + (int64_t)(c < 0 ? 0 : c) * ldx;
+    for (int rr = lane; rr < lpad; rr += 32) {
+      const bool ok = c >= 0 && rr < l;
+      cp_async8(S + rr * kMW + cc, ok ? src + rr : X, ok);
     }
   }
 }
 
-// X_W <- S_W J (64-row chunks of S in smem), written straight to global
+// X_W <- S_W J (S: lpad x 32 in smem), written straight to global.  Warp w owns
+// row tiles w, w+8, .. (<= 7 for lpad <= 448) x all 4 column tiles: up to 28
+// independent DMMA accumulator chains per warp hide the DMMA latency.
 FFB_DEV void apply_cols(const double* S, const double* Js, double* X, int64_t ldx,
                         const int* gcol, int l, int lpad) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int fr = lane >> 2, fk = lane & 3;
-  for (int ch = 0; ch < lpad; ch += 64) {
-    double acc[4][2];
+  const int nrt = lpad >> 3;
+  constexpr int kMaxRT = 7;
+  for (int g0 = 0; g0 < nrt; g0 += 8 * kMaxRT) {
+    double acc[kMaxRT][4][2];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
-    const int rowt = ch + warp * 8;
+    for (int i = 0; i < kMaxRT; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 #pragma unroll
     for (int k0 = 0; k0 < 32; k0 += 4) {
-      const double af = S[(rowt + fr) * kMW + k0 + fk];
+      double bf[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) dmma_884(acc[j][0], acc[j][1], af, Js[(k0 + fk) * 33 + 8 * j + fr]);
+      for (int j = 0; j < 4; ++j) bf[j] = Js[(k0 + fk) * 33 + 8 * j + fr];
+#pragma unroll
+      for (int i = 0; i < kMaxRT; ++i) {
+        const int rt = g0 + warp + 8 * i;
+        if (rt < nrt) {
+          const double af = S[(rt * 8 + fr) * kMW + k0 + fk];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], af, bf[j]);
+        }
+      }
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int i = 0; i < kMaxRT; ++i) {
+      const int rt = g0 + warp + 8 * i;
+      if (rt >= nrt) continue;
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const int row = rowt + (lane >> 2), cc = 8 * j + 2 * (lane & 3) + hh;
-        const int c = gcol[cc];
-        if (c >= 0 && row < l) X[row + (int64_t)c * ldx] = acc[j][hh];
-      }
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int row = rt * 8 + (lane >> 2), cc = 8 * j + 2 * (lane & 3) + hh;
+          const int c = gcol[cc];
+          if (c >= 0 && row < l) X[row + (int64_t)c * ldx] = acc[i][j][hh];
+        }
+    }
   }
 }
 
@@ -149,6 +164,14 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
   const double tol = a.tol;
   const float tolf = (float)a.tol;
 
+  long long tp[6] = {0, 0, 0, 0, 0, 0};
+  long long tc = clock64();
+#define JPROF(i)                              \
+  if (a.prof && tid == 0) {                   \
+    const long long now = clock64();          \
+    tp[i] += now - tc;                        \
+    tc = now;                                 \
+  }
   for (int sweep = 0; sweep < a.max_sweeps; ++sweep) {
     if (tid == 0) s_off = 0.0;
     for (int r = 0; r < nb - 1; ++r) {
@@ -163,84 +186,110 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
         gcol[tid] = c;
       }
       __syncthreads();
-      stage_cols(Ms, a.M, a.ldm, gcol, l, lpad);
-      if (VRES) stage_cols(Vs, a.V, a.ldv, gcol, l, lpad);
+      stage_cols_async(Ms, a.M, a.ldm, gcol, l, lpad);
+      cp_async_commit();
+      cp_async_wait<0>();
       __syncthreads();
-      // fresh Gram G = M_W^T M_W (32 x 32): warp w -> rows 8*(w/2).., cols 16*(w%2)..
+      JPROF(0)
+      // fresh Gram G = M_W^T M_W: warp w sums rows [w*lpad/8, (w+1)*lpad/8) for all
+      // 16 output tiles (16 independent DMMA chains), partials reduced through smem
       {
-        const int r0 = (warp >> 1) * 8, c0 = (warp & 1) * 16;
+        double* part = VRES ? Vs : Gs;   // 8 x 32 x 33 scratch (VRES: V not staged yet)
         const int fr = lane >> 2, fk = lane & 3;
-        double c00 = 0, c01 = 0, c10 = 0, c11 = 0, d00 = 0, d01 = 0, d10 = 0, d11 = 0;
-        int k0 = 0;
-        for (; k0 + 4 < lpad; k0 += 8) {
-          const double af = Ms[(k0 + fk) * kMW + r0 + fr];
-          const double b0 = Ms[(k0 + fk) * kMW + c0 + fr];
-          const double b1 = Ms[(k0 + fk) * kMW + c0 + 8 + fr];
-          const double ag = Ms[(k0 + 4 + fk) * kMW + r0 + fr];
-          const double e0 = Ms[(k0 + 4 + fk) * kMW + c0 + fr];
-          const double e1 = Ms[(k0 + 4 + fk) * kMW + c0 + 8 + fr];
-          dmma_884(c00, c01, af, b0);
-          dmma_884(c10, c11, af, b1);
-          dmma_884(d00, d01, ag, e0);
-          dmma_884(d10, d11, ag, e1);
+        double acc[4][4][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        const int kr = lpad >> 3;                 // rows per warp (multiple of 8)
+        for (int k0 = warp * kr; k0 < (warp + 1) * kr; k0 += 4) {
+          double f[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) f[i] = Ms[(k0 + fk) * kMW + 8 * i + fr];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], f[i], f[j]);
         }
-        for (; k0 < lpad; k0 += 4) {
-          const double af = Ms[(k0 + fk) * kMW + r0 + fr];
-          dmma_884(c00, c01, af, Ms[(k0 + fk) * kMW + c0 + fr]);
-          dmma_884(c10, c11, af, Ms[(k0 + fk) * kMW + c0 + 8 + fr]);
+        if (VRES) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+                part[warp * 32 * 33 + (8 * i + fr) * 33 + 8 * j + 2 * fk + h] = acc[i][j][h];
+          __syncthreads();
+          for (int t = tid; t < 32 * 32; t += nt) {
+            const int r = t >> 5, c = t & 31;
+            double sum = 0.0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) sum += part[w * 32 * 33 + r * 33 + c];
+            Gs[r * 33 + c] = sum;
+          }
+          __syncthreads();
+          // V staging overlaps the inner rotations
+          stage_cols_async(Vs, a.V, a.ldv, gcol, l, lpad);
+          cp_async_commit();
+        } else {
+          // no scratch: accumulate warp partials into Gs with fixed-order passes
+          for (int t = tid; t < 32 * 32; t += nt) Gs[(t >> 5) * 33 + (t & 31)] = 0.0;
+          __syncthreads();
+          for (int w = 0; w < 8; ++w) {
+            if (warp == w) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                  for (int h = 0; h < 2; ++h) Gs[(8 * i + fr) * 33 + 8 * j + 2 * fk + h] += acc[i][j][h];
+            }
+            __syncthreads();
+          }
         }
-        const int rr = r0 + (lane >> 2), cc = c0 + 2 * (lane & 3);
-        Gs[rr * 33 + cc] = c00 + d00;
-        Gs[rr * 33 + cc + 1] = c01 + d01;
-        Gs[rr * 33 + cc + 8] = c10 + d10;
-        Gs[rr * 33 + cc + 9] = c11 + d11;
       }
       for (int t = tid; t < 32 * 32; t += nt) Js[(t >> 5) * 33 + (t & 31)] = ((t >> 5) == (t & 31)) ? 1.0 : 0.0;
       __syncthreads();
+      JPROF(1)
       double off = 0.0;
       const int be = bs + (bs & 1);
       const int n_within = (r == 0) ? be - 1 : 0;
       const int n_cross = a.inner * bs;
-      const int mrow = tid & 31, mpair = tid >> 5;          // pairs mpair, mpair+8
+      // every round pairs all 32 local slots (16 disjoint pairs); thread (pa, pb)
+      // owns the 2x2 block (pair pa rows, pair pb cols) of G and of J
+      const int ba = tid >> 4, bb2 = tid & 15;
       for (int t = 0; t < n_within + n_cross; ++t) {
         if (tid < 16) {
-          int p = -1, q = -1;
+          int p, q;
           if (t < n_within) {
-            const int np = be / 2;
-            if (tid < 2 * np) {
-              const int blk = tid < np ? 0 : 1, k = tid - blk * np;
-              const int xl = rr_player(k, t, be), yl = rr_player(be - 1 - k, t, be);
-              if (xl < bs && yl < bs) {
-                p = blk * bs + xl;
-                q = blk * bs + yl;
-              }
-            }
-          } else if (tid < bs) {
+            const int np = be / 2;                    // pairs per block (bs even: bs/2)
+            const int blk = tid < np ? 0 : 1, k = tid - blk * np;
+            p = blk * bs + rr_player(k, t, be);
+            q = blk * bs + rr_player(be - 1 - k, t, be);
+          } else {
             const int tt = (t - n_within) % bs;
             p = tid;
             q = bs + (tid + tt) % bs;
           }
           double cs = 1.0, sn = 0.0;
-          if (p >= 0 && (gcol[p] < 0 || gcol[q] < 0)) p = -1;
-          if (p >= 0) {
+          if (gcol[p] >= 0 && gcol[q] >= 0) {
             const double aa = Gs[p * 33 + p], bb = Gs[q * 33 + q], cc = Gs[p * 33 + q];
             // threshold / angle in fp32 (only cs^2 + sn^2 = 1 must be exact)
             const float abf = sqrtf((float)aa) * sqrtf((float)bb);
             const float cf = fabsf((float)cc);
             if (cf > tolf * abf) {
               off = fmax(off, (double)(cf / abf));
-              const double zeta = (bb - aa) / (2.0 * cc);
+              // angle entirely in fp32 (t only sets how much of x^T y is removed);
+              // cs = 1/sqrt(1+t^2) in fp64 keeps the rotation exactly orthogonal
+              const float zf = (float)(bb - aa) / (2.0f * (float)cc);
               double tt2;
-              if (fabs(zeta) > 1e15) {
-                tt2 = 0.5 / zeta;
+              if (fabsf(zf) > 1e15f || !isfinite(zf)) {
+                tt2 = 0.5 / ((bb - aa) / (2.0 * cc));
               } else {
-                const float zf = (float)zeta;
-                tt2 = (double)(copysignf(1.0f, zf) / (fabsf(zf) + sqrtf(1.0f + zf * zf)));
+                tt2 = (double)(copysignf(1.0f, zf) / (fabsf(zf) + sqrtf(fmaf(zf, zf, 1.0f))));
               }
               cs = rsqrt(1.0 + tt2 * tt2);
               sn = cs * tt2;
-            } else {
-              p = -1;
             }
           }
           rp[tid] = p;
@@ -249,38 +298,34 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
           rs[tid] = sn;
         }
         __syncthreads();
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int k = mpair + 8 * h;
-          const int p = rp[k];
-          if (p >= 0) {
-            const int q = rq[k];
-            const double c = rc[k], s = rs[k];
-            const double gp = Gs[mrow * 33 + p], gq = Gs[mrow * 33 + q];
-            Gs[mrow * 33 + p] = c * gp - s * gq;
-            Gs[mrow * 33 + q] = s * gp + c * gq;
-            const double jp = Js[mrow * 33 + p], jq = Js[mrow * 33 + q];
-            Js[mrow * 33 + p] = c * jp - s * jq;
-            Js[mrow * 33 + q] = s * jp + c * jq;
-          }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int k = mpair + 8 * h;
-          const int p = rp[k];
-          if (p >= 0) {
-            const int q = rq[k];
-            const double c = rc[k], s = rs[k];
-            const double gp = Gs[p * 33 + mrow], gq = Gs[q * 33 + mrow];
-            Gs[p * 33 + mrow] = c * gp - s * gq;
-            Gs[q * 33 + mrow] = s * gp + c * gq;
-          }
+        {
+          const int pa = rp[ba], qa = rq[ba], pb = rp[bb2], qb = rq[bb2];
+          const double ca = rc[ba], sa = rs[ba], cb = rc[bb2], sb = rs[bb2];
+          // G_blk <- R_a^T G_blk R_b with R = [[c, s], [-s, c]] acting on (p, q)
+          const double g00 = Gs[pa * 33 + pb], g01 = Gs[pa * 33 + qb];
+          const double g10 = Gs[qa * 33 + pb], g11 = Gs[qa * 33 + qb];
+          const double h00 = cb * g00 - sb * g01, h01 = sb * g00 + cb * g01;   // columns
+          const double h10 = cb * g10 - sb * g11, h11 = sb * g10 + cb * g11;
+          // J rows (pa, qa) x columns (pb, qb): J <- J R_b (column rotation only)
+          const double j00 = Js[pa * 33 + pb], j01 = Js[pa * 33 + qb];
+          const double j10 = Js[qa * 33 + pb], j11 = Js[qa * 33 + qb];
+          __syncthreads();
+          Gs[pa * 33 + pb] = ca * h00 - sa * h10;
+          Gs[pa * 33 + qb] = ca * h01 - sa * h11;
+          Gs[qa * 33 + pb] = sa * h00 + ca * h10;
+          Gs[qa * 33 + qb] = sa * h01 + ca * h11;
+          Js[pa * 33 + pb] = cb * j00 - sb * j01;
+          Js[pa * 33 + qb] = sb * j00 + cb * j01;
+          Js[qa * 33 + pb] = cb * j10 - sb * j11;
+          Js[qa * 33 + qb] = sb * j10 + cb * j11;
         }
         __syncthreads();
       }
+      JPROF(2)
       apply_cols(Ms, Js, a.M, a.ldm, gcol, l, lpad);
       if (VRES) {
+        cp_async_wait<0>();
+        __syncthreads();
         apply_cols(Vs, Js, a.V, a.ldv, gcol, l, lpad);
       } else {
         for (int ch = 0; ch < lpad; ch += 64) {
@@ -312,6 +357,8 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
             }
         }
       }
+      __syncthreads();
+      JPROF(3)
       off = warp_max(off);
       if (lane == 0 && off > 0.0)
         atomicMax(reinterpret_cast<unsigned long long*>(&s_off),
@@ -320,12 +367,17 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
       if (tid == 0 && s_off > 0.0)
         atomicMax(reinterpret_cast<unsigned long long*>(a.offmax + sweep),
                   (unsigned long long)__double_as_longlong(s_off));
+      JPROF(4)
       round_barrier<CLUSTER>(a.bar, P);
+      JPROF(5)
     }
     const double om = *((volatile double*)(a.offmax + sweep));
     if (tid == 0 && blockIdx.x == 0) *a.sweeps = sweep + 1;
     if (!(om > tol)) break;
   }
+  if (a.prof && tid == 0 && blockIdx.x == 0)
+    for (int i = 0; i < 6; ++i) a.prof[i] = tp[i];
+#undef JPROF
 }
 
 // sigma_j = ||M[:, j]||; rank sort (descending, ties by index); outputs sorted
@@ -360,12 +412,8 @@ __global__ void jacobi_finish_kernel(const double* M, int64_t ldm, const double*
 }
 
 int jacobi_block_size(int l) {
-  int bs = 16;
-  if (const char* e = getenv("FFB_JACOBI_BS")) bs = atoi(e);
-  if (bs > 16) bs = 16;
-  if (bs < 2) bs = 2;
-  while (bs > 2 && (l + bs - 1) / bs < 4) bs /= 2;   // keep >= 2 block pairs for small l
-  return bs;
+  (void)l;
+  return 16;   // every inner round pairs all 32 staged slots (empty slots rotate trivially)
 }
 
 cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, double* M, int64_t ldm, double* V,
@@ -381,11 +429,15 @@ cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, double* M, int64_t ldm, 
   int inner = 1;
   if (const char* e = getenv("FFB_JACOBI_INNER")) inner = atoi(e);
   if (inner < 1) inner = 1;
-  JacobiArgs a{M, ldm, V, ldv, l, bs, nb, 1e-15 * sqrt((double)l), max_sweeps, bar, offmax, sweeps, inner};
+  static long long* prof = nullptr;
+  if (getenv("FFB_JACOBI_PROF") && !prof) cudaMallocManaged(&prof, 8 * sizeof(long long));
+  JacobiArgs a{M, ldm, V, ldv, l, bs, nb, 1e-15 * sqrt((double)l), max_sweeps, bar, offmax, sweeps, inner, prof};
   const size_t lpad = (size_t)((l + 63) & ~63);
   const size_t fixed = sizeof(double) * (lpad * kMW + 2 * 32 * 33);
-  const bool vres = fixed + sizeof(double) * lpad * kMW <= 220 * 1024;
-  const size_t smem = vres ? fixed + sizeof(double) * lpad * kMW : fixed + sizeof(double) * 64 * kMW;
+  // V region: V_W when resident (>= 8 x 32 x 33 doubles, it doubles as Gram scratch)
+  const size_t vreg = sizeof(double) * (lpad > 256 ? lpad : 256) * kMW;
+  const bool vres = fixed + vreg <= 220 * 1024;
+  const size_t smem = vres ? fixed + vreg : fixed + sizeof(double) * 64 * kMW;
   if (smem > 220 * 1024) return cudaErrorInvalidValue;   // l > ~800 not supported
   const bool cluster = P <= 16 && getenv("FFB_JACOBI_NOCLUSTER") == nullptr;
   void* kern = cluster ? (vres ? (void*)jacobi_kernel<true, true> : (void*)jacobi_kernel<true, false>)
@@ -416,6 +468,11 @@ cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, double* M, int64_t ldm, 
   if (e != cudaSuccess) return e;
   jacobi_finish_kernel<<<1, 1024, sizeof(double) * (size_t)l, st>>>(M, ldm, V, ldv, l, sig, U, ldu,
                                                                     Vo, ldvo, order);
+  if (prof) {
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "jacobi phases (cycles, CTA0): stage %lld gram %lld inner %lld apply %lld off %lld barrier %lld\n",
+            prof[0], prof[1], prof[2], prof[3], prof[4], prof[5]);
+  }
   return cudaGetLastError();
 }
 

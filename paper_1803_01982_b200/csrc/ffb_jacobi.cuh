@@ -16,6 +16,7 @@ struct JacobiArgs {
   double* offmax;    // [max_sweeps]
   int* sweeps;       // sweeps executed
   int inner;         // passes over the cross-block pairs per visit
+  long long* prof;   // optional phase timers (debug)
 };
 
 int jacobi_block_size(int l);
