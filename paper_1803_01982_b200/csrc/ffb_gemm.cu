@@ -8,10 +8,10 @@ namespace ffb {
 
 namespace {
 
-template <int BM, int BN, int BK, int WM, int WN, bool AK, bool BKC, int ST>
-cudaError_t launch_cfg(cudaStream_t st, const GemmArgs& g, dim3 grid) {
+template <int BM, int BN, int BK, int WM, int WN, bool AK, bool BKC, int ST, bool V2>
+cudaError_t launch_cfg1(cudaStream_t st, const GemmArgs& g, dim3 grid) {
   using Cfg = GemmCfg<BM, BN, BK, WM, WN, AK, BKC, ST>;
-  auto kern = gemm_f64_kernel<BM, BN, BK, WM, WN, AK, BKC, ST>;
+  auto kern = gemm_f64_kernel<BM, BN, BK, WM, WN, AK, BKC, ST, V2>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
@@ -19,6 +19,18 @@ cudaError_t launch_cfg(cudaStream_t st, const GemmArgs& g, dim3 grid) {
   }
   kern<<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(g);
   return cudaGetLastError();
+}
+
+// 16-byte pair loads need 16-byte aligned bases and even leading dimensions
+inline bool vec2_ok(const GemmArgs& g) {
+  auto al = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
+  return al(g.A) && al(g.B) && (g.lda % 2 == 0) && (g.ldb % 2 == 0) && (g.k_per % 2 == 0);
+}
+
+template <int BM, int BN, int BK, int WM, int WN, bool AK, bool BKC, int ST>
+cudaError_t launch_cfg(cudaStream_t st, const GemmArgs& g, dim3 grid) {
+  if (vec2_ok(g)) return launch_cfg1<BM, BN, BK, WM, WN, AK, BKC, ST, true>(st, g, grid);
+  return launch_cfg1<BM, BN, BK, WM, WN, AK, BKC, ST, false>(st, g, grid);
 }
 
 struct Shape {

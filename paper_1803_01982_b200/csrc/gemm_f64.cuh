@@ -46,7 +46,76 @@ struct GemmCfg {
   static constexpr size_t kSmem = sizeof(double) * (size_t)STAGES * (kAStage + kBStage);
 };
 
-template <int BM, int BN, int BK, int WM, int WN, bool A_KC, bool B_KC, int STAGES>
+// Operand tile loader: each thread owns a fixed set of (row, k) slots of the
+// tile; global pointers and shared offsets are computed once and advanced by a
+// constant per k-tile.  VEC2: 16-byte cp.async pairs along the contiguous
+// dimension (requires 16-byte aligned base and even leading dimension).
+template <int R, int BK, bool KC, bool VEC2, int NT>
+struct TileLoader {
+  // elements (or pairs) per thread
+  static constexpr int kUnits = (R * BK) / (VEC2 ? 2 : 1);
+  static constexpr int kPer = (kUnits + NT - 1) / NT;
+  static constexpr int LD = KC ? APad<R, BK>::kc : APad<R, BK>::mc;
+  const double* g[kPer];
+  uint32_t soff[kPer];
+  int kk[kPer];      // k index inside the tile of the unit's first element
+  int rr[kPer];      // row (M or N) index of the unit (first element)
+  bool live[kPer];
+
+  FFB_DEV void init(const double* base, int64_t ld, int64_t r0, int64_t rows, int64_t k0, int tid) {
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int idx = tid + u * NT;
+      live[u] = idx < kUnits;
+      int r, k;
+      if (KC) {   // k contiguous: units run along k
+        constexpr int kpr = VEC2 ? BK / 2 : BK;
+        r = idx / kpr;
+        k = (idx % kpr) * (VEC2 ? 2 : 1);
+      } else {    // row contiguous: units run along rows
+        constexpr int rpk = VEC2 ? R / 2 : R;
+        k = idx / rpk;
+        r = (idx % rpk) * (VEC2 ? 2 : 1);
+      }
+      rr[u] = r;
+      kk[u] = k;
+      const int64_t gr = r0 + r;
+      live[u] = live[u] && gr < rows;
+      g[u] = base + (live[u] ? (KC ? (k0 + k) + gr * ld : gr + (k0 + k) * ld) : 0);
+      soff[u] = KC ? (uint32_t)(r * LD + k) : (uint32_t)(k * LD + r);
+    }
+  }
+  // kvalid: number of valid k in this tile (BK except the K tail); rows: bound
+  FFB_DEV void load(double* smem, int kvalid, int64_t r0, int64_t rows, int64_t ld) {
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      if (u * NT + (int)threadIdx.x >= kUnits) continue;
+      double* dst = smem + soff[u];
+      if (VEC2) {
+        int bytes = 0;
+        if (live[u]) {
+          if (KC) {
+            bytes = kk[u] + 1 < kvalid ? 16 : (kk[u] < kvalid ? 8 : 0);
+          } else {
+            bytes = kk[u] < kvalid ? (r0 + rr[u] + 1 < rows ? 16 : 8) : 0;
+          }
+        }
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)),
+                     "l"(bytes ? g[u] : g[0]), "r"(bytes));
+      } else {
+        const bool ok = live[u] && kk[u] < kvalid;
+        cp_async8(dst, ok ? g[u] : g[0], ok);
+      }
+    }
+    (void)ld;
+  }
+  FFB_DEV void advance(int64_t ld) {
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) g[u] += KC ? BK : (int64_t)BK * ld;
+  }
+};
+
+template <int BM, int BN, int BK, int WM, int WN, bool A_KC, bool B_KC, int STAGES, bool VEC2>
 __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES>::kThreads)
     gemm_f64_kernel(GemmArgs g) {
   using Cfg = GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES>;
@@ -65,28 +134,10 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
   const int64_t kend = min(g.K, kbeg + g.k_per);
   const int nk = kbeg < kend ? (int)((kend - kbeg + BK - 1) / BK) : 0;
 
-  auto load_tile = [&](int stage, int64_t k0) {
-    double* as = As + stage * Cfg::kAStage;
-    double* bs = Bs + stage * Cfg::kBStage;
-#pragma unroll 4
-    for (int idx = tid; idx < BM * BK; idx += NT) {
-      int i, kk;
-      if (A_KC) { kk = idx % BK; i = idx / BK; } else { i = idx % BM; kk = idx / BM; }
-      const int64_t gi = i0 + i, gk = k0 + kk;
-      const bool ok = gi < g.M && gk < kend;
-      const double* src = g.A + (ok ? (A_KC ? gk + gi * g.lda : gi + gk * g.lda) : 0);
-      cp_async8(as + (A_KC ? i * ALD + kk : kk * ALD + i), src, ok);
-    }
-#pragma unroll 4
-    for (int idx = tid; idx < BN * BK; idx += NT) {
-      int j, kk;
-      if (B_KC) { kk = idx % BK; j = idx / BK; } else { j = idx % BN; kk = idx / BN; }
-      const int64_t gj = j0 + j, gk = k0 + kk;
-      const bool ok = gj < g.N && gk < kend;
-      const double* src = g.B + (ok ? (B_KC ? gk + gj * g.ldb : gj + gk * g.ldb) : 0);
-      cp_async8(bs + (B_KC ? j * BLD + kk : kk * BLD + j), src, ok);
-    }
-  };
+  TileLoader<BM, BK, A_KC, VEC2, NT> la;
+  TileLoader<BN, BK, B_KC, VEC2, NT> lb;
+  la.init(g.A, g.lda, i0, g.M, kbeg, tid);
+  lb.init(g.B, g.ldb, j0, g.N, kbeg, tid);
 
   double acc[Cfg::kTM][Cfg::kTN][2];
 #pragma unroll
@@ -94,9 +145,21 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
 #pragma unroll
     for (int b = 0; b < Cfg::kTN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
+  int fetched = 0;
+  auto fetch = [&](int stage) {
+    const int64_t k0 = kbeg + (int64_t)fetched * BK;
+    const int64_t krem = kend - k0;
+    const int kvalid = krem < BK ? (int)krem : BK;
+    la.load(As + stage * Cfg::kAStage, kvalid, i0, g.M, g.lda);
+    lb.load(Bs + stage * Cfg::kBStage, kvalid, j0, g.N, g.ldb);
+    la.advance(g.lda);
+    lb.advance(g.ldb);
+    ++fetched;
+  };
+
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) load_tile(s, kbeg + (int64_t)s * BK);
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < nk) fetch(st);
     cp_async_commit();
   }
 
@@ -106,7 +169,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
     __syncthreads();
     {
       const int pf = kt + STAGES - 1;
-      if (pf < nk) load_tile(pf % STAGES, kbeg + (int64_t)pf * BK);
+      if (pf < nk) fetch(pf % STAGES);
       cp_async_commit();
     }
     const double* as = As + (kt % STAGES) * Cfg::kAStage;
