@@ -89,6 +89,7 @@ struct Work {
   int *jsweeps, *jorder;
   double* gpart;
   size_t gpart_cap;
+  unsigned* skcnt;
 };
 
 int64_t max_i(int64_t a, int64_t b) { return a > b ? a : b; }
@@ -181,8 +182,9 @@ size_t carve(const ffb_ctx* ctx, const Dims& D, void* base, size_t cap, Work& w)
     w.jorder = b.take<int>(l);
   }
   // split-K scratch: the rest, at least 4 Mi doubles
-  w.gpart_cap = std::max<size_t>(4u << 20, (size_t)64 * kPanelW * kPanelW);
+  w.gpart_cap = std::max<size_t>(16u << 20, (size_t)64 * kPanelW * kPanelW);
   w.gpart = b.take<double>(w.gpart_cap);
+  w.skcnt = b.take<unsigned>(65536);
   return b.off + kAlign;
 }
 
@@ -323,8 +325,15 @@ int ffb_gemm(ffb_ctx* ctx, void* stream, int64_t M, int64_t N, int64_t K, double
   if (!ctx) return FFB_ERR_ARGUMENT;
   GemmCtx gc;
   gc.sms = ctx->sms;
-  gc.partial = static_cast<double*>(workspace);
-  gc.partial_cap = workspace ? workspace_bytes / sizeof(double) : 0;
+  // workspace: [stream-K counters (64Ki u32, zeroed here) | split-K / stream-K partials]
+  const size_t cnt_bytes = 65536 * sizeof(unsigned);
+  if (workspace && workspace_bytes > cnt_bytes + 4096) {
+    gc.counters = static_cast<unsigned*>(workspace);
+    gc.counter_cap = 65536;
+    cudaMemsetAsync(workspace, 0, cnt_bytes, (cudaStream_t)stream);
+    gc.partial = reinterpret_cast<double*>(static_cast<char*>(workspace) + cnt_bytes);
+    gc.partial_cap = (workspace_bytes - cnt_bytes) / sizeof(double);
+  }
   cudaError_t e = gemm_f64(gc, (cudaStream_t)stream, M, N, K, alpha, A, lda, a_kc != 0, B, ldb,
                            b_kc != 0, beta, C, ldc);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "ffb_gemm");
@@ -381,6 +390,8 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
   e.gc.sms = ctx->sms;
   e.gc.partial = w.gpart;
   e.gc.partial_cap = w.gpart_cap;
+  e.gc.counters = w.skcnt;
+  e.gc.counter_cap = 65536;
   cudaStream_t st = e.st;
   const int64_t l = D.l, s = D.s, L1 = l + 1;
 
@@ -406,6 +417,7 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
 
   // ---------------------------------------------------------------- TRQRCP
   e.ok(cudaMemsetAsync(w.status, 0, sizeof(uint32_t), st));
+  e.ok(cudaMemsetAsync(w.skcnt, 0, sizeof(unsigned) * 65536, st));
   // B = Omega * A (Omega row-major s x m: A-operand with contiguous k)
   e.gemm(s, n, m, 1.0, omega, m, true, A, lda, true, 0.0, w.B, s);
   e.ok(launch_colsq(st, A, lda, m, n, w.colsq));

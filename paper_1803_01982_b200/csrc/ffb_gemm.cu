@@ -21,6 +21,30 @@ cudaError_t launch_cfg1(cudaStream_t st, const GemmArgs& g, dim3 grid) {
   return cudaGetLastError();
 }
 
+// resident CTAs per SM of a tile config (cached)
+template <int BM, int BN, int BK, int WM, int WN, int ST>
+int occupancy() {
+  static int occ = 0;
+  if (!occ) {
+    using Cfg = GemmCfg<BM, BN, BK, WM, WN, true, true, ST>;
+    auto kern = gemm_f64_kernel<BM, BN, BK, WM, WN, true, true, ST, true>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::kThreads, Cfg::kSmem) != cudaSuccess || occ < 1)
+      occ = 1;
+  }
+  return occ;
+}
+
+int occupancy_of(int cfg) {
+  switch (cfg) {
+    case 0: return occupancy<48, 64, 16, 24, 32, 4>();
+    case 1: return occupancy<64, 64, 16, 32, 32, 4>();
+    case 2: return occupancy<96, 64, 16, 48, 32, 4>();
+    case 3: return occupancy<128, 64, 16, 32, 32, 3>();
+    default: return occupancy<128, 96, 16, 32, 48, 3>();
+  }
+}
+
 // 16-byte pair loads need 16-byte aligned bases and even leading dimensions
 inline bool vec2_ok(const GemmArgs& g) {
   auto al = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
@@ -39,15 +63,19 @@ struct Shape {
 
 // Tile selection by M (the output rows): sketch / WT rows have M = s or b <= 96,
 // the tall products (A*Yhat, panel updates) have M = m.
-int pick_cfg(int64_t M) {
+int pick_cfg(int64_t M, int64_t N) {
   if (M <= 48) return 0;
   if (M <= 64) return 1;
   if (M <= 96) return 2;
-  if (M >= 1024) return 3;
+  if (M >= 1024) {
+    // tall products (N = l): pick the N tile with less padding waste
+    const int64_t w64 = (N + 63) / 64 * 64 - N, w96 = (N + 95) / 96 * 96 - N;
+    return (N > 64 && w96 < w64) ? 4 : 3;
+  }
   return 1;
 }
 
-const Shape kShapes[4] = {{48, 64, 16}, {64, 64, 16}, {96, 64, 16}, {128, 64, 16}};
+const Shape kShapes[5] = {{48, 64, 16}, {64, 64, 16}, {96, 64, 16}, {128, 64, 16}, {128, 96, 16}};
 
 template <bool AK, bool BKC>
 cudaError_t launch_layout(int cfg, cudaStream_t st, const GemmArgs& g, dim3 grid) {
@@ -55,7 +83,8 @@ cudaError_t launch_layout(int cfg, cudaStream_t st, const GemmArgs& g, dim3 grid
     case 0: return launch_cfg<48, 64, 16, 24, 32, AK, BKC, 4>(st, g, grid);
     case 1: return launch_cfg<64, 64, 16, 32, 32, AK, BKC, 4>(st, g, grid);
     case 2: return launch_cfg<96, 64, 16, 48, 32, AK, BKC, 4>(st, g, grid);
-    default: return launch_cfg<128, 64, 16, 32, 32, AK, BKC, 4>(st, g, grid);
+    case 3: return launch_cfg<128, 64, 16, 32, 32, AK, BKC, 3>(st, g, grid);
+    default: return launch_cfg<128, 96, 16, 32, 48, AK, BKC, 3>(st, g, grid);
   }
 }
 
@@ -65,9 +94,9 @@ cudaError_t gemm_f64(GemmCtx& c, cudaStream_t st, int64_t M, int64_t N, int64_t 
                      const double* A, int64_t lda, bool akc, const double* B, int64_t ldb, bool bkc,
                      double beta, double* C, int64_t ldc, GemmPartialOut* pout) {
   if (M <= 0 || N <= 0) return cudaSuccess;
-  const int cfg = pick_cfg(M);
+  const int cfg = pick_cfg(M, N);
   const Shape sh = kShapes[cfg];
-  const int64_t gx = (N + sh.bn - 1) / sh.bn, gy = (M + sh.bm - 1) / sh.bm;
+  int64_t gx = (N + sh.bn - 1) / sh.bn, gy = (M + sh.bm - 1) / sh.bm;
   const int64_t tiles = gx * gy;
   const int64_t target = 2LL * c.sms;
   int64_t splits = 1;
@@ -97,6 +126,11 @@ cudaError_t gemm_f64(GemmCtx& c, cudaStream_t st, int64_t M, int64_t N, int64_t 
   g.partial = c.partial;
   g.splits = (int)splits;
   g.force_partial = pout ? 1 : 0;
+  g.sk_per = 0;
+  g.sk_maxseg = 0;
+  g.sk_tiles_n = (int)gx;
+  g.sk_kiters = (K + sh.bk - 1) / sh.bk;
+  g.sk_cnt = nullptr;
   int64_t kper = (K + splits - 1) / splits;
   kper = ((kper + sh.bk - 1) / sh.bk) * sh.bk;
   g.k_per = std::max<int64_t>(kper, sh.bk);
@@ -113,6 +147,45 @@ cudaError_t gemm_f64(GemmCtx& c, cudaStream_t st, int64_t M, int64_t N, int64_t 
     // C = beta * C (alpha * 0): handled by a tile pass with empty K.
     g.splits = 1;
     g.force_partial = pout ? 1 : 0;
+  }
+  // Stream-K (persistent, equal iteration ranges, deterministic fixup) whenever the
+  // classic grid would leave SMs idle: removes split-K wave quantisation.
+  bool use_sk = false;
+  if (!pout && K > 0) {
+    const int64_t slots = (int64_t)c.sms * occupancy_of(cfg);
+    const int64_t kit = g.sk_kiters;
+    const int64_t waves = (tiles + slots - 1) / slots;
+    const double eff = (double)tiles / (double)(waves * slots);
+    if (eff < 0.9 && kit >= 8 && tiles >= 32) {
+      const int64_t total = tiles * kit;
+      // <= 8 CTAs cover any tile (bounded fixup work), >= 4 k-tiles per CTA
+      int64_t G = std::min<int64_t>(std::min<int64_t>(slots, tiles * 8), std::max<int64_t>(1, total / 4));
+      int64_t per = (total + G - 1) / G;
+      G = (total + per - 1) / per;
+      const int64_t maxseg = (per + kit - 1) / kit + 1;
+      const int64_t maxcover = per / kit + 2;   // CTAs covering one tile
+      if ((size_t)G * maxseg * sh.bm * sh.bn <= c.partial_cap && c.counters &&
+          tiles <= (int64_t)c.counter_cap && kit / per + 2 <= 16) {
+        use_sk = true;
+        g.sk_per = per;
+        g.sk_cnt = c.counters;
+        g.sk_maxseg = (int)maxseg;
+        g.splits = 1;
+        gx = G;
+        gy = 1;
+      }
+    }
+  }
+  if (use_sk) {
+    dim3 grid((unsigned)gx, 1, 1);
+    cudaError_t e;
+    if (akc && bkc) e = launch_layout<true, true>(cfg, st, g, grid);
+    else if (akc && !bkc) e = launch_layout<true, false>(cfg, st, g, grid);
+    else if (!akc && bkc) e = launch_layout<false, true>(cfg, st, g, grid);
+    else e = launch_layout<false, false>(cfg, st, g, grid);
+    c.launches += 1;
+    c.flops += 2 * M * N * K;
+    return e;
   }
   dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)g.splits);
   cudaError_t e;

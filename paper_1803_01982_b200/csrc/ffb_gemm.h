@@ -9,6 +9,8 @@ struct GemmCtx {
   int sms = 148;
   double* partial = nullptr;   // split-K scratch
   size_t partial_cap = 0;      // doubles
+  unsigned* counters = nullptr;  // stream-K per-tile arrival counters (zeroed)
+  size_t counter_cap = 0;
   int64_t flops = 0;
   int64_t launches = 0;
 };

@@ -1046,79 +1046,100 @@ cudaError_t launch_ext_row(cudaStream_t st, const double* A, int64_t lda, int64_
   FFB_LAUNCH_CHECK();
 }
 
-// g2 estimate (ffsrqr/srqr.py:49-64): Z = Rtilde^{-1} Omega^T by back
-// substitution, one warp per right-hand side; row norms; first argmax;
+// g2 estimate (ffsrqr/srqr.py:49-64): Z = Rtilde^{-1} Omega^T by right-looking
+// back substitution — column i of Rtilde is the contiguous R[:i+1, arr[i]], so
+// each step reads one coalesced column (prefetched one step ahead) and updates
+// the d right-hand sides of all rows above; row norms; first argmax;
 // g2 = |alpha|/sqrt(d) * max.  Omega is d x (l+1) row-major (numpy C order).
+constexpr int kG2MaxD = 16;
 __global__ void __launch_bounds__(1024) g2_kernel(const double* __restrict__ R, int64_t ldr,
                                                   const int64_t* __restrict__ arr, int64_t l,
                                                   const double* __restrict__ omega, int d, double g,
                                                   double* Z, SrqrScalars* sc) {
+  extern __shared__ double g2s[];
   __shared__ double red_v[32];
   __shared__ int64_t red_i[32];
   __shared__ int sing;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int64_t L1 = l + 1;
+  double* bz = g2s;                  // [d][L1] right-hand sides -> solution
+  double* col = bz + (size_t)d * L1; // [2][L1] double-buffered column of Rtilde
   const double alpha = sc->alpha;
-  if (threadIdx.x == 0) sing = 0;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (tid == 0) sing = 0;
   __syncthreads();
   if (!(alpha > 0.0)) {
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
       sc->g2 = 0.0;
       sc->i_off = 0;
       sc->need_swap = 0;
     }
     return;
   }
-  for (int64_t i = threadIdx.x; i < L1; i += blockDim.x) {
+  for (int64_t i = tid; i < L1; i += nt) {
     const double dv = (i == l) ? alpha : R[i + arr[i] * ldr];
     if (dv == 0.0) sing = 1;
   }
+  for (int64_t t = tid; t < (int64_t)d * L1; t += nt) bz[t] = omega[t];   // row-major d x L1
+  // column l of Rtilde: R[:l, arr[l]] and alpha on the diagonal
+  for (int64_t k = tid; k < L1; k += nt) col[L1 + k] = (k == l) ? alpha : R[k + arr[l] * ldr];
   __syncthreads();
   if (sing) {
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
       sc->status |= kStSingular;
       sc->need_swap = 0;
     }
     return;
   }
-  for (int rhs = wid; rhs < d; rhs += nw) {
-    double* z = Z + (int64_t)rhs * L1;
-    for (int64_t i = l; i >= 0; --i) {
-      double acc = 0.0;
-      for (int64_t j = i + 1 + lane; j <= l; j += 32) {
-        const double rij = (j == l && i == l) ? alpha : R[i + arr[j] * ldr];
-        acc = fma(rij, z[j], acc);
-      }
-      acc = warp_sum(acc);
-      if (lane == 0) {
-        const double dii = (i == l) ? alpha : R[i + arr[i] * ldr];
-        z[i] = (omega[(int64_t)rhs * L1 + i] - acc) / dii;
-      }
-      __syncwarp();
+  for (int64_t i = l; i >= 0; --i) {
+    const bool odd = ((l - i) & 1) != 0;
+    const double* ci = col + (odd ? 0 : L1);   // buffer holding column i (column l in buffer 1)
+    double* cn = col + (odd ? L1 : 0);         // next column (i-1)
+    const double dii = ci[i];
+    // prefetch column i-1 (rows 0..i-1) while updating with column i
+    double pre = 0.0;
+    const int64_t nxt = i - 1;
+    if (nxt >= 0 && tid < nxt + 1) pre = R[tid + arr[nxt] * ldr];
+    for (int64_t t = tid; t < (int64_t)d * i; t += nt) {
+      const int r = (int)(t / i);
+      const int64_t k = t - (int64_t)r * i;
+      bz[(size_t)r * L1 + k] -= ci[k] * (bz[(size_t)r * L1 + i] / dii);
     }
+    if (nxt >= 0) {
+      if (tid < nxt + 1) cn[tid] = pre;
+      for (int64_t k = tid + nt; k <= nxt; k += nt) cn[k] = R[k + arr[nxt] * ldr];
+    }
+    __syncthreads();
+    if (tid < d) bz[(size_t)tid * L1 + i] /= dii;
+    __syncthreads();
   }
-  __syncthreads();
   ArgMax best{-1.0, -1};
-  for (int64_t i = threadIdx.x; i < L1; i += blockDim.x) {
+  for (int64_t i = tid; i < L1; i += nt) {
     double acc = 0.0;
     for (int rhs = 0; rhs < d; ++rhs) {
-      const double v = Z[(int64_t)rhs * L1 + i];
+      const double v = bz[(size_t)rhs * L1 + i];
       acc = fma(v, v, acc);
     }
     best = argmax_better(best, ArgMax{sqrt(acc), i});
   }
   best = block_argmax(best, red_v, red_i);
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     const double g2 = fabs(alpha) / sqrt((double)d) * best.v;
     sc->g2 = g2;
     sc->i_off = best.i;
     sc->need_swap = g2 > g ? 1u : 0u;
   }
+  (void)Z;
 }
 
 cudaError_t launch_g2(cudaStream_t st, const double* R, int64_t ldr, const int64_t* arr, int64_t l,
                       const double* omega, int d, double g, double* Z, SrqrScalars* sc) {
-  g2_kernel<<<1, 32 * (d < 32 ? (d < 1 ? 1 : d) : 32), 0, st>>>(R, ldr, arr, l, omega, d, g, Z, sc);
+  const size_t smem = sizeof(double) * ((size_t)d * (l + 1) + 2 * (size_t)(l + 1));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(g2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  g2_kernel<<<1, 1024, smem, st>>>(R, ldr, arr, l, omega, d, g, Z, sc);
   FFB_LAUNCH_CHECK();
 }
 

@@ -28,6 +28,14 @@ struct GemmArgs {
   int splits;
   int force_partial; // write partial tiles even when splits == 1
   int64_t k_per;     // K range per split (multiple of BK)
+  // stream-K: >0 => persistent grid, CTA b owns iterations [b*sk_per, (b+1)*sk_per)
+  // of the linearised (tile, k-tile) space; every segment goes to
+  // partial[(b*sk_maxseg + local)][BM*BN] and a fixup kernel sums them in order.
+  int64_t sk_per;
+  int sk_maxseg;
+  int sk_tiles_n;    // tiles along N (tile = ty * sk_tiles_n + tx)
+  int64_t sk_kiters; // k-tiles per tile
+  unsigned* sk_cnt;  // per-tile arrival counters (zero; reset by the last arriver)
 };
 
 template <int BM, int BK>
@@ -128,11 +136,45 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm0 = (warp / Cfg::kWarpsN) * WM, wn0 = (warp % Cfg::kWarpsN) * WN;
-  const int64_t i0 = (int64_t)blockIdx.y * BM, j0 = (int64_t)blockIdx.x * BN;
-  const int split = blockIdx.z;
-  const int64_t kbeg = (int64_t)split * g.k_per;
-  const int64_t kend = min(g.K, kbeg + g.k_per);
+  // segment loop: classic grid = one segment; stream-K = this CTA's iteration range
+  int64_t it = 0, it_end = 1;
+  const bool sk = g.sk_per > 0;
+  if (sk) {
+    it = (int64_t)blockIdx.x * g.sk_per;
+    it_end = it + g.sk_per;
+    const int64_t total = g.sk_kiters * ((g.M + BM - 1) / BM) * g.sk_tiles_n;
+    if (it_end > total) it_end = total;
+  }
+  int local_seg = 0;
+  const int64_t first_tile = sk ? it / g.sk_kiters : 0;
+  for (; it < it_end; ++local_seg) {
+  int64_t i0, j0, kbeg, kend;
+  int split;
+  int64_t sk_tile = 0;
+  bool sk_whole = false;
+  if (sk) {
+    const int64_t tile = it / g.sk_kiters;
+    const int64_t kb = it - tile * g.sk_kiters;
+    int64_t ke = g.sk_kiters;
+    if (ke - kb > it_end - it) ke = kb + (it_end - it);
+    i0 = (tile / g.sk_tiles_n) * BM;
+    j0 = (tile % g.sk_tiles_n) * BN;
+    kbeg = kb * BK;
+    kend = ke * BK < g.K ? ke * BK : g.K;
+    split = (int)(blockIdx.x * g.sk_maxseg + (tile - first_tile));
+    sk_tile = tile;
+    sk_whole = (kb == 0 && ke == g.sk_kiters);
+    it += ke - kb;
+  } else {
+    i0 = (int64_t)blockIdx.y * BM;
+    j0 = (int64_t)blockIdx.x * BN;
+    split = blockIdx.z;
+    kbeg = (int64_t)split * g.k_per;
+    kend = min(g.K, kbeg + g.k_per);
+    it = it_end;
+  }
   const int nk = kbeg < kend ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+  __syncthreads();   // previous segment's smem reads done before refilling
 
   TileLoader<BM, BK, A_KC, VEC2, NT> la;
   TileLoader<BN, BK, B_KC, VEC2, NT> lb;
@@ -206,7 +248,14 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
       for (int h = 0; h < 2; ++h) {
         const int64_t gj = j0 + wn0 + b * 8 + 2 * fk + h;
         if (gj >= g.N) continue;
-        if (g.splits == 1 && !g.force_partial) {
+        if (sk) {
+          if (!sk_whole) g.partial[(size_t)split * (BM * BN) + (gi - i0) + (gj - j0) * BM] = acc[a][b][h];
+          else {
+            double* cp = g.C + gi + gj * g.ldc;
+            const double v = g.alpha * acc[a][b][h];
+            *cp = g.beta == 0.0 ? v : v + g.beta * (*cp);
+          }
+        } else if (g.splits == 1 && !g.force_partial) {
           double* cp = g.C + gi + gj * g.ldc;
           const double v = g.alpha * acc[a][b][h];
           *cp = g.beta == 0.0 ? v : v + g.beta * (*cp);
@@ -214,6 +263,76 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
           g.partial[(size_t)split * g.M * g.N + gi + gj * g.M] = acc[a][b][h];
         }
       }
+    }
+  }
+  if (sk && !sk_whole) {
+    // last CTA to finish this tile reduces every segment in CTA order -> C
+    __shared__ int s_last;
+    __syncthreads();
+    const int64_t t0 = sk_tile * g.sk_kiters, t1 = t0 + g.sk_kiters - 1;
+    const int64_t b0 = t0 / g.sk_per, b1 = t1 / g.sk_per;
+    if (tid == 0) {
+      __threadfence();
+      const unsigned old = atomicAdd(g.sk_cnt + sk_tile, 1u);
+      s_last = (old == (unsigned)(b1 - b0));
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      __shared__ const double* segp[16];
+      if (tid <= (int)(b1 - b0) && tid < 16) {
+        const int64_t bq = b0 + tid;
+        const int64_t ft = (bq * g.sk_per) / g.sk_kiters;
+        segp[tid] = g.partial + (size_t)(bq * g.sk_maxseg + (sk_tile - ft)) * (BM * BN);
+      }
+      __syncthreads();
+      const int ns = (int)(b1 - b0 + 1);
+      for (int e = tid; e < BM * BN; e += NT) {
+        const int r = e % BM, c = e / BM;
+        const int64_t gi = i0 + r, gj = j0 + c;
+        if (gi >= g.M || gj >= g.N) continue;
+        double sum = 0.0;
+        for (int q = 0; q < ns; ++q) sum += __ldcg(segp[q] + e);
+        double* cp = g.C + gi + gj * g.ldc;
+        const double v = g.alpha * sum;
+        *cp = g.beta == 0.0 ? v : v + g.beta * (*cp);
+      }
+      if (tid == 0) g.sk_cnt[sk_tile] = 0u;
+    }
+  }
+  }  // segment loop
+}
+
+// Stream-K fixup: C(tile) = alpha * sum over covering CTAs (ascending) + beta * C.
+template <int BM, int BN>
+__global__ void __launch_bounds__(256) gemm_streamk_fixup(GemmArgs g, int64_t ntiles) {
+  const int64_t tile = blockIdx.x;
+  if (tile >= ntiles) return;
+  __shared__ const double* seg[16];
+  __shared__ int nseg;
+  const int64_t i0 = (tile / g.sk_tiles_n) * BM, j0 = (tile % g.sk_tiles_n) * BN;
+  if (threadIdx.x == 0) {
+    const int64_t t0 = tile * g.sk_kiters, t1 = t0 + g.sk_kiters - 1;
+    const int64_t b0 = t0 / g.sk_per, b1 = t1 / g.sk_per;
+    int n = 0;
+    for (int64_t b = b0; b <= b1 && n < 16; ++b, ++n) {
+      const int64_t ft = (b * g.sk_per) / g.sk_kiters;
+      seg[n] = g.partial + (size_t)(b * g.sk_maxseg + (tile - ft)) * (BM * BN);
+    }
+    nseg = n;
+  }
+  __syncthreads();
+  const int ns = nseg;
+  const int64_t rows = g.M - i0 < BM ? g.M - i0 : BM;
+  const int64_t cols = g.N - j0 < BN ? g.N - j0 : BN;
+  for (int c = 0; c < cols; ++c) {
+    for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+      const int e = r + c * BM;
+      double sum = 0.0;
+      for (int q = 0; q < ns; ++q) sum += seg[q][e];
+      double* cp = g.C + (i0 + r) + (j0 + c) * g.ldc;
+      const double v = g.alpha * sum;
+      *cp = g.beta == 0.0 ? v : v + g.beta * (*cp);
     }
   }
 }
