@@ -1,0 +1,106 @@
+"""Batched and multi-GPU drivers (BASELINE configs 4 and 5).
+
+One GPU: independent factorizations run concurrently on several CUDA streams,
+one host thread and one workspace per stream (the C ABI releases the GIL, so
+host threads overlap).  Several GPUs (one process per GPU, torchrun): problems
+are partitioned contiguously — rank r takes [n*r/W, n*(r+1)/W) — and each rank
+factorizes its share with no data-path collective; the only communication is
+an NCCL gather of fixed-size result slots to rank 0.
+"""
+from __future__ import annotations
+
+import threading
+from concurrent.futures import ThreadPoolExecutor
+
+
+def partition(n_problems, world, rank):
+    """Contiguous share of rank `rank`: range(lo, hi)."""
+    lo = (n_problems * rank) // world
+    hi = (n_problems * (rank + 1)) // world
+    return range(lo, hi)
+
+
+def run_streams(problems, solve, n_streams=4, device=None):
+    """Run `solve(problem)` for every problem on `n_streams` CUDA streams.
+
+    `solve` is called inside `torch.cuda.stream(s)`; results keep input order.
+    """
+    import torch
+
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    streams = [torch.cuda.Stream(device=dev) for _ in range(max(1, n_streams))]
+    lock = threading.Lock()
+    free = list(range(len(streams)))
+
+    def _one(p):
+        with lock:
+            sid = free.pop()
+        try:
+            with torch.cuda.device(dev), torch.cuda.stream(streams[sid]):
+                out = solve(p)
+                streams[sid].synchronize()
+                return out
+        finally:
+            with lock:
+                free.append(sid)
+
+    with ThreadPoolExecutor(max_workers=len(streams)) as ex:
+        return list(ex.map(_one, problems))
+
+
+def gather_slots(local_slots, n_problems, slot_shape, rank, world, device, dtype=None):
+    """Gather fixed-size per-problem result slots to rank 0.
+
+    local_slots: tensor (len(partition(...)), *slot_shape) on `device`.
+    Returns the (n_problems, *slot_shape) tensor on rank 0, None elsewhere.
+    Uses torch.distributed.gather (NCCL over NVLink on GPUs, gloo on CPU).
+    """
+    import torch
+    import torch.distributed as dist
+
+    dtype = dtype or local_slots.dtype
+    shares = [len(partition(n_problems, world, r)) for r in range(world)]
+    pad = max(shares)
+    buf = torch.zeros((pad,) + tuple(slot_shape), dtype=dtype, device=device)
+    buf[: local_slots.shape[0]] = local_slots
+    if world == 1:
+        return buf[: shares[0]]
+    if dist.get_backend() == "nccl":
+        # NCCL has no gather: all_gather into a flat buffer (rank 0 keeps it)
+        out = [torch.empty_like(buf) for _ in range(world)]
+        dist.all_gather(out, buf)
+    else:
+        out = [torch.empty_like(buf) for _ in range(world)] if rank == 0 else None
+        dist.gather(buf, out, dst=0)
+    if rank != 0:
+        return None
+    return torch.cat([o[:s] for o, s in zip(out, shares)], dim=0)
+
+
+def flip_flop_batch(make_problem, n_problems, k, l, b, p, seed_of=lambda i: i, n_streams=4,
+                    gather=("u", "s"), solve=None):
+    """Factorize `n_problems` independent matrices across all ranks.
+
+    make_problem(i) -> device matrix for problem i (generated where it is used;
+    A never crosses GPUs).  Returns (results_local, gathered) where gathered maps
+    each name in `gather` to the stacked (n_problems, ...) tensor on rank 0.
+    """
+    import torch
+    import torch.distributed as dist
+
+    from .engine import flip_flop_srqr
+
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    mine = list(partition(n_problems, world, rank))
+    solve = solve or (lambda i: flip_flop_srqr(make_problem(i), k, l=l, b=b, p=p, seed=seed_of(i)))
+    results = run_streams(mine, solve, n_streams=n_streams) if torch.cuda.is_available() else [solve(i) for i in mine]
+    gathered = {}
+    for name in gather:
+        parts = [getattr(r, name) for r in results]
+        parts = [x if isinstance(x, torch.Tensor) else torch.as_tensor(x) for x in parts]
+        dev = parts[0].device if parts else (torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu"))
+        local = torch.stack(parts) if parts else torch.zeros((0,))
+        shape = tuple(local.shape[1:])
+        gathered[name] = gather_slots(local, n_problems, shape, rank, world, dev)
+    return results, gathered

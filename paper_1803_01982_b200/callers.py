@@ -1,0 +1,79 @@
+"""Caller seams: the reference's HOSVD and SVT (IALM) code on the B200 engine.
+
+The reference binds ``flip_flop_srqr`` by name at import in ``tensor.py:18`` and
+``nuclear.py:18``; ``hosvd`` additionally accepts any callable engine
+(``tensor.py:74-75``).  This module provides both seams plus a device-side
+``hosvd`` for the BASELINE config 4 workload (three independent mode
+unfoldings of a 400^3 tensor, ``tensor.py:104-120``).
+"""
+from __future__ import annotations
+
+from .engine import flip_flop_srqr
+
+
+def hosvd_engine(l_extra=10, b=32, p=10, seed=0):
+    """Callable engine for ``ffsrqr.tensor.hosvd(X, ranks, engine=...)``.
+
+    The built-in ``"flipflop"`` engine of the reference hard-codes
+    ``l = r + 5, b = 32, p = 5`` (``tensor.py:79-86``); config 4 needs
+    ``l = r + 10, p = 10``, which is what this default reproduces.
+    """
+
+    def _engine(M, r):
+        m, n = M.shape
+        l = min(r + l_extra, min(m, n) - 1)
+        return flip_flop_srqr(M, r, l=max(l, r), b=b, p=p, seed=seed)
+
+    return _engine
+
+
+def install_into(ffsrqr_module):
+    """Route the reference's own HOSVD/ST-HOSVD and IALM solvers through the engine.
+
+    ``ffsrqr_module`` is the imported reference package; returns the previous
+    bindings so they can be restored.
+    """
+    prev = (ffsrqr_module.tensor.flip_flop_srqr, ffsrqr_module.nuclear.flip_flop_srqr)
+    ffsrqr_module.tensor.flip_flop_srqr = flip_flop_srqr
+    ffsrqr_module.nuclear.flip_flop_srqr = flip_flop_srqr
+    return prev
+
+
+def unfold(X, mode):
+    """Mode-n unfolding with the reference's column order (``tensor.py:21-27``):
+    rows index mode n, columns the remaining modes with the lower mode fastest.
+    Works on numpy arrays and torch tensors (returns a column-major tensor)."""
+    import numpy as np
+
+    if isinstance(X, np.ndarray):
+        return np.reshape(np.moveaxis(X, mode, 0), (X.shape[mode], -1), order="F")
+    import torch
+
+    Xm = torch.movedim(X, mode, 0)
+    rest = Xm.shape[1:]
+    perm = (0,) + tuple(range(Xm.dim() - 1, 0, -1))   # reverse remaining modes
+    M = Xm.permute(*perm).reshape(X.shape[mode], int(torch.tensor(rest).prod()))
+    return M.t().contiguous().t()
+
+
+def hosvd(X, ranks, l_extra=10, b=32, p=10, seed=0, device=None):
+    """Truncated HOSVD (``tensor.py:104-120``) with the flip-flop engine per mode.
+
+    Returns (core, factors, approxes).  The per-mode factorizations are
+    independent (the multi-GPU unit of config 4, see ``batch.py``).
+    """
+    import torch
+
+    Xt = X if isinstance(X, torch.Tensor) else torch.as_tensor(X, dtype=torch.float64)
+    if device is not None or not Xt.is_cuda:
+        Xt = Xt.to(device or "cuda")
+    eng = hosvd_engine(l_extra, b, p, seed)
+    factors, approxes = [], []
+    for mode, r in enumerate(ranks):
+        ap = eng(unfold(Xt, mode), r)
+        approxes.append(ap)
+        factors.append(ap.u if isinstance(ap.u, torch.Tensor) else torch.as_tensor(ap.u, device=Xt.device))
+    G = Xt
+    for mode, U in enumerate(factors):
+        G = torch.movedim(torch.tensordot(U.t(), torch.movedim(G, mode, 0), dims=1), 0, mode)
+    return G, factors, approxes
