@@ -71,7 +71,7 @@ struct Work {
   uint32_t* pbar;
   double *hhW, *hhW2;
   // pivots
-  PivSlot* slots;
+  unsigned long long* prec;
   double *slotdata, *pwork, *gap;
   uint32_t* flags;
   int64_t* hist;
@@ -97,7 +97,9 @@ int64_t max_i(int64_t a, int64_t b) { return a > b ? a : b; }
 // Pivot-kernel geometry: G CTAs (<= #SMs, >= 32 columns each), columns in
 // shared memory when they fit.
 void pivot_geometry(const ffb_ctx* ctx, int64_t n, int64_t s, Work& w) {
-  int G = (int)std::min<int64_t>(ctx ? ctx->sms : 148, std::max<int64_t>(1, (n + 31) / 32));
+  int gmax = std::min(ctx ? ctx->sms : 148, 160);   // kPivMaxK * 32
+  if (const char* ev = getenv("FFB_PIV_G")) gmax = std::max(1, std::min(gmax, atoi(ev)));
+  int G = (int)std::min<int64_t>(gmax, std::max<int64_t>(1, (n + 31) / 32));
   int cpc = (int)((n + G - 1) / G);
   const size_t smem_all = pivots_smem_bytes((int)s, cpc, true);
   w.piv_smem = smem_all <= 200 * 1024;
@@ -142,9 +144,7 @@ size_t carve(const ffb_ctx* ctx, const Dims& D, void* base, size_t cap, Work& w)
   w.hhW = b.take<double>(kPanelW * max_i(l, 1));
   w.hhW2 = b.take<double>(kPanelW * max_i(l, 1));
   pivot_geometry(ctx, n, s, w);
-  w.slots = b.take<PivSlot>(4 * (size_t)w.G);
-  w.slotdata = b.take<double>(2 * (size_t)w.G * s);
-  w.flags = b.take<uint32_t>(w.G);
+  w.prec = b.take<unsigned long long>(2 * (size_t)w.G * pivots_recw((int)s));
   w.hist = b.take<int64_t>(max_i(D.b, 1));
   w.gap = b.take<double>(max_i(l, 1));
   w.pwork = w.piv_smem ? nullptr : b.take<double>((size_t)w.G * pivots_stride((int)s) * w.cpc);
@@ -202,6 +202,11 @@ struct Eng {
     ++launches;
     return e == cudaSuccess;
   }
+  // stream memsets: checked like launches but not counted as kernels
+  bool okm(cudaError_t e) {
+    if (e != cudaSuccess && cerr == cudaSuccess) cerr = e;
+    return e == cudaSuccess;
+  }
   void gemm(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda, bool akc,
             const double* B, int64_t ldb, bool bkc, double beta, double* C, int64_t ldc) {
     if (cerr != cudaSuccess) return;
@@ -214,7 +219,7 @@ struct Eng {
   }
   void memset2d(double* p, int64_t ld, int64_t rows, int64_t cols) {
     if (rows <= 0 || cols <= 0) return;
-    ok(cudaMemset2DAsync(p, ld * sizeof(double), 0, rows * sizeof(double), cols, st));
+    okm(cudaMemset2DAsync(p, ld * sizeof(double), 0, rows * sizeof(double), cols, st));
   }
 
   // Householder panel (Mp x wb, wb <= 64): one fused cooperative kernel
@@ -276,6 +281,7 @@ bool validate(const Dims& D) {
   if (D.mode != FFB_MODE_TRQRCP && D.l + 1 > std::min(D.m, D.n)) return false;
   if (D.b > 64) return false;  // panel kernels are sized for b <= 64
   if (D.s > 128) return false; // pivot kernel holds one sketch column per warp (s <= 128)
+  if (D.n >= 2147483647LL) return false;  // pivot exchange carries 32-bit positions
   return true;
 }
 
@@ -344,27 +350,20 @@ int ffb_block_pivots(ffb_ctx* ctx, void* stream, const double* B, int64_t s, int
                      int64_t ldb, int64_t j0, int64_t bb, int64_t* arr, int64_t* pos, double* gap,
                      void* workspace, size_t workspace_bytes) {
   if (!ctx) return FFB_ERR_ARGUMENT;
-  if (bb < 1 || j0 < 0 || j0 + bb > n) return fail(ctx, FFB_ERR_DIMENSION, "bad pivot block");
+  if (bb < 1 || j0 < 0 || j0 + bb > n || n >= 2147483647LL || s < 1 || s > 128)
+    return fail(ctx, FFB_ERR_DIMENSION, "bad pivot block");
   Work w;
   pivot_geometry(ctx, n, s, w);
   Bump b{static_cast<char*>(workspace), 0, workspace_bytes};
-  w.slots = b.take<PivSlot>(4 * (size_t)w.G);
-  w.slotdata = b.take<double>(2 * (size_t)w.G * s);
-  w.flags = b.take<uint32_t>(w.G);
+  w.prec = b.take<unsigned long long>(2 * (size_t)w.G * pivots_recw((int)s));
   w.hist = b.take<int64_t>(bb);
   w.pwork = w.piv_smem ? nullptr : b.take<double>((size_t)w.G * pivots_stride((int)s) * w.cpc);
   if (!b.ok) return fail(ctx, FFB_ERR_ARGUMENT, "workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = cudaMemsetAsync(w.flags, 0, sizeof(uint32_t) * w.G, st);
-  PivotArgs a{B, ldb, (int)s, n, j0, (int)bb, arr, pos, w.G, w.cpc, 0, w.pwork, w.slots,
-              w.slotdata, w.flags, w.hist, gap};
+  cudaError_t e = cudaMemsetAsync(w.prec, 0, 16 * (size_t)w.G * pivots_recw((int)s), st);
+  PivotArgs a{B, ldb, (int)s, n, j0, (int)bb, arr, pos, w.G, w.cpc, 0, w.pwork, w.prec,
+              pivots_recw((int)s), w.hist, gap};
   if (e == cudaSuccess) {
-    static bool attr[2] = {false, false};
-    if (!attr[w.piv_smem]) {
-      cudaFuncSetAttribute(pivots_kernel_ptr(w.piv_smem), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           210 * 1024);
-      attr[w.piv_smem] = true;
-    }
     e = launch_pivots(st, a, w.piv_smem, w.piv_smem_bytes);
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -416,8 +415,8 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
   }
 
   // ---------------------------------------------------------------- TRQRCP
-  e.ok(cudaMemsetAsync(w.status, 0, sizeof(uint32_t), st));
-  e.ok(cudaMemsetAsync(w.skcnt, 0, sizeof(unsigned) * 65536, st));
+  e.okm(cudaMemsetAsync(w.status, 0, sizeof(uint32_t), st));
+  e.okm(cudaMemsetAsync(w.skcnt, 0, sizeof(unsigned) * 65536, st));
   // B = Omega * A (Omega row-major s x m: A-operand with contiguous k)
   e.gemm(s, n, m, 1.0, omega, m, true, A, lda, true, 0.0, w.B, s);
   e.ok(launch_colsq(st, A, lda, m, n, w.colsq));
@@ -427,19 +426,13 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
   e.memset2d(w.WT, l, l, n);
   e.memset2d(w.R, L1, L1, n);
   {
-    static bool attr[2] = {false, false};
-    if (!attr[w.piv_smem]) {
-      cudaFuncSetAttribute(pivots_kernel_ptr(w.piv_smem), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           210 * 1024);
-      attr[w.piv_smem] = true;
-    }
   }
   for (int64_t j0 = 0; j0 < l && e.cerr == cudaSuccess; j0 += D.b) {
     const int64_t bb = std::min<int64_t>(D.b, l - j0), e1 = j0 + bb;
     // (K2) pivots on the sketch
-    e.ok(cudaMemsetAsync(w.flags, 0, sizeof(uint32_t) * w.G, st));
-    PivotArgs pa{w.B, s, (int)s, n, j0, (int)bb, w.arr, w.pos, w.G, w.cpc, 0, w.pwork, w.slots,
-                 w.slotdata, w.flags, w.hist, out->pivot_gap ? w.gap + j0 : nullptr};
+    e.okm(cudaMemsetAsync(w.prec, 0, 16 * (size_t)w.G * pivots_recw((int)s), st));
+    PivotArgs pa{w.B, s, (int)s, n, j0, (int)bb, w.arr, w.pos, w.G, w.cpc, 0, w.pwork, w.prec,
+                 pivots_recw((int)s), w.hist, out->pivot_gap ? w.gap + j0 : nullptr};
     e.ok(launch_pivots(st, pa, w.piv_smem, w.piv_smem_bytes));
     // (K4) panel P = A[:, piv] - Y[:, :j0] WT[:j0, piv]
     e.ok(launch_gather_cols(st, A, lda, m, w.arr + j0, bb, w.P, m));
@@ -502,7 +495,7 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
   e.gemm(l, l, l, 1.0, w.T, l, false, w.Y, m, false, 0.0, w.TYt, l);
   e.gemm(m, l, l, -1.0, w.Y, m, false, w.TYt, l, true, 0.0, w.Q, m);
   e.ok(launch_add_identity(st, w.Q, m, m, l, 1.0));
-  e.ok(cudaMemsetAsync(w.Q + m * l, 0, sizeof(double) * m, st));
+  e.okm(cudaMemsetAsync(w.Q + m * l, 0, sizeof(double) * m, st));
   e.ok(launch_rinit(st, w.B, s, (int)s, w.arr, n, l, w.r, w.rinit));
   e.ok(launch_anorm(st, w.colsq, n, w.sc));
   auto extend = [&]() {
@@ -541,6 +534,7 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
     e.ok(launch_add_identity(st, w.VsT, l, l, l, 1.0));
     e.ok(launch_jacobi_svd(st, ctx->sms, w.Rt, l, w.VsT, l, (int)l, w.sig, w.Us, l, w.Vo, l, w.jbar,
                            w.joff, w.jsweeps, w.jorder, kMaxSweeps));
+    e.launches += 2;   // prescale + Jacobi + finish kernels
     // (K15) u = Qt[:, :l] Us[:, :k] ; v = Yh Vs[:, :k]
     e.gemm(l, k, l, 1.0, w.Yt, m, true, w.Us, l, true, 0.0, w.W1, l);
     e.gemm(l, k, l, 1.0, w.Tt, l, false, w.W1, l, true, 0.0, w.W2, l);

@@ -66,6 +66,58 @@ FFB_DEV int rr_player(int pos, int r, int nb) {
   return ((pos - 1 + r) % (nb - 1)) + 1;
 }
 
+// slot pair k of inner round t: within-block pairs (round-robin over be slots
+// of each block) for t < n_within, then cross pairs (k, bs + (k + t') % bs)
+constexpr int kBS = 16;   // block size: every inner round pairs all 2 * kBS slots
+
+FFB_DEV void inner_pair(int t, int k, int n_within, int& p, int& q) {
+  if (t < n_within) {
+    constexpr int np = kBS / 2;
+    const int blk = k < np ? 0 : 1, kk = k - blk * np;
+    p = blk * kBS + rr_player(kk, t, kBS);
+    q = blk * kBS + rr_player(kBS - 1 - kk, t, kBS);
+  } else {
+    const int tt = (t - n_within) & (kBS - 1);
+    p = k;
+    q = kBS + ((k + tt) & (kBS - 1));
+  }
+}
+
+// Jacobi rotation (c, s) of slots (p, q) from the current Gram.  Threshold test
+// in fp64 without square roots; the angle t in fp32 with fast intrinsics (t only
+// sets how much of x^T y is removed, its accuracy just affects convergence
+// speed), c = 1/sqrt(1+t^2) refined to fp64 by two Newton steps so the rotation
+// is orthogonal to working precision.  Returns (cc^2, aa*bb) for the caller's
+// off-diagonal measure; c = 1, s = 0 when the pair is already orthogonal.
+FFB_DEV bool rotation(const double* G, const int* gcol, int p, int q, double tol2, double& c,
+                      double& s, double& c2, double& den) {
+  c = 1.0;
+  s = 0.0;
+  c2 = 0.0;
+  den = 1.0;
+  if (gcol[p] < 0 || gcol[q] < 0) return false;
+  const double aa = G[p * 33 + p], bb = G[q * 33 + q], cc = G[p * 33 + q];
+  c2 = cc * cc;
+  den = aa * bb;
+  if (!(c2 > tol2 * den)) return false;
+  const float zf = __fdividef((float)(bb - aa), 2.0f * (float)cc);
+  double t;
+  if (fabsf(zf) < 1e15f) {
+    const float az = fabsf(zf), y = fmaf(az, az, 1.0f);
+    const float tf = __frcp_rn(az + y * rsqrtf(y));
+    t = (double)copysignf(tf, zf);
+  } else {
+    t = cc / (bb - aa);   // ~ 1 / (2 zeta) for huge |zeta| (or cc underflowed in fp32)
+  }
+  const double y = fma(t, t, 1.0);
+  double r = (double)rsqrtf((float)y);
+  r = r * fma(-0.5 * y * r, r, 1.5);
+  r = r * fma(-0.5 * y * r, r, 1.5);
+  c = r;
+  s = r * t;
+  return true;
+}
+
 }  // namespace
 
 // W (<= 32) local columns: M_W (and V_W when VRES) staged in shared memory
@@ -154,15 +206,15 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
   double* Ms = sm;                        // lpad x kMW : M_W (rows >= l zero)
   double* Gs = Ms + (size_t)lpad * kMW;   // 32 x 33
   double* Js = Gs + 32 * 33;              // 32 x 33
-  double* Vs = Js + 32 * 33;              // VRES: lpad x kMW ; else 64 x kMW chunk
+  double* Gs2 = Js + 32 * 33;             // ping-pong partners of Gs / Js
+  double* Js2 = Gs2 + 32 * 33;
+  double* Vs = Js2 + 32 * 33;             // VRES: lpad x kMW ; else 64 x kMW chunk
   __shared__ int gcol[32];
-  __shared__ double rc[16], rs[16];
-  __shared__ int rp[16], rq[16];
   __shared__ double s_off;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int P = gridDim.x;
   const double tol = a.tol;
-  const float tolf = (float)a.tol;
+  const double tol2 = a.tol * a.tol;
 
   long long tp[6] = {0, 0, 0, 0, 0, 0};
   long long tc = clock64();
@@ -251,82 +303,63 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
       for (int t = tid; t < 32 * 32; t += nt) Js[(t >> 5) * 33 + (t & 31)] = ((t >> 5) == (t & 31)) ? 1.0 : 0.0;
       __syncthreads();
       JPROF(1)
-      double off = 0.0;
-      const int be = bs + (bs & 1);
-      const int n_within = (r == 0) ? be - 1 : 0;
-      const int n_cross = a.inner * bs;
-      // every round pairs all 32 local slots (16 disjoint pairs); thread (pa, pb)
-      // owns the 2x2 block (pair pa rows, pair pb cols) of G and of J
+      // every round pairs all 32 local slots (16 disjoint pairs); thread (ba, bb2)
+      // owns the 2x2 block (pair ba rows, pair bb2 cols) of G and of J.  Lane
+      // (x & 15) of each warp computes the rotation of pair x & 15 (no broadcast
+      // step; pair ba's rotation comes by shuffle), and the rotated block goes
+      // into the other buffer: one barrier per round.
+      double offn = 0.0, offd = 1.0;   // running max of G_pq^2 / (G_pp G_qq)
+      const int n_within = (r == 0) ? kBS - 1 : 0;
+      const int n_cross = a.inner * kBS;
       const int ba = tid >> 4, bb2 = tid & 15;
+      const double* Gc = Gs;
+      const double* Jc = Js;
+      double* Gn = Gs2;
+      double* Jn = Js2;
       for (int t = 0; t < n_within + n_cross; ++t) {
-        if (tid < 16) {
-          int p, q;
-          if (t < n_within) {
-            const int np = be / 2;                    // pairs per block (bs even: bs/2)
-            const int blk = tid < np ? 0 : 1, k = tid - blk * np;
-            p = blk * bs + rr_player(k, t, be);
-            q = blk * bs + rr_player(be - 1 - k, t, be);
-          } else {
-            const int tt = (t - n_within) % bs;
-            p = tid;
-            q = bs + (tid + tt) % bs;
-          }
-          double cs = 1.0, sn = 0.0;
-          if (gcol[p] >= 0 && gcol[q] >= 0) {
-            const double aa = Gs[p * 33 + p], bb = Gs[q * 33 + q], cc = Gs[p * 33 + q];
-            // threshold / angle in fp32 (only cs^2 + sn^2 = 1 must be exact)
-            const float abf = sqrtf((float)aa) * sqrtf((float)bb);
-            const float cf = fabsf((float)cc);
-            if (cf > tolf * abf) {
-              off = fmax(off, (double)(cf / abf));
-              // angle entirely in fp32 (t only sets how much of x^T y is removed);
-              // cs = 1/sqrt(1+t^2) in fp64 keeps the rotation exactly orthogonal
-              const float zf = (float)(bb - aa) / (2.0f * (float)cc);
-              double tt2;
-              if (fabsf(zf) > 1e15f || !isfinite(zf)) {
-                tt2 = 0.5 / ((bb - aa) / (2.0 * cc));
-              } else {
-                tt2 = (double)(copysignf(1.0f, zf) / (fabsf(zf) + sqrtf(fmaf(zf, zf, 1.0f))));
-              }
-              cs = rsqrt(1.0 + tt2 * tt2);
-              sn = cs * tt2;
-            }
-          }
-          rp[tid] = p;
-          rq[tid] = q;
-          rc[tid] = cs;
-          rs[tid] = sn;
+        int pa2, qa2, pb2, qb2;
+        inner_pair(t, ba, n_within, pa2, qa2);
+        inner_pair(t, bb2, n_within, pb2, qb2);
+        const double g00 = Gc[pa2 * 33 + pb2], g01 = Gc[pa2 * 33 + qb2];
+        const double g10 = Gc[qa2 * 33 + pb2], g11 = Gc[qa2 * 33 + qb2];
+        const double j00 = Jc[pa2 * 33 + pb2], j01 = Jc[pa2 * 33 + qb2];
+        const double j10 = Jc[qa2 * 33 + pb2], j11 = Jc[qa2 * 33 + qb2];
+        double cb, sb, c2b, denb;
+        const bool rot = rotation(Gc, gcol, pb2, qb2, tol2, cb, sb, c2b, denb);
+        // lane ba of this warp has bb2 == ba: its rotation is pair ba's
+        const double ca = __shfl_sync(0xffffffffu, cb, ba);
+        const double sa = __shfl_sync(0xffffffffu, sb, ba);
+        if (rot && ba == bb2 && c2b * offd > offn * denb) {
+          offn = c2b;
+          offd = denb;
         }
+        // G_blk <- R_a^T G_blk R_b with R = [[c, s], [-s, c]] acting on (p, q)
+        const double h00 = cb * g00 - sb * g01, h01 = sb * g00 + cb * g01;   // columns
+        const double h10 = cb * g10 - sb * g11, h11 = sb * g10 + cb * g11;
+        Gn[pa2 * 33 + pb2] = ca * h00 - sa * h10;
+        Gn[pa2 * 33 + qb2] = ca * h01 - sa * h11;
+        Gn[qa2 * 33 + pb2] = sa * h00 + ca * h10;
+        Gn[qa2 * 33 + qb2] = sa * h01 + ca * h11;
+        // J rows (pa, qa) x columns (pb, qb): J <- J R_b (column rotation only)
+        Jn[pa2 * 33 + pb2] = cb * j00 - sb * j01;
+        Jn[pa2 * 33 + qb2] = sb * j00 + cb * j01;
+        Jn[qa2 * 33 + pb2] = cb * j10 - sb * j11;
+        Jn[qa2 * 33 + qb2] = sb * j10 + cb * j11;
         __syncthreads();
-        {
-          const int pa = rp[ba], qa = rq[ba], pb = rp[bb2], qb = rq[bb2];
-          const double ca = rc[ba], sa = rs[ba], cb = rc[bb2], sb = rs[bb2];
-          // G_blk <- R_a^T G_blk R_b with R = [[c, s], [-s, c]] acting on (p, q)
-          const double g00 = Gs[pa * 33 + pb], g01 = Gs[pa * 33 + qb];
-          const double g10 = Gs[qa * 33 + pb], g11 = Gs[qa * 33 + qb];
-          const double h00 = cb * g00 - sb * g01, h01 = sb * g00 + cb * g01;   // columns
-          const double h10 = cb * g10 - sb * g11, h11 = sb * g10 + cb * g11;
-          // J rows (pa, qa) x columns (pb, qb): J <- J R_b (column rotation only)
-          const double j00 = Js[pa * 33 + pb], j01 = Js[pa * 33 + qb];
-          const double j10 = Js[qa * 33 + pb], j11 = Js[qa * 33 + qb];
-          __syncthreads();
-          Gs[pa * 33 + pb] = ca * h00 - sa * h10;
-          Gs[pa * 33 + qb] = ca * h01 - sa * h11;
-          Gs[qa * 33 + pb] = sa * h00 + ca * h10;
-          Gs[qa * 33 + qb] = sa * h01 + ca * h11;
-          Js[pa * 33 + pb] = cb * j00 - sb * j01;
-          Js[pa * 33 + qb] = sb * j00 + cb * j01;
-          Js[qa * 33 + pb] = cb * j10 - sb * j11;
-          Js[qa * 33 + qb] = sb * j10 + cb * j11;
-        }
-        __syncthreads();
+        const double* tg = Gc;
+        Gc = Gn;
+        Gn = const_cast<double*>(tg);
+        const double* tj = Jc;
+        Jc = Jn;
+        Jn = const_cast<double*>(tj);
       }
+      double off = offn > 0.0 ? sqrt(offn / offd) : 0.0;
       JPROF(2)
-      apply_cols(Ms, Js, a.M, a.ldm, gcol, l, lpad);
+      apply_cols(Ms, Jc, a.M, a.ldm, gcol, l, lpad);
       if (VRES) {
         cp_async_wait<0>();
         __syncthreads();
-        apply_cols(Vs, Js, a.V, a.ldv, gcol, l, lpad);
+        apply_cols(Vs, Jc, a.V, a.ldv, gcol, l, lpad);
       } else {
         for (int ch = 0; ch < lpad; ch += 64) {
           __syncthreads();
@@ -345,7 +378,7 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
           for (int k0 = 0; k0 < 32; k0 += 4) {
             const double af = Vs[(warp * 8 + fr) * kMW + k0 + fk];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) dmma_884(acc[j][0], acc[j][1], af, Js[(k0 + fk) * 33 + 8 * j + fr]);
+            for (int j = 0; j < 4; ++j) dmma_884(acc[j][0], acc[j][1], af, Jc[(k0 + fk) * 33 + 8 * j + fr]);
           }
 #pragma unroll
           for (int j = 0; j < 4; ++j)
@@ -380,12 +413,38 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
 #undef JPROF
 }
 
+// M <- 2^-e M with 2^e ~ max |M| (exact power-of-two scaling): keeps the Gram
+// entries and their fp32 images in range whatever the scale of A.  e -> sweeps[1].
+__global__ void jacobi_prescale_kernel(double* M, int64_t ldm, int l, int* sweeps) {
+  __shared__ double red[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  double mx = 0.0;
+  for (int idx = tid; idx < l * l; idx += blockDim.x) {
+    const int j = idx / l, i = idx - j * l;
+    mx = fmax(mx, fabs(M[i + (int64_t)j * ldm]));
+  }
+  mx = warp_max(mx);
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  mx = 0.0;
+  for (int w = 0; w < nw; ++w) mx = fmax(mx, red[w]);
+  const int e = (mx > 0.0 && isfinite(mx)) ? ilogb(mx) : 0;
+  if (tid == 0) sweeps[1] = e;
+  if (e == 0) return;
+  const double sc = ldexp(1.0, -e);
+  for (int idx = tid; idx < l * l; idx += blockDim.x) {
+    const int j = idx / l, i = idx - j * l;
+    M[i + (int64_t)j * ldm] *= sc;
+  }
+}
+
 // sigma_j = ||M[:, j]||; rank sort (descending, ties by index); outputs sorted
 // sigma, U = M_j / sigma_j (zero column when sigma_j == 0) and V columns.
 __global__ void jacobi_finish_kernel(const double* M, int64_t ldm, const double* V, int64_t ldv,
                                      int l, double* sig, double* U, int64_t ldu, double* Vo,
-                                     int64_t ldvo, int* order) {
+                                     int64_t ldvo, int* order, const int* sweeps) {
   extern __shared__ double nrm[];
+  const double unscale = ldexp(1.0, sweeps[1]);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   for (int j = warp; j < l; j += nw) {
     double acc = 0.0;
@@ -399,7 +458,7 @@ __global__ void jacobi_finish_kernel(const double* M, int64_t ldm, const double*
     const double sj = nrm[j];
     for (int q = 0; q < l; ++q) rank += (nrm[q] > sj) || (nrm[q] == sj && q < j);
     order[rank] = j;
-    sig[rank] = sj;
+    sig[rank] = sj * unscale;
   }
   __syncthreads();
   for (int idx = tid; idx < l * l; idx += blockDim.x) {
@@ -433,7 +492,7 @@ cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, double* M, int64_t ldm, 
   if (getenv("FFB_JACOBI_PROF") && !prof) cudaMallocManaged(&prof, 8 * sizeof(long long));
   JacobiArgs a{M, ldm, V, ldv, l, bs, nb, 1e-15 * sqrt((double)l), max_sweeps, bar, offmax, sweeps, inner, prof};
   const size_t lpad = (size_t)((l + 63) & ~63);
-  const size_t fixed = sizeof(double) * (lpad * kMW + 2 * 32 * 33);
+  const size_t fixed = sizeof(double) * (lpad * kMW + 4 * 32 * 33);
   // V region: V_W when resident (>= 8 x 32 x 33 doubles, it doubles as Gram scratch)
   const size_t vreg = sizeof(double) * (lpad > 256 ? lpad : 256) * kMW;
   const bool vres = fixed + vreg <= 220 * 1024;
@@ -446,6 +505,7 @@ cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, double* M, int64_t ldm, 
   cudaError_t e = cudaMemsetAsync(bar, 0, 2 * sizeof(uint32_t), st);
   if (e == cudaSuccess) e = cudaMemsetAsync(offmax, 0, sizeof(double) * max_sweeps, st);
   if (e != cudaSuccess) return e;
+  jacobi_prescale_kernel<<<1, 1024, 0, st>>>(M, ldm, l, sweeps);
   void* args[] = {&a};
   if (cluster) {
     if (P > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -467,7 +527,7 @@ cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, double* M, int64_t ldm, 
   }
   if (e != cudaSuccess) return e;
   jacobi_finish_kernel<<<1, 1024, sizeof(double) * (size_t)l, st>>>(M, ldm, V, ldv, l, sig, U, ldu,
-                                                                    Vo, ldvo, order);
+                                                                    Vo, ldvo, order, sweeps);
   if (prof) {
     cudaStreamSynchronize(st);
     fprintf(stderr, "jacobi phases (cycles, CTA0): stage %lld gram %lld inner %lld apply %lld off %lld barrier %lld\n",

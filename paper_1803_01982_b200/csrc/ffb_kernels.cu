@@ -5,6 +5,8 @@
 // array arr[pos] = column (with its inverse pos[column]) replaces the
 // reference's physical reorders (ffsrqr/sketch.py:70-72,120-121).
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "ffb_common.cuh"
 #include "ffb_kernels.cuh"
@@ -25,6 +27,31 @@ FFB_DEV uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+// LL ("low-latency") exchange words: 32-bit payload + 32-bit step tag in one
+// single-copy-atomic 64-bit word, so readers validate data by its tag and no
+// fence or flag is needed between producer and consumers.
+FFB_DEV unsigned long long ll_pack(uint32_t data, uint32_t tag) {
+  return ((unsigned long long)tag << 32) | data;
+}
+FFB_DEV uint32_t ll_tag(unsigned long long w) { return (uint32_t)(w >> 32); }
+FFB_DEV uint32_t ll_data(unsigned long long w) { return (uint32_t)w; }
+FFB_DEV void st_ll2(unsigned long long* p, unsigned long long x, unsigned long long y) {
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};\n" ::"l"(p), "l"(x), "l"(y) : "memory");
+}
+FFB_DEV void ld_ll2(const unsigned long long* p, unsigned long long& x, unsigned long long& y) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(x), "=l"(y) : "l"(p) : "memory");
+}
+
+// opaque select: keeps unrolled "pick element q of a register array" chains from
+// being turned into a dynamically indexed (local-memory) array by the compiler
+FFB_DEV double sel_f64(bool c, double a, double b) {
+  double r;
+  asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\tselp.f64 %0, %1, %2, p;\n\t}"
+      : "=d"(r)
+      : "d"(a), "d"(b), "r"((unsigned)c));
+  return r;
 }
 
 static inline unsigned nblk(int64_t work, int per) {
@@ -137,23 +164,34 @@ FFB_DEV Cand2 warp_top2(Cand2 c) {
 // 4 threads per column (interleaved rows).  kGroups column groups per CTA.
 constexpr int kPivThreads = 256;
 constexpr int kPivGroups = kPivThreads / 4;
+constexpr int kPivMaxK = 5;   // CTAs per lane in the header exchange (G <= 160)
 
-// exact warp argmax: largest r, ties -> lowest position (two shuffle passes)
+// exact warp argmax: largest r, ties -> lowest position.  r >= 0 for every
+// candidate (norms; the downdate clamps at 0), so the IEEE bit pattern orders
+// like the value: key = bits + 1 (0 = no candidate), reduced with three redux
+// instructions (max hi word, max lo word among the hi winners, min position).
+// Positions are < 2^31 (checked at the boundary).
 FFB_DEV void warp_best(double& r, int64_t& p) {
-  double m = (p >= 0) ? r : -1.0;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  int64_t q = (p >= 0 && r == m) ? p : INT64_MAX;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const int64_t t = __shfl_xor_sync(0xffffffffu, q, o);
-    q = t < q ? t : q;
+  const unsigned long long key =
+      p >= 0 ? (unsigned long long)__double_as_longlong(r > 0.0 ? r : 0.0) + 1ull : 0ull;
+  const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  const bool top = key != 0ull && hi == mhi && lo == mlo;
+  const unsigned pm = __reduce_min_sync(0xffffffffu, top ? (unsigned)p : 0xffffffffu);
+  if (pm == 0xffffffffu) {
+    r = -1.0;
+    p = -1;
+  } else {
+    r = __longlong_as_double((long long)((((unsigned long long)mhi << 32) | mlo) - 1ull));
+    p = (int64_t)pm;
   }
-  r = m;
-  p = (q == INT64_MAX) ? -1 : q;
 }
 
-template <bool SMEM>
+// RQ > 0: every column group owns at most one column and keeps its rows
+// (sub + 4q, q < RQ) in registers; shared memory gets a write-through copy that
+// the publish step reads.  RQ == 0: generic shared/global-memory loop.
+template <bool SMEM, int RQ>
 __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int s = a.s, cpc = a.cpc, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -181,6 +219,14 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
   }
   for (int c = tid; c < nc; c += kPivThreads) pp[c] = a.pos[c0 + c];
   __syncthreads();
+  double x[RQ > 0 ? RQ : 1];
+  if constexpr (RQ > 0) {
+#pragma unroll
+    for (int q = 0; q < RQ; ++q) {
+      const int i = sub + 4 * q;
+      x[q] = (grp < nc && i < s) ? W[(size_t)grp * sP + i] : 0.0;
+    }
+  }
   // initial norms and local top-2 over positions >= j0
   {
     Cand2 cd{-1.0, -1, -1.0, -1};
@@ -201,53 +247,88 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
   }
   __syncthreads();
 
+  long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tlast = clock64();
+#define PPROF(i)                        \
+  if (a.prof && tid == 0) {             \
+    const long long tn = clock64();     \
+    tp[i] += tn - tlast;                \
+    tlast = tn;                         \
+  }
   for (int j = 0; j < a.bb; ++j) {
     const int64_t P = a.j0 + j;
     const int par = j & 1;
     if (warp == 0) {
-      // ---- local candidate -> publish -> global pick -> reflector (one warp)
+      // ---- local candidate -> publish (tagged LL words, no fences) -> global
+      // pick -> reflector, all in warp 0
+      const uint32_t tag = (uint32_t)(j + 1);
+      unsigned long long* base = a.rec + (size_t)par * a.G * a.recw;
       Cand2 cd = lane < (kPivThreads / 32) ? wc[lane] : Cand2{-1.0, -1, -1.0, -1};
       if (a.gap) {
         cd = warp_top2(cd);
       } else {
         warp_best(cd.r1, cd.p1);
+        cd.r2 = -1.0;
+        cd.p2 = -1;
       }
-      PivSlot* slot = a.slots + (size_t)par * a.G * 2;
-      double* sdata = a.slotdata + ((size_t)par * a.G + blockIdx.x) * s;
-      if (cd.p1 >= 0) {
-        // local column holding position cd.p1 (positions are unique)
-        int cl = -1;
-        for (int c = lane; c < nc; c += 32)
-          if (pp[c] == cd.p1) cl = c;
-        for (int o = 16; o > 0; o >>= 1) cl = max(cl, __shfl_xor_sync(0xffffffffu, cl, o));
-        const double* col = W + (size_t)cl * sP;
-        for (int i = lane; i < s; i += 32) sdata[i] = col[i];
-      }
-      if (lane == 0) {
-        slot[2 * blockIdx.x] = PivSlot{cd.r1, cd.p1};
-        slot[2 * blockIdx.x + 1] = PivSlot{cd.r2, cd.p2};
-      }
-      // __syncwarp orders the lanes' writes before lane 0's (cumulative) release
-      __syncwarp();
-      if (lane == 0) st_release_u32(a.flags + blockIdx.x, (uint32_t)(j + 1));
-      // poll every owned flag with relaxed loads (pipelined), then one fence
       {
-        const uint32_t tgt = (uint32_t)(j + 1);
-        bool done;
-        do {
-          done = true;
-          for (int t = lane; t < a.G; t += 32) done &= ld_relaxed_u32(a.flags + t) >= tgt;
-        } while (!__all_sync(0xffffffffu, done));
-        __threadfence();
+        unsigned long long* rec = base + (size_t)blockIdx.x * a.recw;
+        if (cd.p1 >= 0) {
+          // local column holding position cd.p1 (positions are unique)
+          int cl = -1;
+          for (int c = lane; c < nc; c += 32)
+            if (pp[c] == cd.p1) cl = c;
+          cl = (int)__reduce_max_sync(0xffffffffu, (unsigned)(cl + 1)) - 1;
+          const double* col = W + (size_t)cl * sP;
+          for (int i = j + lane; i < s; i += 32) {
+            const double x = col[i];
+            st_ll2(rec + 8 + 2 * i, ll_pack((uint32_t)__double2loint(x), tag),
+                   ll_pack((uint32_t)__double2hiint(x), tag));
+          }
+        }
+        if (lane == 0)
+          st_ll2(rec, ll_pack((uint32_t)__double2loint(cd.r1), tag),
+                 ll_pack((uint32_t)__double2hiint(cd.r1), tag));
+        if (lane == 1)
+          st_ll2(rec + 2, ll_pack((uint32_t)(int32_t)cd.p1, tag), ll_pack((uint32_t)(int32_t)cd.p2, tag));
+        if (lane == 2 && a.gap)
+          st_ll2(rec + 4, ll_pack((uint32_t)__double2loint(cd.r2), tag),
+                 ll_pack((uint32_t)__double2hiint(cd.r2), tag));
       }
+      PPROF(0)
+      // every CTA's header: lane handles CTAs lane + 32k; all loads in flight at once
+      unsigned long long h[kPivMaxK][4];
+      unsigned need = 0;
+#pragma unroll
+      for (int k = 0; k < kPivMaxK; ++k)
+        if (lane + 32 * k < a.G) need |= 1u << k;
+      do {
+#pragma unroll
+        for (int k = 0; k < kPivMaxK; ++k)
+          if (need & (1u << k)) {
+            const unsigned long long* rc = base + (size_t)(lane + 32 * k) * a.recw;
+            ld_ll2(rc, h[k][0], h[k][1]);
+            ld_ll2(rc + 2, h[k][2], h[k][3]);
+          }
+#pragma unroll
+        for (int k = 0; k < kPivMaxK; ++k)
+          if ((need & (1u << k)) && ll_tag(h[k][0]) == tag && ll_tag(h[k][1]) == tag &&
+              ll_tag(h[k][2]) == tag && ll_tag(h[k][3]) == tag)
+            need &= ~(1u << k);
+      } while (__any_sync(0xffffffffu, need != 0));
+      PPROF(1)
+      // global pick: largest r, ties to the lowest position; winner CTA tracked
       Cand2 g{-1.0, -1, -1.0, -1};
-      int wcta = -1;
-      for (int t = lane; t < a.G; t += 32) {
-        const PivSlot b0 = slot[2 * t];
-        if (cand_better(b0.r, b0.pos, g.r1, g.p1)) wcta = t;
-        cand_push(g, b0.r, b0.pos);
-      }
-      // winner CTA = the one whose best equals the global best (positions unique)
+      int bc = -1;
+#pragma unroll
+      for (int k = 0; k < kPivMaxK; ++k)
+        if (lane + 32 * k < a.G) {
+          const double rr = __hiloint2double((int)ll_data(h[k][1]), (int)ll_data(h[k][0]));
+          const int64_t pq = (int64_t)(int32_t)ll_data(h[k][2]);
+          if (cand_better(rr, pq, g.r1, g.p1)) bc = lane + 32 * k;
+          cand_push(g, rr, pq);
+        }
+      const int64_t mine = g.p1;
       Cand2 gw = g;
       if (a.gap) {
         gw = warp_top2(g);
@@ -255,33 +336,61 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
         warp_best(gw.r1, gw.p1);
         gw.p2 = -1;
       }
-      int wc_cta = -1;
-      for (int t = lane; t < a.G; t += 32)
-        if (slot[2 * t].pos == gw.p1 && gw.p1 >= 0) wc_cta = t;
-      for (int o = 16; o > 0; o >>= 1) wc_cta = max(wc_cta, __shfl_xor_sync(0xffffffffu, wc_cta, o));
-      (void)wcta;
-      // runner-up = max(other CTAs' bests, winner CTA's second)
+      const bool holder = gw.p1 >= 0 && mine == gw.p1;
+      const int wc_cta = (int)__reduce_max_sync(0xffffffffu, holder ? (unsigned)(bc + 1) : 0u) - 1;
       double second = (gw.p2 >= 0) ? gw.r2 : -1.0;
-      if (wc_cta >= 0) {
-        const PivSlot w2 = slot[2 * wc_cta + 1];
-        if (w2.pos >= 0) second = fmax(second, w2.r);
+      if (a.gap && wc_cta >= 0) {
+        // runner-up inside the winner CTA (gap tracing only: one more load)
+        const unsigned long long* rc = base + (size_t)wc_cta * a.recw;
+        unsigned long long w2, w3, w4, w5;
+        do {
+          ld_ll2(rc + 2, w2, w3);
+          ld_ll2(rc + 4, w4, w5);
+        } while (ll_tag(w3) != tag || ll_tag(w4) != tag || ll_tag(w5) != tag);
+        if ((int32_t)ll_data(w3) >= 0)
+          second = fmax(second, __hiloint2double((int)ll_data(w5), (int)ll_data(w4)));
       }
       const int64_t wpos = gw.p1 >= 0 ? gw.p1 : P;
-      // winner column -> reflector for rows j..s-1 (ffsrqr/qr.py:21-43)
-      const double* wd = a.slotdata + ((size_t)par * a.G + (wc_cta >= 0 ? wc_cta : 0)) * s;
+      PPROF(2)
+      // winner column rows j..s-1 -> reflector (ffsrqr/qr.py:21-43)
       double xv[4];
+      {
+        const unsigned long long* wrec = base + (size_t)(wc_cta >= 0 ? wc_cta : 0) * a.recw + 8;
+        unsigned long long xw[4][2];
+        unsigned xneed = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = lane + 32 * q;
+          if (i >= j && i < s && wc_cta >= 0) xneed |= 1u << q;
+          xw[q][0] = xw[q][1] = 0ull;
+        }
+        do {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (xneed & (1u << q)) ld_ll2(wrec + 2 * (lane + 32 * q), xw[q][0], xw[q][1]);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if ((xneed & (1u << q)) && ll_tag(xw[q][0]) == tag && ll_tag(xw[q][1]) == tag)
+              xneed &= ~(1u << q);
+        } while (__any_sync(0xffffffffu, xneed != 0));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = lane + 32 * q;
+          xv[q] = (i >= j && i < s && wc_cta >= 0)
+                      ? __hiloint2double((int)ll_data(xw[q][1]), (int)ll_data(xw[q][0]))
+                      : 0.0;
+        }
+      }
       double tsq = 0.0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int i = lane + 32 * q;
-        xv[q] = (i < s && gw.p1 >= 0) ? wd[i] : 0.0;
         if (i > j && i < s) tsq = fma(xv[q], xv[q], tsq);
       }
       tsq = warp_sum(tsq);
       double xsel = 0.0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (q == (j >> 5)) xsel = xv[q];
+      for (int q = 0; q < 4; ++q) xsel = sel_f64(q == (j >> 5), xv[q], xsel);
       const double x0 = __shfl_sync(0xffffffffu, xsel, j & 31);
       double tau = 0.0, div = 1.0;
       if (tsq != 0.0) {
@@ -306,39 +415,95 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
           if (a.gap) a.gap[j] = (gw.r1 > 0.0 && second >= 0.0) ? (gw.r1 - second) / gw.r1 : 1.0;
         }
       }
+      PPROF(3)
     }
     __syncthreads();
+    PPROF(4)
     // ---- all threads: swap bookkeeping, reflector application, downdate
     const double tau = s_tau;
     const int64_t wpos = s_wpos;
     Cand2 cd{-1.0, -1, -1.0, -1};
-    for (int c = grp; c < nc; c += kPivGroups) {
-      int64_t p = pp[c];
-      if (p == wpos) p = P;
-      else if (p == P) p = wpos;
-      if (sub == 0) pp[c] = p;
-      if (p <= P) continue;
-      double* col = W + (size_t)c * sP;
-      if (tau != 0.0) {
-        double wsum = 0.0;
-        for (int i = j + sub; i < s; i += 4) wsum = fma(vv[i], col[i], wsum);
-        wsum += __shfl_xor_sync(gmask, wsum, 1);
-        wsum += __shfl_xor_sync(gmask, wsum, 2);
-        const double wt = wsum * tau;
-        for (int i = j + sub; i < s; i += 4) col[i] = fma(-vv[i], wt, col[i]);
+    if constexpr (RQ > 0) {
+      const int c = grp;
+      if (c < nc) {
+        int64_t p = pp[c];
+        if (p == wpos) p = P;
+        else if (p == P) p = wpos;
+        if (sub == 0) pp[c] = p;
+        if (p > P) {
+          double* col = W + (size_t)c * sP;
+          if (tau != 0.0) {
+            double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+            for (int q = 0; q < RQ; ++q) {
+              const int i = sub + 4 * q;
+              if (i >= j && i < s) {
+                if (q & 1) w1 = fma(vv[i], x[q], w1);
+                else w0 = fma(vv[i], x[q], w0);
+              }
+            }
+            double wsum = w0 + w1;
+            wsum += __shfl_xor_sync(gmask, wsum, 1);
+            wsum += __shfl_xor_sync(gmask, wsum, 2);
+            const double wt = wsum * tau;
+#pragma unroll
+            for (int q = 0; q < RQ; ++q) {
+              const int i = sub + 4 * q;
+              if (i >= j && i < s) {
+                x[q] = fma(-vv[i], wt, x[q]);
+                col[i] = x[q];
+              }
+            }
+          }
+          double xj = 0.0;
+#pragma unroll
+          for (int q = 0; q < RQ; ++q) xj = sel_f64(q == (j >> 2), x[q], xj);
+          const double rj = __shfl_sync(gmask, xj, (lane & ~3) | (j & 3));
+          double rr = r[c] - rj * rj;
+          if (rr < 1e-8 * r0[c] || rr < 0.0) {
+            double t = 0.0;
+#pragma unroll
+            for (int q = 0; q < RQ; ++q) {
+              const int i = sub + 4 * q;
+              if (i > j && i < s) t = fma(x[q], x[q], t);
+            }
+            t += __shfl_xor_sync(gmask, t, 1);
+            t += __shfl_xor_sync(gmask, t, 2);
+            rr = t > 0.0 ? t : 0.0;
+          }
+          if (sub == 0) r[c] = rr;
+          cand_push(cd, rr, p);
+        }
       }
-      __syncwarp(gmask);
-      const double rj = col[j];
-      double rr = r[c] - rj * rj;
-      if (rr < 1e-8 * r0[c] || rr < 0.0) {
-        double t = 0.0;
-        for (int i = j + 1 + sub; i < s; i += 4) t = fma(col[i], col[i], t);
-        t += __shfl_xor_sync(gmask, t, 1);
-        t += __shfl_xor_sync(gmask, t, 2);
-        rr = t > 0.0 ? t : 0.0;
+    } else {
+      for (int c = grp; c < nc; c += kPivGroups) {
+        int64_t p = pp[c];
+        if (p == wpos) p = P;
+        else if (p == P) p = wpos;
+        if (sub == 0) pp[c] = p;
+        if (p <= P) continue;
+        double* col = W + (size_t)c * sP;
+        if (tau != 0.0) {
+          double wsum = 0.0;
+          for (int i = j + sub; i < s; i += 4) wsum = fma(vv[i], col[i], wsum);
+          wsum += __shfl_xor_sync(gmask, wsum, 1);
+          wsum += __shfl_xor_sync(gmask, wsum, 2);
+          const double wt = wsum * tau;
+          for (int i = j + sub; i < s; i += 4) col[i] = fma(-vv[i], wt, col[i]);
+        }
+        __syncwarp(gmask);
+        const double rj = col[j];
+        double rr = r[c] - rj * rj;
+        if (rr < 1e-8 * r0[c] || rr < 0.0) {
+          double t = 0.0;
+          for (int i = j + 1 + sub; i < s; i += 4) t = fma(col[i], col[i], t);
+          t += __shfl_xor_sync(gmask, t, 1);
+          t += __shfl_xor_sync(gmask, t, 2);
+          rr = t > 0.0 ? t : 0.0;
+        }
+        if (sub == 0) r[c] = rr;
+        cand_push(cd, rr, p);
       }
-      if (sub == 0) r[c] = rr;
-      cand_push(cd, rr, p);
     }
     if (a.gap) {
       cd = warp_top2(cd);
@@ -349,7 +514,11 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
     }
     if (lane == 0) wc[warp] = cd;
     __syncthreads();
+    PPROF(5)
   }
+#undef PPROF
+  if (a.prof && tid == 0)
+    for (int i = 0; i < 6; ++i) atomicAdd((unsigned long long*)&a.prof[i], (unsigned long long)tp[i]);
   for (int c = tid; c < nc; c += kPivThreads) a.pos[c0 + c] = pp[c];
 }
 
@@ -361,22 +530,64 @@ size_t pivots_smem_bytes(int s, int cpc, bool smem_mode) {
   return b;
 }
 
+// record: [0..1] best r, [2] best position, [3] runner-up position, [4..5]
+// runner-up r, [6..7] pad, then rows 0..s-1 of the candidate column (2 words each)
+int pivots_recw(int s) { return (8 + 2 * s + 15) / 16 * 16; }
+
 int pivots_stride(int s) {
   int sP = s;
   while (sP % 16 != 4) ++sP;
   return sP;
 }
 
-void* pivots_kernel_ptr(bool smem_mode) {
-  return smem_mode ? (void*)pivots_kernel<true> : (void*)pivots_kernel<false>;
+int pivots_rq(int s, int cpc, bool smem_mode) {
+  if (!smem_mode || cpc > kPivGroups) return 0;
+  return s <= 32 ? 8 : s <= 64 ? 16 : s <= 96 ? 24 : 32;
+}
+
+void* pivots_kernel_ptr(bool smem_mode, int rq) {
+  if (!smem_mode) return (void*)pivots_kernel<false, 0>;
+  switch (rq) {
+    case 8: return (void*)pivots_kernel<true, 8>;
+    case 16: return (void*)pivots_kernel<true, 16>;
+    case 24: return (void*)pivots_kernel<true, 24>;
+    case 32: return (void*)pivots_kernel<true, 32>;
+    default: return (void*)pivots_kernel<true, 0>;
+  }
 }
 
 cudaError_t launch_pivots(cudaStream_t st, const PivotArgs& a, bool smem_mode, size_t smem) {
   PivotArgs args = a;
   args.sP = pivots_stride(a.s);
+  static long long* prof = nullptr;
+  if (getenv("FFB_PIV_PROF") && !prof) cudaMallocManaged(&prof, 8 * sizeof(long long));
+  if (prof) {
+    for (int i = 0; i < 8; ++i) prof[i] = 0;
+    args.prof = prof;
+  }
   void* kargs[] = {&args};
-  return cudaLaunchCooperativeKernel(pivots_kernel_ptr(smem_mode), dim3(a.G), dim3(kPivThreads),
-                                     kargs, smem, st);
+  void* kern = pivots_kernel_ptr(smem_mode, pivots_rq(a.s, a.cpc, smem_mode));
+  static void* attr_done[8] = {};
+  for (void*& k : attr_done) {
+    if (k == kern) break;
+    if (!k) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+      k = kern;
+      break;
+    }
+  }
+  cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3(a.G),
+                                              dim3(kPivThreads), kargs, smem, st);
+  if (prof && e == cudaSuccess) {
+    cudaStreamSynchronize(st);
+    const double d = (double)a.G * a.bb;
+    fprintf(stderr,
+            "[piv prof] G=%d bb=%d s=%d cpc=%d cycles/step: publish %.0f wait %.0f pick %.0f refl %.0f "
+            "sync %.0f apply %.0f\n",
+            a.G, a.bb, a.s, a.cpc, prof[0] / d, prof[1] / d, prof[2] / d, prof[3] / d, prof[4] / d,
+            prof[5] / d);
+  }
+  return e;
 }
 
 // ------------------------------------------------------- gathers / copies

@@ -13,11 +13,6 @@ enum : uint32_t {
   kStZeroPivot = 1u << 3,       // exact zero on a TRQRCP R11 diagonal (sketch update)
 };
 
-struct PivSlot {
-  double r;
-  int64_t pos;
-};
-
 struct PivotArgs {
   const double* B;
   int64_t ldb;
@@ -31,11 +26,11 @@ struct PivotArgs {
   int cpc;
   int sP;              // padded per-column stride (set by launch_pivots)
   double* work;        // !smem mode: G * sP * cpc
-  PivSlot* slots;      // [2][G][2]: per CTA best and runner-up
-  double* slotdata;    // [2][G][s]
-  uint32_t* flags;     // [G], zero on entry
+  unsigned long long* rec;  // [2][G][recw] tagged exchange records, zero on entry
+  int recw;            // words per record (pivots_recw(s))
   int64_t* hist;       // [bb] winning positions
   double* gap;         // [bb] relative top-2 gap per step (certified near-tie evidence)
+  long long* prof;     // optional [G][8] phase cycle sums (FFB_PIV_PROF)
 };
 
 // Scalars block shared between SRQR kernels and the host (device memory).
@@ -60,7 +55,9 @@ cudaError_t launch_iota2(cudaStream_t st, int64_t* arr, int64_t* pos, int64_t n)
 cudaError_t launch_pivots(cudaStream_t st, const PivotArgs& a, bool smem_mode, size_t smem);
 size_t pivots_smem_bytes(int s, int cpc, bool smem_mode);
 int pivots_stride(int s);
-void* pivots_kernel_ptr(bool smem_mode);
+int pivots_recw(int s);
+void* pivots_kernel_ptr(bool smem_mode, int rq);
+int pivots_rq(int s, int cpc, bool smem_mode);
 
 cudaError_t launch_gather_cols(cudaStream_t st, const double* src, int64_t ld_src, int64_t rows,
                                const int64_t* idx, int64_t ncols, double* dst, int64_t ld_dst);

@@ -13,6 +13,8 @@
 // Results are deterministic (fixed reduction order).  Replaces 11-14 launches of
 // GEMM + single-CTA kernels per panel.
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "ffb_common.cuh"
 #include "ffb_panel.cuh"
@@ -169,6 +171,14 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
   const int ww = w * w;
   const int bi = bi_of(tid), bj = bj_of(tid);
   bool zero = false;
+  long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tlast = clock64();
+#define QPROF(i)                                    \
+  if (a.prof && tid == 0 && blockIdx.x == 0) {      \
+    const long long tn = clock64();                 \
+    tp[i] += tn - tlast;                            \
+    tlast = tn;                                     \
+  }
 
   for (int pass = 0; pass < 3; ++pass) {
     const double* src = pass == 0 ? a.X : (pass == 1 ? a.Qa : a.Qb);
@@ -185,18 +195,36 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
       dmma64(gacc, Cs, true, Cs, (rows + 3) & ~3);
     }
     acc_store_global(gacc, a.part + (size_t)blockIdx.x * ww, w, 0, w, w);
+    QPROF(0)
     grid_sync(a.bar, G);
     // (b) distributed fixed-order reduction
     {
+      // 8 threads per element: thread k sums partials k, k+8, .. (independent
+      // loads in flight), then a fixed 3-level shuffle tree -> deterministic
       const int per = (ww + G - 1) / G;
       const int e0 = blockIdx.x * per, e1 = e0 + per < ww ? e0 + per : ww;
-      for (int e = e0 + tid; e < e1; e += nt) {
+      const int k8 = tid & 7;
+      for (int eb = e0; eb < e1; eb += nt >> 3) {
+        const int e = eb + (tid >> 3);
         double s = 0.0;
-        for (int c = 0; c < G; ++c) s += a.part[(size_t)c * ww + e];
-        a.Gg[e] = s;
+        if (e < e1) {
+          double v[4] = {0.0, 0.0, 0.0, 0.0};
+          int c = k8;
+          for (; c + 24 < G; c += 32) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] += a.part[(size_t)(c + 8 * u) * ww + e];
+          }
+          for (; c < G; c += 8) v[0] += a.part[(size_t)c * ww + e];
+          s = (v[0] + v[1]) + (v[2] + v[3]);
+        }
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        s += __shfl_xor_sync(0xffffffffu, s, 4);
+        if (e < e1 && k8 == 0) a.Gg[e] = s;
       }
     }
     grid_sync(a.bar, G);
+    QPROF(1)
     // (c) every CTA: shifted Cholesky + inverse (redundant, no broadcast step)
     Tile g;
 #pragma unroll
@@ -290,6 +318,7 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
       store(x, Xs);
       __syncthreads();
     }
+    QPROF(2)
     // Racc <- R * Racc (pass 0: Racc = R; zero panel: Racc = 0), DMMA via Ws
     if (zero) {
       for (int t = tid; t < kW * kW; t += nt) Ra[(t >> 6) * kL + (t & 63)] = 0.0;
@@ -308,8 +337,10 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
       __syncthreads();
       apply_upper(Cs, rows, w, Xs, dst, Mp, c0);
     }
+    QPROF(3)
   }
   grid_sync(a.bar, G);   // Q = Qa complete (top w rows visible to every CTA)
+  QPROF(4)
 
   // (e) Householder reconstruction (redundant in every CTA)
   double* Ls = Rs;
@@ -345,6 +376,7 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
     for (int i = tid; i < kW; i += nt) Dd[i] = 1.0;
     __syncthreads();
   }
+  QPROF(5)
   if (blockIdx.x == 0) {
     // T = -U L^{-T}  (DMMA, into Ws is not possible: Ws holds Li) -> use Ra's
     // neighbour?  Ra is still needed for R; compute into registers per warp tile.
@@ -376,6 +408,10 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
       apply_upper(Ys, rows, w, Ui, a.Y, a.ldy, c0);
     }
   }
+  QPROF(6)
+#undef QPROF
+  if (a.prof && tid == 0 && blockIdx.x == 0)
+    for (int i = 0; i < 7; ++i) a.prof[i] = tp[i];
 }
 
 size_t panel_smem_bytes() { return sizeof(double) * (size_t)(4 * kW * kL + kCH * kL + 256); }
@@ -399,11 +435,22 @@ cudaError_t launch_panel_qr(cudaStream_t st, int sms, const double* X, int64_t l
   }
   const int G = panel_grid(sms, Mp);
   PanelArgs a{X, ldx, Mp, w, Y, ldy, T, ldt, R, ldr, Qa, Qb, part, Gg, bar, status,
-              (int)((Mp + G - 1) / G)};
+              (int)((Mp + G - 1) / G), nullptr};
+  static long long* prof = nullptr;
+  if (getenv("FFB_PANEL_PROF") && !prof) cudaMallocManaged(&prof, 8 * sizeof(long long));
+  a.prof = prof;
   cudaError_t e = cudaMemsetAsync(bar, 0, 2 * sizeof(uint32_t), st);
   if (e != cudaSuccess) return e;
   void* args[] = {&a};
-  return cudaLaunchCooperativeKernel((void*)panel_qr_kernel, dim3(G), dim3(256), args, smem, st);
+  e = cudaLaunchCooperativeKernel((void*)panel_qr_kernel, dim3(G), dim3(256), args, smem, st);
+  if (prof && e == cudaSuccess) {
+    cudaStreamSynchronize(st);
+    fprintf(stderr,
+            "[panel prof] Mp=%lld w=%d G=%d cycles: gram %lld reduce %lld factor %lld apply %lld "
+            "gsync %lld recon %lld TY %lld\n",
+            (long long)Mp, w, G, prof[0], prof[1], prof[2], prof[3], prof[4], prof[5], prof[6]);
+  }
+  return e;
 }
 
 }  // namespace ffb

@@ -23,6 +23,7 @@ struct PanelArgs {
   uint32_t* bar;   // [2] grid barrier
   uint32_t* status;
   int rpc;         // rows per CTA
+  long long* prof; // optional [8] phase cycles of CTA 0 (FFB_PANEL_PROF)
 };
 
 size_t panel_smem_bytes();
