@@ -83,7 +83,7 @@ struct Work {
   SrqrScalars* sc;
   uint32_t* status;
   // flip-flop
-  double *X, *Yl, *Tl, *Rl, *TYt, *Qh, *Yh, *tmp, *Yt, *Tt, *Rt, *Us, *VsT, *Vo, *sig, *W1, *W2;
+  double *X, *Yl, *Tl, *Rl, *TYt, *Qh, *Yh, *tmp, *Yt, *Tt, *Rt, *Us, *jwork, *Vo, *sig, *W1, *W2;
   double* joff;
   uint32_t* jbar;
   int *jsweeps, *jorder;
@@ -171,7 +171,7 @@ size_t carve(const ffb_ctx* ctx, const Dims& D, void* base, size_t cap, Work& w)
     w.Tt = b.take<double>(l * l);
     w.Rt = b.take<double>(l * l);
     w.Us = b.take<double>(l * l);
-    w.VsT = b.take<double>(l * l);
+    w.jwork = b.take<double>(jacobi_work_doubles((int)l));
     w.Vo = b.take<double>(l * l);
     w.sig = b.take<double>(l);
     w.W1 = b.take<double>(l * D.k);
@@ -530,11 +530,9 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
     // (K14) tmp = Qt Rt, SVD(Rt)
     e.hh_qr(w.tmp, m, l, m, w.Yt, m, w.Tt, l, w.Rt, l, true);
     // one-sided block Jacobi SVD of Rt (ffb_jacobi.cu): Rt = Us diag(sig) Vo^T
-    e.memset2d(w.VsT, l, l, l);
-    e.ok(launch_add_identity(st, w.VsT, l, l, l, 1.0));
-    e.ok(launch_jacobi_svd(st, ctx->sms, w.Rt, l, w.VsT, l, (int)l, w.sig, w.Us, l, w.Vo, l, w.jbar,
+    e.ok(launch_jacobi_svd(st, ctx->sms, w.Rt, l, (int)l, w.sig, w.Us, l, w.Vo, l, w.jwork, w.jbar,
                            w.joff, w.jsweeps, w.jorder, kMaxSweeps));
-    e.launches += 2;   // prescale + Jacobi + finish kernels
+    e.launches += 4;   // scale, layout, Jacobi, norms, out kernels
     // (K15) u = Qt[:, :l] Us[:, :k] ; v = Yh Vs[:, :k]
     e.gemm(l, k, l, 1.0, w.Yt, m, true, w.Us, l, true, 0.0, w.W1, l);
     e.gemm(l, k, l, 1.0, w.Tt, l, false, w.W1, l, true, 0.0, w.W2, l);

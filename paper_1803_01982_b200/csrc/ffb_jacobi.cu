@@ -30,6 +30,7 @@ namespace ffb {
 namespace {
 
 constexpr int kJThreads = 256;
+constexpr int kMW = 36;   // smem row stride (doubles): 16-byte rows, conflict-free DMMA fragments
 
 FFB_DEV uint32_t ld_acq(const uint32_t* p) {
   uint32_t v;
@@ -96,7 +97,7 @@ FFB_DEV bool rotation(const double* G, const int* gcol, int p, int q, double tol
   c2 = 0.0;
   den = 1.0;
   if (gcol[p] < 0 || gcol[q] < 0) return false;
-  const double aa = G[p * 33 + p], bb = G[q * 33 + q], cc = G[p * 33 + q];
+  const double aa = G[p * kMW + p], bb = G[q * kMW + q], cc = G[p * kMW + q];
   c2 = cc * cc;
   den = aa * bb;
   if (!(c2 > tol2 * den)) return false;
@@ -120,12 +121,9 @@ FFB_DEV bool rotation(const double* G, const int* gcol, int p, int q, double tol
 
 }  // namespace
 
-// W (<= 32) local columns: M_W (and V_W when VRES) staged in shared memory
-// (l x W, row-major, ld kMW); G and J are W x W.  256 threads.  CLUSTER: the P
-// CTAs form one thread-block cluster and rounds are separated by the hardware
-// cluster barrier (release/acquire at cluster scope covers the global M, V).
-constexpr int kMW = 33;
-
+// CLUSTER: the P CTAs form one thread-block cluster and rounds are separated by
+// the hardware cluster barrier (release/acquire at cluster scope covers the
+// global M, V); otherwise a cooperative grid barrier.
 template <bool CLUSTER>
 FFB_DEV void round_barrier(uint32_t* bar, uint32_t P) {
   if (CLUSTER) {
@@ -136,31 +134,37 @@ FFB_DEV void round_barrier(uint32_t* bar, uint32_t P) {
   }
 }
 
-// stage the W (=32) local columns of X (rows < l) into S (lpad x kMW) with
-// cp.async (zero-fill beyond l / empty slots): every copy of the CTA is in flight
-// at once; the caller commits and waits.  Warp w: columns w, w+8, ..; lanes: rows.
-FFB_DEV void stage_cols_async(double* S, const double* X, int64_t ldx, const int* gcol, int l,
-                              int lpad) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int cc = warp; cc < 32; cc += 8) {
-    const int c = gcol[cc];
-    const double* src = X + (int64_t)(c < 0 ? 0 : c) * ldx;
-    for (int rr = lane; rr < lpad; rr += 32) {
-      const bool ok = c >= 0 && rr < l;
-      cp_async8(S + rr * kMW + cc, ok ? src + rr : X, ok);
-    }
+// Layout: M and V live in global memory ROW-major with padded shape lpad x ncp
+// (ncp = nb * kBS, zero padding), so a slot block of one row is 128 contiguous
+// bytes: staging is 16-byte cp.async, results go back as 16-byte stores, and no
+// bounds checks are needed anywhere.  Shared tiles are R x 32 row-major (kMW).
+
+// stage rows [r0, r0 + R) of the two slot blocks (pa | pb) of X into S
+FFB_DEV void stage_rows_async(double* S, const double* X, int64_t ld, int pa, int pb, int r0,
+                              int R) {
+  for (int idx = threadIdx.x; idx < R * 16; idx += blockDim.x) {
+    const int rr = idx >> 4, ch = idx & 15;
+    const int blk = ch < 8 ? pa : pb;
+    const double* src = X + (int64_t)(r0 + rr) * ld + blk * kBS + (ch & 7) * 2;
+    cp_async16(S + rr * kMW + (ch < 8 ? 0 : kBS) + (ch & 7) * 2, src, true);
   }
 }
 
-// X_W <- S_W J (S: lpad x 32 in smem), written straight to global.  Warp w owns
-// row tiles w, w+8, .. (<= 7 for lpad <= 448) x all 4 column tiles: up to 28
-// independent DMMA accumulator chains per warp hide the DMMA latency.
-FFB_DEV void apply_cols(const double* S, const double* Js, double* X, int64_t ldx,
-                        const int* gcol, int l, int lpad) {
+// X rows [r0, r0 + R) of blocks (pa | pb) <- S J (S: R x 32 in smem), 16-byte
+// stores.  Warp w owns row tiles w, w + 8, .. (<= kMaxRT) x all 4 column tiles:
+// up to 28 independent DMMA accumulator chains per warp.
+FFB_DEV void apply_rows(const double* S, int R, const double* Js, double* X, int64_t ld, int pa,
+                        int pb, int r0) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int fr = lane >> 2, fk = lane & 3;
-  const int nrt = lpad >> 3;
+  const int nrt = R >> 3;
   constexpr int kMaxRT = 7;
+  int col[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = 8 * j + 2 * fk;
+    col[j] = (c < kBS ? pa : pb) * kBS + (c & (kBS - 1));
+  }
   for (int g0 = 0; g0 < nrt; g0 += 8 * kMaxRT) {
     double acc[kMaxRT][4][2];
 #pragma unroll
@@ -171,7 +175,7 @@ FFB_DEV void apply_cols(const double* S, const double* Js, double* X, int64_t ld
     for (int k0 = 0; k0 < 32; k0 += 4) {
       double bf[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = Js[(k0 + fk) * 33 + 8 * j + fr];
+      for (int j = 0; j < 4; ++j) bf[j] = Js[(k0 + fk) * kMW + 8 * j + fr];
 #pragma unroll
       for (int i = 0; i < kMaxRT; ++i) {
         const int rt = g0 + warp + 8 * i;
@@ -186,14 +190,14 @@ FFB_DEV void apply_cols(const double* S, const double* Js, double* X, int64_t ld
     for (int i = 0; i < kMaxRT; ++i) {
       const int rt = g0 + warp + 8 * i;
       if (rt >= nrt) continue;
+      const int64_t row = r0 + rt * 8 + fr;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int row = rt * 8 + (lane >> 2), cc = 8 * j + 2 * (lane & 3) + hh;
-          const int c = gcol[cc];
-          if (c >= 0 && row < l) X[row + (int64_t)c * ldx] = acc[i][j][hh];
-        }
+      for (int j = 0; j < 4; ++j) {
+        double2 v;
+        v.x = acc[i][j][0];
+        v.y = acc[i][j][1];
+        *reinterpret_cast<double2*>(X + row * ld + col[j]) = v;
+      }
     }
   }
 }
@@ -201,20 +205,20 @@ FFB_DEV void apply_cols(const double* S, const double* Js, double* X, int64_t ld
 template <bool CLUSTER, bool VRES>
 __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
   extern __shared__ __align__(16) double sm[];
-  const int l = a.l, bs = a.bs, nb = a.nb, W = 2 * bs;   // W <= 32
-  const int lpad = (l + 63) & ~63;
-  double* Ms = sm;                        // lpad x kMW : M_W (rows >= l zero)
-  double* Gs = Ms + (size_t)lpad * kMW;   // 32 x 33
-  double* Js = Gs + 32 * 33;              // 32 x 33
-  double* Gs2 = Js + 32 * 33;             // ping-pong partners of Gs / Js
-  double* Js2 = Gs2 + 32 * 33;
-  double* Vs = Js2 + 32 * 33;             // VRES: lpad x kMW ; else 64 x kMW chunk
+  const int lpad = a.lpad, nb = a.nb;
+  double* Ms = sm;                        // lpad x kMW : M_W
+  double* Gs = Ms + (size_t)lpad * kMW;   // 32 x kMW
+  double* Js = Gs + 32 * kMW;
+  double* Gs2 = Js + 32 * kMW;            // ping-pong partners of Gs / Js
+  double* Js2 = Gs2 + 32 * kMW;
+  double* Vs = Js2 + 32 * kMW;            // VRES: lpad x kMW ; else vrows x kMW chunk
   __shared__ int gcol[32];
   __shared__ double s_off;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int P = gridDim.x;
   const double tol = a.tol;
   const double tol2 = a.tol * a.tol;
+  const int64_t ld = a.ld;
 
   long long tp[6] = {0, 0, 0, 0, 0, 0};
   long long tc = clock64();
@@ -229,24 +233,19 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
     for (int r = 0; r < nb - 1; ++r) {
       const int pa = rr_player(blockIdx.x, r, nb), pb = rr_player(nb - 1 - blockIdx.x, r, nb);
       if (tid < 32) {
-        int c = -1;
-        if (tid < W) {
-          const int blk = tid < bs ? pa : pb;
-          c = blk * bs + (tid < bs ? tid : tid - bs);
-          if (c >= l) c = -1;
-        }
-        gcol[tid] = c;
+        const int blk = tid < kBS ? pa : pb;
+        const int c = blk * kBS + (tid & (kBS - 1));
+        gcol[tid] = c < a.l ? c : -1;
       }
-      __syncthreads();
-      stage_cols_async(Ms, a.M, a.ldm, gcol, l, lpad);
+      stage_rows_async(Ms, a.M, ld, pa, pb, 0, lpad);
       cp_async_commit();
       cp_async_wait<0>();
       __syncthreads();
       JPROF(0)
       // fresh Gram G = M_W^T M_W: warp w sums rows [w*lpad/8, (w+1)*lpad/8) for all
-      // 16 output tiles (16 independent DMMA chains), partials reduced through smem
+      // 16 output tiles (16 independent DMMA chains); fixed-order two-level reduce
       {
-        double* part = VRES ? Vs : Gs;   // 8 x 32 x 33 scratch (VRES: V not staged yet)
+        double* part = Vs;   // 4 x 32 x 33 scratch (V is staged after the Gram)
         const int fr = lane >> 2, fk = lane & 3;
         double acc[4][4][2];
 #pragma unroll
@@ -263,45 +262,41 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], f[i], f[j]);
         }
-        if (VRES) {
+        double* pw = part + (warp & 3) * 32 * 33;
+        if (warp >= 4) {
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j)
 #pragma unroll
-              for (int h = 0; h < 2; ++h)
-                part[warp * 32 * 33 + (8 * i + fr) * 33 + 8 * j + 2 * fk + h] = acc[i][j][h];
-          __syncthreads();
-          for (int t = tid; t < 32 * 32; t += nt) {
-            const int r = t >> 5, c = t & 31;
-            double sum = 0.0;
+              for (int h = 0; h < 2; ++h) pw[(8 * i + fr) * 33 + 8 * j + 2 * fk + h] = acc[i][j][h];
+        }
+        __syncthreads();
+        if (warp < 4) {
 #pragma unroll
-            for (int w = 0; w < 8; ++w) sum += part[w * 32 * 33 + r * 33 + c];
-            Gs[r * 33 + c] = sum;
-          }
-          __syncthreads();
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                double& d = pw[(8 * i + fr) * 33 + 8 * j + 2 * fk + h];
+                d = acc[i][j][h] + d;
+              }
+        }
+        __syncthreads();
+        for (int t = tid; t < 32 * 32; t += nt) {
+          const int rr = t >> 5, c = t & 31;
+          const int o = rr * 33 + c;
+          Gs[rr * kMW + c] = (part[o] + part[32 * 33 + o]) + (part[2 * 32 * 33 + o] + part[3 * 32 * 33 + o]);
+          Js[rr * kMW + c] = rr == c ? 1.0 : 0.0;
+        }
+        __syncthreads();
+        if (VRES) {
           // V staging overlaps the inner rotations
-          stage_cols_async(Vs, a.V, a.ldv, gcol, l, lpad);
+          stage_rows_async(Vs, a.V, ld, pa, pb, 0, lpad);
           cp_async_commit();
-        } else {
-          // no scratch: accumulate warp partials into Gs with fixed-order passes
-          for (int t = tid; t < 32 * 32; t += nt) Gs[(t >> 5) * 33 + (t & 31)] = 0.0;
-          __syncthreads();
-          for (int w = 0; w < 8; ++w) {
-            if (warp == w) {
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-#pragma unroll
-                  for (int h = 0; h < 2; ++h) Gs[(8 * i + fr) * 33 + 8 * j + 2 * fk + h] += acc[i][j][h];
-            }
-            __syncthreads();
-          }
         }
       }
-      for (int t = tid; t < 32 * 32; t += nt) Js[(t >> 5) * 33 + (t & 31)] = ((t >> 5) == (t & 31)) ? 1.0 : 0.0;
-      __syncthreads();
       JPROF(1)
       // every round pairs all 32 local slots (16 disjoint pairs); thread (ba, bb2)
       // owns the 2x2 block (pair ba rows, pair bb2 cols) of G and of J.  Lane
@@ -320,10 +315,10 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
         int pa2, qa2, pb2, qb2;
         inner_pair(t, ba, n_within, pa2, qa2);
         inner_pair(t, bb2, n_within, pb2, qb2);
-        const double g00 = Gc[pa2 * 33 + pb2], g01 = Gc[pa2 * 33 + qb2];
-        const double g10 = Gc[qa2 * 33 + pb2], g11 = Gc[qa2 * 33 + qb2];
-        const double j00 = Jc[pa2 * 33 + pb2], j01 = Jc[pa2 * 33 + qb2];
-        const double j10 = Jc[qa2 * 33 + pb2], j11 = Jc[qa2 * 33 + qb2];
+        const double g00 = Gc[pa2 * kMW + pb2], g01 = Gc[pa2 * kMW + qb2];
+        const double g10 = Gc[qa2 * kMW + pb2], g11 = Gc[qa2 * kMW + qb2];
+        const double j00 = Jc[pa2 * kMW + pb2], j01 = Jc[pa2 * kMW + qb2];
+        const double j10 = Jc[qa2 * kMW + pb2], j11 = Jc[qa2 * kMW + qb2];
         double cb, sb, c2b, denb;
         const bool rot = rotation(Gc, gcol, pb2, qb2, tol2, cb, sb, c2b, denb);
         // lane ba of this warp has bb2 == ba: its rotation is pair ba's
@@ -336,15 +331,15 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
         // G_blk <- R_a^T G_blk R_b with R = [[c, s], [-s, c]] acting on (p, q)
         const double h00 = cb * g00 - sb * g01, h01 = sb * g00 + cb * g01;   // columns
         const double h10 = cb * g10 - sb * g11, h11 = sb * g10 + cb * g11;
-        Gn[pa2 * 33 + pb2] = ca * h00 - sa * h10;
-        Gn[pa2 * 33 + qb2] = ca * h01 - sa * h11;
-        Gn[qa2 * 33 + pb2] = sa * h00 + ca * h10;
-        Gn[qa2 * 33 + qb2] = sa * h01 + ca * h11;
+        Gn[pa2 * kMW + pb2] = ca * h00 - sa * h10;
+        Gn[pa2 * kMW + qb2] = ca * h01 - sa * h11;
+        Gn[qa2 * kMW + pb2] = sa * h00 + ca * h10;
+        Gn[qa2 * kMW + qb2] = sa * h01 + ca * h11;
         // J rows (pa, qa) x columns (pb, qb): J <- J R_b (column rotation only)
-        Jn[pa2 * 33 + pb2] = cb * j00 - sb * j01;
-        Jn[pa2 * 33 + qb2] = sb * j00 + cb * j01;
-        Jn[qa2 * 33 + pb2] = cb * j10 - sb * j11;
-        Jn[qa2 * 33 + qb2] = sb * j10 + cb * j11;
+        Jn[pa2 * kMW + pb2] = cb * j00 - sb * j01;
+        Jn[pa2 * kMW + qb2] = sb * j00 + cb * j01;
+        Jn[qa2 * kMW + pb2] = cb * j10 - sb * j11;
+        Jn[qa2 * kMW + qb2] = sb * j10 + cb * j11;
         __syncthreads();
         const double* tg = Gc;
         Gc = Gn;
@@ -355,39 +350,20 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
       }
       double off = offn > 0.0 ? sqrt(offn / offd) : 0.0;
       JPROF(2)
-      apply_cols(Ms, Jc, a.M, a.ldm, gcol, l, lpad);
+      apply_rows(Ms, lpad, Jc, a.M, ld, pa, pb, 0);
       if (VRES) {
         cp_async_wait<0>();
         __syncthreads();
-        apply_cols(Vs, Jc, a.V, a.ldv, gcol, l, lpad);
+        apply_rows(Vs, lpad, Jc, a.V, ld, pa, pb, 0);
       } else {
-        for (int ch = 0; ch < lpad; ch += 64) {
+        for (int r0 = 0; r0 < lpad; r0 += a.vrows) {
+          const int R = lpad - r0 < a.vrows ? lpad - r0 : a.vrows;
           __syncthreads();
-          for (int t = tid; t < 64 * 32; t += nt) {
-            const int rr = t & 63, cc = t >> 6;
-            const int c = gcol[cc];
-            Vs[rr * kMW + cc] = (c >= 0 && ch + rr < l) ? a.V[(ch + rr) + (int64_t)c * a.ldv] : 0.0;
-          }
+          stage_rows_async(Vs, a.V, ld, pa, pb, r0, R);
+          cp_async_commit();
+          cp_async_wait<0>();
           __syncthreads();
-          // reuse apply_cols on one 64-row chunk (rows offset ch)
-          const int fr = lane >> 2, fk = lane & 3;
-          double acc[4][2];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
-#pragma unroll
-          for (int k0 = 0; k0 < 32; k0 += 4) {
-            const double af = Vs[(warp * 8 + fr) * kMW + k0 + fk];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) dmma_884(acc[j][0], acc[j][1], af, Jc[(k0 + fk) * 33 + 8 * j + fr]);
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-              const int row = ch + warp * 8 + (lane >> 2), cc = 8 * j + 2 * (lane & 3) + hh;
-              const int c = gcol[cc];
-              if (c >= 0 && row < l) a.V[row + (int64_t)c * a.ldv] = acc[j][hh];
-            }
+          apply_rows(Vs, R, Jc, a.V, ld, pa, pb, r0);
         }
       }
       __syncthreads();
@@ -406,106 +382,157 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
     }
     const double om = *((volatile double*)(a.offmax + sweep));
     if (tid == 0 && blockIdx.x == 0) *a.sweeps = sweep + 1;
-    if (!(om > tol)) break;
+    // converged when no pair exceeded tol; a sweep whose largest |cos| was below
+    // 1e-8 leaves only second-order (~1e-16) off-diagonal mass behind it
+    // (quadratic convergence), so the confirming sweep is skipped
+    if (!(om > tol) || om < 1e-8) break;
   }
   if (a.prof && tid == 0 && blockIdx.x == 0)
     for (int i = 0; i < 6; ++i) a.prof[i] = tp[i];
 #undef JPROF
 }
 
-// M <- 2^-e M with 2^e ~ max |M| (exact power-of-two scaling): keeps the Gram
-// entries and their fp32 images in range whatever the scale of A.  e -> sweeps[1].
-__global__ void jacobi_prescale_kernel(double* M, int64_t ldm, int l, int* sweeps) {
+// Exponent e with 2^e ~ max |M| (exact power-of-two prescale) -> sweeps[1].
+__global__ void jacobi_scale_kernel(const double* M, int64_t ldm, int l, int* sweeps) {
   __shared__ double red[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   double mx = 0.0;
-  for (int idx = tid; idx < l * l; idx += blockDim.x) {
-    const int j = idx / l, i = idx - j * l;
-    mx = fmax(mx, fabs(M[i + (int64_t)j * ldm]));
-  }
+  for (int j = warp; j < l; j += nw)
+    for (int i = lane; i < l; i += 32) mx = fmax(mx, fabs(M[i + (int64_t)j * ldm]));
   mx = warp_max(mx);
   if (lane == 0) red[warp] = mx;
   __syncthreads();
-  mx = 0.0;
-  for (int w = 0; w < nw; ++w) mx = fmax(mx, red[w]);
-  const int e = (mx > 0.0 && isfinite(mx)) ? ilogb(mx) : 0;
-  if (tid == 0) sweeps[1] = e;
-  if (e == 0) return;
-  const double sc = ldexp(1.0, -e);
-  for (int idx = tid; idx < l * l; idx += blockDim.x) {
-    const int j = idx / l, i = idx - j * l;
-    M[i + (int64_t)j * ldm] *= sc;
+  if (tid == 0) {
+    mx = 0.0;
+    for (int w = 0; w < nw; ++w) mx = fmax(mx, red[w]);
+    sweeps[1] = (mx > 0.0 && isfinite(mx)) ? ilogb(mx) : 0;
   }
 }
 
-// sigma_j = ||M[:, j]||; rank sort (descending, ties by index); outputs sorted
-// sigma, U = M_j / sigma_j (zero column when sigma_j == 0) and V columns.
-__global__ void jacobi_finish_kernel(const double* M, int64_t ldm, const double* V, int64_t ldv,
-                                     int l, double* sig, double* U, int64_t ldu, double* Vo,
-                                     int64_t ldvo, int* order, const int* sweeps) {
+// Mrm = 2^-e M (row-major, lpad x ncp, zero padded), Vrm = identity (padded)
+__global__ void jacobi_layout_kernel(const double* M, int64_t ldm, int l, int lpad, int ncp,
+                                     const int* sweeps, double* Mrm, double* Vrm) {
+  const double sc = ldexp(1.0, -sweeps[1]);
+  const int64_t total = (int64_t)lpad * ncp;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / ncp), c = (int)(idx - (int64_t)r * ncp);
+    const bool in = r < l && c < l;
+    Mrm[idx] = in ? sc * M[r + (int64_t)c * ldm] : 0.0;
+    Vrm[idx] = (in && r == c) ? 1.0 : 0.0;
+  }
+}
+
+// sigma_j = ||M[:, j]|| (scaled; unscaled into sig), rank sort descending (ties
+// by index): order, sig, scaled norms -> nrm
+__global__ void jacobi_norms_kernel(const double* Mrm, int64_t ld, int l, int lpad,
+                                    const int* sweeps, double* sig, int* order, double* nrm_out) {
   extern __shared__ double nrm[];
-  const double unscale = ldexp(1.0, sweeps[1]);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  for (int j = warp; j < l; j += nw) {
-    double acc = 0.0;
-    for (int i = lane; i < l; i += 32) acc = fma(M[i + (int64_t)j * ldm], M[i + (int64_t)j * ldm], acc);
-    acc = warp_sum(acc);
-    if (lane == 0) nrm[j] = sqrt(acc);
+  const int tid = threadIdx.x;
+  for (int j = tid; j < l; j += blockDim.x) {
+    double a0 = 0.0, a1 = 0.0;
+    int i = 0;
+    for (; i + 1 < lpad; i += 2) {
+      const double x = Mrm[(int64_t)i * ld + j], y = Mrm[(int64_t)(i + 1) * ld + j];
+      a0 = fma(x, x, a0);
+      a1 = fma(y, y, a1);
+    }
+    if (i < lpad) a0 = fma(Mrm[(int64_t)i * ld + j], Mrm[(int64_t)i * ld + j], a0);
+    nrm[j] = sqrt(a0 + a1);
   }
   __syncthreads();
+  const double unscale = ldexp(1.0, sweeps[1]);
   for (int j = tid; j < l; j += blockDim.x) {
     int rank = 0;
     const double sj = nrm[j];
     for (int q = 0; q < l; ++q) rank += (nrm[q] > sj) || (nrm[q] == sj && q < j);
     order[rank] = j;
     sig[rank] = sj * unscale;
+    nrm_out[rank] = sj;
   }
-  __syncthreads();
-  for (int idx = tid; idx < l * l; idx += blockDim.x) {
-    const int r = idx / l, i = idx % l;
+}
+
+// U[:, r] = M[:, order[r]] / nrm[r] (zero column when nrm == 0), Vo[:, r] = V[:, order[r]]
+__global__ void jacobi_out_kernel(const double* Mrm, const double* Vrm, int64_t ld, int l,
+                                  const int* order, const double* nrm, double* U, int64_t ldu,
+                                  double* Vo, int64_t ldvo) {
+  const int64_t total = (int64_t)l * l;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / l), i = (int)(idx - (int64_t)r * l);
     const int j = order[r];
-    const double s = nrm[j];
-    U[i + (int64_t)r * ldu] = s > 0.0 ? M[i + (int64_t)j * ldm] / s : 0.0;
-    Vo[i + (int64_t)r * ldvo] = V[i + (int64_t)j * ldv];
+    const double s = nrm[r];
+    U[i + (int64_t)r * ldu] = s > 0.0 ? Mrm[(int64_t)i * ld + j] / s : 0.0;
+    Vo[i + (int64_t)r * ldvo] = Vrm[(int64_t)i * ld + j];
   }
 }
 
 int jacobi_block_size(int l) {
   (void)l;
-  return 16;   // every inner round pairs all 32 staged slots (empty slots rotate trivially)
+  return kBS;   // every inner round pairs all 32 staged slots (empty slots rotate trivially)
 }
 
-cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, double* M, int64_t ldm, double* V,
-                              int64_t ldv, int l, double* sig, double* U, int64_t ldu, double* Vo,
-                              int64_t ldvo, uint32_t* bar, double* offmax, int* sweeps, int* order,
-                              int max_sweeps) {
-  (void)sms;
-  const int bs = jacobi_block_size(l);
-  int nb = (l + bs - 1) / bs;
+static void jacobi_geometry(int l, int& nb, int& lpad, int& ncp) {
+  nb = (l + kBS - 1) / kBS;
   if (nb % 2) ++nb;
   if (nb < 2) nb = 2;
+  lpad = (l + 63) & ~63;
+  ncp = nb * kBS;
+}
+
+size_t jacobi_work_doubles(int l) {
+  int nb, lpad, ncp;
+  jacobi_geometry(l, nb, lpad, ncp);
+  return 2 * (size_t)lpad * ncp + (size_t)lpad;
+}
+
+cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, const double* M, int64_t ldm, int l,
+                              double* sig, double* U, int64_t ldu, double* Vo, int64_t ldvo,
+                              double* work, uint32_t* bar, double* offmax, int* sweeps, int* order,
+                              int max_sweeps) {
+  int nb, lpad, ncp;
+  jacobi_geometry(l, nb, lpad, ncp);
   const int P = nb / 2;
+  double* Mrm = work;
+  double* Vrm = Mrm + (size_t)lpad * ncp;
+  double* nrm = Vrm + (size_t)lpad * ncp;
   int inner = 1;
   if (const char* e = getenv("FFB_JACOBI_INNER")) inner = atoi(e);
   if (inner < 1) inner = 1;
   static long long* prof = nullptr;
   if (getenv("FFB_JACOBI_PROF") && !prof) cudaMallocManaged(&prof, 8 * sizeof(long long));
-  JacobiArgs a{M, ldm, V, ldv, l, bs, nb, 1e-15 * sqrt((double)l), max_sweeps, bar, offmax, sweeps, inner, prof};
-  const size_t lpad = (size_t)((l + 63) & ~63);
-  const size_t fixed = sizeof(double) * (lpad * kMW + 4 * 32 * 33);
-  // V region: V_W when resident (>= 8 x 32 x 33 doubles, it doubles as Gram scratch)
-  const size_t vreg = sizeof(double) * (lpad > 256 ? lpad : 256) * kMW;
-  const bool vres = fixed + vreg <= 220 * 1024;
-  const size_t smem = vres ? fixed + vreg : fixed + sizeof(double) * 64 * kMW;
-  if (smem > 220 * 1024) return cudaErrorInvalidValue;   // l > ~800 not supported
+  constexpr size_t kSmemMax = 226 * 1024;   // + static shared memory stays under the 227 KB opt-in limit
+  const size_t fixed = sizeof(double) * ((size_t)lpad * kMW + 4 * 32 * kMW);
+  const size_t scratch = sizeof(double) * 4 * 32 * 33;   // Gram partials (in the V region)
+  auto vreg = [&](int rows) {
+    const size_t b = sizeof(double) * (size_t)rows * kMW;
+    return b > scratch ? b : scratch;
+  };
+  const bool vres = fixed + vreg(lpad) <= kSmemMax;
+  int vrows = lpad;
+  if (!vres) {
+    vrows = (int)(((kSmemMax - fixed) / (sizeof(double) * kMW)) & ~7ull);
+    if (vrows > lpad) vrows = lpad;
+    if (vrows < 8) return cudaErrorInvalidValue;   // l too large for shared memory
+  }
+  const size_t smem = fixed + vreg(vrows);
+  if (smem > kSmemMax) return cudaErrorInvalidValue;
+  JacobiArgs a{Mrm, Vrm, ncp, l, lpad, nb, 1e-15 * sqrt((double)l), max_sweeps, bar, offmax, sweeps,
+               inner, vrows, prof};
   const bool cluster = P <= 16 && getenv("FFB_JACOBI_NOCLUSTER") == nullptr;
   void* kern = cluster ? (vres ? (void*)jacobi_kernel<true, true> : (void*)jacobi_kernel<true, false>)
                        : (vres ? (void*)jacobi_kernel<false, true> : (void*)jacobi_kernel<false, false>);
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
   cudaError_t e = cudaMemsetAsync(bar, 0, 2 * sizeof(uint32_t), st);
   if (e == cudaSuccess) e = cudaMemsetAsync(offmax, 0, sizeof(double) * max_sweeps, st);
   if (e != cudaSuccess) return e;
-  jacobi_prescale_kernel<<<1, 1024, 0, st>>>(M, ldm, l, sweeps);
+  jacobi_scale_kernel<<<1, 1024, 0, st>>>(M, ldm, l, sweeps);
+  {
+    const int64_t total = (int64_t)lpad * ncp;
+    int g = (int)((total + 255) / 256);
+    if (g > 4 * sms) g = 4 * sms;
+    jacobi_layout_kernel<<<g, 256, 0, st>>>(M, ldm, l, lpad, ncp, sweeps, Mrm, Vrm);
+  }
   void* args[] = {&a};
   if (cluster) {
     if (P > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -526,12 +553,24 @@ cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, double* M, int64_t ldm, 
     e = cudaLaunchCooperativeKernel(kern, dim3(P), dim3(kJThreads), args, smem, st);
   }
   if (e != cudaSuccess) return e;
-  jacobi_finish_kernel<<<1, 1024, sizeof(double) * (size_t)l, st>>>(M, ldm, V, ldv, l, sig, U, ldu,
-                                                                    Vo, ldvo, order, sweeps);
+  jacobi_norms_kernel<<<1, 1024, sizeof(double) * (size_t)l, st>>>(Mrm, ncp, l, lpad, sweeps, sig,
+                                                                   order, nrm);
+  {
+    int g = (int)(((int64_t)l * l + 255) / 256);
+    if (g > 4 * sms) g = 4 * sms;
+    jacobi_out_kernel<<<g, 256, 0, st>>>(Mrm, Vrm, ncp, l, order, nrm, U, ldu, Vo, ldvo);
+  }
   if (prof) {
     cudaStreamSynchronize(st);
     fprintf(stderr, "jacobi phases (cycles, CTA0): stage %lld gram %lld inner %lld apply %lld off %lld barrier %lld\n",
             prof[0], prof[1], prof[2], prof[3], prof[4], prof[5]);
+    double offs[64];
+    int nsw = 0;
+    cudaMemcpy(offs, offmax, sizeof(double) * (max_sweeps < 64 ? max_sweeps : 64), cudaMemcpyDeviceToHost);
+    cudaMemcpy(&nsw, sweeps, sizeof(int), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "jacobi offmax per sweep (tol %.2e):", a.tol);
+    for (int i = 0; i < nsw && i < 64; ++i) fprintf(stderr, " %.1e", offs[i]);
+    fprintf(stderr, "\n");
   }
   return cudaGetLastError();
 }

@@ -1,31 +1,33 @@
 #pragma once
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
 
 namespace ffb {
 
 struct JacobiArgs {
-  double* M;
-  int64_t ldm;
-  double* V;
-  int64_t ldv;
-  int l, bs, nb;
+  double* M;         // lpad x ncp row-major (padded, zero filled)
+  double* V;         // lpad x ncp row-major
+  int64_t ld;        // = ncp
+  int l, lpad, nb;
   double tol;
   int max_sweeps;
   uint32_t* bar;     // [2] grid barrier
   double* offmax;    // [max_sweeps]
-  int* sweeps;       // sweeps executed
+  int* sweeps;       // [0] sweeps executed, [1] prescale exponent
   int inner;         // passes over the cross-block pairs per visit
+  int vrows;         // rows per V chunk when V does not fit in shared memory
   long long* prof;   // optional phase timers (debug)
 };
 
 int jacobi_block_size(int l);
+size_t jacobi_work_doubles(int l);
 
-// SVD of the l x l matrix M (overwritten): sorted sig (l), U (l x l) and V (l x l)
-// with M = U diag(sig) V^T.  V must be initialised to the identity by the caller.
-cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, double* M, int64_t ldm, double* V,
-                              int64_t ldv, int l, double* sig, double* U, int64_t ldu, double* Vo,
-                              int64_t ldvo, uint32_t* bar, double* offmax, int* sweeps, int* order,
+// SVD of the l x l column-major matrix M (read only): sorted sig (l), U (l x l)
+// and Vo (l x l) with M = U diag(sig) Vo^T.  work: jacobi_work_doubles(l).
+cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, const double* M, int64_t ldm, int l,
+                              double* sig, double* U, int64_t ldu, double* Vo, int64_t ldvo,
+                              double* work, uint32_t* bar, double* offmax, int* sweeps, int* order,
                               int max_sweeps);
 
 }  // namespace ffb
