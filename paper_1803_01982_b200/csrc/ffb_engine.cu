@@ -108,7 +108,7 @@ void pivot_geometry(const ffb_ctx* ctx, int64_t n, int64_t s, Work& w) {
   w.piv_smem_bytes = pivots_smem_bytes((int)s, cpc, w.piv_smem);
 }
 
-constexpr int kMaxSweeps = 40;
+constexpr int kMaxSweeps = 30;   // LAPACK dgesvj's sweep cap
 
 size_t carve(const ffb_ctx* ctx, const Dims& D, void* base, size_t cap, Work& w) {
   Bump b{static_cast<char*>(base), 0, cap};
@@ -171,7 +171,7 @@ size_t carve(const ffb_ctx* ctx, const Dims& D, void* base, size_t cap, Work& w)
     w.Tt = b.take<double>(l * l);
     w.Rt = b.take<double>(l * l);
     w.Us = b.take<double>(l * l);
-    w.jwork = b.take<double>(jacobi_work_doubles((int)l));
+    w.jwork = b.take<double>(jacobi_work_doubles((int)l, kMaxSweeps));
     w.Vo = b.take<double>(l * l);
     w.sig = b.take<double>(l);
     w.W1 = b.take<double>(l * D.k);
@@ -282,6 +282,7 @@ bool validate(const Dims& D) {
   if (D.b > 64) return false;  // panel kernels are sized for b <= 64
   if (D.s > 128) return false; // pivot kernel holds one sketch column per warp (s <= 128)
   if (D.n >= 2147483647LL) return false;  // pivot exchange carries 32-bit positions
+  if (D.mode == FFB_MODE_FLIPFLOP && D.l > 512) return false;  // Jacobi SVD: <= 16 block pairs
   return true;
 }
 
@@ -532,7 +533,7 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
     // one-sided block Jacobi SVD of Rt (ffb_jacobi.cu): Rt = Us diag(sig) Vo^T
     e.ok(launch_jacobi_svd(st, ctx->sms, w.Rt, l, (int)l, w.sig, w.Us, l, w.Vo, l, w.jwork, w.jbar,
                            w.joff, w.jsweeps, w.jorder, kMaxSweeps));
-    e.launches += 4;   // scale, layout, Jacobi, norms, out kernels
+    e.launches += 5;   // scale, layout, Jacobi, V replay, norms, out kernels
     // (K15) u = Qt[:, :l] Us[:, :k] ; v = Yh Vs[:, :k]
     e.gemm(l, k, l, 1.0, w.Yt, m, true, w.Us, l, true, 0.0, w.W1, l);
     e.gemm(l, k, l, 1.0, w.Tt, l, false, w.W1, l, true, 0.0, w.W2, l);

@@ -202,7 +202,79 @@ FFB_DEV void apply_rows(const double* S, int R, const double* Js, double* X, int
   }
 }
 
-template <bool CLUSTER, bool VRES>
+// V accumulation replayed concurrently with the Jacobi rounds (fused launch):
+// V = prod over rounds of the block-diagonal rotations J recorded per visit.
+// Every ROW of V evolves independently (row <- row J on the pair's 32 columns),
+// so replay CTA v owns rows [8v, 8v + 8) in shared memory and applies each round
+// as soon as the Jacobi CTAs publish it (a.progress, release/acquire), warp w
+// taking pair slots w, w + 8, .. (disjoint columns) with DMMA 8 x 32 x 32.  The
+// replay runs on otherwise idle SMs, off the Jacobi critical path.
+FFB_DEV void v_apply_pair(double* vr, int ldv, const double* J, int pa, int pb) {
+  const int lane = threadIdx.x & 31, fr = lane >> 2, fk = lane & 3;
+  double bf[8][4], af[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bf[k][j] = J[(4 * k + fk) * 32 + 8 * j + fr];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int c = 4 * k + fk;
+    af[k] = vr[fr * ldv + (c < kBS ? pa : pb) * kBS + (c & (kBS - 1))];
+  }
+  double acc[4][2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) dmma_884(acc[j][0], acc[j][1], af[k], bf[k][j]);
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = 8 * j + 2 * fk + h;
+      vr[fr * ldv + (c < kBS ? pa : pb) * kBS + (c & (kBS - 1))] = acc[j][h];
+    }
+}
+
+FFB_DEV void v_replay(const JacobiArgs& a, int vcta, double* vr) {
+  __shared__ int s_go;
+  const int row0 = vcta * 8;
+  if (row0 >= a.lpad) return;
+  const int tid = threadIdx.x, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int ncp = (int)a.ld, ldv = ncp + 4, nb = a.nb, P = a.P;
+  for (int t = tid; t < 8 * ncp; t += blockDim.x) {
+    const int rr = t / ncp, c = t - rr * ncp;
+    vr[rr * ldv + c] = (row0 + rr == c && c < a.l) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int q = 0;; ++q) {
+    if (tid == 0) {
+      int go;
+      for (;;) {
+        if (ld_acq(a.progress) > (uint32_t)q) { go = 1; break; }
+        const uint32_t fin = ld_acq(a.progress + 1);
+        if (fin != 0u && (uint32_t)q + 1u >= fin) { go = 0; break; }
+        __nanosleep(256);
+      }
+      s_go = go;
+    }
+    __syncthreads();
+    if (!s_go) break;
+    const int r = q % (nb - 1);
+    for (int slot = warp; slot < P; slot += nw)
+      v_apply_pair(vr, ldv, a.jhist + ((size_t)q * P + slot) * 1024, rr_player(slot, r, nb),
+                   rr_player(nb - 1 - slot, r, nb));
+    __syncthreads();
+  }
+  for (int t = tid; t < 8 * ncp; t += blockDim.x) {
+    const int rr = t / ncp, c = t - rr * ncp;
+    a.V[(int64_t)(row0 + rr) * ncp + c] = vr[rr * ldv + c];
+  }
+}
+
+template <bool CLUSTER>
 __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int lpad = a.lpad, nb = a.nb;
@@ -211,11 +283,15 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
   double* Js = Gs + 32 * kMW;
   double* Gs2 = Js + 32 * kMW;            // ping-pong partners of Gs / Js
   double* Js2 = Gs2 + 32 * kMW;
-  double* Vs = Js2 + 32 * kMW;            // VRES: lpad x kMW ; else vrows x kMW chunk
+  double* part = Js2 + 32 * kMW;          // 4 x 32 x 33 Gram partials
   __shared__ int gcol[32];
   __shared__ double s_off;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
-  const int P = gridDim.x;
+  if ((int)blockIdx.x >= a.P) {   // fused launch: V replay CTAs (see v_replay)
+    v_replay(a, (int)blockIdx.x - a.P, sm);
+    return;
+  }
+  const int P = a.P;
   const double tol = a.tol;
   const double tol2 = a.tol * a.tol;
   const int64_t ld = a.ld;
@@ -245,7 +321,6 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
       // fresh Gram G = M_W^T M_W: warp w sums rows [w*lpad/8, (w+1)*lpad/8) for all
       // 16 output tiles (16 independent DMMA chains); fixed-order two-level reduce
       {
-        double* part = Vs;   // 4 x 32 x 33 scratch (V is staged after the Gram)
         const int fr = lane >> 2, fk = lane & 3;
         double acc[4][4][2];
 #pragma unroll
@@ -291,11 +366,6 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
           Js[rr * kMW + c] = rr == c ? 1.0 : 0.0;
         }
         __syncthreads();
-        if (VRES) {
-          // V staging overlaps the inner rotations
-          stage_rows_async(Vs, a.V, ld, pa, pb, 0, lpad);
-          cp_async_commit();
-        }
       }
       JPROF(1)
       // every round pairs all 32 local slots (16 disjoint pairs); thread (ba, bb2)
@@ -351,20 +421,10 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
       double off = offn > 0.0 ? sqrt(offn / offd) : 0.0;
       JPROF(2)
       apply_rows(Ms, lpad, Jc, a.M, ld, pa, pb, 0);
-      if (VRES) {
-        cp_async_wait<0>();
-        __syncthreads();
-        apply_rows(Vs, lpad, Jc, a.V, ld, pa, pb, 0);
-      } else {
-        for (int r0 = 0; r0 < lpad; r0 += a.vrows) {
-          const int R = lpad - r0 < a.vrows ? lpad - r0 : a.vrows;
-          __syncthreads();
-          stage_rows_async(Vs, a.V, ld, pa, pb, r0, R);
-          cp_async_commit();
-          cp_async_wait<0>();
-          __syncthreads();
-          apply_rows(Vs, R, Jc, a.V, ld, pa, pb, r0);
-        }
+      // record this visit's J for the deferred V accumulation (jacobi_v_kernel)
+      {
+        double* jh = a.jhist + (((size_t)sweep * (nb - 1) + r) * P + blockIdx.x) * 1024;
+        for (int t = tid; t < 1024; t += nt) jh[t] = Jc[(t >> 5) * kMW + (t & 31)];
       }
       __syncthreads();
       JPROF(3)
@@ -378,6 +438,11 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
                   (unsigned long long)__double_as_longlong(s_off));
       JPROF(4)
       round_barrier<CLUSTER>(a.bar, P);
+      // publish progress to the V replay CTAs: J of every finished round is visible
+      if (a.fused && tid == 0 && blockIdx.x == 0) {
+        __threadfence();
+        st_rel(a.progress, (uint32_t)(sweep * (nb - 1) + r + 1));
+      }
       JPROF(5)
     }
     const double om = *((volatile double*)(a.offmax + sweep));
@@ -385,11 +450,93 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
     // converged when no pair exceeded tol; a sweep whose largest |cos| was below
     // 1e-8 leaves only second-order (~1e-16) off-diagonal mass behind it
     // (quadratic convergence), so the confirming sweep is skipped
-    if (!(om > tol) || om < 1e-8) break;
+    if (!(om > tol) || om < 1e-8 || sweep + 1 == a.max_sweeps) {
+      if (a.fused && tid == 0 && blockIdx.x == 0) st_rel(a.progress + 1, (uint32_t)((sweep + 1) * (nb - 1) + 1));
+      break;
+    }
   }
   if (a.prof && tid == 0 && blockIdx.x == 0)
     for (int i = 0; i < 6; ++i) a.prof[i] = tp[i];
 #undef JPROF
+}
+
+// Deferred V accumulation.  V = prod over (sweep, round) of the block-diagonal
+// rotations J recorded by jacobi_kernel; every ROW of V evolves independently
+// (row_i <- row_i J on the pair's 32 columns), so CTA g owns rows [8g, 8g + 8)
+// in shared memory and replays the whole rotation history: warp w applies the
+// pair slots w, w + 8, .. of each round (disjoint columns, one barrier per
+// round) with DMMA (8 x 32 x 32 per pair), prefetching the next pair's J
+// fragments from L2 while the current one computes.  Replaces 2 l^2 x 32 DMMA
+// flops per round on the serial Jacobi critical path with a short parallel pass.
+constexpr int kVRows = 8;
+__global__ void __launch_bounds__(512) jacobi_v_kernel(const double* jhist, int nb, int P, int l,
+                                                      int ncp, const int* sweeps, double* Vrm) {
+  extern __shared__ __align__(16) double vr[];   // kVRows x (ncp + 4)
+  const int ldv = ncp + 4;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int fr = lane >> 2, fk = lane & 3;
+  const int row0 = blockIdx.x * kVRows;
+  for (int t = tid; t < kVRows * ncp; t += blockDim.x) {
+    const int rr = t / ncp, c = t - rr * ncp;
+    vr[rr * ldv + c] = (row0 + rr == c && c < l) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int S = sweeps[0];
+  const int nrounds = S * (nb - 1);
+  auto jptr = [&](int q, int slot) { return jhist + ((size_t)q * P + slot) * 1024; };
+  auto load_b = [&](double (&b)[8][4], const double* J) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[k][j] = J[(4 * k + fk) * 32 + 8 * j + fr];
+  };
+  // one pair update: rows' 32 columns of blocks (pa | pb) <- (...) J
+  auto apply = [&](const double (&b)[8][4], int pa, int pb) {
+    double af[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int c = 4 * k + fk;
+      af[k] = vr[fr * ldv + (c < kBS ? pa : pb) * kBS + (c & (kBS - 1))];
+    }
+    double acc[4][2];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_884(acc[j][0], acc[j][1], af[k], b[k][j]);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = 8 * j + 2 * fk + h;
+        vr[fr * ldv + (c < kBS ? pa : pb) * kBS + (c & (kBS - 1))] = acc[j][h];
+      }
+  };
+  // one warp per pair slot (blockDim = 32 * P): every warp has exactly one item
+  // per round; the next round's J fragments are in flight while this one computes
+  double b0[8][4], b1[8][4];
+  const int slot = warp;
+  if (nrounds > 0) load_b(b0, jptr(0, slot));
+  for (int q = 0; q < nrounds; q += 2) {
+    {
+      const int r = q % (nb - 1);
+      if (q + 1 < nrounds) load_b(b1, jptr(q + 1, slot));
+      apply(b0, rr_player(slot, r, nb), rr_player(nb - 1 - slot, r, nb));
+      __syncthreads();
+    }
+    if (q + 1 < nrounds) {
+      const int r = (q + 1) % (nb - 1);
+      if (q + 2 < nrounds) load_b(b0, jptr(q + 2, slot));
+      apply(b1, rr_player(slot, r, nb), rr_player(nb - 1 - slot, r, nb));
+      __syncthreads();
+    }
+  }
+  for (int t = tid; t < kVRows * ncp; t += blockDim.x) {
+    const int rr = t / ncp, c = t - rr * ncp;
+    Vrm[(int64_t)(row0 + rr) * ncp + c] = vr[rr * ldv + c];
+  }
 }
 
 // Exponent e with 2^e ~ max |M| (exact power-of-two prescale) -> sweeps[1].
@@ -409,9 +556,9 @@ __global__ void jacobi_scale_kernel(const double* M, int64_t ldm, int l, int* sw
   }
 }
 
-// Mrm = 2^-e M (row-major, lpad x ncp, zero padded), Vrm = identity (padded)
+// Mrm = 2^-e M (row-major, lpad x ncp, zero padded)
 __global__ void jacobi_layout_kernel(const double* M, int64_t ldm, int l, int lpad, int ncp,
-                                     const int* sweeps, double* Mrm, double* Vrm) {
+                                     const int* sweeps, double* Mrm) {
   const double sc = ldexp(1.0, -sweeps[1]);
   const int64_t total = (int64_t)lpad * ncp;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -419,7 +566,6 @@ __global__ void jacobi_layout_kernel(const double* M, int64_t ldm, int l, int lp
     const int r = (int)(idx / ncp), c = (int)(idx - (int64_t)r * ncp);
     const bool in = r < l && c < l;
     Mrm[idx] = in ? sc * M[r + (int64_t)c * ldm] : 0.0;
-    Vrm[idx] = (in && r == c) ? 1.0 : 0.0;
   }
 }
 
@@ -480,10 +626,11 @@ static void jacobi_geometry(int l, int& nb, int& lpad, int& ncp) {
   ncp = nb * kBS;
 }
 
-size_t jacobi_work_doubles(int l) {
+size_t jacobi_work_doubles(int l, int max_sweeps) {
   int nb, lpad, ncp;
   jacobi_geometry(l, nb, lpad, ncp);
-  return 2 * (size_t)lpad * ncp + (size_t)lpad;
+  // Mrm, Vrm, norms, J history (max_sweeps x rounds x pairs x 32 x 32)
+  return 2 * (size_t)lpad * ncp + (size_t)lpad + (size_t)max_sweeps * (nb - 1) * (nb / 2) * 1024;
 }
 
 cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, const double* M, int64_t ldm, int l,
@@ -496,34 +643,21 @@ cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, const double* M, int64_t
   double* Mrm = work;
   double* Vrm = Mrm + (size_t)lpad * ncp;
   double* nrm = Vrm + (size_t)lpad * ncp;
+  double* jhist = nrm + lpad;
   int inner = 1;
   if (const char* e = getenv("FFB_JACOBI_INNER")) inner = atoi(e);
   if (inner < 1) inner = 1;
   static long long* prof = nullptr;
   if (getenv("FFB_JACOBI_PROF") && !prof) cudaMallocManaged(&prof, 8 * sizeof(long long));
   constexpr size_t kSmemMax = 226 * 1024;   // + static shared memory stays under the 227 KB opt-in limit
-  const size_t fixed = sizeof(double) * ((size_t)lpad * kMW + 4 * 32 * kMW);
-  const size_t scratch = sizeof(double) * 4 * 32 * 33;   // Gram partials (in the V region)
-  auto vreg = [&](int rows) {
-    const size_t b = sizeof(double) * (size_t)rows * kMW;
-    return b > scratch ? b : scratch;
-  };
-  const bool vres = fixed + vreg(lpad) <= kSmemMax;
-  int vrows = lpad;
-  if (!vres) {
-    vrows = (int)(((kSmemMax - fixed) / (sizeof(double) * kMW)) & ~7ull);
-    if (vrows > lpad) vrows = lpad;
-    if (vrows < 8) return cudaErrorInvalidValue;   // l too large for shared memory
-  }
-  const size_t smem = fixed + vreg(vrows);
-  if (smem > kSmemMax) return cudaErrorInvalidValue;
-  JacobiArgs a{Mrm, Vrm, ncp, l, lpad, nb, 1e-15 * sqrt((double)l), max_sweeps, bar, offmax, sweeps,
-               inner, vrows, prof};
+  const size_t smem = sizeof(double) * ((size_t)lpad * kMW + 4 * 32 * kMW + 4 * 32 * 33);
+  if (smem > kSmemMax) return cudaErrorInvalidValue;   // l > ~560 not supported
+  JacobiArgs a{Mrm, jhist, ncp, l, lpad, nb, 1e-15 * sqrt((double)l), max_sweeps, bar, offmax,
+               sweeps, inner, prof, P, Vrm, bar + 2, 0};
   const bool cluster = P <= 16 && getenv("FFB_JACOBI_NOCLUSTER") == nullptr;
-  void* kern = cluster ? (vres ? (void*)jacobi_kernel<true, true> : (void*)jacobi_kernel<true, false>)
-                       : (vres ? (void*)jacobi_kernel<false, true> : (void*)jacobi_kernel<false, false>);
+  void* kern = cluster ? (void*)jacobi_kernel<true> : (void*)jacobi_kernel<false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
-  cudaError_t e = cudaMemsetAsync(bar, 0, 2 * sizeof(uint32_t), st);
+  cudaError_t e = cudaMemsetAsync(bar, 0, 4 * sizeof(uint32_t), st);
   if (e == cudaSuccess) e = cudaMemsetAsync(offmax, 0, sizeof(double) * max_sweeps, st);
   if (e != cudaSuccess) return e;
   jacobi_scale_kernel<<<1, 1024, 0, st>>>(M, ldm, l, sweeps);
@@ -531,28 +665,57 @@ cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, const double* M, int64_t
     const int64_t total = (int64_t)lpad * ncp;
     int g = (int)((total + 255) / 256);
     if (g > 4 * sms) g = 4 * sms;
-    jacobi_layout_kernel<<<g, 256, 0, st>>>(M, ldm, l, lpad, ncp, sweeps, Mrm, Vrm);
+    jacobi_layout_kernel<<<g, 256, 0, st>>>(M, ldm, l, lpad, ncp, sweeps, Mrm);
   }
-  void* args[] = {&a};
+  bool fused_ok = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (prof) {
+    cudaEventCreate(&ev0);
+    cudaEventCreate(&ev1);
+    cudaEventRecord(ev0, st);
+  }
   if (cluster) {
     if (P > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(P);
-    cfg.blockDim = dim3(kJThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = P;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    e = cudaLaunchKernelExC(&cfg, kern, args);
+    // fused: cluster 0 iterates, clusters 1.. replay V concurrently (cooperative
+    // launch guarantees co-residency for the progress spin-wait)
+    const int vctas = lpad / kVRows;
+    const int nvc = (vctas + P - 1) / P;
+    const bool try_fused = getenv("FFB_JACOBI_NOFUSE") == nullptr && P * (1 + nvc) <= sms;
+    for (int attempt = try_fused ? 0 : 1; attempt < 2 && !fused_ok; ++attempt) {
+      a.fused = attempt == 0 ? 1 : 0;
+      void* args[] = {&a};
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(a.fused ? P * (1 + nvc) : P);
+      cfg.blockDim = dim3(kJThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[2];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = P;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      attr[1].id = cudaLaunchAttributeCooperative;
+      attr[1].val.cooperative = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = a.fused ? 2 : 1;
+      e = cudaLaunchKernelExC(&cfg, kern, args);
+      if (e == cudaSuccess) {
+        fused_ok = a.fused != 0;
+        if (!a.fused) break;
+      } else {
+        (void)cudaGetLastError();
+        if (!a.fused) return e;
+      }
+    }
   } else {
+    void* args[] = {&a};
     e = cudaLaunchCooperativeKernel(kern, dim3(P), dim3(kJThreads), args, smem, st);
+    if (e != cudaSuccess) return e;
   }
-  if (e != cudaSuccess) return e;
+  if (!fused_ok)
+    jacobi_v_kernel<<<lpad / kVRows, 32 * P, sizeof(double) * kVRows * (ncp + 4), st>>>(
+        jhist, nb, P, l, ncp, sweeps, Vrm);
+  if (prof) cudaEventRecord(ev1, st);
   jacobi_norms_kernel<<<1, 1024, sizeof(double) * (size_t)l, st>>>(Mrm, ncp, l, lpad, sweeps, sig,
                                                                    order, nrm);
   {
@@ -562,13 +725,16 @@ cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, const double* M, int64_t
   }
   if (prof) {
     cudaStreamSynchronize(st);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev0, ev1);
+    fprintf(stderr, "jacobi iteration + V: %.3f ms\n", ms);
     fprintf(stderr, "jacobi phases (cycles, CTA0): stage %lld gram %lld inner %lld apply %lld off %lld barrier %lld\n",
             prof[0], prof[1], prof[2], prof[3], prof[4], prof[5]);
     double offs[64];
     int nsw = 0;
     cudaMemcpy(offs, offmax, sizeof(double) * (max_sweeps < 64 ? max_sweeps : 64), cudaMemcpyDeviceToHost);
     cudaMemcpy(&nsw, sweeps, sizeof(int), cudaMemcpyDeviceToHost);
-    fprintf(stderr, "jacobi offmax per sweep (tol %.2e):", a.tol);
+    fprintf(stderr, "jacobi fused=%d offmax per sweep (tol %.2e):", (int)fused_ok, a.tol);
     for (int i = 0; i < nsw && i < 64; ++i) fprintf(stderr, " %.1e", offs[i]);
     fprintf(stderr, "\n");
   }

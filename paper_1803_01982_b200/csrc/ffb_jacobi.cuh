@@ -7,7 +7,7 @@ namespace ffb {
 
 struct JacobiArgs {
   double* M;         // lpad x ncp row-major (padded, zero filled)
-  double* V;         // lpad x ncp row-major
+  double* jhist;     // [max_sweeps][nb - 1][nb / 2][32 x 32] recorded rotations
   int64_t ld;        // = ncp
   int l, lpad, nb;
   double tol;
@@ -16,12 +16,15 @@ struct JacobiArgs {
   double* offmax;    // [max_sweeps]
   int* sweeps;       // [0] sweeps executed, [1] prescale exponent
   int inner;         // passes over the cross-block pairs per visit
-  int vrows;         // rows per V chunk when V does not fit in shared memory
   long long* prof;   // optional phase timers (debug)
+  int P;             // Jacobi CTAs (block pairs); CTAs >= P replay V (fused launch)
+  double* V;         // lpad x ncp row-major V (written by the replay)
+  uint32_t* progress;  // [0] rounds published, [1] total rounds + 1 when done
+  int fused;
 };
 
 int jacobi_block_size(int l);
-size_t jacobi_work_doubles(int l);
+size_t jacobi_work_doubles(int l, int max_sweeps);
 
 // SVD of the l x l column-major matrix M (read only): sorted sig (l), U (l x l)
 // and Vo (l x l) with M = U diag(sig) Vo^T.  work: jacobi_work_doubles(l).
