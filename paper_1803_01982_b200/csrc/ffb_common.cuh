@@ -9,6 +9,16 @@ namespace ffb {
 
 constexpr int kWarp = 32;
 
+// 1/x to ~1 ulp: MUFU reciprocal seed + two Newton steps (no IEEE division
+// subroutine on the critical path of sequential factorizations)
+FFB_DEV double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = r * fma(-x, r, 2.0);
+  r = r * fma(-x, r, 2.0);
+  return r;
+}
+
 FFB_DEV double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -283,6 +283,7 @@ bool validate(const Dims& D) {
   if (D.s > 128) return false; // pivot kernel holds one sketch column per warp (s <= 128)
   if (D.n >= 2147483647LL) return false;  // pivot exchange carries 32-bit positions
   if (D.mode == FFB_MODE_FLIPFLOP && D.l > 512) return false;  // Jacobi SVD: <= 16 block pairs
+  if (D.mode != FFB_MODE_TRQRCP && D.l > 1022) return false;  // g2 solve: one thread per row
   return true;
 }
 

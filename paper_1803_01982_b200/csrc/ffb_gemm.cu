@@ -1,5 +1,7 @@
 // Host dispatcher for the FP64 DMMA GEMM engine (tile configs x operand layouts).
 #include <algorithm>
+#include <cstdlib>
+#include <cstdio>
 
 #include "ffb_gemm.h"
 #include "gemm_f64.cuh"
@@ -8,10 +10,10 @@ namespace ffb {
 
 namespace {
 
-template <int BM, int BN, int BK, int WM, int WN, bool AK, bool BKC, int ST, bool V2>
-cudaError_t launch_cfg1(cudaStream_t st, const GemmArgs& g, dim3 grid) {
+template <int BM, int BN, int BK, int WM, int WN, bool AK, bool BKC, int ST, bool V2, bool SK>
+cudaError_t launch_cfg2(cudaStream_t st, const GemmArgs& g, dim3 grid) {
   using Cfg = GemmCfg<BM, BN, BK, WM, WN, AK, BKC, ST>;
-  auto kern = gemm_f64_kernel<BM, BN, BK, WM, WN, AK, BKC, ST, V2>;
+  auto kern = gemm_f64_kernel<BM, BN, BK, WM, WN, AK, BKC, ST, V2, SK>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
@@ -21,13 +23,19 @@ cudaError_t launch_cfg1(cudaStream_t st, const GemmArgs& g, dim3 grid) {
   return cudaGetLastError();
 }
 
+template <int BM, int BN, int BK, int WM, int WN, bool AK, bool BKC, int ST, bool V2>
+cudaError_t launch_cfg1(cudaStream_t st, const GemmArgs& g, dim3 grid) {
+  if (g.sk_per > 0) return launch_cfg2<BM, BN, BK, WM, WN, AK, BKC, ST, V2, true>(st, g, grid);
+  return launch_cfg2<BM, BN, BK, WM, WN, AK, BKC, ST, V2, false>(st, g, grid);
+}
+
 // resident CTAs per SM of a tile config (cached)
 template <int BM, int BN, int BK, int WM, int WN, int ST>
 int occupancy() {
   static int occ = 0;
   if (!occ) {
     using Cfg = GemmCfg<BM, BN, BK, WM, WN, true, true, ST>;
-    auto kern = gemm_f64_kernel<BM, BN, BK, WM, WN, true, true, ST, true>;
+    auto kern = gemm_f64_kernel<BM, BN, BK, WM, WN, true, true, ST, true, true>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::kThreads, Cfg::kSmem) != cudaSuccess || occ < 1)
       occ = 1;
@@ -41,7 +49,9 @@ int occupancy_of(int cfg) {
     case 1: return occupancy<64, 64, 16, 32, 32, 4>();
     case 2: return occupancy<96, 64, 16, 48, 32, 4>();
     case 3: return occupancy<128, 64, 16, 32, 32, 3>();
-    default: return occupancy<128, 96, 16, 32, 48, 3>();
+    case 4: return occupancy<128, 96, 16, 32, 48, 3>();
+    case 5: return occupancy<16, 64, 16, 16, 16, 4>();
+    default: return occupancy<32, 64, 16, 16, 32, 4>();
   }
 }
 
@@ -63,10 +73,19 @@ struct Shape {
 
 // Tile selection by M (the output rows): sketch / WT rows have M = s or b <= 96,
 // the tall products (A*Yhat, panel updates) have M = m.
-int pick_cfg(int64_t M, int64_t N) {
+int pick_cfg(int64_t M, int64_t N, int64_t K) {
+  static int forced = -2;
+  if (forced == -2) {
+    const char* e = getenv("FFB_GEMM_CFG");
+    forced = e ? atoi(e) : -1;
+  }
+  if (forced >= 0) return forced > 6 ? 6 : forced;
+  if (M <= 16) return 5;
+  if (M <= 32) return 6;
   if (M <= 48) return 0;
   if (M <= 64) return 1;
   if (M <= 96) return 2;
+  if (M >= 1024 && K < 512) return 0;   // tall, short K: many small tiles fill the SMs
   if (M >= 1024) {
     // tall products (N = l): pick the N tile with less padding waste
     const int64_t w64 = (N + 63) / 64 * 64 - N, w96 = (N + 95) / 96 * 96 - N;
@@ -75,7 +94,9 @@ int pick_cfg(int64_t M, int64_t N) {
   return 1;
 }
 
-const Shape kShapes[5] = {{48, 64, 16}, {64, 64, 16}, {96, 64, 16}, {128, 64, 16}, {128, 96, 16}};
+// 0..5 as below, 6 = 32 x 64 (shared by the default cases)
+const Shape kShapes[7] = {{48, 64, 16},  {64, 64, 16}, {96, 64, 16}, {128, 64, 16},
+                          {128, 96, 16}, {16, 64, 16}, {32, 64, 16}};
 
 template <bool AK, bool BKC>
 cudaError_t launch_layout(int cfg, cudaStream_t st, const GemmArgs& g, dim3 grid) {
@@ -84,7 +105,9 @@ cudaError_t launch_layout(int cfg, cudaStream_t st, const GemmArgs& g, dim3 grid
     case 1: return launch_cfg<64, 64, 16, 32, 32, AK, BKC, 4>(st, g, grid);
     case 2: return launch_cfg<96, 64, 16, 48, 32, AK, BKC, 4>(st, g, grid);
     case 3: return launch_cfg<128, 64, 16, 32, 32, AK, BKC, 3>(st, g, grid);
-    default: return launch_cfg<128, 96, 16, 32, 48, AK, BKC, 3>(st, g, grid);
+    case 4: return launch_cfg<128, 96, 16, 32, 48, AK, BKC, 3>(st, g, grid);
+    case 5: return launch_cfg<16, 64, 16, 16, 16, AK, BKC, 4>(st, g, grid);
+    default: return launch_cfg<32, 64, 16, 16, 32, AK, BKC, 4>(st, g, grid);
   }
 }
 
@@ -94,7 +117,11 @@ cudaError_t gemm_f64(GemmCtx& c, cudaStream_t st, int64_t M, int64_t N, int64_t 
                      const double* A, int64_t lda, bool akc, const double* B, int64_t ldb, bool bkc,
                      double beta, double* C, int64_t ldc, GemmPartialOut* pout) {
   if (M <= 0 || N <= 0) return cudaSuccess;
-  const int cfg = pick_cfg(M, N);
+  const int cfg = pick_cfg(M, N, K);
+  static int glog = -1;
+  if (glog < 0) glog = getenv("FFB_GEMM_LOG") ? 1 : 0;
+  if (glog) fprintf(stderr, "[gemm] M=%lld N=%lld K=%lld akc=%d bkc=%d cfg=%d\n", (long long)M, (long long)N,
+                    (long long)K, (int)akc, (int)bkc, cfg);
   const Shape sh = kShapes[cfg];
   int64_t gx = (N + sh.bn - 1) / sh.bn, gy = (M + sh.bm - 1) / sh.bm;
   const int64_t tiles = gx * gy;
@@ -151,12 +178,18 @@ cudaError_t gemm_f64(GemmCtx& c, cudaStream_t st, int64_t M, int64_t N, int64_t 
   // Stream-K (persistent, equal iteration ranges, deterministic fixup) whenever the
   // classic grid would leave SMs idle: removes split-K wave quantisation.
   bool use_sk = false;
-  if (!pout && K > 0) {
+  static int sk_mode = -2;   // FFB_GEMM_SK: 0 = never, 1 = auto (default)
+  if (sk_mode == -2) {
+    const char* e = getenv("FFB_GEMM_SK");
+    sk_mode = e ? atoi(e) : 1;
+  }
+  if (!pout && K > 0 && sk_mode != 0) {
     const int64_t slots = (int64_t)c.sms * occupancy_of(cfg);
     const int64_t kit = g.sk_kiters;
     const int64_t waves = (tiles + slots - 1) / slots;
     const double eff = (double)tiles / (double)(waves * slots);
-    if (eff < 0.9 && kit >= 8 && tiles >= 32) {
+    // short K: the fixup would cost more than the tail it removes
+    if (eff < 0.9 && kit >= 32 && tiles >= 32) {
       const int64_t total = tiles * kit;
       // <= 8 CTAs cover any tile (bounded fixup work), >= 4 k-tiles per CTA
       int64_t G = std::min<int64_t>(std::min<int64_t>(slots, tiles * 8), std::max<int64_t>(1, total / 4));

@@ -10,6 +10,7 @@
 
 #include "ffb_common.cuh"
 #include "ffb_kernels.cuh"
+#include "ffb_tile64.cuh"
 
 namespace ffb {
 
@@ -981,42 +982,32 @@ cudaError_t launch_fix_rrows(cudaStream_t st, double* R, int64_t ldr, int64_t j0
 __global__ void __launch_bounds__(256) triinv_upper_kernel(const double* __restrict__ Rb,
                                                            int64_t ldrb, int w, double* Rinv,
                                                            uint32_t* status) {
+  using namespace tile64;
   extern __shared__ __align__(16) double dsm[];
-  double* R = dsm;
-  double* X = R + kMaxW * kSLD;
+  double* U = dsm;                 // 64 x kTL
+  double* X = U + 64 * kTL;        // 64 x kTL
+  double* S = X + 64 * kTL;        // 1024 scratch
+  __shared__ int zp;
   const int tid = threadIdx.x, nt = blockDim.x;
-  bool zp = false;
-  for (int t = tid; t < w * w; t += nt) {
-    const int i = t % w, j = t / w;
-    R[i * kSLD + j] = Rb[i + j * ldrb];
-    X[i * kSLD + j] = 0.0;
+  if (tid == 0) zp = 0;
+  for (int t = tid; t < 64 * 64; t += nt) {
+    const int i = t >> 6, j = t & 63;
+    U[i * kTL + j] = (i < w && j < w) ? Rb[i + (int64_t)j * ldrb] : 0.0;
   }
   __syncthreads();
-  const int c = tid >> 2, sub = tid & 3;
-  for (int i = w - 1; i >= 0; --i) {
-    double acc = 0.0;
-    if (c < w && c >= i)
-      for (int k = i + 1 + sub; k <= c; k += 4) acc = fma(R[i * kSLD + k], X[k * kSLD + c], acc);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    if (c < w && c >= i && sub == 0) {
-      const double d = R[i * kSLD + i];
-      if (d != 0.0) X[i * kSLD + c] = ((i == c ? 1.0 : 0.0) - acc) / d;
-      else zp = true;
-    }
-    __syncthreads();
-  }
+  if (tid < w && U[tid * kTL + tid] == 0.0) zp = 1;
+  inv_upper_blk(U, w, X, S);
   for (int t = tid; t < w * w; t += nt) {
     const int i = t % w, j = t / w;
-    Rinv[i + j * w] = X[i * kSLD + j];
+    Rinv[i + j * w] = X[i * kTL + j];
   }
-  if (zp) atomicOr(status, kStZeroPivot);
+  if (tid == 0 && zp) atomicOr(status, kStZeroPivot);
 }
 
 cudaError_t launch_triinv_upper(cudaStream_t st, const double* Rb, int64_t ldrb, int w,
                                 double* Rinv, uint32_t* status) {
   static bool init = false;
-  constexpr int kSm = 2 * kMaxW * kSLD * sizeof(double);
+  constexpr int kSm = (2 * 64 * tile64::kTL + 1024) * sizeof(double);
   if (!init) {
     cudaFuncSetAttribute(triinv_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSm);
     init = true;
@@ -1258,22 +1249,24 @@ cudaError_t launch_ext_row(cudaStream_t st, const double* A, int64_t lda, int64_
 }
 
 // g2 estimate (ffsrqr/srqr.py:49-64): Z = Rtilde^{-1} Omega^T by right-looking
-// back substitution — column i of Rtilde is the contiguous R[:i+1, arr[i]], so
-// each step reads one coalesced column (prefetched one step ahead) and updates
-// the d right-hand sides of all rows above; row norms; first argmax;
-// g2 = |alpha|/sqrt(d) * max.  Omega is d x (l+1) row-major (numpy C order).
+// back substitution; row norms; first argmax; g2 = |alpha|/sqrt(d) * max.
+// Thread k owns row k of Z (its d right-hand sides live in registers).  Step i:
+// the owner of row i (already final) divides by Rtilde_ii and publishes z_i;
+// one barrier; every row k < i does z_k -= Rtilde_ki z_i.  Column values
+// Rtilde_ki = R[k, arr[i]] are prefetched four steps ahead (register ring with
+// static roles).  Omega is d x (l+1) row-major (numpy C order).
 constexpr int kG2MaxD = 16;
-__global__ void __launch_bounds__(1024) g2_kernel(const double* __restrict__ R, int64_t ldr,
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT) g2_kernel(const double* __restrict__ R, int64_t ldr,
                                                   const int64_t* __restrict__ arr, int64_t l,
                                                   const double* __restrict__ omega, int d, double g,
                                                   double* Z, SrqrScalars* sc) {
-  extern __shared__ double g2s[];
+  extern __shared__ int64_t g2cols[];   // [l+1] arrangement (column of Rtilde -> R column)
+  __shared__ double zb[2][kG2MaxD];
   __shared__ double red_v[32];
   __shared__ int64_t red_i[32];
   __shared__ int sing;
-  const int64_t L1 = l + 1;
-  double* bz = g2s;                  // [d][L1] right-hand sides -> solution
-  double* col = bz + (size_t)d * L1; // [2][L1] double-buffered column of Rtilde
+  const int L1 = (int)(l + 1);
   const double alpha = sc->alpha;
   const int tid = threadIdx.x, nt = blockDim.x;
   if (tid == 0) sing = 0;
@@ -1286,13 +1279,12 @@ __global__ void __launch_bounds__(1024) g2_kernel(const double* __restrict__ R, 
     }
     return;
   }
-  for (int64_t i = tid; i < L1; i += nt) {
-    const double dv = (i == l) ? alpha : R[i + arr[i] * ldr];
+  for (int i = tid; i < L1; i += nt) {
+    const int64_t c = arr[i];
+    g2cols[i] = c;
+    const double dv = (i == l) ? alpha : R[i + c * ldr];
     if (dv == 0.0) sing = 1;
   }
-  for (int64_t t = tid; t < (int64_t)d * L1; t += nt) bz[t] = omega[t];   // row-major d x L1
-  // column l of Rtilde: R[:l, arr[l]] and alpha on the diagonal
-  for (int64_t k = tid; k < L1; k += nt) col[L1 + k] = (k == l) ? alpha : R[k + arr[l] * ldr];
   __syncthreads();
   if (sing) {
     if (tid == 0) {
@@ -1301,37 +1293,53 @@ __global__ void __launch_bounds__(1024) g2_kernel(const double* __restrict__ R, 
     }
     return;
   }
-  for (int64_t i = l; i >= 0; --i) {
-    const bool odd = ((l - i) & 1) != 0;
-    const double* ci = col + (odd ? 0 : L1);   // buffer holding column i (column l in buffer 1)
-    double* cn = col + (odd ? L1 : 0);         // next column (i-1)
-    const double dii = ci[i];
-    // prefetch column i-1 (rows 0..i-1) while updating with column i
-    double pre = 0.0;
-    const int64_t nxt = i - 1;
-    if (nxt >= 0 && tid < nxt + 1) pre = R[tid + arr[nxt] * ldr];
-    for (int64_t t = tid; t < (int64_t)d * i; t += nt) {
-      const int r = (int)(t / i);
-      const int64_t k = t - (int64_t)r * i;
-      bz[(size_t)r * L1 + k] -= ci[k] * (bz[(size_t)r * L1 + i] / dii);
+  const int k = tid;   // this thread's row (L1 <= 1024)
+  const double dkk = k < L1 ? (k == (int)l ? alpha : R[k + g2cols[k] * ldr]) : 1.0;
+  const double rdkk = 1.0 / dkk;   // the solve multiplies by the inverted diagonal
+  // Rtilde_{k,col}: column l is (R[:l, arr[l]]; alpha); rows above the column only
+  auto colval = [&](int col) -> double {
+    return (col >= 0 && k < col) ? R[k + g2cols[col] * ldr] : 0.0;
+  };
+  double nrm2 = 0.0;
+  for (int r0 = 0; r0 < d; r0 += kG2MaxD) {   // right-hand sides in chunks of 16
+    const int dc = d - r0 < kG2MaxD ? d - r0 : kG2MaxD;
+    double z[kG2MaxD];
+#pragma unroll
+    for (int r = 0; r < kG2MaxD; ++r)
+      z[r] = (r < dc && k < L1) ? omega[(int64_t)(r0 + r) * L1 + k] : 0.0;
+    double c0 = colval(L1 - 1), c1 = colval(L1 - 2), c2 = colval(L1 - 3), c3 = colval(L1 - 4);
+    auto step = [&](int i, double& cslot) {
+      const int par = i & 1;
+      if (k == i) {
+#pragma unroll
+        for (int r = 0; r < kG2MaxD; ++r)
+          if (r < dc) {
+            z[r] = z[r] * rdkk;
+            zb[par][r] = z[r];
+          }
+      }
+      __syncthreads();
+      const double c = cslot;
+      cslot = colval(i - 4);   // ring slot now serves step i - 4
+      if (k < i) {
+#pragma unroll
+        for (int r = 0; r < kG2MaxD; ++r)
+          if (r < dc) z[r] = fma(-c, zb[par][r], z[r]);
+      }
+    };
+    for (int i = L1 - 1; i >= 0; i -= 4) {
+      step(i, c0);
+      if (i - 1 >= 0) step(i - 1, c1);
+      if (i - 2 >= 0) step(i - 2, c2);
+      if (i - 3 >= 0) step(i - 3, c3);
     }
-    if (nxt >= 0) {
-      if (tid < nxt + 1) cn[tid] = pre;
-      for (int64_t k = tid + nt; k <= nxt; k += nt) cn[k] = R[k + arr[nxt] * ldr];
-    }
-    __syncthreads();
-    if (tid < d) bz[(size_t)tid * L1 + i] /= dii;
+#pragma unroll
+    for (int r = 0; r < kG2MaxD; ++r)
+      if (r < dc) nrm2 = fma(z[r], z[r], nrm2);
     __syncthreads();
   }
   ArgMax best{-1.0, -1};
-  for (int64_t i = tid; i < L1; i += nt) {
-    double acc = 0.0;
-    for (int rhs = 0; rhs < d; ++rhs) {
-      const double v = bz[(size_t)rhs * L1 + i];
-      acc = fma(v, v, acc);
-    }
-    best = argmax_better(best, ArgMax{sqrt(acc), i});
-  }
+  if (k < L1) best = ArgMax{sqrt(nrm2), (int64_t)k};
   best = block_argmax(best, red_v, red_i);
   if (tid == 0) {
     const double g2 = fabs(alpha) / sqrt((double)d) * best.v;
@@ -1344,13 +1352,11 @@ __global__ void __launch_bounds__(1024) g2_kernel(const double* __restrict__ R, 
 
 cudaError_t launch_g2(cudaStream_t st, const double* R, int64_t ldr, const int64_t* arr, int64_t l,
                       const double* omega, int d, double g, double* Z, SrqrScalars* sc) {
-  const size_t smem = sizeof(double) * ((size_t)d * (l + 1) + 2 * (size_t)(l + 1));
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(g2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
-  g2_kernel<<<1, 1024, smem, st>>>(R, ldr, arr, l, omega, d, g, Z, sc);
+  if (l + 1 > 1024) return cudaErrorInvalidValue;
+  const size_t smem = sizeof(int64_t) * (size_t)(l + 1);
+  const int threads = (int)((l + 1 + 31) / 32 * 32);
+  if (threads <= 512) g2_kernel<512><<<1, threads, smem, st>>>(R, ldr, arr, l, omega, d, g, Z, sc);
+  else g2_kernel<1024><<<1, threads, smem, st>>>(R, ldr, arr, l, omega, d, g, Z, sc);
   FFB_LAUNCH_CHECK();
 }
 

@@ -57,14 +57,20 @@ FFB_DEV void grid_sync(uint32_t* bar, uint32_t nblocks) {
 }
 
 // Stage rows [c0, c0+rows) of src (ld lds) into Cs (kCH x kL), zero padding for
-// rows >= rows (to a multiple of 4) and columns >= w, so DMMA tiles see zeros.
+// rows >= rows and columns >= w, so DMMA tiles see zeros.  All 16 copies of a
+// thread are in flight at once (cp.async, zero-fill); waits before returning.
 FFB_DEV void load_chunk(double* Cs, const double* src, int64_t lds, int64_t c0, int rows, int w) {
-  // kCH == 64: thread -> (row = t & 63, col = t >> 6); consecutive threads read
-  // consecutive rows of one column (coalesced), no integer division
-  for (int t = threadIdx.x; t < kCH * kW; t += blockDim.x) {
+  // thread -> (row = t & 63, col = t >> 6): consecutive threads read consecutive
+  // rows of one column (coalesced)
+#pragma unroll
+  for (int u = 0; u < (kCH * kW) / 256; ++u) {
+    const int t = threadIdx.x + 256 * u;
     const int rr = t & 63, cc = t >> 6;
-    Cs[rr * kL + cc] = (rr < rows && cc < w) ? src[(c0 + rr) + (int64_t)cc * lds] : 0.0;
+    const bool ok = rr < rows && cc < w;
+    cp_async8(Cs + rr * kL + cc, ok ? src + (c0 + rr) + (int64_t)cc * lds : src, ok);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
 }
 
 // Warp tile of a 64 x 64 product: warp -> rows 16*(warp/2)..+16, cols 32*(warp%2)..+32.
@@ -162,6 +168,7 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
   double* Cs = Ra + kW * kL;          // staged chunk of rows (kCH x w) / Ui
   double* Ws = Cs + kCH * kL;         // Linv / row stage
   double* buf = Ws + kW * kL;         // 256 doubles of broadcast scratch
+  double* Sx = buf + 256;             // 1024 doubles: blocked-inverse scratch
   __shared__ double Dd[kW];
   __shared__ double red[8];
   const int tid = threadIdx.x, nt = blockDim.x, G = gridDim.x, w = a.w;
@@ -171,7 +178,7 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
   const int ww = w * w;
   const int bi = bi_of(tid), bj = bj_of(tid);
   bool zero = false;
-  long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tp[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long tlast = clock64();
 #define QPROF(i)                                    \
   if (a.prof && tid == 0 && blockIdx.x == 0) {      \
@@ -311,12 +318,12 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
           for (int j = 0; j < 4; ++j)
             if (bi + i == bj + j && bi + i < w) g.v[i][j] += sh;
       }
-      const bool ok = chol_upper(g, w, Rs, buf);
+      QPROF(2)
+      const bool ok = chol_upper1(g, w, Rs, buf);
       if (!ok && blockIdx.x == 0 && tid == 0) atomicOr(a.status, 2u /* kStCholFail */);
-      Tile x;
-      inv_upper(Rs, w, x, buf);
-      store(x, Xs);
-      __syncthreads();
+      QPROF(8)
+      inv_upper_blk(Rs, w, Xs, Sx);
+      QPROF(9)
     }
     QPROF(2)
     // Racc <- R * Racc (pass 0: Racc = R; zero panel: Racc = 0), DMMA via Ws
@@ -329,11 +336,12 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
       __syncthreads();
       for (int t = tid; t < kW * kW; t += nt) Ra[(t >> 6) * kL + (t & 63)] = Ws[(t >> 6) * kL + (t & 63)];
     }
-    // (d) own rows <- rows * R^-1
+    // (d) own rows <- rows * R^-1 (a single-chunk CTA still holds its rows in Cs)
+    const bool one_chunk = r1 - r0 <= kCH;
     for (int64_t c0 = r0; c0 < r1; c0 += kCH) {
       const int rows = (int)(r1 - c0 < kCH ? r1 - c0 : kCH);
       __syncthreads();
-      load_chunk(Cs, src, lds, c0, rows, w);
+      if (!one_chunk) load_chunk(Cs, src, lds, c0, rows, w);
       __syncthreads();
       apply_upper(Cs, rows, w, Xs, dst, Mp, c0);
     }
@@ -354,16 +362,16 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         q.v[i][j] = (bi + i < w && bj + j < w) ? a.Qa[(bi + i) + (int64_t)(bj + j) * Mp] : 0.0;
+    QPROF(5)
     sign_lu(q, w, Ls, Us, Dd, buf);
-    Tile x;
-    inv_upper(Us, w, x, buf);        // zero pivots -> zero row and column
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) x.v[i][j] *= (bi + i < w) ? Dd[bi + i] : 0.0;
-    store(x, Ui);                    // Ui = D * U^-1
-    inv_unit_lower(Ls, w, x, buf);
-    store(x, Li);
+    QPROF(10)
+    inv_upper_blk(Us, w, Ui, Sx);    // zero pivots -> zero rows
+    inv_unit_lower_blk(Ls, w, Li, Sx);
+    QPROF(11)
+    for (int t = tid; t < kW * kW; t += nt) {   // Ui = D * U^-1
+      const int r = t >> 6, c = t & 63;
+      Ui[r * kL + c] *= (r < w) ? Dd[r] : 0.0;
+    }
     __syncthreads();
   } else {
     for (int t = tid; t < kW * kW; t += nt) {
@@ -411,10 +419,10 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
   QPROF(6)
 #undef QPROF
   if (a.prof && tid == 0 && blockIdx.x == 0)
-    for (int i = 0; i < 7; ++i) a.prof[i] = tp[i];
+    for (int i = 0; i < 12; ++i) a.prof[i] = tp[i];
 }
 
-size_t panel_smem_bytes() { return sizeof(double) * (size_t)(4 * kW * kL + kCH * kL + 256); }
+size_t panel_smem_bytes() { return sizeof(double) * (size_t)(4 * kW * kL + kCH * kL + 256 + 1024); }
 
 int panel_grid(int sms, int64_t Mp) {
   int64_t g = (Mp + 63) / 64;
@@ -437,7 +445,7 @@ cudaError_t launch_panel_qr(cudaStream_t st, int sms, const double* X, int64_t l
   PanelArgs a{X, ldx, Mp, w, Y, ldy, T, ldt, R, ldr, Qa, Qb, part, Gg, bar, status,
               (int)((Mp + G - 1) / G), nullptr};
   static long long* prof = nullptr;
-  if (getenv("FFB_PANEL_PROF") && !prof) cudaMallocManaged(&prof, 8 * sizeof(long long));
+  if (getenv("FFB_PANEL_PROF") && !prof) cudaMallocManaged(&prof, 12 * sizeof(long long));
   a.prof = prof;
   cudaError_t e = cudaMemsetAsync(bar, 0, 2 * sizeof(uint32_t), st);
   if (e != cudaSuccess) return e;
@@ -447,8 +455,9 @@ cudaError_t launch_panel_qr(cudaStream_t st, int sms, const double* X, int64_t l
     cudaStreamSynchronize(st);
     fprintf(stderr,
             "[panel prof] Mp=%lld w=%d G=%d cycles: gram %lld reduce %lld factor %lld apply %lld "
-            "gsync %lld recon %lld TY %lld\n",
-            (long long)Mp, w, G, prof[0], prof[1], prof[2], prof[3], prof[4], prof[5], prof[6]);
+            "gsync %lld recon %lld TY %lld | chol %lld inv %lld signlu %lld inv2 %lld\n",
+            (long long)Mp, w, G, prof[0], prof[1], prof[2], prof[3], prof[4], prof[5], prof[6],
+            prof[8], prof[9], prof[10], prof[11]);
   }
   return e;
 }

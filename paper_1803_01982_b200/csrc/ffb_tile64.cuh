@@ -218,7 +218,7 @@ FFB_DEV void sign_lu(Tile& q, int w, double* Ls, double* Us, double* Dd, double*
     if (fabs(z) == 1.0) d = z > 0.0 ? 1.0 : -1.0;   // identity reflector (tail == 0)
     else d = z > 0.0 ? -1.0 : 1.0;                  // pivot -(1+|z|) = -tau
     const double ucc = d * z - 1.0;
-    const double sc = ucc != 0.0 ? d / ucc : 0.0;
+    const double sc = ucc != 0.0 ? d * fast_rcp(ucc) : 0.0;
     if (tid < 64) {
       const int r = tid;
       if (r < c) Us[r * kTL + c] = d * col[r];
@@ -241,6 +241,227 @@ FFB_DEV void sign_lu(Tile& q, int w, double* Ls, double* Us, double* Dd, double*
       for (int j = 0; j < 4; ++j) q.v[i][j] = fma(-li[i], rj[j], q.v[i][j]);
   }
   __syncthreads();
+}
+
+
+// ---------------------------------------------------------------------------
+// Blocked versions (256 threads).  The sequential part of a 64x64 triangular
+// inverse is confined to the four 16x16 diagonal blocks, which are inverted
+// simultaneously (16 steps, one barrier each: thread t works on block t/64,
+// column t%16, rows (t%64)/16 + 4q); the off-diagonal blocks then follow from
+// two levels of block products X12 = -X11 A12 X22 (16 -> 32 -> 64).  Entries at
+// index >= w are treated as identity.  S: >= 1024 doubles of scratch.
+
+// X = U^{-1} (U upper triangular in Us, kTL), written to Xs (kTL, full 64x64).
+// Zero pivots give zero rows (as inv_upper).
+FFB_DEV void inv_upper_blk(const double* Us, int w, double* Xs, double* S) {
+  const int tid = threadIdx.x, b = tid >> 6, lt = tid & 63, j = lt & 15, i0 = lt >> 4;
+  const int o = 16 * b;
+  auto uval = [&](int r, int c) -> double {
+    if (r >= w || c >= w) return r == c ? 1.0 : 0.0;
+    return Us[r * kTL + c];
+  };
+  double x[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) x[q] = (i0 + 4 * q == j) ? 1.0 : 0.0;
+  // zero the strictly lower blocks of X (never written below)
+  for (int t = tid; t < 64 * 64; t += blockDim.x) {
+    const int r = t >> 6, c = t & 63;
+    if ((r >> 4) > (c >> 4)) Xs[r * kTL + c] = 0.0;
+  }
+  for (int s = 15; s >= 0; --s) {
+    double* row = S + (s & 1) * 64;   // [4 blocks][16]
+    const double d = uval(o + s, o + s);
+    const double inv = d != 0.0 ? 1.0 / d : 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (i0 + 4 * q == s) {
+        x[q] *= inv;
+        row[16 * b + j] = x[q];
+      }
+    __syncthreads();
+    const double rs = row[16 * b + j];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + 4 * q;
+      if (i < s) x[q] = fma(-uval(o + i, o + s), rs, x[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) Xs[(o + i0 + 4 * q) * kTL + o + j] = x[q];
+  __syncthreads();
+  // level 1: blocks (0,1) and (2,3): T = U12 X22 (S), X12 = -X11 T; thread -> (k, r, c, c+8)
+  // (entries of Us beyond w are zero off the diagonal: callers zero-fill)
+  {
+    const int k = tid >> 7, e = tid & 127, r = e >> 3, c = e & 7, oo = 32 * k;
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const double u = Us[(oo + r) * kTL + oo + 16 + q];
+      a0 = fma(u, Xs[(oo + 16 + q) * kTL + oo + 16 + c], a0);
+      a1 = fma(u, Xs[(oo + 16 + q) * kTL + oo + 24 + c], a1);
+    }
+    S[128 + k * 256 + r * 16 + c] = a0;
+    S[128 + k * 256 + r * 16 + c + 8] = a1;
+    __syncthreads();
+    a0 = a1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const double x = q >= r ? Xs[(oo + r) * kTL + oo + q] : 0.0;
+      a0 = fma(x, S[128 + k * 256 + q * 16 + c], a0);
+      a1 = fma(x, S[128 + k * 256 + q * 16 + c + 8], a1);
+    }
+    Xs[(oo + r) * kTL + oo + 16 + c] = -a0;
+    Xs[(oo + r) * kTL + oo + 24 + c] = -a1;
+    __syncthreads();
+  }
+  // level 2: T = U12 X22 (32x32, S), X12 = -X11 T; thread -> (r, c + 8 m), m < 4
+  {
+    const int r = tid >> 3, c = tid & 7;
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+    for (int q = 0; q < 32; ++q) {
+      const double u = Us[r * kTL + 32 + q];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) a[m] = fma(u, Xs[(32 + q) * kTL + 32 + c + 8 * m], a[m]);
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) S[r * 32 + c + 8 * m] = a[m];
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 4; ++m) a[m] = 0.0;
+#pragma unroll 8
+    for (int q = 0; q < 32; ++q) {
+      const double x = q >= r ? Xs[r * kTL + q] : 0.0;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) a[m] = fma(x, S[q * 32 + c + 8 * m], a[m]);
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) Xs[r * kTL + 32 + c + 8 * m] = -a[m];
+    __syncthreads();
+  }
+}
+
+// X = L^{-1} (L unit lower triangular in Ls, kTL) -> Xs (kTL, full 64x64).
+FFB_DEV void inv_unit_lower_blk(const double* Ls, int w, double* Xs, double* S) {
+  const int tid = threadIdx.x, b = tid >> 6, lt = tid & 63, j = lt & 15, i0 = lt >> 4;
+  const int o = 16 * b;
+  auto lval = [&](int r, int c) -> double {
+    if (r == c) return 1.0;
+    if (r >= w || c >= w) return 0.0;
+    return Ls[r * kTL + c];
+  };
+  double x[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) x[q] = (i0 + 4 * q == j) ? 1.0 : 0.0;
+  for (int t = tid; t < 64 * 64; t += blockDim.x) {
+    const int r = t >> 6, c = t & 63;
+    if ((r >> 4) < (c >> 4)) Xs[r * kTL + c] = 0.0;
+  }
+  for (int s = 0; s < 16; ++s) {
+    double* row = S + (s & 1) * 64;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (i0 + 4 * q == s) row[16 * b + j] = x[q];
+    __syncthreads();
+    const double rs = row[16 * b + j];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + 4 * q;
+      if (i > s) x[q] = fma(-lval(o + i, o + s), rs, x[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) Xs[(o + i0 + 4 * q) * kTL + o + j] = x[q];
+  __syncthreads();
+  // level 1: X21 = -X22 (L21 X11); thread -> (k, r, c, c+8)  (Ls off-diagonal
+  // entries beyond w are zero: callers zero-fill)
+  {
+    const int k = tid >> 7, e = tid & 127, r = e >> 3, c = e & 7, oo = 32 * k;
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const double lv = Ls[(oo + 16 + r) * kTL + oo + q];
+      a0 = fma(lv, Xs[(oo + q) * kTL + oo + c], a0);
+      a1 = fma(lv, Xs[(oo + q) * kTL + oo + c + 8], a1);
+    }
+    S[128 + k * 256 + r * 16 + c] = a0;
+    S[128 + k * 256 + r * 16 + c + 8] = a1;
+    __syncthreads();
+    a0 = a1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const double x = q <= r ? Xs[(oo + 16 + r) * kTL + oo + 16 + q] : 0.0;
+      a0 = fma(x, S[128 + k * 256 + q * 16 + c], a0);
+      a1 = fma(x, S[128 + k * 256 + q * 16 + c + 8], a1);
+    }
+    Xs[(oo + 16 + r) * kTL + oo + c] = -a0;
+    Xs[(oo + 16 + r) * kTL + oo + c + 8] = -a1;
+    __syncthreads();
+  }
+  // level 2: X21 = -X22 (L21 X11) with 32x32 blocks
+  {
+    const int r = tid >> 3, c = tid & 7;
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+    for (int q = 0; q < 32; ++q) {
+      const double lv = Ls[(32 + r) * kTL + q];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) a[m] = fma(lv, Xs[q * kTL + c + 8 * m], a[m]);
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) S[r * 32 + c + 8 * m] = a[m];
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 4; ++m) a[m] = 0.0;
+#pragma unroll 8
+    for (int q = 0; q < 32; ++q) {
+      const double x = q <= r ? Xs[(32 + r) * kTL + 32 + q] : 0.0;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) a[m] = fma(x, S[q * 32 + c + 8 * m], a[m]);
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) Xs[(32 + r) * kTL + c + 8 * m] = -a[m];
+    __syncthreads();
+  }
+}
+
+// Upper Cholesky with one barrier per step: the owners of row j of the updated
+// Gram publish it (double-buffered), every thread derives the R entries it
+// needs itself.  Same contract as chol_upper.
+FFB_DEV bool chol_upper1(Tile& g, int w, double* Rs, double* buf) {
+  const int tid = threadIdx.x, bi = bi_of(tid), bj = bj_of(tid);
+  bool ok = true;
+  for (int t = tid; t < 64 * 64; t += blockDim.x) Rs[(t >> 6) * kTL + (t & 63)] = 0.0;
+  for (int j = 0; j < w; ++j) {
+    double* row = buf + (j & 1) * 64;
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+      if (j == bi + ii) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) row[bj + c] = g.v[ii][c];
+      }
+    __syncthreads();
+    double d = row[j];
+    if (!(d > 0.0) || !isfinite(d)) {
+      ok = false;
+      d = d > 0.0 ? d : 1e-300;
+    }
+    const double inv = rsqrt(d), rjj = d * inv;
+    if (tid < w) Rs[j * kTL + tid] = tid > j ? row[tid] * inv : (tid == j ? rjj : 0.0);
+    double rr[4], rc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      rr[q] = (bi + q > j && bi + q < w) ? row[bi + q] * inv : 0.0;
+      rc[q] = (bj + q > j && bj + q < w) ? row[bj + q] * inv : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) g.v[i][c] = fma(-rr[i], rc[c], g.v[i][c]);
+  }
+  __syncthreads();
+  return ok;
 }
 
 }  // namespace tile64

@@ -51,7 +51,9 @@ struct GemmCfg {
   static constexpr int kTM = WM / 8, kTN = WN / 8;
   static constexpr int kAStage = A_KC ? BM * APad<BM, BK>::kc : BK * APad<BM, BK>::mc;
   static constexpr int kBStage = B_KC ? BN * APad<BN, BK>::kc : BK * APad<BN, BK>::mc;
-  static constexpr size_t kSmem = sizeof(double) * (size_t)STAGES * (kAStage + kBStage);
+  static constexpr size_t kStages = (size_t)STAGES * (kAStage + kBStage);
+  static constexpr size_t kCTile = (size_t)(BM + 1) * BN;   // epilogue staging
+  static constexpr size_t kSmem = sizeof(double) * (kStages > kCTile ? kStages : kCTile);
 };
 
 // Operand tile loader: each thread owns a fixed set of (row, k) slots of the
@@ -123,7 +125,8 @@ struct TileLoader {
   }
 };
 
-template <int BM, int BN, int BK, int WM, int WN, bool A_KC, bool B_KC, int STAGES, bool VEC2>
+template <int BM, int BN, int BK, int WM, int WN, bool A_KC, bool B_KC, int STAGES, bool VEC2,
+          bool SK>
 __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES>::kThreads)
     gemm_f64_kernel(GemmArgs g) {
   using Cfg = GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES>;
@@ -138,7 +141,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
   const int wm0 = (warp / Cfg::kWarpsN) * WM, wn0 = (warp % Cfg::kWarpsN) * WN;
   // segment loop: classic grid = one segment; stream-K = this CTA's iteration range
   int64_t it = 0, it_end = 1;
-  const bool sk = g.sk_per > 0;
+  constexpr bool sk = SK;
   if (sk) {
     it = (int64_t)blockIdx.x * g.sk_per;
     it_end = it + g.sk_per;
@@ -216,53 +219,80 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
     }
     const double* as = As + (kt % STAGES) * Cfg::kAStage;
     const double* bs = Bs + (kt % STAGES) * Cfg::kBStage;
-#pragma unroll
-    for (int k4 = 0; k4 < BK; k4 += 4) {
-      double af[Cfg::kTM], bf[Cfg::kTN];
+    // fragments double-buffered across the k4 steps: the loads for step k4 + 4
+    // are issued before the DMMAs of step k4, so no DMMA waits on a fresh LDS and
+    // no LDS overwrites a register an in-flight DMMA still reads
+    double af[2][Cfg::kTM], bf[2][Cfg::kTN];
+    auto load_frag = [&](int k4, double (&a_)[Cfg::kTM], double (&b_)[Cfg::kTN]) {
 #pragma unroll
       for (int a = 0; a < Cfg::kTM; ++a) {
         const int r = wm0 + a * 8 + fr, kk = k4 + fk;
-        af[a] = A_KC ? as[r * ALD + kk] : as[kk * ALD + r];
+        a_[a] = A_KC ? as[r * ALD + kk] : as[kk * ALD + r];
       }
 #pragma unroll
       for (int b = 0; b < Cfg::kTN; ++b) {
         const int c = wn0 + b * 8 + fr, kk = k4 + fk;
-        bf[b] = B_KC ? bs[c * BLD + kk] : bs[kk * BLD + c];
+        b_[b] = B_KC ? bs[c * BLD + kk] : bs[kk * BLD + c];
       }
+    };
+    load_frag(0, af[0], bf[0]);
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      const int cur = (k4 >> 2) & 1;
+      if (k4 + 4 < BK) load_frag(k4 + 4, af[cur ^ 1], bf[cur ^ 1]);
 #pragma unroll
       for (int a = 0; a < Cfg::kTM; ++a)
 #pragma unroll
-        for (int b = 0; b < Cfg::kTN; ++b) dmma_884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        for (int b = 0; b < Cfg::kTN; ++b)
+          dmma_884(acc[a][b][0], acc[a][b][1], af[cur][a], bf[cur][b]);
     }
   }
   cp_async_wait<0>();
 
-  // Epilogue.
+  // Epilogue: stage the accumulator tile in shared memory (column-major, ld
+  // BM + 1), then one compact coalesced loop writes it out (C, a split-K slab
+  // or a stream-K segment).  Keeps the kernel's code small (instruction cache)
+  // and the global stores contiguous along M.
+  constexpr int CLD = BM + 1;
+  __syncthreads();
+  double* Ct = smem;
 #pragma unroll
-  for (int a = 0; a < Cfg::kTM; ++a) {
-    const int64_t gi = i0 + wm0 + a * 8 + fr;
-    if (gi >= g.M) continue;
+  for (int a = 0; a < Cfg::kTM; ++a)
 #pragma unroll
-    for (int b = 0; b < Cfg::kTN; ++b) {
+    for (int b = 0; b < Cfg::kTN; ++b)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t gj = j0 + wn0 + b * 8 + 2 * fk + h;
-        if (gj >= g.N) continue;
-        if (sk) {
-          if (!sk_whole) g.partial[(size_t)split * (BM * BN) + (gi - i0) + (gj - j0) * BM] = acc[a][b][h];
-          else {
-            double* cp = g.C + gi + gj * g.ldc;
-            const double v = g.alpha * acc[a][b][h];
-            *cp = g.beta == 0.0 ? v : v + g.beta * (*cp);
-          }
-        } else if (g.splits == 1 && !g.force_partial) {
-          double* cp = g.C + gi + gj * g.ldc;
-          const double v = g.alpha * acc[a][b][h];
-          *cp = g.beta == 0.0 ? v : v + g.beta * (*cp);
-        } else {
-          g.partial[(size_t)split * g.M * g.N + gi + gj * g.M] = acc[a][b][h];
-        }
-      }
+      for (int h = 0; h < 2; ++h)
+        Ct[(wm0 + a * 8 + fr) + (wn0 + b * 8 + 2 * fk + h) * CLD] = acc[a][b][h];
+  __syncthreads();
+  {
+    // destination: 0 = C (alpha, beta), 1 = partial slab (raw)
+    int mode;
+    double* dst;
+    int64_t ldd;
+    if (sk) {
+      mode = sk_whole ? 0 : 1;
+      dst = sk_whole ? g.C + i0 + j0 * g.ldc : g.partial + (size_t)split * (BM * BN);
+      ldd = sk_whole ? g.ldc : BM;
+    } else if (g.splits == 1 && !g.force_partial) {
+      mode = 0;
+      dst = g.C + i0 + j0 * g.ldc;
+      ldd = g.ldc;
+    } else {
+      mode = 1;
+      dst = g.partial + (size_t)split * g.M * g.N + i0 + j0 * g.M;
+      ldd = g.M;
+    }
+    const int rmax = g.M - i0 < BM ? (int)(g.M - i0) : BM;
+    const int cmax = g.N - j0 < BN ? (int)(g.N - j0) : BN;
+    const double alpha = g.alpha, beta = g.beta;
+#pragma unroll 1
+    for (int e = tid; e < BM * BN; e += NT) {
+      const int r = e % BM, c = e / BM;
+      if (r >= rmax || c >= cmax) continue;
+      const double v = Ct[r + c * CLD];
+      double* cp = dst + r + (int64_t)c * ldd;
+      if (mode == 1) *cp = v;
+      else *cp = beta == 0.0 ? alpha * v : alpha * v + beta * (*cp);
     }
   }
   if (sk && !sk_whole) {
