@@ -51,7 +51,8 @@ int occupancy_of(int cfg) {
     case 3: return occupancy<128, 64, 16, 32, 32, 3>();
     case 4: return occupancy<128, 96, 16, 32, 48, 3>();
     case 5: return occupancy<16, 64, 16, 16, 16, 4>();
-    default: return occupancy<32, 64, 16, 16, 32, 4>();
+    case 6: return occupancy<32, 64, 16, 16, 32, 4>();
+    default: return occupancy<32, 32, 16, 16, 16, 4>();
   }
 }
 
@@ -79,8 +80,12 @@ int pick_cfg(int64_t M, int64_t N, int64_t K) {
     const char* e = getenv("FFB_GEMM_CFG");
     forced = e ? atoi(e) : -1;
   }
-  if (forced >= 0) return forced > 6 ? 6 : forced;
+  if (forced >= 0) return forced > 7 ? 7 : forced;
   if (M <= 16) return 5;
+  // small outputs with short K (no split-K to fill the GPU): 32 x 32 tiles so the
+  // work spreads over many SMs instead of a few large tiles
+  const int64_t tiles64 = ((M + 63) / 64) * ((N + 63) / 64);
+  if (tiles64 < 148 && K < 1024) return 7;
   if (M <= 32) return 6;
   if (M <= 48) return 0;
   if (M <= 64) return 1;
@@ -94,9 +99,8 @@ int pick_cfg(int64_t M, int64_t N, int64_t K) {
   return 1;
 }
 
-// 0..5 as below, 6 = 32 x 64 (shared by the default cases)
-const Shape kShapes[7] = {{48, 64, 16},  {64, 64, 16}, {96, 64, 16}, {128, 64, 16},
-                          {128, 96, 16}, {16, 64, 16}, {32, 64, 16}};
+const Shape kShapes[8] = {{48, 64, 16},  {64, 64, 16}, {96, 64, 16}, {128, 64, 16},
+                          {128, 96, 16}, {16, 64, 16}, {32, 64, 16}, {32, 32, 16}};
 
 template <bool AK, bool BKC>
 cudaError_t launch_layout(int cfg, cudaStream_t st, const GemmArgs& g, dim3 grid) {
@@ -107,7 +111,8 @@ cudaError_t launch_layout(int cfg, cudaStream_t st, const GemmArgs& g, dim3 grid
     case 3: return launch_cfg<128, 64, 16, 32, 32, AK, BKC, 3>(st, g, grid);
     case 4: return launch_cfg<128, 96, 16, 32, 48, AK, BKC, 3>(st, g, grid);
     case 5: return launch_cfg<16, 64, 16, 16, 16, AK, BKC, 4>(st, g, grid);
-    default: return launch_cfg<32, 64, 16, 16, 32, AK, BKC, 4>(st, g, grid);
+    case 6: return launch_cfg<32, 64, 16, 16, 32, AK, BKC, 4>(st, g, grid);
+    default: return launch_cfg<32, 32, 16, 16, 16, AK, BKC, 4>(st, g, grid);
   }
 }
 

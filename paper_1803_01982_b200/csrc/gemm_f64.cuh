@@ -285,14 +285,27 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
     const int rmax = g.M - i0 < BM ? (int)(g.M - i0) : BM;
     const int cmax = g.N - j0 < BN ? (int)(g.N - j0) : BN;
     const double alpha = g.alpha, beta = g.beta;
+    const bool rd = mode == 0 && beta != 0.0;
+    // C reads are issued 8 at a time before their uses (no serial L2 round trips)
+    constexpr int EPT = (BM * BN + NT - 1) / NT;
+    constexpr int G8 = 8;
 #pragma unroll 1
-    for (int e = tid; e < BM * BN; e += NT) {
-      const int r = e % BM, c = e / BM;
-      if (r >= rmax || c >= cmax) continue;
-      const double v = Ct[r + c * CLD];
-      double* cp = dst + r + (int64_t)c * ldd;
-      if (mode == 1) *cp = v;
-      else *cp = beta == 0.0 ? alpha * v : alpha * v + beta * (*cp);
+    for (int q0 = 0; q0 < EPT; q0 += G8) {
+      double cv[G8];
+#pragma unroll
+      for (int u = 0; u < G8; ++u) {
+        const int e = tid + (q0 + u) * NT;
+        const int r = e % BM, c = e / BM;
+        cv[u] = (rd && q0 + u < EPT && e < BM * BN && r < rmax && c < cmax) ? dst[r + (int64_t)c * ldd] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < G8; ++u) {
+        const int e = tid + (q0 + u) * NT;
+        const int r = e % BM, c = e / BM;
+        if (q0 + u >= EPT || e >= BM * BN || r >= rmax || c >= cmax) continue;
+        const double v = Ct[r + c * CLD];
+        dst[r + (int64_t)c * ldd] = mode == 1 ? v : (rd ? alpha * v + beta * cv[u] : alpha * v);
+      }
     }
   }
   if (sk && !sk_whole) {
