@@ -111,6 +111,104 @@ def make_workload(name, seed, device):
     return cfg, A
 
 
+def k13_traffic(workload):
+    """DRAM bytes per launch of the roofline kernel from the committed ncu capture
+    (profiles/*_k13_ncu.json, `ncu --set full`), or None."""
+    import glob
+
+    best, src = None, None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_k13_ncu.json"))):
+        try:
+            with open(path) as f:
+                d = json.load(f)
+        except (OSError, ValueError):
+            continue
+        if d.get("workload") == workload:
+            best, src = d, os.path.relpath(path, ROOT)
+    if best is None:
+        return None, None
+    return best["dram_bytes_read"] + best["dram_bytes_write"], src
+
+
+def run_batched(args):
+    """cfg4 / cfg5: independent problems partitioned contiguously over the ranks
+    (paper_1803_01982_b200.batch.partition); each rank factorizes its share, then
+    the singular values and certificates are gathered to rank 0 (the only
+    collective).  Strong scaling: the total number of problems is fixed."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1803_01982_b200 as ffb
+    from paper_1803_01982_b200 import batch, workloads
+
+    ws, rank, local = dist_init()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = workloads.CONFIGS[args.workload]
+    mine = list(batch.partition(cfg.batch, ws, rank))
+    if args.workload == "cfg4":
+        unf = workloads.torch_tensor_unfoldings(seed=0, device=dev)
+        probs = {i: unf[i] for i in mine}
+        seed_of = lambda i: 0
+    else:
+        probs = {i: workloads.torch_matrix("cfg5", seed=i, device=dev) for i in mine}
+        seed_of = lambda i: i
+    m, n = cfg.m, cfg.n
+
+    def step():
+        res = [ffb.flip_flop_srqr(probs[i], cfg.k, l=cfg.l, b=cfg.b, p=cfg.p, seed=seed_of(i))
+               for i in mine]
+        local_s = torch.stack([r.s for r in res]) if res else torch.zeros((0, cfg.k), dtype=torch.float64, device=dev)
+        return batch.gather_slots(local_s, cfg.batch, (cfg.k,), rank, ws, dev)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(args.steps):
+        gathered = step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if ws > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank == 0:
+        flop_alg = ffb.flip_flop_flop_formula(m, n, cfg.l, cfg.b, cfg.p) * cfg.batch
+        achieved = flop_alg / (ms * 1e-3) / 1e12
+        line = {
+            "metric": METRIC, "value": cfg.batch * 1000.0 / ms, "unit": "factorizations/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Haar factors / Tucker tensor, BASELINE spectra, device-generated)",
+            "config": {"workload": args.workload, "m": m, "n": n, "k": cfg.k, "p": cfg.p, "b": cfg.b,
+                       "l": cfg.l, "batch": cfg.batch,
+                       "parallelism": f"partitioned x{ws} (contiguous), NCCL gather of s to rank 0",
+                       "l2_flush": "per-problem A %d MB, batch >> L2" % (m * n * 8 // 2**20)},
+            "step_roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                              "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+                              "flop_alg": flop_alg},
+            "clocks": clk,
+            "gathered": list(gathered.shape) if gathered is not None else None,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def cpu_oracle_sample(A_host, cfg, budget_s=30.0):
     """Time the CPU oracle (reference algorithm port) on the same matrix."""
     import oracle
@@ -175,6 +273,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload in ("cfg4", "cfg5"):
+        return run_batched(args)
 
     import torch
     import torch.distributed as dist
@@ -282,6 +382,7 @@ def main():
 
     if rank == 0:
         achieved = flop_alg / (ms * 1e-3) / 1e12
+        traffic, traffic_src = k13_traffic(args.workload)
         line = {
             "metric": METRIC, "value": value, "unit": "factorizations/s", "n_gpus": ws,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
@@ -297,7 +398,9 @@ def main():
                               "peak_source": "measured DMMA peak, profiles/r01_fp64_peak.md"},
             "roofline": {"bound": "tensor", "kernel": "K13 A*Qhat DMMA GEMM (m x l x n)",
                          "achieved": g_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": g_tflops / FP64_PEAK_TFLOPS, "traffic": None,
+                         "frac": g_tflops / FP64_PEAK_TFLOPS, "traffic": traffic,
+                         "traffic_source": traffic_src,
+                         "algorithmic_bytes": 8 * (m * n + n * l + m * l),
                          "ms_per_launch": gms,
                          "peak_source": "measured DMMA peak (MEASURED_PEAKS.json has no FP64)"},
             "gpu_launches": kernels * args.steps,
