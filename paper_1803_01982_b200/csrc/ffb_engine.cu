@@ -38,6 +38,27 @@ struct ffb_ctx {
 
 namespace {
 
+// Host staging is per calling thread, so independent problems can be driven from
+// several host threads / CUDA streams on one context (batch.run_streams).
+struct HostStage {
+  double* pinned = nullptr;        // g2 Gaussians
+  size_t cap = 0;
+  SrqrScalars* sc = nullptr;       // certificate scalars read back after the pipeline
+  ~HostStage() {
+    if (pinned) cudaFreeHost(pinned);
+    if (sc) cudaFreeHost(sc);
+  }
+};
+thread_local HostStage t_host;
+
+// small stream-ordered read-back (never the legacy default stream, so problems
+// driven on other streams are not serialised)
+inline cudaError_t d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  return e;
+}
+
 constexpr int kPanelW = 64;
 constexpr size_t kAlign = 256;
 
@@ -400,15 +421,15 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
   // reference's RNG and staged now so the pipeline never waits for the host.
   auto stage_gauss = [&](int64_t swaps) -> int {
     const size_t cnt = (size_t)D.d * L1;
-    if (ctx->pinned_cap < cnt) {
-      if (ctx->pinned) cudaFreeHost(ctx->pinned);
-      cudaMallocHost(&ctx->pinned, cnt * sizeof(double));
-      ctx->pinned_cap = cnt;
+    if (t_host.cap < cnt) {
+      if (t_host.pinned) cudaFreeHost(t_host.pinned);
+      cudaMallocHost(&t_host.pinned, cnt * sizeof(double));
+      t_host.cap = cnt;
     }
     cudaStreamSynchronize(st);  // previous staging copy may still read the buffer
-    if (!gauss || gauss(gauss_user, D.seed, 1000 + (uint64_t)swaps, D.d, L1, ctx->pinned) != 0)
+    if (!gauss || gauss(gauss_user, D.seed, 1000 + (uint64_t)swaps, D.d, L1, t_host.pinned) != 0)
       return fail(ctx, FFB_ERR_ARGUMENT, "gauss callback failed");
-    e.ok(cudaMemcpyAsync(w.g2om, ctx->pinned, cnt * sizeof(double), cudaMemcpyHostToDevice, st));
+    e.ok(cudaMemcpyAsync(w.g2om, t_host.pinned, cnt * sizeof(double), cudaMemcpyHostToDevice, st));
     return FFB_OK;
   };
   if (mode != FFB_MODE_TRQRCP) {
@@ -484,7 +505,7 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
     if (e.cerr != cudaSuccess) return cuda_fail(ctx, e.cerr, "trqrcp launch");
     if (se != cudaSuccess) return cuda_fail(ctx, se, "trqrcp");
     uint32_t stw = 0;
-    cudaMemcpy(&stw, w.status, sizeof(stw), cudaMemcpyDeviceToHost);
+    d2h(&stw, w.status, sizeof(stw), st);
     out->status_bits = stw;
     out->flops = e.gc.flops;
     out->kernels = e.gc.launches + e.launches;
@@ -549,15 +570,16 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
   if (mode == FFB_MODE_FLIPFLOP) flipflop();
 
   auto read_sc = [&]() -> cudaError_t {
-    e.ok(cudaMemcpyAsync(ctx->sc_host, w.sc, sizeof(SrqrScalars), cudaMemcpyDeviceToHost, st));
+    if (!t_host.sc) cudaMallocHost(&t_host.sc, sizeof(SrqrScalars));
+    e.ok(cudaMemcpyAsync(t_host.sc, w.sc, sizeof(SrqrScalars), cudaMemcpyDeviceToHost, st));
     return cudaStreamSynchronize(st);
   };
   cudaError_t se = read_sc();
   if (e.cerr != cudaSuccess) return cuda_fail(ctx, e.cerr, "launch");
   if (se != cudaSuccess) return cuda_fail(ctx, se, "srqr");
-  SrqrScalars sc = *ctx->sc_host;
+  SrqrScalars sc = *t_host.sc;
   uint32_t stw = 0;
-  cudaMemcpy(&stw, w.status, sizeof(stw), cudaMemcpyDeviceToHost);
+  d2h(&stw, w.status, sizeof(stw), st);
   stw |= sc.status;
   out->status_bits = stw;
   if (stw & kStNonFinite) return fail(ctx, FFB_ERR_NUMERICAL, "non-finite values in input or factors");
@@ -571,7 +593,7 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
       if (swaps >= 50 * l) {
         pack_and_outputs();
         se = read_sc();
-        sc = *ctx->sc_host;
+        sc = *t_host.sc;
         out->alpha = sc.alpha; out->g1 = sc.g1; out->g2 = sc.g2; out->r22 = sc.r22;
         out->tau_bound = sc.tau; out->tau_hat_bound = sc.tau_hat; out->swaps = swaps;
         return fail(ctx, FFB_ERR_CERTIFICATION, "swap cap reached");
@@ -584,14 +606,14 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
       extend();
       se = read_sc();
       if (e.cerr != cudaSuccess || se != cudaSuccess) return cuda_fail(ctx, e.cerr ? e.cerr : se, "swap");
-      sc = *ctx->sc_host;
+      sc = *t_host.sc;
       if (!(sc.alpha > 0.0)) break;
       int rc = stage_gauss(swaps);
       if (rc) return rc;
       e.ok(launch_g2(st, w.R, L1, w.arr, l, w.g2om, (int)D.d, D.g, w.g2z, w.sc));
       se = read_sc();
       if (e.cerr != cudaSuccess || se != cudaSuccess) return cuda_fail(ctx, e.cerr ? e.cerr : se, "swap g2");
-      sc = *ctx->sc_host;
+      sc = *t_host.sc;
       if (sc.status & kStSingular) return fail(ctx, FFB_ERR_SINGULAR_TRAILING, "zero diagonal in leading triangular block");
       if (!sc.need_swap) break;
     }
@@ -600,11 +622,11 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
     se = read_sc();
     if (e.cerr != cudaSuccess) return cuda_fail(ctx, e.cerr, "launch");
     if (se != cudaSuccess) return cuda_fail(ctx, se, "flipflop");
-    sc = *ctx->sc_host;
+    sc = *t_host.sc;
   }
   if (mode == FFB_MODE_FLIPFLOP) {
     int sweeps = 0;
-    cudaMemcpy(&sweeps, w.jsweeps, sizeof(int), cudaMemcpyDeviceToHost);
+    d2h(&sweeps, w.jsweeps, sizeof(int), st);
     out->svd_sweeps = sweeps;
     if (sweeps >= kMaxSweeps) return fail(ctx, FFB_ERR_NUMERICAL, "small SVD did not converge");
   }

@@ -91,7 +91,8 @@ def _workspace(torch, device, nbytes):
 
 _omega_cache = {}
 _omega_lock = threading.Lock()
-_OMEGA_CACHE_MAX = 8
+_OMEGA_CACHE_MAX = 256              # entries
+_OMEGA_CACHE_BYTES = 1 << 30        # and bytes of device memory
 
 
 def _omega(torch, dev, s, m, seed):
@@ -106,10 +107,23 @@ def _omega(torch, dev, s, m, seed):
             return om
     om = torch.from_numpy(rng.gaussian(s, m, seed, rng.STREAM_SKETCH)).to(dev)
     with _omega_lock:
-        if len(_omega_cache) >= _OMEGA_CACHE_MAX:
+        while _omega_cache and (len(_omega_cache) >= _OMEGA_CACHE_MAX or
+                                sum(v.numel() * 8 for v in _omega_cache.values()) + om.numel() * 8
+                                > _OMEGA_CACHE_BYTES):
             _omega_cache.pop(next(iter(_omega_cache)))
         _omega_cache[key] = om
     return om
+
+
+def prefetch_omega(keys, device=None, threads=8):
+    """Generate and cache Omega for many (s, m, seed) on host threads in parallel
+    (numpy's Philox releases the GIL), e.g. before a batch of independent problems."""
+    import torch
+    from concurrent.futures import ThreadPoolExecutor
+
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    with ThreadPoolExecutor(max_workers=max(1, threads)) as ex:
+        list(ex.map(lambda k: _omega(torch, dev, k[0], k[1], k[2]), keys))
 
 
 @_capi.GAUSS_CB
