@@ -15,6 +15,7 @@
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "ffb_common.cuh"
 #include "ffb_panel.cuh"
@@ -187,10 +188,17 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
     tlast = tn;                                     \
   }
 
+  // pass 2 only runs when pass 1 was still far from orthogonal: after a first-order
+  // pass with max|Q^T Q - I| = e the error is O(e^2), so e <= 1e-7 already leaves
+  // ~1e-14 (the decision uses the reduced Gram, identical in every CTA)
+  double em_prev = 1.0;
+  const double* qfin = a.Qa;
   for (int pass = 0; pass < 3; ++pass) {
+    if (pass == 2 && em_prev <= 1e-7) break;
     const double* src = pass == 0 ? a.X : (pass == 1 ? a.Qa : a.Qb);
     const int64_t lds = pass == 0 ? a.ldx : Mp;
     double* dst = pass == 1 ? a.Qb : a.Qa;
+    qfin = dst;
     // (a) local Gram of rows [r0, r1) on DMMA (Cs^T Cs per staged chunk)
     Acc64 gacc;
     acc_zero(gacc);
@@ -267,6 +275,8 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
       for (int q = 0; q < (nt >> 5); ++q) em = fmax(em, red[q]);
       __syncthreads();
       first_order = em <= 1e-5;
+      em_prev = em;
+      if (a.prof && tid == 0 && blockIdx.x == 0) a.prof[12 + pass] = __double_as_longlong(em);
     }
     if (zp) {
       for (int t = tid; t < kW * kW; t += nt) {
@@ -361,7 +371,7 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        q.v[i][j] = (bi + i < w && bj + j < w) ? a.Qa[(bi + i) + (int64_t)(bj + j) * Mp] : 0.0;
+        q.v[i][j] = (bi + i < w && bj + j < w) ? qfin[(bi + i) + (int64_t)(bj + j) * Mp] : 0.0;
     QPROF(5)
     sign_lu(q, w, Ls, Us, Dd, buf);
     QPROF(10)
@@ -411,7 +421,7 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
     for (int64_t c0 = y0; c0 < r1; c0 += kCH) {
       const int rows = (int)(r1 - c0 < kCH ? r1 - c0 : kCH);
       __syncthreads();
-      load_chunk(Ys, a.Qa, Mp, c0, rows, w);
+      load_chunk(Ys, qfin, Mp, c0, rows, w);
       __syncthreads();
       apply_upper(Ys, rows, w, Ui, a.Y, a.ldy, c0);
     }
@@ -431,6 +441,12 @@ int panel_grid(int sms, int64_t Mp) {
   return (int)g;
 }
 
+static double bits_to_double(long long b) {
+  double d;
+  memcpy(&d, &b, sizeof(d));
+  return d;
+}
+
 cudaError_t launch_panel_qr(cudaStream_t st, int sms, const double* X, int64_t ldx, int64_t Mp,
                             int w, double* Y, int64_t ldy, double* T, int64_t ldt, double* R,
                             int64_t ldr, double* Qa, double* Qb, double* part, double* Gg,
@@ -445,7 +461,7 @@ cudaError_t launch_panel_qr(cudaStream_t st, int sms, const double* X, int64_t l
   PanelArgs a{X, ldx, Mp, w, Y, ldy, T, ldt, R, ldr, Qa, Qb, part, Gg, bar, status,
               (int)((Mp + G - 1) / G), nullptr};
   static long long* prof = nullptr;
-  if (getenv("FFB_PANEL_PROF") && !prof) cudaMallocManaged(&prof, 12 * sizeof(long long));
+  if (getenv("FFB_PANEL_PROF") && !prof) cudaMallocManaged(&prof, 16 * sizeof(long long));
   a.prof = prof;
   cudaError_t e = cudaMemsetAsync(bar, 0, 2 * sizeof(uint32_t), st);
   if (e != cudaSuccess) return e;
@@ -455,9 +471,9 @@ cudaError_t launch_panel_qr(cudaStream_t st, int sms, const double* X, int64_t l
     cudaStreamSynchronize(st);
     fprintf(stderr,
             "[panel prof] Mp=%lld w=%d G=%d cycles: gram %lld reduce %lld factor %lld apply %lld "
-            "gsync %lld recon %lld TY %lld | chol %lld inv %lld signlu %lld inv2 %lld\n",
+            "gsync %lld recon %lld TY %lld | chol %lld inv %lld signlu %lld inv2 %lld | em1 %.1e em2 %.1e\n",
             (long long)Mp, w, G, prof[0], prof[1], prof[2], prof[3], prof[4], prof[5], prof[6],
-            prof[8], prof[9], prof[10], prof[11]);
+            prof[8], prof[9], prof[10], prof[11], bits_to_double(prof[13]), bits_to_double(prof[14]));
   }
   return e;
 }
