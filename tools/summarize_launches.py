@@ -43,7 +43,10 @@ def main(path, skip=0):
         agg[f][1] += v
     print(f"launches={len(rows)} total={tot/1e6:.3f} ms (serialised, cold-cache)")
     for f, (c, v) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
-        print(f"{v/1e6:9.3f} ms {100*v/tot:5.1f}%  x{c:4d}  {f[:110]}")
+        try:
+            print(f"{v/1e6:9.3f} ms {100*v/tot:5.1f}%  x{c:4d}  {f[:110]}")
+        except BrokenPipeError:
+            sys.exit(0)
 
 
 if __name__ == "__main__":
