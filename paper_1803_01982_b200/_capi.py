@@ -23,7 +23,8 @@ FFB_MODE_SRQR = 1
 FFB_MODE_FLIPFLOP = 2
 
 EXPORTS = ("ffb_ctx_create", "ffb_ctx_destroy", "ffb_last_error", "ffb_version",
-           "ffb_workspace_query", "ffb_run", "ffb_flipflop", "ffb_gemm", "ffb_block_pivots")
+           "ffb_workspace_query", "ffb_run", "ffb_flipflop", "ffb_gemm", "ffb_block_pivots",
+           "ffb_run_batched")
 
 
 class Params(C.Structure):
@@ -56,6 +57,13 @@ class Result(C.Structure):
         ("svd_sweeps", C.c_int32),
         ("i_off_trace", C.c_int64 * 64),
     ]
+
+
+class BatchItem(C.Structure):
+    _fields_ = [("stream", C.c_void_p), ("mode", C.c_int), ("A", C.c_void_p),
+                ("m", C.c_int64), ("n", C.c_int64), ("lda", C.c_int64), ("prm", Params),
+                ("omega", C.c_void_p), ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
+                ("out", C.POINTER(Result)), ("status", C.c_int)]
 
 
 GAUSS_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_int64, C.c_int64,
@@ -96,6 +104,9 @@ def load(path=LIB_PATH):
                                      C.c_int64, C.POINTER(Params), C.c_void_p, GAUSS_CB,
                                      C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(Result)]
         lib.ffb_flipflop.restype = C.c_int
+        lib.ffb_run_batched.argtypes = [C.c_void_p, C.POINTER(BatchItem), C.c_int64, C.c_int,
+                                        GAUSS_CB, C.c_void_p]
+        lib.ffb_run_batched.restype = C.c_int
         lib.ffb_gemm.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
                                  C.c_double, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_int64,
                                  C.c_int, C.c_double, C.c_void_p, C.c_int64, C.c_void_p,

@@ -16,6 +16,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <atomic>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../../include/ffb200.h"
@@ -31,6 +34,7 @@ struct ffb_ctx {
   int sms = 148;
   int max_coop_blocks_smem = 0;
   std::string err;
+  std::mutex err_mu;               // problems of a batch may fail concurrently
   double* pinned = nullptr;        // host staging for g2 Gaussians
   size_t pinned_cap = 0;
   SrqrScalars* sc_host = nullptr;  // pinned
@@ -286,7 +290,10 @@ struct Eng {
 };
 
 int fail(ffb_ctx* ctx, int code, const std::string& msg) {
-  if (ctx) ctx->err = msg;
+  if (ctx) {
+    std::lock_guard<std::mutex> g(ctx->err_mu);
+    ctx->err = msg;
+  }
   return code;
 }
 
@@ -650,3 +657,27 @@ int ffb_flipflop(ffb_ctx* ctx, void* stream, const double* A, int64_t m, int64_t
 }
 
 }  // extern "C"
+
+extern "C" int ffb_run_batched(ffb_ctx* ctx, ffb_batch_item* items, int64_t count, int max_threads,
+                               ffb_gauss_cb gauss, void* gauss_user) {
+  if (!ctx || (count > 0 && !items)) return FFB_ERR_ARGUMENT;
+  if (count <= 0) return FFB_OK;
+  int nt = max_threads < 1 ? 1 : max_threads;
+  if (nt > count) nt = (int)count;
+  std::atomic<int64_t> next{0};
+  auto worker = [&]() {
+    cudaSetDevice(ctx->device);
+    for (int64_t i = next++; i < count; i = next++) {
+      ffb_batch_item& it = items[i];
+      it.status = ffb_run(ctx, it.stream, it.mode, it.A, it.m, it.n, it.lda, &it.prm, it.omega,
+                          gauss, gauss_user, it.workspace, it.workspace_bytes, it.out);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; ++t) pool.emplace_back(worker);
+  worker();
+  for (auto& t : pool) t.join();
+  for (int64_t i = 0; i < count; ++i)
+    if (items[i].status != FFB_OK) return items[i].status;
+  return FFB_OK;
+}

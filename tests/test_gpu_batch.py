@@ -64,3 +64,48 @@ def test_hosvd_exact_tucker(ffb):
     for mode, F in enumerate(factors):
         Xr = np.moveaxis(np.tensordot(F.cpu().numpy(), np.moveaxis(Xr, mode, 0), axes=1), 0, mode)
     assert np.linalg.norm(Xr - X) / np.linalg.norm(X) < 1e-12
+
+
+def test_c_abi_run_batched(ffb):
+    """ffb_run_batched (C ABI, one host thread per in-flight problem) matches
+    one-at-a-time ffb_run bitwise."""
+    import ctypes as C
+
+    from paper_1803_01982_b200 import _capi, engine
+
+    lib = _capi.load()
+    ctx = _capi.context(0)
+    n_prob, k, l, b, p = 4, 30, 40, 16, 8
+    As = [_mat(i) for i in range(n_prob)]
+    want = [ffb.flip_flop_srqr(As[i], k, l=l, b=b, p=p, seed=i) for i in range(n_prob)]
+    items = (_capi.BatchItem * n_prob)()
+    keep = []
+    streams = [torch.cuda.Stream() for _ in range(n_prob)]
+    for i, A in enumerate(As):
+        m, n = A.shape
+        Ad = A.t().contiguous().t()
+        prm = _capi.Params(k, l, b, p, min(l, 10), 0.5, 2.0, i)
+        nb = C.c_size_t()
+        assert lib.ffb_workspace_query(m, n, C.byref(prm), _capi.FFB_MODE_FLIPFLOP, C.byref(nb)) == 0
+        ws = torch.empty(nb.value, dtype=torch.uint8, device="cuda")
+        om = engine._omega(torch, torch.device("cuda", 0), b + p, m, i)
+        s = torch.empty(k, dtype=torch.float64, device="cuda")
+        u = torch.empty((k, m), dtype=torch.float64, device="cuda").t()
+        v = torch.empty((k, n), dtype=torch.float64, device="cuda").t()
+        perm = torch.empty(n, dtype=torch.int64, device="cuda")
+        res = _capi.Result()
+        res.s, res.u, res.ldu, res.v, res.ldv, res.perm = s.data_ptr(), u.data_ptr(), m, v.data_ptr(), n, perm.data_ptr()
+        it = items[i]
+        it.stream, it.mode, it.A, it.m, it.n, it.lda = streams[i].cuda_stream, _capi.FFB_MODE_FLIPFLOP, Ad.data_ptr(), m, n, m
+        it.prm, it.omega, it.workspace, it.workspace_bytes = prm, om.data_ptr(), ws.data_ptr(), ws.numel()
+        it.out = C.pointer(res)
+        keep.append((Ad, ws, om, s, u, v, perm, res))
+    torch.cuda.synchronize()
+    rc = lib.ffb_run_batched(ctx, items, n_prob, 3, engine._gauss_cb, None)
+    torch.cuda.synchronize()
+    assert rc == 0, _capi.last_error(ctx)
+    for i in range(n_prob):
+        assert items[i].status == 0
+        s = keep[i][3]
+        assert torch.equal(s, want[i].s)
+        assert torch.equal(keep[i][6], want[i].meta["srqr"].fact.perm if isinstance(want[i].meta["srqr"].fact.perm, torch.Tensor) else torch.as_tensor(want[i].meta["srqr"].fact.perm, device="cuda"))
