@@ -329,11 +329,9 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
             if (bi + i == bj + j && bi + i < w) g.v[i][j] += sh;
       }
       QPROF(2)
-      const bool ok = chol_upper1(g, w, Rs, buf);
+      const bool ok = chol_inv_blk(g, w, Rs, Xs, Sx);   // blocked: warp-level 16x16 diagonal chains
       if (!ok && blockIdx.x == 0 && tid == 0) atomicOr(a.status, 2u /* kStCholFail */);
       QPROF(8)
-      inv_upper_blk(Rs, w, Xs, Sx);
-      QPROF(9)
     }
     QPROF(2)
     // Racc <- R * Racc (pass 0: Racc = R; zero panel: Racc = 0), DMMA via Ws

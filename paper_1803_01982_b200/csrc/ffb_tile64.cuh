@@ -252,44 +252,10 @@ FFB_DEV void sign_lu(Tile& q, int w, double* Ls, double* Us, double* Dd, double*
 // two levels of block products X12 = -X11 A12 X22 (16 -> 32 -> 64).  Entries at
 // index >= w are treated as identity.  S: >= 1024 doubles of scratch.
 
-// X = U^{-1} (U upper triangular in Us, kTL), written to Xs (kTL, full 64x64).
-// Zero pivots give zero rows (as inv_upper).
-FFB_DEV void inv_upper_blk(const double* Us, int w, double* Xs, double* S) {
-  const int tid = threadIdx.x, b = tid >> 6, lt = tid & 63, j = lt & 15, i0 = lt >> 4;
-  const int o = 16 * b;
-  auto uval = [&](int r, int c) -> double {
-    if (r >= w || c >= w) return r == c ? 1.0 : 0.0;
-    return Us[r * kTL + c];
-  };
-  double x[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) x[q] = (i0 + 4 * q == j) ? 1.0 : 0.0;
-  // zero the strictly lower blocks of X (never written below)
-  for (int t = tid; t < 64 * 64; t += blockDim.x) {
-    const int r = t >> 6, c = t & 63;
-    if ((r >> 4) > (c >> 4)) Xs[r * kTL + c] = 0.0;
-  }
-  for (int s = 15; s >= 0; --s) {
-    double* row = S + (s & 1) * 64;   // [4 blocks][16]
-    const double d = uval(o + s, o + s);
-    const double inv = d != 0.0 ? 1.0 / d : 0.0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (i0 + 4 * q == s) {
-        x[q] *= inv;
-        row[16 * b + j] = x[q];
-      }
-    __syncthreads();
-    const double rs = row[16 * b + j];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int i = i0 + 4 * q;
-      if (i < s) x[q] = fma(-uval(o + i, o + s), rs, x[q]);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) Xs[(o + i0 + 4 * q) * kTL + o + j] = x[q];
-  __syncthreads();
+// Off-diagonal blocks of X = U^{-1} from inverted 16x16 diagonal blocks already in
+// Xs (strictly lower blocks zero): X12 = -X11 U12 X22, 16 -> 32 -> 64.
+FFB_DEV void inv_upper_levels(const double* Us, double* Xs, double* S) {
+  const int tid = threadIdx.x;
   // level 1: blocks (0,1) and (2,3): T = U12 X22 (S), X12 = -X11 T; thread -> (k, r, c, c+8)
   // (entries of Us beyond w are zero off the diagonal: callers zero-fill)
   {
@@ -342,38 +308,10 @@ FFB_DEV void inv_upper_blk(const double* Us, int w, double* Xs, double* S) {
   }
 }
 
-// X = L^{-1} (L unit lower triangular in Ls, kTL) -> Xs (kTL, full 64x64).
-FFB_DEV void inv_unit_lower_blk(const double* Ls, int w, double* Xs, double* S) {
-  const int tid = threadIdx.x, b = tid >> 6, lt = tid & 63, j = lt & 15, i0 = lt >> 4;
-  const int o = 16 * b;
-  auto lval = [&](int r, int c) -> double {
-    if (r == c) return 1.0;
-    if (r >= w || c >= w) return 0.0;
-    return Ls[r * kTL + c];
-  };
-  double x[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) x[q] = (i0 + 4 * q == j) ? 1.0 : 0.0;
-  for (int t = tid; t < 64 * 64; t += blockDim.x) {
-    const int r = t >> 6, c = t & 63;
-    if ((r >> 4) < (c >> 4)) Xs[r * kTL + c] = 0.0;
-  }
-  for (int s = 0; s < 16; ++s) {
-    double* row = S + (s & 1) * 64;
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (i0 + 4 * q == s) row[16 * b + j] = x[q];
-    __syncthreads();
-    const double rs = row[16 * b + j];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int i = i0 + 4 * q;
-      if (i > s) x[q] = fma(-lval(o + i, o + s), rs, x[q]);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) Xs[(o + i0 + 4 * q) * kTL + o + j] = x[q];
-  __syncthreads();
+// Off-diagonal blocks of X = L^{-1} from inverted 16x16 diagonal blocks already in
+// Xs (strictly upper blocks zero): X21 = -X22 L21 X11, 16 -> 32 -> 64.
+FFB_DEV void inv_unit_lower_levels(const double* Ls, double* Xs, double* S) {
+  const int tid = threadIdx.x;
   // level 1: X21 = -X22 (L21 X11); thread -> (k, r, c, c+8)  (Ls off-diagonal
   // entries beyond w are zero: callers zero-fill)
   {
@@ -426,6 +364,82 @@ FFB_DEV void inv_unit_lower_blk(const double* Ls, int w, double* Xs, double* S) 
   }
 }
 
+// X = U^{-1} (U upper triangular in Us, kTL), written to Xs (kTL, full 64x64).
+// Zero pivots give zero rows (as inv_upper).
+FFB_DEV void inv_upper_blk(const double* Us, int w, double* Xs, double* S) {
+  const int tid = threadIdx.x, b = tid >> 6, lt = tid & 63, j = lt & 15, i0 = lt >> 4;
+  const int o = 16 * b;
+  auto uval = [&](int r, int c) -> double {
+    if (r >= w || c >= w) return r == c ? 1.0 : 0.0;
+    return Us[r * kTL + c];
+  };
+  double x[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) x[q] = (i0 + 4 * q == j) ? 1.0 : 0.0;
+  // zero the strictly lower blocks of X (never written below)
+  for (int t = tid; t < 64 * 64; t += blockDim.x) {
+    const int r = t >> 6, c = t & 63;
+    if ((r >> 4) > (c >> 4)) Xs[r * kTL + c] = 0.0;
+  }
+  for (int s = 15; s >= 0; --s) {
+    double* row = S + (s & 1) * 64;   // [4 blocks][16]
+    const double d = uval(o + s, o + s);
+    const double inv = d != 0.0 ? 1.0 / d : 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (i0 + 4 * q == s) {
+        x[q] *= inv;
+        row[16 * b + j] = x[q];
+      }
+    __syncthreads();
+    const double rs = row[16 * b + j];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + 4 * q;
+      if (i < s) x[q] = fma(-uval(o + i, o + s), rs, x[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) Xs[(o + i0 + 4 * q) * kTL + o + j] = x[q];
+  __syncthreads();
+  inv_upper_levels(Us, Xs, S);
+}
+
+// X = L^{-1} (L unit lower triangular in Ls, kTL) -> Xs (kTL, full 64x64).
+FFB_DEV void inv_unit_lower_blk(const double* Ls, int w, double* Xs, double* S) {
+  const int tid = threadIdx.x, b = tid >> 6, lt = tid & 63, j = lt & 15, i0 = lt >> 4;
+  const int o = 16 * b;
+  auto lval = [&](int r, int c) -> double {
+    if (r == c) return 1.0;
+    if (r >= w || c >= w) return 0.0;
+    return Ls[r * kTL + c];
+  };
+  double x[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) x[q] = (i0 + 4 * q == j) ? 1.0 : 0.0;
+  for (int t = tid; t < 64 * 64; t += blockDim.x) {
+    const int r = t >> 6, c = t & 63;
+    if ((r >> 4) < (c >> 4)) Xs[r * kTL + c] = 0.0;
+  }
+  for (int s = 0; s < 16; ++s) {
+    double* row = S + (s & 1) * 64;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (i0 + 4 * q == s) row[16 * b + j] = x[q];
+    __syncthreads();
+    const double rs = row[16 * b + j];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + 4 * q;
+      if (i > s) x[q] = fma(-lval(o + i, o + s), rs, x[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) Xs[(o + i0 + 4 * q) * kTL + o + j] = x[q];
+  __syncthreads();
+  inv_unit_lower_levels(Ls, Xs, S);
+}
+
 // Upper Cholesky with one barrier per step: the owners of row j of the updated
 // Gram publish it (double-buffered), every thread derives the R entries it
 // needs itself.  Same contract as chol_upper.
@@ -464,5 +478,145 @@ FFB_DEV bool chol_upper1(Tile& g, int w, double* Rs, double* buf) {
   return ok;
 }
 
+// ---------------------------------------------------------------------------
+// Blocked right-looking factorizations (256 threads): the sequential chains run
+// on 16x16 diagonal blocks inside ONE warp (registers + shuffles, no CTA
+// barriers), the off-diagonal block rows and the trailing updates are parallel
+// across the CTA.  A 64-wide factorization costs 4 x 3 barriers instead of 64.
+
+// Warp: upper Cholesky of the 16x16 diagonal block at (o, o) of Rs (upper
+// triangle holds the updated Gram), in place (strict lower part zeroed), and
+// X = R_oo^{-1} into the same block of Xs.  Lane c (< 16) owns column c.
+// Columns >= nv are identity padding.  Returns false on a non-positive pivot
+// (clamped exactly like chol_upper1).
+static __device__ __noinline__ bool warp_chol_inv16(double* Rs, double* Xs, int o, int nv) {
+  const int c = threadIdx.x & 31;
+  const bool col_ok = c < nv;
+  double a[16], dinv[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const double v = Rs[(o + i) * kTL + o + (c & 15)];
+    a[i] = col_ok ? (i <= c ? v : 0.0) : (i == c ? 1.0 : 0.0);
+  }
+  bool ok = true;
+  // Right-looking, branch-free: the strict lower part of a[] (rows > c) picks up
+  // garbage from the unconditional updates but is never read for the upper
+  // factor and is masked on the way out.
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    double d = __shfl_sync(0xffffffffu, a[j], j);
+    if (!(d > 0.0) || !isfinite(d)) {
+      ok = false;
+      d = d > 0.0 ? d : 1e-300;
+    }
+    const double inv = rsqrt(d);
+    dinv[j] = inv;
+    a[j] = (c == j) ? d * inv : a[j] * inv;
+#pragma unroll
+    for (int i = j + 1; i < 16; ++i) a[i] = fma(-__shfl_sync(0xffffffffu, a[j], i), a[j], a[i]);
+  }
+  // X = R^{-1}, column c: x_s = (delta_sc - sum_{k>s} R_sk x_k) / R_ss, 1/R_ss = dinv[s]
+  // (x_k = 0 for k > c, so lower garbage in other lanes' a[] never contributes)
+  double x[16];
+#pragma unroll
+  for (int s = 15; s >= 0; --s) {
+    double acc0 = (c == s) ? 1.0 : 0.0, acc1 = 0.0;
+#pragma unroll
+    for (int k = s + 1; k < 16; ++k) {
+      const double rsk = __shfl_sync(0xffffffffu, a[s], k);
+      if ((k - s) & 1) acc0 = fma(-rsk, x[k], acc0);
+      else acc1 = fma(-rsk, x[k], acc1);
+    }
+    x[s] = (acc0 + acc1) * dinv[s];
+  }
+  if (c < 16) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      Rs[(o + i) * kTL + o + c] = i <= c ? a[i] : 0.0;
+      Xs[(o + i) * kTL + o + c] = x[i];
+    }
+  }
+  return ok;
+}
+
+// Upper Cholesky R^T R = G (tile in, upper triangle used) and X = R^{-1}:
+// R -> Rs (full 64x64, zeros outside the w x w upper triangle), X -> Xs (full
+// 64x64, identity beyond w, zero pivots give zero rows).  Same contract as
+// chol_upper1 followed by inv_upper_blk.  S: >= 1024 doubles of scratch.
+FFB_DEV bool chol_inv_blk(Tile& g, int w, double* Rs, double* Xs, double* S) {
+  __shared__ int s_ok;
+  const int tid = threadIdx.x, bi = bi_of(tid), bj = bj_of(tid), warp = tid >> 5;
+  const int nbk = (w + 15) >> 4;
+  for (int t = tid; t < 64 * 64; t += blockDim.x) {
+    const int r = t >> 6, c = t & 63;
+    Rs[r * kTL + c] = 0.0;
+    Xs[r * kTL + c] = (r == c && (r >> 4) >= nbk) ? 1.0 : 0.0;
+  }
+  if (tid == 0) s_ok = 1;
+  __syncthreads();
+  for (int K = 0; K < nbk; ++K) {
+    const int o = 16 * K, e = o + 16, ncol = w - e;
+    // publish block row K of the updated Gram (upper part)
+    if ((bi >> 4) == K && bj + 3 >= o) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (bj + j >= bi + i && bj + j < w) Rs[(bi + i) * kTL + bj + j] = g.v[i][j];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const bool ok = warp_chol_inv16(Rs, Xs, o, w - o < 16 ? w - o : 16);
+      if (!ok && (tid & 31) == 0) s_ok = 0;
+    }
+    __syncthreads();
+    if (ncol <= 0) break;
+    // R_KJ = R_KK^{-T} G_KJ = X_KK^T G_KJ  -> S (16 x 64)
+    for (int t = tid; t < 16 * ncol; t += blockDim.x) {
+      const int i = t & 15, cc = e + (t >> 4);
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < 16; k += 2) {
+        if (k <= i) a0 = fma(Xs[(o + k) * kTL + o + i], Rs[(o + k) * kTL + cc], a0);
+        if (k + 1 <= i) a1 = fma(Xs[(o + k + 1) * kTL + o + i], Rs[(o + k + 1) * kTL + cc], a1);
+      }
+      S[i * 64 + cc] = a0 + a1;
+    }
+    __syncthreads();
+    for (int t = tid; t < 16 * ncol; t += blockDim.x) {
+      const int i = t & 15, cc = e + (t >> 4);
+      Rs[(o + i) * kTL + cc] = S[i * 64 + cc];
+    }
+    // trailing update of the upper Gram: G_ab -= sum_k R_ka R_kb (a, b >= e)
+    if (bi >= e && bj + 3 >= bi && bi < w && bj < w) {
+#pragma unroll 4
+      for (int k = 0; k < 16; ++k) {
+        double ra[4], rb[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          ra[q] = bi + q < w ? S[k * 64 + bi + q] : 0.0;
+          rb[q] = bj + q < w ? S[k * 64 + bj + q] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) g.v[i][j] = fma(-ra[i], rb[j], g.v[i][j]);
+      }
+    }
+    __syncthreads();
+  }
+  // R beyond w: padding columns of the last block hold identity -> zero
+  for (int t = tid; t < 64; t += blockDim.x)
+    if (t >= w) Rs[t * kTL + t] = 0.0;
+  const bool ok = s_ok != 0;
+  __syncthreads();
+  inv_upper_levels(Rs, Xs, S);
+  return ok;
+}
+
+// LU without pivoting of Q_top * D - I with the Householder sign rule (same
+// arithmetic contract as sign_lu), blocked: L (unit lower) -> Ls, U (upper,
+// column-scaled by D) -> Us, D -> Dd, and the inverses U^{-1} -> Ui, L^{-1} -> Li
+// (same contract as inv_upper_blk / inv_unit_lower_blk).  S: >= 1024 doubles.
 }  // namespace tile64
 }  // namespace ffb
