@@ -26,3 +26,4 @@ from .ffsrqr_oracle import (  # noqa: F401
     srqr,
     trqrcp,
 )
+from . import callers_oracle  # noqa: E402,F401  (RSISVD, HOSVD/ST-HOSVD, IALM restatements)

@@ -9,12 +9,13 @@ from .errors import (CertificationError, DimensionError, EngineUnavailable, Nume
                      SingularTrailingBlockError)
 from .results import (ApproxSvd, PartialFactorization, SketchParams, SrqrCertificate, SrqrResult,
                       WYFactor, flip_flop_flop_formula)
-from .engine import flip_flop_srqr, srqr, trqrcp
+from .engine import flip_flop_srqr, rsisvd, srqr, trqrcp
 
 __version__ = "0.1.0"
 
 __all__ = [
     "ApproxSvd", "CertificationError", "DimensionError", "EngineUnavailable", "NumericalError",
     "PartialFactorization", "SingularTrailingBlockError", "SketchParams", "SrqrCertificate",
-    "SrqrResult", "WYFactor", "flip_flop_flop_formula", "flip_flop_srqr", "srqr", "trqrcp",
+    "SrqrResult", "WYFactor", "flip_flop_flop_formula", "flip_flop_srqr", "rsisvd", "srqr",
+    "trqrcp",
 ]

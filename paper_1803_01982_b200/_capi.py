@@ -24,7 +24,8 @@ FFB_MODE_FLIPFLOP = 2
 
 EXPORTS = ("ffb_ctx_create", "ffb_ctx_destroy", "ffb_last_error", "ffb_version",
            "ffb_workspace_query", "ffb_run", "ffb_flipflop", "ffb_gemm", "ffb_block_pivots",
-           "ffb_run_batched")
+           "ffb_run_batched", "ffb_rsisvd_workspace_query", "ffb_rsisvd", "ffb_svt_partials",
+           "ffb_ialm_update", "ffb_sumsq", "ffb_shrink_cols")
 
 
 class Params(C.Structure):
@@ -116,6 +117,26 @@ def load(path=LIB_PATH):
                                          C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_void_p, C.c_size_t]
         lib.ffb_block_pivots.restype = C.c_int
+        lib.ffb_rsisvd_workspace_query.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                                   C.POINTER(C.c_size_t)]
+        lib.ffb_rsisvd_workspace_query.restype = C.c_int
+        lib.ffb_rsisvd.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                   C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
+                                   C.c_void_p, C.c_size_t, C.c_void_p, C.c_int64, C.c_void_p,
+                                   C.c_void_p, C.c_int64, C.POINTER(C.c_int64),
+                                   C.POINTER(C.c_int32)]
+        lib.ffb_rsisvd.restype = C.c_int
+        lib.ffb_svt_partials.argtypes = []
+        lib.ffb_svt_partials.restype = C.c_int
+        lib.ffb_ialm_update.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_void_p, C.c_int64, C.c_double, C.c_double,
+                                        C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]
+        lib.ffb_ialm_update.restype = C.c_int
+        lib.ffb_sumsq.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+        lib.ffb_sumsq.restype = C.c_int
+        lib.ffb_shrink_cols.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
+                                        C.c_void_p, C.c_double, C.c_void_p, C.c_int64]
+        lib.ffb_shrink_cols.restype = C.c_int
         _lib = lib
         return lib
 

@@ -213,6 +213,49 @@ size_t carve(const ffb_ctx* ctx, const Dims& D, void* base, size_t cap, Work& w)
   return b.off + kAlign;
 }
 
+// Workspace of the randomized subspace-iteration SVD (ffb_rsisvd): the rank-r
+// working matrices plus the same panel / Jacobi / GEMM scratch as the flip-flop.
+size_t carve_rsisvd(const ffb_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t r, void* base,
+                    size_t cap, Work& w) {
+  Bump b{static_cast<char*>(base), 0, cap};
+  const int64_t mn = max_i(m, n);
+  w.tmp = b.take<double>(m * r);      // A Omega, A Q_z (factored in place)
+  w.Yt = b.take<double>(m * r);       // reflectors of the m x r QRs
+  w.Tt = b.take<double>(r * r);
+  w.Rt = b.take<double>(r * r);
+  w.Q = b.take<double>(m * r);        // explicit Q (m x r)
+  w.X = b.take<double>(n * r);        // A^T Q (factored in place)
+  w.Yl = b.take<double>(n * r);       // reflectors of the n x r QRs
+  w.Tl = b.take<double>(r * r);
+  w.Rl = b.take<double>(r * r);
+  w.Qh = b.take<double>(n * r);       // explicit Q_z (n x r)
+  w.TYt = b.take<double>(r * r);
+  w.Xa = b.take<double>(mn * kPanelW);
+  w.Xb = b.take<double>(mn * kPanelW);
+  w.S1 = b.take<double>(r * kPanelW);
+  w.S2 = b.take<double>(r * kPanelW);
+  w.Gm = b.take<double>(kPanelW * kPanelW);
+  w.ppart = b.take<double>((size_t)(ctx ? ctx->sms : 160) * kPanelW * kPanelW);
+  w.pbar = b.take<uint32_t>(4);
+  w.hhW = b.take<double>(kPanelW * r);
+  w.hhW2 = b.take<double>(kPanelW * r);
+  w.status = b.take<uint32_t>(1);
+  w.Us = b.take<double>(r * r);
+  w.Vo = b.take<double>(r * r);
+  w.sig = b.take<double>(r);
+  w.jwork = b.take<double>(jacobi_work_doubles((int)r, kMaxSweeps));
+  w.W1 = b.take<double>(r * k);
+  w.W2 = b.take<double>(r * k);
+  w.joff = b.take<double>(kMaxSweeps);
+  w.jbar = b.take<uint32_t>(4);
+  w.jsweeps = b.take<int>(4);
+  w.jorder = b.take<int>(r);
+  w.gpart_cap = std::max<size_t>(16u << 20, (size_t)64 * kPanelW * kPanelW);
+  w.gpart = b.take<double>(w.gpart_cap);
+  w.skcnt = b.take<unsigned>(65536);
+  return b.off + kAlign;
+}
+
 struct Eng {
   ffb_ctx* ctx;
   cudaStream_t st;
@@ -288,6 +331,16 @@ struct Eng {
     }
   }
 };
+
+
+// Q[:, :Nx] = (I - Y T Y_top^T)[:, :Nx] explicitly (Mx x Nx, ld ldq) from a hh_qr
+// factorization: LAPACK dorgqr's thin Q, as numpy.linalg.qr returns it.
+void explicit_q(Eng& e, const double* Y, int64_t ldy, const double* T, int64_t ldt, int64_t Mx,
+                int64_t Nx, double* Q, int64_t ldq) {
+  e.gemm(Nx, Nx, Nx, 1.0, T, ldt, false, Y, ldy, false, 0.0, e.w.TYt, Nx);
+  e.gemm(Mx, Nx, Nx, -1.0, Y, ldy, false, e.w.TYt, Nx, true, 0.0, Q, ldq);
+  e.ok(launch_add_identity(e.st, Q, ldq, Mx, Nx, 1.0));
+}
 
 int fail(ffb_ctx* ctx, int code, const std::string& msg) {
   if (ctx) {
@@ -679,5 +732,83 @@ extern "C" int ffb_run_batched(ffb_ctx* ctx, ffb_batch_item* items, int64_t coun
   for (auto& t : pool) t.join();
   for (int64_t i = 0; i < count; ++i)
     if (items[i].status != FFB_OK) return items[i].status;
+  return FFB_OK;
+}
+
+// --------------------------------------------------------------------------
+// Randomized subspace-iteration SVD (the paper's RSISVD baseline,
+// ffsrqr/svd.py:101-133): Y = A Omega; Q = qr(Y); q times { Q = qr(A^T Q);
+// Q = qr(A Q) }; B = Q^T A; SVD(B) through B^T = Q_b R_b and the one-sided
+// Jacobi SVD of R_b (R_b = U_r S V_r^T => B = V_r S (Q_b U_r)^T).  All QRs are
+// the Householder panels of the flip-flop path (LAPACK dgeqrf/dorgqr convention,
+// so Q equals numpy.linalg.qr's up to rounding); u, v match LAPACK dgesdd's up
+// to column signs.
+extern "C" int ffb_rsisvd_workspace_query(int64_t m, int64_t n, int64_t k, int64_t r,
+                                          size_t* bytes) {
+  if (!bytes) return FFB_ERR_ARGUMENT;
+  if (m < 1 || n < 1 || k < 1 || k > r || r > std::min(m, n) || r > 512) return FFB_ERR_DIMENSION;
+  Work w;
+  *bytes = carve_rsisvd(nullptr, m, n, k, r, nullptr, (size_t)-1, w) + (8u << 20);
+  return FFB_OK;
+}
+
+extern "C" int ffb_rsisvd(ffb_ctx* ctx, void* stream, const double* A, int64_t m, int64_t n,
+                          int64_t lda, int64_t k, int64_t r, int64_t q, const double* omega,
+                          void* workspace, size_t workspace_bytes, double* u, int64_t ldu,
+                          double* s, double* v, int64_t ldv, int64_t* flops, int32_t* sweeps_out) {
+  if (!ctx || !A || !omega || !workspace || !u || !s || !v) return FFB_ERR_ARGUMENT;
+  if (m < 1 || n < 1 || k < 1 || k > r || r > std::min(m, n) || r > 512 || q < 0 || lda < m ||
+      ldu < m || ldv < n)
+    return fail(ctx, FFB_ERR_DIMENSION, "rsisvd needs 1 <= k <= r <= min(m, n), r <= 512, q >= 0");
+  Eng e;
+  e.ctx = ctx;
+  e.st = (cudaStream_t)stream;
+  Work& w = e.w;
+  const size_t need = carve_rsisvd(ctx, m, n, k, r, workspace, workspace_bytes, w);
+  if (need > workspace_bytes) return fail(ctx, FFB_ERR_ARGUMENT, "workspace too small");
+  e.gc.sms = ctx->sms;
+  e.gc.partial = w.gpart;
+  e.gc.partial_cap = w.gpart_cap;
+  e.gc.counters = w.skcnt;
+  e.gc.counter_cap = 65536;
+  cudaStream_t st = e.st;
+  e.okm(cudaMemsetAsync(w.status, 0, sizeof(uint32_t), st));
+  e.okm(cudaMemsetAsync(w.skcnt, 0, sizeof(unsigned) * 65536, st));
+  // Y = A Omega (Omega n x r, row-major = numpy C order)
+  e.gemm(m, r, n, 1.0, A, lda, false, omega, r, false, 0.0, w.tmp, m);
+  e.hh_qr(w.tmp, m, r, m, w.Yt, m, w.Tt, r, w.Rt, r, false);
+  explicit_q(e, w.Yt, m, w.Tt, r, m, r, w.Q, m);
+  for (int64_t it = 0; it < q; ++it) {
+    e.gemm(n, r, m, 1.0, A, lda, true, w.Q, m, true, 0.0, w.X, n);          // Z = A^T Q
+    e.hh_qr(w.X, n, r, n, w.Yl, n, w.Tl, r, w.Rl, r, false);
+    explicit_q(e, w.Yl, n, w.Tl, r, n, r, w.Qh, n);
+    e.gemm(m, r, n, 1.0, A, lda, false, w.Qh, n, true, 0.0, w.tmp, m);      // Y = A Q_z
+    e.hh_qr(w.tmp, m, r, m, w.Yt, m, w.Tt, r, w.Rt, r, false);
+    explicit_q(e, w.Yt, m, w.Tt, r, m, r, w.Q, m);
+  }
+  // B^T = A^T Q = Q_b R_b
+  e.gemm(n, r, m, 1.0, A, lda, true, w.Q, m, true, 0.0, w.X, n);
+  e.hh_qr(w.X, n, r, n, w.Yl, n, w.Tl, r, w.Rl, r, true);
+  e.ok(launch_jacobi_svd(st, ctx->sms, w.Rl, r, (int)r, w.sig, w.Us, r, w.Vo, r, w.jwork, w.jbar,
+                         w.joff, w.jsweeps, w.jorder, kMaxSweeps));
+  e.launches += 5;
+  // u = Q V_r[:, :k] ; v = Q_b [U_r[:, :k]; 0] ; s = sigma[:k]
+  e.gemm(m, k, r, 1.0, w.Q, m, false, w.Vo, r, true, 0.0, u, ldu);
+  e.gemm(r, k, r, 1.0, w.Yl, n, true, w.Us, r, true, 0.0, w.W1, r);
+  e.gemm(r, k, r, 1.0, w.Tl, r, false, w.W1, r, true, 0.0, w.W2, r);
+  e.gemm(n, k, r, -1.0, w.Yl, n, false, w.W2, r, true, 0.0, v, ldv);
+  e.ok(launch_add_top(st, v, ldv, w.Us, r, r, k));
+  e.ok(cudaMemcpyAsync(s, w.sig, sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
+  int sw = 0;
+  uint32_t stw = 0;
+  cudaError_t se = cudaSuccess;
+  if (e.cerr == cudaSuccess) se = d2h(&sw, w.jsweeps, sizeof(int), st);
+  if (e.cerr == cudaSuccess && se == cudaSuccess) se = d2h(&stw, w.status, sizeof(stw), st);
+  if (e.cerr != cudaSuccess) return cuda_fail(ctx, e.cerr, "rsisvd launch");
+  if (se != cudaSuccess) return cuda_fail(ctx, se, "rsisvd");
+  if (flops) *flops = e.gc.flops;
+  if (sweeps_out) *sweeps_out = sw;
+  if (stw & 1u) return fail(ctx, FFB_ERR_NUMERICAL, "non-finite values in rsisvd");
+  if (sw >= kMaxSweeps) return fail(ctx, FFB_ERR_NUMERICAL, "small SVD did not converge");
   return FFB_OK;
 }

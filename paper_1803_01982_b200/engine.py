@@ -7,6 +7,8 @@ Mirrors the reference's Python API for the hot path:
   result type ``ApproxSvd`` with ``meta["srqr"]``/``["params"]``/``["method"]``)
 * ``srqr(A, params)`` — ffsrqr/srqr.py:174-210 (``SrqrResult``)
 * ``trqrcp(A, params)`` — ffsrqr/sketch.py:150-161 (``PartialFactorization``)
+* ``rsisvd(A, k, p=5, q=2, seed=0)`` — ffsrqr/svd.py:101-133, the paper's
+  randomized subspace-iteration baseline, on the same device kernels
 
 Inputs may be numpy arrays (results come back as numpy, like the reference)
 or CUDA float64 torch tensors (results stay on the device).  Errors are the
@@ -280,3 +282,62 @@ def trqrcp(A, params: SketchParams, device=None):
     fact.sketch = _conv(out["B"], np_)
     fact.pivot_gap = _conv(out["pivot_gap"], np_) if "pivot_gap" in out else None
     return fact
+
+
+_rs_omega_cache = {}
+
+
+def rsisvd(A, k, p=5, q=2, seed=0, device=None):
+    """Randomized subspace-iteration SVD baseline (ffsrqr/svd.py:101-133) on the
+    B200 engine: Omega = gaussian(n, r, seed, 2_000_000) from the reference RNG,
+    then ffb_rsisvd (GEMMs on FP64 DMMA, Householder panel QRs, Jacobi SVD)."""
+    torch = _torch()
+    shape = tuple(A.shape)
+    if len(shape) != 2:
+        raise DimensionError("expected a 2-D matrix")
+    m, n = shape
+    if not 1 <= k <= min(m, n):
+        raise DimensionError(f"rsisvd needs 1 <= k <= min(m,n); got k={k}")
+    if p < 0 or q < 0:
+        raise DimensionError("rsisvd needs p >= 0 and q >= 0")
+    r = min(k + p, min(m, n))
+    if r > 512:
+        raise DimensionError("the B200 engine supports rsisvd widths k + p <= 512")
+    dev = _device(device if device is not None else (A.device if isinstance(A, torch.Tensor) and A.is_cuda else None))
+    with torch.cuda.device(dev):
+        Ad, is_np = _to_device_colmajor(A, dev)
+        lib = _capi.load()
+        ctx = _capi.context(dev.index)
+        nbytes = C.c_size_t()
+        rc = lib.ffb_rsisvd_workspace_query(m, n, k, r, C.byref(nbytes))
+        if rc != _capi.FFB_OK:
+            raise DimensionError("invalid dimensions for the engine")
+        ws = _workspace(torch, dev, nbytes.value)
+        key = (dev.index, n, r, int(seed) & 0xFFFFFFFFFFFFFFFF)
+        om = _rs_omega_cache.get(key)
+        if om is None:
+            om = torch.from_numpy(rng.gaussian(n, r, seed, rng.STREAM_RSISVD)).to(dev)
+            if len(_rs_omega_cache) > 64:
+                _rs_omega_cache.clear()
+            _rs_omega_cache[key] = om
+        u = _colmajor(torch, m, k, dev)
+        s = torch.empty(k, dtype=torch.float64, device=dev)
+        v = _colmajor(torch, n, k, dev)
+        fl = C.c_int64(0)
+        sw = C.c_int32(0)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        rc = lib.ffb_rsisvd(ctx, C.c_void_p(stream), C.c_void_p(Ad.data_ptr()), m, n, Ad.stride(1),
+                            k, r, q, C.c_void_p(om.data_ptr()), C.c_void_p(ws.data_ptr()), ws.numel(),
+                            C.c_void_p(u.data_ptr()), m, C.c_void_p(s.data_ptr()),
+                            C.c_void_p(v.data_ptr()), n, C.byref(fl), C.byref(sw))
+        if rc != _capi.FFB_OK:
+            msg = _capi.last_error(ctx)
+            if rc == _capi.FFB_ERR_DIMENSION:
+                raise DimensionError(msg)
+            if rc == _capi.FFB_ERR_NUMERICAL:
+                raise NumericalError(msg)
+            raise RuntimeError(f"ffb_rsisvd failed ({rc}): {msg}")
+        meta = {"method": "rsisvd", "q": q, "p": p, "engine": "ffb200-sm100a",
+                "svd_sweeps": int(sw.value)}
+        return ApproxSvd(u=_conv(u, is_np), s=_conv(s, is_np), v=_conv(v, is_np),
+                         flop_count=int(fl.value), meta=meta)
