@@ -387,6 +387,26 @@ def main():
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": ems, "path": "paper_1803_01982_b200.flip_flop_srqr(pinned host tensor)"}
 
+    # the paper's competitor on the same device kernels: RSISVD,
+    # rank k, oversampling p, q = 2 power steps (ffsrqr/svd.py:101-133)
+    rsi = None
+    if rank == 0 and ws == 1:
+        def rs_step():
+            return ffb.rsisvd(A, k, p=p, q=2, seed=0)
+        rs = rs_step()
+        torch.cuda.synchronize()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nrs = max(1, min(args.steps, 5))
+        r0.record(st)
+        for _ in range(nrs):
+            rs = rs_step()
+        r1.record(st)
+        torch.cuda.synchronize()
+        rms = r0.elapsed_time(r1) / nrs
+        rsi = {"value": 1000.0 / rms, "unit": "factorizations/s", "ms_per_step": rms,
+               "config": f"k={k}, p={p}, q=2", "path": "paper_1803_01982_b200.rsisvd",
+               "sigma_k_rel_vs_flipflop": float(abs(rs.s[-1] - ap_.s[-1]) / ap_.s[-1])}
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         A_np = A_host.t().numpy() if A_host is not None else A.cpu().numpy()
@@ -424,6 +444,7 @@ def main():
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "rsisvd_same_device": rsi,
             "certificate": {"swaps": ap_.meta["srqr"].cert.swaps, "g2": ap_.meta["srqr"].cert.g2},
         }
         print(json.dumps(line), flush=True)

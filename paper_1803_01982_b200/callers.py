@@ -57,23 +57,24 @@ def unfold(X, mode):
 
 
 def hosvd(X, ranks, l_extra=10, b=32, p=10, seed=0, device=None):
-    """Truncated HOSVD (``tensor.py:104-120``) with the flip-flop engine per mode.
+    """Truncated HOSVD (``tensor.py:104-120``) with the flip-flop engine per mode
+    and the core formed by DMMA n-mode products (``tensor.nmode_product``).
 
     Returns (core, factors, approxes).  The per-mode factorizations are
     independent (the multi-GPU unit of config 4, see ``batch.py``).
     """
     import torch
 
-    Xt = X if isinstance(X, torch.Tensor) else torch.as_tensor(X, dtype=torch.float64)
-    if device is not None or not Xt.is_cuda:
-        Xt = Xt.to(device or "cuda")
+    from . import tensor
+
+    Xt = tensor.to_device(X, device)
     eng = hosvd_engine(l_extra, b, p, seed)
     factors, approxes = [], []
     for mode, r in enumerate(ranks):
-        ap = eng(unfold(Xt, mode), r)
+        ap = eng(tensor.unfold(Xt, mode), r)
         approxes.append(ap)
         factors.append(ap.u if isinstance(ap.u, torch.Tensor) else torch.as_tensor(ap.u, device=Xt.device))
     G = Xt
     for mode, U in enumerate(factors):
-        G = torch.movedim(torch.tensordot(U.t(), torch.movedim(G, mode, 0), dims=1), 0, mode)
+        G = tensor.nmode_product(G, U.t(), mode)
     return G, factors, approxes
