@@ -90,13 +90,13 @@ FFB_DEV void inner_pair(int t, int k, int n_within, int& p, int& q) {
 // speed), c = 1/sqrt(1+t^2) refined to fp64 by two Newton steps so the rotation
 // is orthogonal to working precision.  Returns (cc^2, aa*bb) for the caller's
 // off-diagonal measure; c = 1, s = 0 when the pair is already orthogonal.
-FFB_DEV bool rotation(const double* G, const int* gcol, int p, int q, double tol2, double& c,
-                      double& s, double& c2, double& den) {
+FFB_DEV bool rotation(const double* G, int p, int q, double tol2, double& c, double& s,
+                      double& c2, double& den) {
   c = 1.0;
   s = 0.0;
   c2 = 0.0;
   den = 1.0;
-  if (gcol[p] < 0 || gcol[q] < 0) return false;
+  // padding slots hold zero columns: aa * bb = 0 fails the threshold test below
   const double aa = G[p * kMW + p], bb = G[q * kMW + q], cc = G[p * kMW + q];
   c2 = cc * cc;
   den = aa * bb;
@@ -284,7 +284,6 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
   double* Gs2 = Js + 32 * kMW;            // ping-pong partners of Gs / Js
   double* Js2 = Gs2 + 32 * kMW;
   double* part = Js2 + 32 * kMW;          // 4 x 32 x 33 Gram partials
-  __shared__ int gcol[32];
   __shared__ double s_off;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   if ((int)blockIdx.x >= a.P) {   // fused launch: V replay CTAs (see v_replay)
@@ -308,11 +307,6 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
     if (tid == 0) s_off = 0.0;
     for (int r = 0; r < nb - 1; ++r) {
       const int pa = rr_player(blockIdx.x, r, nb), pb = rr_player(nb - 1 - blockIdx.x, r, nb);
-      if (tid < 32) {
-        const int blk = tid < kBS ? pa : pb;
-        const int c = blk * kBS + (tid & (kBS - 1));
-        gcol[tid] = c < a.l ? c : -1;
-      }
       stage_rows_async(Ms, a.M, ld, pa, pb, 0, lpad);
       cp_async_commit();
       cp_async_wait<0>();
@@ -381,16 +375,14 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
       const double* Jc = Js;
       double* Gn = Gs2;
       double* Jn = Js2;
-      for (int t = 0; t < n_within + n_cross; ++t) {
-        int pa2, qa2, pb2, qb2;
-        inner_pair(t, ba, n_within, pa2, qa2);
-        inner_pair(t, bb2, n_within, pb2, qb2);
-        const double g00 = Gc[pa2 * kMW + pb2], g01 = Gc[pa2 * kMW + qb2];
-        const double g10 = Gc[qa2 * kMW + pb2], g11 = Gc[qa2 * kMW + qb2];
-        const double j00 = Jc[pa2 * kMW + pb2], j01 = Jc[pa2 * kMW + qb2];
-        const double j10 = Jc[qa2 * kMW + pb2], j11 = Jc[qa2 * kMW + qb2];
+      auto step = [&](int pa2, int qa2, int pb2, int qb2) {
+        const int ra = pa2 * kMW, rq = qa2 * kMW;
+        const double g00 = Gc[ra + pb2], g01 = Gc[ra + qb2];
+        const double g10 = Gc[rq + pb2], g11 = Gc[rq + qb2];
+        const double j00 = Jc[ra + pb2], j01 = Jc[ra + qb2];
+        const double j10 = Jc[rq + pb2], j11 = Jc[rq + qb2];
         double cb, sb, c2b, denb;
-        const bool rot = rotation(Gc, gcol, pb2, qb2, tol2, cb, sb, c2b, denb);
+        const bool rot = rotation(Gc, pb2, qb2, tol2, cb, sb, c2b, denb);
         // lane ba of this warp has bb2 == ba: its rotation is pair ba's
         const double ca = __shfl_sync(0xffffffffu, cb, ba);
         const double sa = __shfl_sync(0xffffffffu, sb, ba);
@@ -401,15 +393,15 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
         // G_blk <- R_a^T G_blk R_b with R = [[c, s], [-s, c]] acting on (p, q)
         const double h00 = cb * g00 - sb * g01, h01 = sb * g00 + cb * g01;   // columns
         const double h10 = cb * g10 - sb * g11, h11 = sb * g10 + cb * g11;
-        Gn[pa2 * kMW + pb2] = ca * h00 - sa * h10;
-        Gn[pa2 * kMW + qb2] = ca * h01 - sa * h11;
-        Gn[qa2 * kMW + pb2] = sa * h00 + ca * h10;
-        Gn[qa2 * kMW + qb2] = sa * h01 + ca * h11;
+        Gn[ra + pb2] = ca * h00 - sa * h10;
+        Gn[ra + qb2] = ca * h01 - sa * h11;
+        Gn[rq + pb2] = sa * h00 + ca * h10;
+        Gn[rq + qb2] = sa * h01 + ca * h11;
         // J rows (pa, qa) x columns (pb, qb): J <- J R_b (column rotation only)
-        Jn[pa2 * kMW + pb2] = cb * j00 - sb * j01;
-        Jn[pa2 * kMW + qb2] = sb * j00 + cb * j01;
-        Jn[qa2 * kMW + pb2] = cb * j10 - sb * j11;
-        Jn[qa2 * kMW + qb2] = sb * j10 + cb * j11;
+        Jn[ra + pb2] = cb * j00 - sb * j01;
+        Jn[ra + qb2] = sb * j00 + cb * j01;
+        Jn[rq + pb2] = cb * j10 - sb * j11;
+        Jn[rq + qb2] = sb * j10 + cb * j11;
         __syncthreads();
         const double* tg = Gc;
         Gc = Gn;
@@ -417,6 +409,17 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
         const double* tj = Jc;
         Jc = Jn;
         Jn = const_cast<double*>(tj);
+      };
+      for (int t = 0; t < n_within; ++t) {
+        int pa2, qa2, pb2, qb2;
+        inner_pair(t, ba, n_within, pa2, qa2);
+        inner_pair(t, bb2, n_within, pb2, qb2);
+        step(pa2, qa2, pb2, qb2);
+      }
+      // cross pairs (k, kBS + (k + t) % kBS): index math without branches
+      for (int t = 0; t < n_cross; ++t) {
+        const int tt = t & (kBS - 1);
+        step(ba, kBS + ((ba + tt) & (kBS - 1)), bb2, kBS + ((bb2 + tt) & (kBS - 1)));
       }
       double off = offn > 0.0 ? sqrt(offn / offd) : 0.0;
       JPROF(2)
