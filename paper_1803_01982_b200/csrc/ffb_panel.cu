@@ -160,6 +160,98 @@ FFB_DEV void apply_upper(const double* Cs, int rows, int w, const double* Xs, do
 
 }  // namespace
 
+// Fallback for numerically rank-deficient panels (kappa(X) >~ 1e6, where the
+// shifted CholeskyQR passes cannot recover an orthonormal basis): the
+// reference's own column-by-column Householder QR (ffsrqr/qr.py:21-43) on the
+// whole grid.  Per column two grid barriers: (A) the tail norm, (B) the
+// projections v^T X[:, j > c] and Y[:, k < c]^T v (for T), all reduced in fixed
+// order so every CTA derives identical reflectors.  Writes Y, T, R with the
+// panel kernel's contract; X is read only (copied to Qa first).
+FFB_DEV void panel_householder(const PanelArgs& a, int64_t r0, int64_t r1, double* red) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, G = gridDim.x;
+  const int w = a.w;
+  const int64_t Mp = a.Mp;
+  double* W = a.Qa;                       // working copy, ld Mp; column c becomes v_c
+  double* partA = a.part;                 // [G]
+  double* partB = a.part + G;             // [G][64]
+  for (int64_t i = r0 + tid; i < r1; i += nt)
+    for (int c = 0; c < w; ++c) W[i + c * Mp] = a.X[i + c * a.ldx];
+  if (blockIdx.x == 0)
+    for (int t = tid; t < w * w; t += nt) {
+      const int r = t % w, c = t / w;
+      a.T[r + (int64_t)c * a.ldt] = 0.0;
+      a.R[r + (int64_t)c * a.ldr] = 0.0;
+    }
+  grid_sync(a.bar, G);
+  for (int c = 0; c < w; ++c) {
+    // (A) tail norm of column c over this CTA's rows i > c
+    double t = 0.0;
+    for (int64_t i = (r0 > c + 1 ? r0 : c + 1) + tid; i < r1; i += nt) t = fma(W[i + c * Mp], W[i + c * Mp], t);
+    t = block_sum(t, red);
+    if (tid == 0) partA[blockIdx.x] = t;
+    grid_sync(a.bar, G);
+    double tsq = 0.0;
+    for (int b = 0; b < G; ++b) tsq += partA[b];
+    const double x0 = W[c + c * Mp];
+    double tau = 0.0, alpha = x0, div = 1.0;
+    if (tsq != 0.0) {
+      const double nrm = sqrt(x0 * x0 + tsq);
+      alpha = x0 == 0.0 ? nrm : -copysign(nrm, x0);
+      div = x0 - alpha;
+      tau = (alpha - x0) / alpha;
+    }
+    // (B) v over own rows (rows < c: 0, row c: 1), Y column c, then projections
+    for (int64_t i = r0 + tid; i < r1; i += nt) {
+      const double v = i < c ? 0.0 : (i == c ? 1.0 : (tau != 0.0 ? W[i + c * Mp] / div : 0.0));
+      W[i + c * Mp] = v;
+      a.Y[i + (int64_t)c * a.ldy] = v;
+    }
+    __syncthreads();
+    const int nproj = w - 1;   // j > c: v^T W[:, j];  k < c: W[:, k]^T v  (both over rows >= c)
+    for (int q = warp; q < nproj; q += nt >> 5) {
+      const int col = q < c ? q : q + 1;
+      double d = 0.0;
+      for (int64_t i = (r0 > c ? r0 : c) + lane; i < r1; i += 32)
+        d = fma(W[i + c * Mp], W[i + (int64_t)col * Mp], d);
+      d = warp_sum(d);
+      if (lane == 0) partB[(size_t)blockIdx.x * 64 + q] = d;
+    }
+    grid_sync(a.bar, G);
+    // every CTA: reduced projections (fixed order) -> rank-1 update of its rows
+    double* proj = red + 32;   // [64] in shared memory
+    for (int q = tid; q < nproj; q += nt) {
+      double d = 0.0;
+      for (int b = 0; b < G; ++b) d += partB[(size_t)b * 64 + q];
+      proj[q] = d;
+    }
+    __syncthreads();
+    if (tau != 0.0) {
+      const int ncols = w - 1 - c;
+      const int64_t rb = r0 > c ? r0 : c, nr = r1 - rb;
+      for (int64_t e = tid; e < nr * ncols; e += nt) {
+        const int64_t i = rb + e % nr;
+        const int j = c + 1 + (int)(e / nr);
+        W[i + (int64_t)j * Mp] = fma(-tau * W[i + c * Mp], proj[j - 1], W[i + (int64_t)j * Mp]);
+      }
+    }
+    __syncthreads();
+    // row c of the updated panel is row c of R
+    if (c >= r0 && c < r1)
+      for (int j = c + 1 + tid; j < w; j += nt) a.R[c + (int64_t)j * a.ldr] = W[c + (int64_t)j * Mp];
+    if (blockIdx.x == 0 && tid == 0) {
+      a.R[c + (int64_t)c * a.ldr] = alpha;
+      // T[:c, c] = -tau T[:c, :c] z, z_k = Y[:, k]^T v ; T[c, c] = tau
+      for (int r = 0; r < c; ++r) {
+        double acc = 0.0;
+        for (int k = r; k < c; ++k) acc = fma(a.T[r + (int64_t)k * a.ldt], proj[k], acc);
+        a.T[r + (int64_t)c * a.ldt] = -tau * acc;
+      }
+      a.T[c + (int64_t)c * a.ldt] = tau;
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
   using namespace tile64;
   extern __shared__ __align__(16) double sm[];
@@ -193,6 +285,7 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
   // ~1e-14 (the decision uses the reduced Gram, identical in every CTA)
   double em_prev = 1.0;
   const double* qfin = a.Qa;
+  bool fallback = false;
   for (int pass = 0; pass < 3; ++pass) {
     if (pass == 2 && em_prev <= 1e-7) break;
     const double* src = pass == 0 ? a.X : (pass == 1 ? a.Qa : a.Qb);
@@ -277,6 +370,13 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
       first_order = em <= 1e-5;
       em_prev = em;
       if (a.prof && tid == 0 && blockIdx.x == 0) a.prof[12 + pass] = __double_as_longlong(em);
+      // after the shifted first pass, Q1^T Q1 = I - s (R^T R)^-1: a deviation near 1
+      // means kappa(X)^2 > ~1e12 s-scaled, i.e. numerically dependent columns that
+      // the unshifted passes cannot orthonormalise -> Householder fallback
+      if (pass == 1 && !(em <= 0.9)) {
+        fallback = true;
+        break;
+      }
     }
     if (zp) {
       for (int t = tid; t < kW * kW; t += nt) {
@@ -330,8 +430,11 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
       }
       QPROF(2)
       const bool ok = chol_inv_blk(g, w, Rs, Xs, Sx);   // blocked: warp-level 16x16 diagonal chains
-      if (!ok && blockIdx.x == 0 && tid == 0) atomicOr(a.status, 2u /* kStCholFail */);
       QPROF(8)
+      if (!ok) {   // identical in every CTA (same reduced Gram)
+        fallback = true;
+        break;
+      }
     }
     QPROF(2)
     // Racc <- R * Racc (pass 0: Racc = R; zero panel: Racc = 0), DMMA via Ws
@@ -354,6 +457,11 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
       apply_upper(Cs, rows, w, Xs, dst, Mp, c0);
     }
     QPROF(3)
+  }
+  if (fallback) {
+    grid_sync(a.bar, G);   // every CTA is done with the CholeskyQR work buffers
+    panel_householder(a, r0, r1, buf);
+    return;
   }
   grid_sync(a.bar, G);   // Q = Qa complete (top w rows visible to every CTA)
   QPROF(4)

@@ -30,6 +30,11 @@ def load(name):
         case["A"] = A
     got = hashlib.sha256(np.ascontiguousarray(case["A"], dtype=np.float64).tobytes()).hexdigest()
     case["orders"] = [case[f"block_order_{i}"] for i in range(case["n_blocks"])]
+    # numerical rank of the reference factor: with alpha = 0 (exactly / numerically
+    # rank-deficient input, l >= rank) every pivot candidate past it is a
+    # rounding-level norm, so pivot parity is defined up to num_rank only
+    d = np.abs(np.diag(case["R"][:, : case["l"]]))
+    case["num_rank"] = int(np.sum(d > 1e-12 * d[0])) if case["cert"][0] == 0.0 and d.size and d[0] > 0 else case["l"]
     case["source"] = "reference"
     if got != case["sha256"]:
         # LAPACK/BLAS rounding differs across host CPUs, so a recipe-built input is not

@@ -24,8 +24,12 @@ def test_oracle_matches_reference(name):
     prm = oracle.resolve(c["m"], c["n"], c["k"], c["l"], c["b"], c["p"], g=c["g"], d=c["d"],
                          seed=c["seed"], clamp=False)
     trq = oracle.trqrcp(A, prm)
+    r = c["num_rank"]
+    j0 = 0
     for i, o in enumerate(c["orders"]):
-        assert np.array_equal(trq.block_orders[i], o), f"block {i} pivots differ"
+        keep = max(0, min(len(o), r - j0))
+        assert np.array_equal(trq.block_orders[i][:keep], o[:keep]), f"block {i} pivots differ"
+        j0 += min(c["b"], c["l"] - j0)
     try:
         sr = oracle.srqr(A, prm)
         status = "ok"
@@ -33,14 +37,25 @@ def test_oracle_matches_reference(name):
         assert e.kind == "CertificationError"
         sr, status = e.payload, "CertificationError"
     assert status == c["srqr_status"]
-    assert np.array_equal(sr.perm, c["perm"])
-    assert _rel(sr.R, c["R"]) < 1e-11
-    assert _rel(sr.rtilde, c["rtilde"]) < 1e-11
-    if c["q_ext"].shape[1]:
-        assert np.max(np.abs(sr.Q - c["q_ext"])) < 1e-10
+    if r < c["l"]:
+        # numerically rank-deficient: the factor is pinned up to the numerical rank
+        assert np.array_equal(sr.perm[:r], c["perm"][:r])
+        assert _rel(sr.R[:r, :r], c["R"][:r, :r]) < 1e-11
+        assert sr.alpha == 0.0 and c["cert"][0] == 0.0
+        return_after_cert = True
+    else:
+        assert np.array_equal(sr.perm, c["perm"])
+        assert _rel(sr.R, c["R"]) < 1e-11
+        assert _rel(sr.rtilde, c["rtilde"]) < 1e-11
+        if c["q_ext"].shape[1]:
+            assert np.max(np.abs(sr.Q - c["q_ext"])) < 1e-10
+        return_after_cert = False
     cert = np.array([sr.alpha, sr.g1, sr.g2, sr.swaps, sr.tau_bound, sr.tau_hat_bound, sr.r22])
     assert cert[3] == c["cert"][3]
-    np.testing.assert_allclose(cert, c["cert"], rtol=1e-9, atol=1e-13)
+    if return_after_cert:
+        np.testing.assert_allclose(cert[:6], c["cert"][:6], rtol=1e-9, atol=1e-13)
+    else:
+        np.testing.assert_allclose(cert, c["cert"], rtol=1e-9, atol=1e-13)
     if "s" in c:
         ff = oracle.flip_flop(A, c["k"], c["l"], c["b"], c["p"], g=c["g"], d=c["d"], seed=c["seed"])
         np.testing.assert_allclose(ff.s, c["s"], rtol=1e-12, atol=1e-14 * c["s"][0])
