@@ -119,12 +119,14 @@ struct Work {
 
 int64_t max_i(int64_t a, int64_t b) { return a > b ? a : b; }
 
-// Pivot-kernel geometry: G CTAs (<= #SMs, >= 32 columns each), columns in
+// Pivot-kernel geometry: G CTAs (<= #SMs, ~64 columns each), columns in
 // shared memory when they fit.
 void pivot_geometry(const ffb_ctx* ctx, int64_t n, int64_t s, Work& w) {
   int gmax = std::min(ctx ? ctx->sms : 148, 160);   // kPivMaxK * 32
   if (const char* ev = getenv("FFB_PIV_G")) gmax = std::max(1, std::min(gmax, atoi(ev)));
-  int G = (int)std::min<int64_t>(gmax, std::max<int64_t>(1, (n + 31) / 32));
+  // 64 columns per CTA (the register-resident maximum) when the grid allows:
+  // fewer CTAs shorten the per-step all-CTA exchange
+  int G = (int)std::min<int64_t>(gmax, std::max<int64_t>(1, (n + 63) / 64));
   int cpc = (int)((n + G - 1) / G);
   const size_t smem_all = pivots_smem_bytes((int)s, cpc, true);
   w.piv_smem = smem_all <= 200 * 1024;
