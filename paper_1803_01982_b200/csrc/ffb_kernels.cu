@@ -409,9 +409,8 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
         s_tau = tau;
         s_wpos = wpos;
         if (blockIdx.x == 0) {
-          const int64_t t = a.arr[P];
-          a.arr[P] = a.arr[wpos];
-          a.arr[wpos] = t;
+          // arr (the inverse of pos) is rebuilt from pos after the loop: no global
+          // loads on CTA 0's per-step critical path
           a.hist[j] = wpos;
           if (a.gap) a.gap[j] = (gw.r1 > 0.0 && second >= 0.0) ? (gw.r1 - second) / gw.r1 : 1.0;
         }
@@ -520,7 +519,10 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
 #undef PPROF
   if (a.prof && tid == 0)
     for (int i = 0; i < 6; ++i) atomicAdd((unsigned long long*)&a.prof[i], (unsigned long long)tp[i]);
-  for (int c = tid; c < nc; c += kPivThreads) a.pos[c0 + c] = pp[c];
+  for (int c = tid; c < nc; c += kPivThreads) {
+    a.pos[c0 + c] = pp[c];
+    a.arr[pp[c]] = c0 + c;    // arr[pos[c]] = c: every position is owned by exactly one column
+  }
 }
 
 size_t pivots_smem_bytes(int s, int cpc, bool smem_mode) {
