@@ -362,6 +362,24 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
         __syncthreads();
       }
       JPROF(1)
+      // A visit whose pairs all pass the threshold test leaves M_W unchanged
+      // (J = I): skip the rotation chain and the write-back.  This is the
+      // converged tail of the last sweeps; the test is rotation()'s.
+      __shared__ int s_active;
+      if (tid == 0) s_active = 0;
+      __syncthreads();
+      {
+        bool act = false;
+        for (int t = tid; t < 32 * 32; t += nt) {
+          const int p = t >> 5, q = t & 31;
+          if (p >= q || (r != 0 && !(p < kBS && q >= kBS))) continue;
+          const double gpq = Gs[p * kMW + q];
+          act |= gpq * gpq > tol2 * (Gs[p * kMW + p] * Gs[q * kMW + q]);
+        }
+        if (__any_sync(0xffffffffu, act) && lane == 0) s_active = 1;
+      }
+      __syncthreads();
+      const bool active = s_active != 0;
       // every round pairs all 32 local slots (16 disjoint pairs); thread (ba, bb2)
       // owns the 2x2 block (pair ba rows, pair bb2 cols) of G and of J.  Lane
       // (x & 15) of each warp computes the rotation of pair x & 15 (no broadcast
@@ -410,20 +428,20 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
         Jc = Jn;
         Jn = const_cast<double*>(tj);
       };
-      for (int t = 0; t < n_within; ++t) {
+      for (int t = 0; active && t < n_within; ++t) {
         int pa2, qa2, pb2, qb2;
         inner_pair(t, ba, n_within, pa2, qa2);
         inner_pair(t, bb2, n_within, pb2, qb2);
         step(pa2, qa2, pb2, qb2);
       }
       // cross pairs (k, kBS + (k + t) % kBS): index math without branches
-      for (int t = 0; t < n_cross; ++t) {
+      for (int t = 0; active && t < n_cross; ++t) {
         const int tt = t & (kBS - 1);
         step(ba, kBS + ((ba + tt) & (kBS - 1)), bb2, kBS + ((bb2 + tt) & (kBS - 1)));
       }
       double off = offn > 0.0 ? sqrt(offn / offd) : 0.0;
       JPROF(2)
-      apply_rows(Ms, lpad, Jc, a.M, ld, pa, pb, 0);
+      if (active) apply_rows(Ms, lpad, Jc, a.M, ld, pa, pb, 0);
       // record this visit's J for the deferred V accumulation (jacobi_v_kernel)
       {
         double* jh = a.jhist + (((size_t)sweep * (nb - 1) + r) * P + blockIdx.x) * 1024;
