@@ -481,8 +481,7 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
     QPROF(5)
     sign_lu(q, w, Ls, Us, Dd, buf);
     QPROF(10)
-    inv_upper_blk(Us, w, Ui, Sx);    // zero pivots -> zero rows
-    inv_unit_lower_blk(Ls, w, Li, Sx);
+    inv_upper_lower_blk(Us, Ls, w, Ui, Li, Sx);   // zero pivots -> zero rows of U^-1
     QPROF(11)
     for (int t = tid; t < kW * kW; t += nt) {   // Ui = D * U^-1
       const int r = t >> 6, c = t & 63;

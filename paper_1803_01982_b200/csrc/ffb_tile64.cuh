@@ -618,5 +618,65 @@ FFB_DEV bool chol_inv_blk(Tile& g, int w, double* Rs, double* Xs, double* S) {
 // arithmetic contract as sign_lu), blocked: L (unit lower) -> Ls, U (upper,
 // column-scaled by D) -> Us, D -> Dd, and the inverses U^{-1} -> Ui, L^{-1} -> Li
 // (same contract as inv_upper_blk / inv_unit_lower_blk).  S: >= 1024 doubles.
+// U^{-1} (Us upper, zero pivots -> zero rows) into Ui and L^{-1} (Ls unit lower)
+// into Li together: the eight 16x16 diagonal-block inverses run one per warp
+// from shared memory (no CTA barriers), then the block-product levels.  Same
+// contract as inv_upper_blk + inv_unit_lower_blk.  S: >= 1024 doubles.
+FFB_DEV void inv_upper_lower_blk(const double* Us, const double* Ls, int w, double* Ui, double* Li,
+                                 double* S) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int t = tid; t < 64 * 64; t += blockDim.x) {
+    const int r = t >> 6, c = t & 63;
+    if ((r >> 4) > (c >> 4)) Ui[r * kTL + c] = 0.0;
+    if ((r >> 4) < (c >> 4)) Li[r * kTL + c] = 0.0;
+  }
+  {
+    const int o = 16 * (warp & 3), c = lane & 15;
+    double x[16];
+    if (warp < 4) {
+      auto uval = [&](int r, int k) -> double {
+        if (o + r >= w || o + k >= w) return r == k ? 1.0 : 0.0;
+        return Us[(o + r) * kTL + o + k];
+      };
+#pragma unroll
+      for (int s = 15; s >= 0; --s) {
+        double acc0 = (c == s) ? 1.0 : 0.0, acc1 = 0.0;
+#pragma unroll
+        for (int k = s + 1; k < 16; ++k) {
+          if ((k - s) & 1) acc0 = fma(-uval(s, k), x[k], acc0);
+          else acc1 = fma(-uval(s, k), x[k], acc1);
+        }
+        const double d = uval(s, s);
+        x[s] = (acc0 + acc1) * (d != 0.0 ? 1.0 / d : 0.0);
+      }
+      if (lane < 16)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) Ui[(o + i) * kTL + o + c] = x[i];
+    } else {
+      auto lval = [&](int r, int k) -> double {
+        if (r == k) return 1.0;
+        if (o + r >= w || o + k >= w) return 0.0;
+        return Ls[(o + r) * kTL + o + k];
+      };
+#pragma unroll
+      for (int s = 0; s < 16; ++s) {
+        double acc0 = (c == s) ? 1.0 : 0.0, acc1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < s; ++k) {
+          if ((s - k) & 1) acc0 = fma(-lval(s, k), x[k], acc0);
+          else acc1 = fma(-lval(s, k), x[k], acc1);
+        }
+        x[s] = acc0 + acc1;
+      }
+      if (lane < 16)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) Li[(o + i) * kTL + o + c] = x[i];
+    }
+  }
+  __syncthreads();
+  inv_upper_levels(Us, Ui, S);
+  inv_unit_lower_levels(Ls, Li, S);
+}
+
 }  // namespace tile64
 }  // namespace ffb
