@@ -55,7 +55,6 @@ int occupancy_of(int cfg) {
     case 7: return occupancy<32, 32, 16, 16, 16, 4>();
     case 8: return occupancy<64, 288, 16, 32, 72, 3>();
     case 9: return occupancy<64, 144, 16, 32, 72, 3>();
-    case 11: return occupancy<128, 144, 16, 32, 72, 3>();
     default: return occupancy<64, 216, 16, 32, 72, 3>();
   }
 }
@@ -84,7 +83,7 @@ int pick_cfg(int64_t M, int64_t N, int64_t K) {
     const char* e = getenv("FFB_GEMM_CFG");
     forced = e ? atoi(e) : -1;
   }
-  if (forced >= 0) return forced > 11 ? 11 : forced;
+  if (forced >= 0) return forced > 10 ? 10 : forced;
   if (M <= 16) return 5;
   // small outputs with short K (no split-K to fill the GPU): 32 x 32 tiles so the
   // work spreads over many SMs instead of a few large tiles
@@ -95,8 +94,8 @@ int pick_cfg(int64_t M, int64_t N, int64_t K) {
   if (M <= 64) return 1;
   if (M <= 96) return 2;
   if (M >= 1024 && K < 512) return 0;   // tall, short K: many small tiles fill the SMs
-  // (configs 8, 10 and 11 -- one wide N tile per row block, the big operand read
-  // from HBM once -- measured slower than 64 x 144: FFB_GEMM_CFG only)
+  // (configs 8 and 10 -- one wide N tile per row block, the big operand read from
+  // HBM once -- and 128 x 144 / 64 x 128 tiles measured slower than 64 x 144)
   if (M >= 1024 && N > 192) return 9;   // tall, wide N (A*Yhat at l = 272 / 420): 64 x 144
                                        // tiles + stream-K: 28.4 / 30.1 TF vs 25.5 / 23.7 (128 x 96)
   if (M >= 1024) {
@@ -107,9 +106,9 @@ int pick_cfg(int64_t M, int64_t N, int64_t K) {
   return 1;
 }
 
-const Shape kShapes[12] = {{48, 64, 16},  {64, 64, 16}, {96, 64, 16},  {128, 64, 16},
+const Shape kShapes[11] = {{48, 64, 16},  {64, 64, 16}, {96, 64, 16},  {128, 64, 16},
                            {128, 96, 16}, {16, 64, 16}, {32, 64, 16},  {32, 32, 16},
-                           {64, 288, 16}, {64, 144, 16}, {64, 216, 16}, {128, 144, 16}};
+                           {64, 288, 16}, {64, 144, 16}, {64, 216, 16}};
 
 template <bool AK, bool BKC>
 cudaError_t launch_layout(int cfg, cudaStream_t st, const GemmArgs& g, dim3 grid) {
@@ -124,7 +123,6 @@ cudaError_t launch_layout(int cfg, cudaStream_t st, const GemmArgs& g, dim3 grid
     case 7: return launch_cfg<32, 32, 16, 16, 16, AK, BKC, 4>(st, g, grid);
     case 8: return launch_cfg<64, 288, 16, 32, 72, AK, BKC, 3>(st, g, grid);
     case 9: return launch_cfg<64, 144, 16, 32, 72, AK, BKC, 3>(st, g, grid);
-    case 11: return launch_cfg<128, 144, 16, 32, 72, AK, BKC, 3>(st, g, grid);
     default: return launch_cfg<64, 216, 16, 32, 72, AK, BKC, 3>(st, g, grid);
   }
 }
