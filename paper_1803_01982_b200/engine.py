@@ -231,14 +231,16 @@ def _srqr_result(out):
     np_ = out["is_numpy"]
     prm = out["params"]
     l = prm.l
-    Q = _conv(out["Q"], np_)
-    fact = PartialFactorization(R=_conv(out["R"], np_), perm=_conv(out["perm"], np_), k=l,
-                                q_dense=Q[:, :l])
+    Q = out["Q"]
+    # numpy callers get numpy R / Q / R-tilde on first access (results._HostOnAccess)
+    fact = PartialFactorization(R=out["R"], perm=_conv(out["perm"], np_), k=l, q_dense=Q[:, :l])
+    fact._host = np_
     cert = SrqrCertificate(alpha=abs(out["alpha"]), g1=out["g1"], g2=out["g2"],
                            swaps=out["swaps"], tau_bound=out["tau"],
                            tau_hat_bound=out["tau_hat"])
-    return SrqrResult(fact=fact, cert=cert, r22_norm_estimate=out["r22"],
-                      rtilde=_conv(out["rtilde"], np_), q_ext=Q)
+    res = SrqrResult(fact=fact, cert=cert, r22_norm_estimate=out["r22"], rtilde=out["rtilde"], q_ext=Q)
+    res._host = np_
+    return res
 
 
 def flip_flop_srqr(A, k, l=None, b=32, p=5, epsilon=0.5, g=2.0, d=None, seed=0, device=None,

@@ -83,9 +83,29 @@ class WYFactor:
         return C - Y @ (TT @ (Y.T @ C))
 
 
+class _HostOnAccess:
+    """Large factor arrays of a numpy-in call stay in HBM until first read, then
+    are copied to the host once (numpy out, like the reference): a caller that
+    only uses u, s, v (the HOSVD / SVT callers, tensor.py:114, nuclear.py:74)
+    never pays the PCIe transfer of R, Q and R-tilde."""
+
+    _lazy_fields = ()
+    _host = False
+
+    def __getattribute__(self, name):
+        v = object.__getattribute__(self, name)
+        if name in type(self)._lazy_fields and hasattr(v, "detach") and \
+                object.__getattribute__(self, "_host"):
+            v = v.detach().cpu().numpy()
+            object.__setattr__(self, name, v)
+        return v
+
+
 @dataclass
-class PartialFactorization:
+class PartialFactorization(_HostOnAccess):
     """A[:, perm] ~ Q[:, :k] @ R with R k-by-n."""
+
+    _lazy_fields = ("R", "q_dense")
 
     R: object
     perm: object
@@ -115,7 +135,9 @@ class SrqrCertificate:
 
 
 @dataclass
-class SrqrResult:
+class SrqrResult(_HostOnAccess):
+    _lazy_fields = ("rtilde", "q_ext")
+
     fact: PartialFactorization
     cert: SrqrCertificate
     r22_norm_estimate: float
