@@ -315,6 +315,15 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
       // fresh Gram G = M_W^T M_W: warp w sums rows [w*lpad/8, (w+1)*lpad/8) for all
       // 16 output tiles (16 independent DMMA chains); fixed-order two-level reduce
       {
+        // Round 0 of a sweep: the full Gram, upper tiles only (i <= j, mirrored).
+        // Later rounds: only the fresh cross block M_a^T M_b (4 of the 16 8x8
+        // tiles); the diagonal blocks are the rotated ones the previous owners of
+        // blocks a and b left in gdiag (exact Grams of the current columns up to
+        // the rounding of <= 16 two-sided updates, reset every sweep).  The
+        // rotations stay exactly orthogonal whatever G they were computed from,
+        // and sigma comes from fresh column norms, so only the rotation angles
+        // see that rounding.
+        const bool cross_only = r > 0;
         const int fr = lane >> 2, fk = lane & 3;
         double acc[4][4][2];
 #pragma unroll
@@ -322,21 +331,33 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
         const int kr = lpad >> 3;                 // rows per warp (multiple of 8)
-        for (int k0 = warp * kr; k0 < (warp + 1) * kr; k0 += 4) {
-          double f[4];
+        if (cross_only) {
+          for (int k0 = warp * kr; k0 < (warp + 1) * kr; k0 += 4) {
+            double f[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) f[i] = Ms[(k0 + fk) * kMW + 8 * i + fr];
+            for (int i = 0; i < 4; ++i) f[i] = Ms[(k0 + fk) * kMW + 8 * i + fr];
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < 2; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], f[i], f[j]);
+              for (int j = 2; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], f[i], f[j]);
+          }
+        } else {
+          for (int k0 = warp * kr; k0 < (warp + 1) * kr; k0 += 4) {
+            double f[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) f[i] = Ms[(k0 + fk) * kMW + 8 * i + fr];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+              for (int j = i; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], f[i], f[j]);
+          }
         }
         double* pw = part + (warp & 3) * 32 * 33;
         if (warp >= 4) {
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+            for (int j = i; j < 4; ++j)
 #pragma unroll
               for (int h = 0; h < 2; ++h) pw[(8 * i + fr) * 33 + 8 * j + 2 * fk + h] = acc[i][j][h];
         }
@@ -345,7 +366,7 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+            for (int j = i; j < 4; ++j)
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 double& d = pw[(8 * i + fr) * 33 + 8 * j + 2 * fk + h];
@@ -353,10 +374,18 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
               }
         }
         __syncthreads();
+        const double* da = a.gdiag + (size_t)pa * kBS * kBS;
+        const double* db = a.gdiag + (size_t)pb * kBS * kBS;
         for (int t = tid; t < 32 * 32; t += nt) {
           const int rr = t >> 5, c = t & 31;
-          const int o = rr * 33 + c;
-          Gs[rr * kMW + c] = (part[o] + part[32 * 33 + o]) + (part[2 * 32 * 33 + o] + part[3 * 32 * 33 + o]);
+          const int ru = rr < c ? rr : c, cu = rr < c ? c : rr;   // upper-triangle source
+          const int o = ru * 33 + cu;
+          double g;
+          if (cross_only && (rr < kBS) == (c < kBS))
+            g = rr < kBS ? da[rr * kBS + c] : db[(rr - kBS) * kBS + (c - kBS)];
+          else
+            g = (part[o] + part[32 * 33 + o]) + (part[2 * 32 * 33 + o] + part[3 * 32 * 33 + o]);
+          Gs[rr * kMW + c] = g;
           Js[rr * kMW + c] = rr == c ? 1.0 : 0.0;
         }
         __syncthreads();
@@ -440,6 +469,16 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
         step(ba, kBS + ((ba + tt) & (kBS - 1)), bb2, kBS + ((bb2 + tt) & (kBS - 1)));
       }
       double off = offn > 0.0 ? sqrt(offn / offd) : 0.0;
+      // the rotated diagonal blocks travel with their columns to the next owners
+      {
+        double* da = a.gdiag + (size_t)pa * kBS * kBS;
+        double* db = a.gdiag + (size_t)pb * kBS * kBS;
+        for (int t = tid; t < 2 * kBS * kBS; t += nt) {
+          const int blk = t / (kBS * kBS), e = t - blk * kBS * kBS, rr = e / kBS, c = e - rr * kBS;
+          const int o = blk * kBS;
+          (blk ? db : da)[e] = Gc[(o + rr) * kMW + o + c];
+        }
+      }
       JPROF(2)
       if (active) apply_rows(Ms, lpad, Jc, a.M, ld, pa, pb, 0);
       // record this visit's J for the deferred V accumulation (jacobi_v_kernel)
@@ -650,8 +689,9 @@ static void jacobi_geometry(int l, int& nb, int& lpad, int& ncp) {
 size_t jacobi_work_doubles(int l, int max_sweeps) {
   int nb, lpad, ncp;
   jacobi_geometry(l, nb, lpad, ncp);
-  // Mrm, Vrm, norms, J history (max_sweeps x rounds x pairs x 32 x 32)
-  return 2 * (size_t)lpad * ncp + (size_t)lpad + (size_t)max_sweeps * (nb - 1) * (nb / 2) * 1024;
+  // Mrm, Vrm, norms, J history (max_sweeps x rounds x pairs x 32 x 32), diagonal Gram blocks
+  return 2 * (size_t)lpad * ncp + (size_t)lpad + (size_t)max_sweeps * (nb - 1) * (nb / 2) * 1024 +
+         (size_t)nb * kBS * kBS;
 }
 
 cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, const double* M, int64_t ldm, int l,
@@ -665,6 +705,7 @@ cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, const double* M, int64_t
   double* Vrm = Mrm + (size_t)lpad * ncp;
   double* nrm = Vrm + (size_t)lpad * ncp;
   double* jhist = nrm + lpad;
+  double* gdiag = jhist + (size_t)max_sweeps * (nb - 1) * P * 1024;
   int inner = 1;
   if (const char* e = getenv("FFB_JACOBI_INNER")) inner = atoi(e);
   if (inner < 1) inner = 1;
@@ -674,7 +715,7 @@ cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, const double* M, int64_t
   const size_t smem = sizeof(double) * ((size_t)lpad * kMW + 4 * 32 * kMW + 4 * 32 * 33);
   if (smem > kSmemMax) return cudaErrorInvalidValue;   // l > ~560 not supported
   JacobiArgs a{Mrm, jhist, ncp, l, lpad, nb, 1e-15 * sqrt((double)l), max_sweeps, bar, offmax,
-               sweeps, inner, prof, P, Vrm, bar + 2, 0};
+               sweeps, inner, prof, P, Vrm, bar + 2, 0, gdiag};
   const bool cluster = P <= 16 && getenv("FFB_JACOBI_NOCLUSTER") == nullptr;
   void* kern = cluster ? (void*)jacobi_kernel<true> : (void*)jacobi_kernel<false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);

@@ -21,6 +21,7 @@ struct JacobiArgs {
   double* V;         // lpad x ncp row-major V (written by the replay)
   uint32_t* progress;  // [0] rounds published, [1] total rounds + 1 when done
   int fused;
+  double* gdiag;     // [nb][kBS x kBS] diagonal Gram blocks carried between rounds
 };
 
 int jacobi_block_size(int l);
