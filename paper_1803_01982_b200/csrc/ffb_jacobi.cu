@@ -278,6 +278,9 @@ template <bool CLUSTER>
 __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int lpad = a.lpad, nb = a.nb;
+  // rows >= l of M are zero padding: stage, Gram and apply stop at l rounded up
+  // to 32 (whole 4-row k-steps for each of the 8 warps)
+  const int lrows = ((a.l + 31) & ~31) < lpad ? ((a.l + 31) & ~31) : lpad;
   double* Ms = sm;                        // lpad x kMW : M_W
   double* Gs = Ms + (size_t)lpad * kMW;   // 32 x kMW
   double* Js = Gs + 32 * kMW;
@@ -307,7 +310,7 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
     if (tid == 0) s_off = 0.0;
     for (int r = 0; r < nb - 1; ++r) {
       const int pa = rr_player(blockIdx.x, r, nb), pb = rr_player(nb - 1 - blockIdx.x, r, nb);
-      stage_rows_async(Ms, a.M, ld, pa, pb, 0, lpad);
+      stage_rows_async(Ms, a.M, ld, pa, pb, 0, lrows);
       cp_async_commit();
       cp_async_wait<0>();
       __syncthreads();
@@ -330,7 +333,7 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
         for (int i = 0; i < 4; ++i)
 #pragma unroll
           for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-        const int kr = lpad >> 3;                 // rows per warp (multiple of 8)
+        const int kr = lrows >> 3;                // rows per warp (multiple of 4)
         if (cross_only) {
           for (int k0 = warp * kr; k0 < (warp + 1) * kr; k0 += 4) {
             double f[4];
@@ -480,7 +483,7 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
         }
       }
       JPROF(2)
-      if (active) apply_rows(Ms, lpad, Jc, a.M, ld, pa, pb, 0);
+      if (active) apply_rows(Ms, lrows, Jc, a.M, ld, pa, pb, 0);
       // record this visit's J for the deferred V accumulation (jacobi_v_kernel)
       {
         double* jh = a.jhist + (((size_t)sweep * (nb - 1) + r) * P + blockIdx.x) * 1024;
