@@ -5,8 +5,8 @@ Drop-in for the reference ``ffsrqr`` hot path: ``flip_flop_srqr``, ``srqr``,
 (IALM) solvers.  Compute runs in hand-written CUDA (libffb200.so, C ABI in
 include/ffb200.h); this package is host glue only and has no CPU fallback.
 """
-from .errors import (CertificationError, DimensionError, EngineUnavailable, NumericalError,
-                     SingularTrailingBlockError)
+from .errors import (CertificationError, DimensionError, EngineUnavailable, NonFiniteInputError,
+                     NumericalError, SingularTrailingBlockError)
 from .results import (ApproxSvd, PartialFactorization, SketchParams, SrqrCertificate, SrqrResult,
                       WYFactor, flip_flop_flop_formula)
 from .engine import flip_flop_srqr, rsisvd, srqr, trqrcp
@@ -14,7 +14,8 @@ from .engine import flip_flop_srqr, rsisvd, srqr, trqrcp
 __version__ = "0.1.0"
 
 __all__ = [
-    "ApproxSvd", "CertificationError", "DimensionError", "EngineUnavailable", "NumericalError",
+    "ApproxSvd", "CertificationError", "DimensionError", "EngineUnavailable", "NonFiniteInputError",
+    "NumericalError",
     "PartialFactorization", "SingularTrailingBlockError", "SketchParams", "SrqrCertificate",
     "SrqrResult", "WYFactor", "flip_flop_flop_formula", "flip_flop_srqr", "rsisvd", "srqr",
     "trqrcp",

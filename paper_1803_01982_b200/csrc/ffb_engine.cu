@@ -505,6 +505,7 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
   // B = Omega * A (Omega row-major s x m: A-operand with contiguous k)
   e.gemm(s, n, m, 1.0, omega, m, true, A, lda, true, 0.0, w.B, s);
   e.ok(launch_colsq(st, A, lda, m, n, w.colsq));
+  e.ok(launch_finite_check(st, w.colsq, (size_t)n, w.status));   // NaN / Inf anywhere in A
   e.ok(launch_iota2(st, w.arr, w.pos, n));
   e.memset2d(w.Y, m, m, l);
   e.memset2d(w.T, l, l, l);

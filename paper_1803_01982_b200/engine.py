@@ -25,8 +25,8 @@ import threading
 import numpy as np
 
 from . import _capi, rng
-from .errors import (CertificationError, DimensionError, EngineUnavailable, NumericalError,
-                     SingularTrailingBlockError)
+from .errors import (CertificationError, DimensionError, EngineUnavailable, NonFiniteInputError,
+                     NumericalError, SingularTrailingBlockError)
 from .results import (ApproxSvd, PartialFactorization, SketchParams, SrqrCertificate, SrqrResult,
                       WYFactor)
 
@@ -217,6 +217,8 @@ def run(A, params: SketchParams, mode, device=None, trace_gaps=False):
         if rc == _capi.FFB_ERR_CERTIFICATION:
             raise CertificationError(msg, result=_srqr_result(out))
         if rc == _capi.FFB_ERR_NUMERICAL:
+            if out["status_bits"] & 1:          # kStNonFinite: NaN / Inf in A or a factor
+                raise NonFiniteInputError(msg)
             raise NumericalError(msg)
         raise RuntimeError(f"ffb_run failed ({rc}): {msg}")
 

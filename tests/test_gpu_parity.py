@@ -225,3 +225,20 @@ def test_torch_input_stays_on_device(ffb):
     ap = ffb.flip_flop_srqr(At, c["k"], l=c["l"], b=c["b"], p=c["p"], seed=c["seed"])
     assert ap.u.is_cuda and ap.v.is_cuda
     np.testing.assert_allclose(ap.s.cpu().numpy(), c["s"], rtol=RTOL_SV)
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf])
+def test_non_finite_input_raises(ffb, bad):
+    """NaN / Inf in A: the reference fails with scipy's ValueError("array must not
+    contain infs or NaNs") (sketch.py:75-83); the engine raises
+    NonFiniteInputError, which is both that ValueError and a NumericalError, in
+    every mode."""
+    A = np.random.default_rng(0).standard_normal((60, 40))
+    A[3, 5] = bad
+    for call in (lambda: ffb.flip_flop_srqr(A, 5, l=8),
+                 lambda: ffb.srqr(A, ffb.SketchParams(k=5, l=8)),
+                 lambda: ffb.trqrcp(A, ffb.SketchParams(k=5, l=8))):
+        with pytest.raises(ValueError):
+            call()
+        with pytest.raises(ffb.NumericalError):
+            call()
