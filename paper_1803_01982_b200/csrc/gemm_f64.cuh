@@ -71,8 +71,10 @@ struct TileLoader {
   int kk[kPer];      // k index inside the tile of the unit's first element
   int rr[kPer];      // row (M or N) index of the unit (first element)
   bool live[kPer];
+  bool all_live;     // every row of the tile is in range (interior tiles)
 
   FFB_DEV void init(const double* base, int64_t ld, int64_t r0, int64_t rows, int64_t k0, int tid) {
+    all_live = r0 + R <= rows;
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
       const int idx = tid + u * NT;
@@ -118,6 +120,18 @@ struct TileLoader {
       }
     }
     (void)ld;
+  }
+  // interior tile with a full k-tile: no per-unit bounds, no zero-fill sizes
+  FFB_DEV void load_full(double* smem) {
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      if (kUnits % NT != 0 && u * NT + (int)threadIdx.x >= kUnits) continue;
+      double* dst = smem + soff[u];
+      if (VEC2)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(g[u]));
+      else
+        cp_async8(dst, g[u], true);
+    }
   }
   FFB_DEV void advance(int64_t ld) {
 #pragma unroll
@@ -195,8 +209,10 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
     const int64_t k0 = kbeg + (int64_t)fetched * BK;
     const int64_t krem = kend - k0;
     const int kvalid = krem < BK ? (int)krem : BK;
-    la.load(As + stage * Cfg::kAStage, kvalid, i0, g.M, g.lda);
-    lb.load(Bs + stage * Cfg::kBStage, kvalid, j0, g.N, g.ldb);
+    if (kvalid == BK && la.all_live) la.load_full(As + stage * Cfg::kAStage);
+    else la.load(As + stage * Cfg::kAStage, kvalid, i0, g.M, g.lda);
+    if (kvalid == BK && lb.all_live) lb.load_full(Bs + stage * Cfg::kBStage);
+    else lb.load(Bs + stage * Cfg::kBStage, kvalid, j0, g.N, g.ldb);
     la.advance(g.lda);
     lb.advance(g.ldb);
     ++fetched;
@@ -330,15 +346,34 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
       }
       __syncthreads();
       const int ns = (int)(b1 - b0 + 1);
-      for (int e = tid; e < BM * BN; e += NT) {
-        const int r = e % BM, c = e / BM;
-        const int64_t gi = i0 + r, gj = j0 + c;
-        if (gi >= g.M || gj >= g.N) continue;
-        double sum = 0.0;
-        for (int q = 0; q < ns; ++q) sum += __ldcg(segp[q] + e);
-        double* cp = g.C + gi + gj * g.ldc;
-        const double v = g.alpha * sum;
-        *cp = g.beta == 0.0 ? v : v + g.beta * (*cp);
+      // 8 elements per thread per pass: their segment loads are in flight together
+      // (each element still sums its segments in ascending order)
+      constexpr int EPT = (BM * BN + NT - 1) / NT;
+      for (int e0 = 0; e0 < EPT; e0 += 8) {
+        double sum[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sum[u] = 0.0;
+        for (int q = 0; q < ns; ++q) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = tid + (e0 + u) * NT;
+            v[u] = (e0 + u < EPT && e < BM * BN) ? __ldcg(segp[q] + e) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) sum[u] += v[u];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = tid + (e0 + u) * NT;
+          if (e0 + u >= EPT || e >= BM * BN) continue;
+          const int r = e % BM, c = e / BM;
+          const int64_t gi = i0 + r, gj = j0 + c;
+          if (gi >= g.M || gj >= g.N) continue;
+          double* cp = g.C + gi + gj * g.ldc;
+          const double v = g.alpha * sum[u];
+          *cp = g.beta == 0.0 ? v : v + g.beta * (*cp);
+        }
       }
       if (tid == 0) g.sk_cnt[sk_tile] = 0u;
     }
