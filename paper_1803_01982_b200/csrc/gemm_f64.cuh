@@ -41,7 +41,9 @@ struct GemmArgs {
 template <int BM, int BK>
 struct APad {
   static constexpr int kc = BK + ((4 - BK % 16) + 16) % 16;        // (BK+pad) % 16 == 4
-  static constexpr int mc = BM + ((8 - BM % 16) + 16) % 16;        // (BM+pad) % 16 == 8
+  // (BM+pad) % 16 == 4: a 64-bit fragment load's half-warp (4 k-rows x 4 rows)
+  // then hits 16 distinct bank pairs (8 mod 16 put k-rows 0 and 2 on one bank)
+  static constexpr int mc = BM + ((4 - BM % 16) + 16) % 16;
 };
 
 template <int BM, int BN, int BK, int WM, int WN, bool A_KC, bool B_KC, int STAGES>
@@ -72,6 +74,7 @@ struct TileLoader {
   int rr[kPer];      // row (M or N) index of the unit (first element)
   bool live[kPer];
   bool all_live;     // every row of the tile is in range (interior tiles)
+  int nbf[kPer];     // cp.async source bytes of a full k-tile (row tail zero-filled)
 
   FFB_DEV void init(const double* base, int64_t ld, int64_t r0, int64_t rows, int64_t k0, int tid) {
     all_live = r0 + R <= rows;
@@ -94,6 +97,7 @@ struct TileLoader {
       const int64_t gr = r0 + r;
       live[u] = live[u] && gr < rows;
       g[u] = base + (live[u] ? (KC ? (k0 + k) + gr * ld : gr + (k0 + k) * ld) : 0);
+      nbf[u] = !live[u] ? 0 : (VEC2 ? ((KC || gr + 1 < rows) ? 16 : 8) : 8);
       soff[u] = KC ? (uint32_t)(r * LD + k) : (uint32_t)(k * LD + r);
     }
   }
@@ -131,6 +135,19 @@ struct TileLoader {
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(g[u]));
       else
         cp_async8(dst, g[u], true);
+    }
+  }
+  // full k-tile of an edge tile: per-unit byte counts fixed at init
+  FFB_DEV void load_kfull(double* smem) {
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      if (kUnits % NT != 0 && u * NT + (int)threadIdx.x >= kUnits) continue;
+      double* dst = smem + soff[u];
+      if (VEC2)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)),
+                     "l"(nbf[u] ? g[u] : g[0]), "r"(nbf[u]));
+      else
+        cp_async8(dst, nbf[u] ? g[u] : g[0], nbf[u] != 0);
     }
   }
   FFB_DEV void advance(int64_t ld) {
@@ -209,10 +226,15 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
     const int64_t k0 = kbeg + (int64_t)fetched * BK;
     const int64_t krem = kend - k0;
     const int kvalid = krem < BK ? (int)krem : BK;
-    if (kvalid == BK && la.all_live) la.load_full(As + stage * Cfg::kAStage);
-    else la.load(As + stage * Cfg::kAStage, kvalid, i0, g.M, g.lda);
-    if (kvalid == BK && lb.all_live) lb.load_full(Bs + stage * Cfg::kBStage);
-    else lb.load(Bs + stage * Cfg::kBStage, kvalid, j0, g.N, g.ldb);
+    if (kvalid == BK) {
+      if (la.all_live) la.load_full(As + stage * Cfg::kAStage);
+      else la.load_kfull(As + stage * Cfg::kAStage);
+      if (lb.all_live) lb.load_full(Bs + stage * Cfg::kBStage);
+      else lb.load_kfull(Bs + stage * Cfg::kBStage);
+    } else {
+      la.load(As + stage * Cfg::kAStage, kvalid, i0, g.M, g.lda);
+      lb.load(Bs + stage * Cfg::kBStage, kvalid, j0, g.N, g.ldb);
+    }
     la.advance(g.lda);
     lb.advance(g.ldb);
     ++fetched;
