@@ -20,6 +20,27 @@ def partition(n_problems, world, rank):
     return range(lo, hi)
 
 
+_pools = {}
+_pools_lock = threading.Lock()
+
+
+def _pool(dev, n_streams):
+    """Persistent (streams, host threads) per device and width: the engine keeps
+    its workspace and pinned staging per host thread, so reusing the threads keeps
+    cudaMalloc / cudaMallocHost (both synchronising) out of every later batch."""
+    import torch
+
+    key = (dev.index, n_streams)
+    with _pools_lock:
+        ent = _pools.get(key)
+        if ent is None:
+            streams = [torch.cuda.Stream(device=dev) for _ in range(n_streams)]
+            ent = (streams, ThreadPoolExecutor(max_workers=n_streams), threading.Lock(),
+                   list(range(n_streams)))
+            _pools[key] = ent
+        return ent
+
+
 def run_streams(problems, solve, n_streams=4, device=None):
     """Run `solve(problem)` for every problem on `n_streams` CUDA streams.
 
@@ -28,9 +49,9 @@ def run_streams(problems, solve, n_streams=4, device=None):
     import torch
 
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-    streams = [torch.cuda.Stream(device=dev) for _ in range(max(1, n_streams))]
-    lock = threading.Lock()
-    free = list(range(len(streams)))
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    streams, ex, lock, free = _pool(dev, max(1, n_streams))
 
     def _one(p):
         with lock:
@@ -44,8 +65,7 @@ def run_streams(problems, solve, n_streams=4, device=None):
             with lock:
                 free.append(sid)
 
-    with ThreadPoolExecutor(max_workers=len(streams)) as ex:
-        return list(ex.map(_one, problems))
+    return list(ex.map(_one, problems))
 
 
 def gather_slots(local_slots, n_problems, slot_shape, rank, world, device, dtype=None):
