@@ -88,12 +88,22 @@ int pick_cfg(int64_t M, int64_t N, int64_t K) {
   // small outputs with short K (no split-K to fill the GPU): 32 x 32 tiles so the
   // work spreads over many SMs instead of a few large tiles
   const int64_t tiles64 = ((M + 63) / 64) * ((N + 63) / 64);
-  if (tiles64 < 148 && K < 1024) return 7;
+  static int smallk = -2;  // FFB_GEMM_SMALL: tile config of small short-K products (tuning)
+  if (smallk == -2) {
+    const char* e = getenv("FFB_GEMM_SMALL");
+    smallk = e ? atoi(e) : 7;
+  }
+  if (tiles64 < 148 && K < 1024) return smallk;
   if (M <= 32) return 6;
   if (M <= 48) return 0;
   if (M <= 64) return 1;
   if (M <= 96) return 2;
-  if (M >= 1024 && K < 512) return 0;   // tall, short K: many small tiles fill the SMs
+  static int tallk = -2;   // FFB_GEMM_TALLK: tile config of tall short-K products (tuning)
+  if (tallk == -2) {
+    const char* e = getenv("FFB_GEMM_TALLK");
+    tallk = e ? atoi(e) : 0;
+  }
+  if (M >= 1024 && K < 512) return tallk;   // tall, short K: many small tiles fill the SMs
   // (configs 8 and 10 -- one wide N tile per row block, the big operand read from
   // HBM once -- and 128 x 144 / 64 x 128 tiles measured slower than 64 x 144)
   if (M >= 1024 && N > 192) return 9;   // tall, wide N (A*Yhat at l = 272 / 420): 64 x 144
