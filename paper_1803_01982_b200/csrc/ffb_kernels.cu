@@ -483,20 +483,47 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
         if (sub == 0) pp[c] = p;
         if (p <= P) continue;
         double* col = W + (size_t)c * sP;
+        // rows j.. of the column in registers (s <= 128: <= 32 per thread): one L2
+        // round trip per column for the load, none for row j or the guard recompute
+        constexpr int kSQ = 32;
+        double x[kSQ];
+#pragma unroll
+        for (int q = 0; q < kSQ; ++q) {
+          const int i = j + sub + 4 * q;
+          x[q] = i < s ? col[i] : 0.0;
+        }
         if (tau != 0.0) {
-          double wsum = 0.0;
-          for (int i = j + sub; i < s; i += 4) wsum = fma(vv[i], col[i], wsum);
+          double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+          for (int q = 0; q < kSQ; ++q) {
+            const int i = j + sub + 4 * q;
+            if (i < s) {
+              if (q & 1) w1 = fma(vv[i], x[q], w1);
+              else w0 = fma(vv[i], x[q], w0);
+            }
+          }
+          double wsum = w0 + w1;
           wsum += __shfl_xor_sync(gmask, wsum, 1);
           wsum += __shfl_xor_sync(gmask, wsum, 2);
           const double wt = wsum * tau;
-          for (int i = j + sub; i < s; i += 4) col[i] = fma(-vv[i], wt, col[i]);
+#pragma unroll
+          for (int q = 0; q < kSQ; ++q) {
+            const int i = j + sub + 4 * q;
+            if (i < s) {
+              x[q] = fma(-vv[i], wt, x[q]);
+              col[i] = x[q];
+            }
+          }
         }
-        __syncwarp(gmask);
-        const double rj = col[j];
+        const double rj = __shfl_sync(gmask, x[0], lane & ~3);   // row j: sub 0, q 0
         double rr = r[c] - rj * rj;
         if (rr < 1e-8 * r0[c] || rr < 0.0) {
           double t = 0.0;
-          for (int i = j + 1 + sub; i < s; i += 4) t = fma(col[i], col[i], t);
+#pragma unroll
+          for (int q = 0; q < kSQ; ++q) {
+            const int i = j + sub + 4 * q;
+            if (i > j && i < s) t = fma(x[q], x[q], t);
+          }
           t += __shfl_xor_sync(gmask, t, 1);
           t += __shfl_xor_sync(gmask, t, 2);
           rr = t > 0.0 ? t : 0.0;
