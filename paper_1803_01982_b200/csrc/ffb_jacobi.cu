@@ -651,13 +651,19 @@ __global__ void jacobi_norms_kernel(const double* Mrm, int64_t ld, int l, int lp
   }
   __syncthreads();
   const double unscale = ldexp(1.0, sweeps[1]);
+  // total order even for NaN norms (non-finite input, reported afterwards by the
+  // status word): NaN sorts last, so `order` is always a permutation
+  auto key = [](double v) { return v == v ? v : -1.0; };
   for (int j = tid; j < l; j += blockDim.x) {
     int rank = 0;
-    const double sj = nrm[j];
-    for (int q = 0; q < l; ++q) rank += (nrm[q] > sj) || (nrm[q] == sj && q < j);
+    const double sj = key(nrm[j]);
+    for (int q = 0; q < l; ++q) {
+      const double kq = key(nrm[q]);
+      rank += (kq > sj) || (kq == sj && q < j);
+    }
     order[rank] = j;
-    sig[rank] = sj * unscale;
-    nrm_out[rank] = sj;
+    sig[rank] = nrm[j] * unscale;
+    nrm_out[rank] = nrm[j];
   }
 }
 
