@@ -162,7 +162,7 @@ size_t carve(const ffb_ctx* ctx, const Dims& D, void* base, size_t cap, Work& w)
   w.Gm = b.take<double>(kPanelW * kPanelW);
   w.ppart = b.take<double>((size_t)(ctx ? ctx->sms : 160) * kPanelW * kPanelW);
   w.pbar = b.take<uint32_t>(4);
-  w.Rinv = b.take<double>(kPanelW * kPanelW);
+  w.Rinv = b.take<double>(max_i(kPanelW * kPanelW, bmax * bmax));
   w.Ut = b.take<double>(kPanelW * kPanelW);
   w.Dv = b.take<double>(kPanelW);
   w.Rb = b.take<double>(bmax * bmax);
@@ -292,6 +292,22 @@ struct Eng {
     okm(cudaMemset2DAsync(p, ld * sizeof(double), 0, rows * sizeof(double), cols, st));
   }
 
+  // Rinv (ld bb) = Rb^{-1} for the upper-triangular bb x bb block factor (ld bb):
+  // one tile kernel for bb <= 64, else the 2 x 2 block form
+  // [A B; 0 C]^{-1} = [A^-1, -A^-1 B C^-1; 0, C^-1] with two tile inverses + 2 GEMMs
+  void tri_inverse(const double* Rb, int64_t bb, double* Rinv) {
+    if (bb <= kPanelW) {
+      ok(launch_triinv_upper(st, Rb, bb, (int)bb, Rinv, bb, w.status));
+      return;
+    }
+    const int64_t h = kPanelW, t = bb - kPanelW;
+    ok(launch_triinv_upper(st, Rb, bb, (int)h, Rinv, bb, w.status));
+    ok(launch_triinv_upper(st, Rb + h + h * bb, bb, (int)t, Rinv + h + h * bb, bb, w.status));
+    memset2d(Rinv + h, bb, t, h);
+    gemm(h, t, t, 1.0, Rb + h * bb, bb, false, Rinv + h + h * bb, bb, true, 0.0, w.S2, h);
+    gemm(h, t, h, -1.0, Rinv, bb, false, w.S2, h, true, 0.0, Rinv + h * bb, bb);
+  }
+
   // Householder panel (Mp x wb, wb <= 64): one fused cooperative kernel
   // (shifted CholeskyQR3 + Householder reconstruction, ffb_panel.cu).
   void recon(const double* Xp, int64_t Mp, int wb, int64_t ldx, double* Yp, int64_t ldy,
@@ -362,7 +378,7 @@ bool validate(const Dims& D) {
   if (D.b < 1 || D.p < 0 || D.s > D.m) return false;
   if (D.d < 1 || D.d > D.l) return false;
   if (D.mode != FFB_MODE_TRQRCP && D.l + 1 > std::min(D.m, D.n)) return false;
-  if (D.b > 64) return false;  // panel kernels are sized for b <= 64
+  if (D.b > 128) return false; // block inverse covers b <= 128 (and s = b + p <= 128 below)
   if (D.s > 128) return false; // pivot kernel holds one sketch column per warp (s <= 128)
   if (D.n >= 2147483647LL) return false;  // pivot exchange carries 32-bit positions
   if (D.mode == FFB_MODE_FLIPFLOP && D.l > 512) return false;  // Jacobi SVD: <= 16 block pairs
@@ -545,7 +561,7 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
     // sketch update B[:, trailing] -= (B_piv R11^{-1}) R12
     if (e1 < n) {
       e.ok(launch_gather_cols(st, w.B, s, s, w.arr + j0, bb, w.Bp, s));
-      e.ok(launch_triinv_upper(st, w.Rb, bb, (int)bb, w.Rinv, w.status));
+      e.tri_inverse(w.Rb, bb, w.Rinv);
       e.gemm(s, bb, bb, 1.0, w.Bp, s, false, w.Rinv, bb, true, 0.0, w.Z, s);
       e.gemm(s, n, bb, -1.0, w.Z, s, false, w.R + j0, L1, true, 1.0, w.B, s);
     }

@@ -1010,7 +1010,7 @@ cudaError_t launch_fix_rrows(cudaStream_t st, double* R, int64_t ldr, int64_t j0
 // reference would fall back to lstsq there (ffsrqr/sketch.py:75-83).
 __global__ void __launch_bounds__(256) triinv_upper_kernel(const double* __restrict__ Rb,
                                                            int64_t ldrb, int w, double* Rinv,
-                                                           uint32_t* status) {
+                                                           int64_t ldo, uint32_t* status) {
   using namespace tile64;
   extern __shared__ __align__(16) double dsm[];
   double* U = dsm;                 // 64 x kTL
@@ -1028,20 +1028,20 @@ __global__ void __launch_bounds__(256) triinv_upper_kernel(const double* __restr
   inv_upper_blk(U, w, X, S);
   for (int t = tid; t < w * w; t += nt) {
     const int i = t % w, j = t / w;
-    Rinv[i + j * w] = X[i * kTL + j];
+    Rinv[i + j * ldo] = X[i * kTL + j];
   }
   if (tid == 0 && zp) atomicOr(status, kStZeroPivot);
 }
 
 cudaError_t launch_triinv_upper(cudaStream_t st, const double* Rb, int64_t ldrb, int w,
-                                double* Rinv, uint32_t* status) {
+                                double* Rinv, int64_t ldo, uint32_t* status) {
   static bool init = false;
   constexpr int kSm = (2 * 64 * tile64::kTL + 1024) * sizeof(double);
   if (!init) {
     cudaFuncSetAttribute(triinv_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSm);
     init = true;
   }
-  triinv_upper_kernel<<<1, 256, kSm, st>>>(Rb, ldrb, w, Rinv, status);
+  triinv_upper_kernel<<<1, 256, kSm, st>>>(Rb, ldrb, w, Rinv, ldo, status);
   FFB_LAUNCH_CHECK();
 }
 

@@ -82,7 +82,7 @@ cudaError_t launch_signlu(cudaStream_t st, const double* Qtop, int64_t ldq, int 
 cudaError_t launch_fix_rrows(cudaStream_t st, double* R, int64_t ldr, int64_t j0, int bb,
                              const int64_t* arr, const double* Rb, int64_t ldrb);
 cudaError_t launch_triinv_upper(cudaStream_t st, const double* Rb, int64_t ldrb, int w,
-                                double* Rinv, uint32_t* status);
+                                double* Rinv, int64_t ldo, uint32_t* status);
 
 // SRQR.
 cudaError_t launch_rinit(cudaStream_t st, const double* B, int64_t ldb, int s, const int64_t* arr,

@@ -148,8 +148,8 @@ def run(A, params: SketchParams, mode, device=None, trace_gaps=False):
         prm = params.resolve(m, n)
         if mode != _capi.FFB_MODE_TRQRCP and prm.l + 1 > min(m, n):
             raise DimensionError(f"srqr needs l+1 <= min(m,n); got l={prm.l}, min={min(m, n)}")
-        if prm.b > 64:
-            raise DimensionError("the B200 engine supports block sizes b <= 64")
+        if prm.b > 128:
+            raise DimensionError("the B200 engine supports block sizes b <= 128")
         if prm.b + prm.p > 128:
             raise DimensionError("the B200 engine supports sketch sizes b + p <= 128")
         lib = _capi.load()

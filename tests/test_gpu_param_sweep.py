@@ -1,5 +1,5 @@
 """GPU vs the CPU oracle over a parameter grid the goldens do not cover: block
-sizes b in {8, 16, 24, 48, 64}, oversampling p in {0, 3, 16}, wide and tall
+sizes b in {8, 16, 24, 48, 64, 96, 128}, oversampling p in {0, 3, 16}, wide and tall
 shapes, l = min(m, n) - 1 (the reference's upper limit, svd.py:53-55), d and g
 variants and the swap path.  Same bar as the golden tests: identical pivots
 (or a certified near-tie), sigma / diag(L) / certificate within 1e-10
@@ -22,6 +22,8 @@ CASES = [
     (256, 256, 50, 60, 32, 10, 1.2, None, "flat", 6),     # cycles to the 50 l swap cap
     (400, 300, 25, 35, 32, 5, 1.05, 3, "noisy", 7),       # 3 swaps with d = 3
     (150, 150, 10, 149, 32, 5, 2.0, None, "exp", 8),      # l = min(m, n) - 1
+    (600, 400, 100, 150, 96, 16, 2.0, None, "poly", 9),   # b > 64: blocked R11^-1
+    (500, 300, 120, 140, 128, 0, 2.0, None, "exp", 10),   # b = 128, p = 0
 ]
 
 
