@@ -200,10 +200,12 @@ FFB_DEV void panel_householder(const PanelArgs& a, int64_t r0, int64_t r1, doubl
       div = x0 - alpha;
       tau = (alpha - x0) / alpha;
     }
-    // (B) v over own rows (rows < c: 0, row c: 1), Y column c, then projections
+    // (B) v over own rows (rows < c: 0, row c: 1), Y column c, then projections.
+    // W[c, c] itself is left alone (v_c = 1 is implicit below): other CTAs read
+    // it as x0 above with no barrier in between.
     for (int64_t i = r0 + tid; i < r1; i += nt) {
       const double v = i < c ? 0.0 : (i == c ? 1.0 : (tau != 0.0 ? W[i + c * Mp] / div : 0.0));
-      W[i + c * Mp] = v;
+      if (i != c) W[i + c * Mp] = v;
       a.Y[i + (int64_t)c * a.ldy] = v;
     }
     __syncthreads();
@@ -212,7 +214,7 @@ FFB_DEV void panel_householder(const PanelArgs& a, int64_t r0, int64_t r1, doubl
       const int col = q < c ? q : q + 1;
       double d = 0.0;
       for (int64_t i = (r0 > c ? r0 : c) + lane; i < r1; i += 32)
-        d = fma(W[i + c * Mp], W[i + (int64_t)col * Mp], d);
+        d = fma(i == c ? 1.0 : W[i + c * Mp], W[i + (int64_t)col * Mp], d);
       d = warp_sum(d);
       if (lane == 0) partB[(size_t)blockIdx.x * 64 + q] = d;
     }
@@ -231,7 +233,7 @@ FFB_DEV void panel_householder(const PanelArgs& a, int64_t r0, int64_t r1, doubl
       for (int64_t e = tid; e < nr * ncols; e += nt) {
         const int64_t i = rb + e % nr;
         const int j = c + 1 + (int)(e / nr);
-        W[i + (int64_t)j * Mp] = fma(-tau * W[i + c * Mp], proj[j - 1], W[i + (int64_t)j * Mp]);
+        W[i + (int64_t)j * Mp] = fma(-tau * (i == c ? 1.0 : W[i + c * Mp]), proj[j - 1], W[i + (int64_t)j * Mp]);
       }
     }
     __syncthreads();
