@@ -542,7 +542,12 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
 size_t panel_smem_bytes() { return sizeof(double) * (size_t)(4 * kW * kL + kCH * kL + 256 + 1024); }
 
 int panel_grid(int sms, int64_t Mp) {
-  int64_t g = (Mp + 63) / 64;
+  static int rpc = -1;   // rows per CTA (FFB_PANEL_RPC tuning knob)
+  if (rpc < 0) {
+    const char* e = getenv("FFB_PANEL_RPC");
+    rpc = e ? std::max(16, atoi(e)) : 64;
+  }
+  int64_t g = (Mp + rpc - 1) / rpc;
   if (g > sms) g = sms;
   if (g < 1) g = 1;
   return (int)g;
