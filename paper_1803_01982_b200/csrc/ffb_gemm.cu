@@ -55,6 +55,7 @@ int occupancy_of(int cfg) {
     case 7: return occupancy<32, 32, 16, 16, 16, 4>();
     case 8: return occupancy<64, 288, 16, 32, 72, 3>();
     case 9: return occupancy<64, 144, 16, 32, 72, 3>();
+    case 11: return occupancy<80, 64, 16, 40, 32, 4>();
     default: return occupancy<64, 216, 16, 32, 72, 3>();
   }
 }
@@ -83,7 +84,7 @@ int pick_cfg(int64_t M, int64_t N, int64_t K) {
     const char* e = getenv("FFB_GEMM_CFG");
     forced = e ? atoi(e) : -1;
   }
-  if (forced >= 0) return forced > 10 ? 10 : forced;
+  if (forced >= 0) return forced > 11 ? 11 : forced;
   if (M <= 16) return 5;
   // small outputs with short K (no split-K to fill the GPU): 32 x 32 tiles so the
   // work spreads over many SMs instead of a few large tiles
@@ -97,6 +98,12 @@ int pick_cfg(int64_t M, int64_t N, int64_t K) {
   if (M <= 32) return 6;
   if (M <= 48) return 0;
   if (M <= 64) return 1;
+  static int m80 = -2;   // FFB_GEMM_M80: tile config of 64 < M <= 80 (the sketch, s = 80)
+  if (m80 == -2) {
+    const char* e = getenv("FFB_GEMM_M80");
+    m80 = e ? atoi(e) : 11;
+  }
+  if (M <= 80) return m80;
   if (M <= 96) return 2;
   static int tallk = -2;   // FFB_GEMM_TALLK: tile config of tall short-K products (tuning)
   if (tallk == -2) {
@@ -116,9 +123,9 @@ int pick_cfg(int64_t M, int64_t N, int64_t K) {
   return 1;
 }
 
-const Shape kShapes[11] = {{48, 64, 16},  {64, 64, 16}, {96, 64, 16},  {128, 64, 16},
+const Shape kShapes[12] = {{48, 64, 16},  {64, 64, 16}, {96, 64, 16},  {128, 64, 16},
                            {128, 96, 16}, {16, 64, 16}, {32, 64, 16},  {32, 32, 16},
-                           {64, 288, 16}, {64, 144, 16}, {64, 216, 16}};
+                           {64, 288, 16}, {64, 144, 16}, {64, 216, 16}, {80, 64, 16}};
 
 template <bool AK, bool BKC>
 cudaError_t launch_layout(int cfg, cudaStream_t st, const GemmArgs& g, dim3 grid) {
@@ -133,6 +140,7 @@ cudaError_t launch_layout(int cfg, cudaStream_t st, const GemmArgs& g, dim3 grid
     case 7: return launch_cfg<32, 32, 16, 16, 16, AK, BKC, 4>(st, g, grid);
     case 8: return launch_cfg<64, 288, 16, 32, 72, AK, BKC, 3>(st, g, grid);
     case 9: return launch_cfg<64, 144, 16, 32, 72, AK, BKC, 3>(st, g, grid);
+    case 11: return launch_cfg<80, 64, 16, 40, 32, AK, BKC, 4>(st, g, grid);
     default: return launch_cfg<64, 216, 16, 32, 72, AK, BKC, 3>(st, g, grid);
   }
 }

@@ -48,7 +48,7 @@ def test_gemm_engine_layouts(ffb):
     ctx = _capi.context(0)
     g = torch.Generator(device="cuda").manual_seed(0)
     ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
-    for (M, N, K) in [(80, 8192, 8192), (64, 1000, 2000), (2000, 60, 1000), (48, 37, 5),
+    for (M, N, K) in [(80, 8192, 8192), (72, 300, 2500), (65, 777, 4100), (64, 1000, 2000), (2000, 60, 1000), (48, 37, 5),
                       (130, 70, 257), (7, 9, 11)]:
         for akc in (0, 1):
             for bkc in (0, 1):
