@@ -48,19 +48,32 @@ struct HostStage {
   double* pinned = nullptr;        // g2 Gaussians
   size_t cap = 0;
   SrqrScalars* sc = nullptr;       // certificate scalars read back after the pipeline
+  unsigned char* small = nullptr;  // 256 B: small read-backs (status words, sweep counts)
   ~HostStage() {
     if (pinned) cudaFreeHost(pinned);
     if (sc) cudaFreeHost(sc);
+    if (small) cudaFreeHost(small);
   }
 };
 thread_local HostStage t_host;
 
-// small stream-ordered read-back (never the legacy default stream, so problems
-// driven on other streams are not serialised)
+// small stream-ordered read-back (<= 256 B).  An SM kernel writes the pinned
+// staging word (UVA) instead of a D2H memcpy: the copy engines' queues, where
+// another stream's large transfer may be in flight, stay off the critical path.
 inline cudaError_t d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) {
-  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
+  if (!t_host.small) {
+    cudaError_t e = cudaMallocHost(&t_host.small, 256);
+    if (e != cudaSuccess) return e;
+  }
+  cudaError_t e = launch_copy_bytes(st, src, t_host.small, bytes);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) memcpy(dst, t_host.small, bytes);
   return e;
+}
+
+// device-to-device copies on the SMs (see d2h)
+inline cudaError_t d2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  return launch_copy_bytes(st, src, dst, bytes);
 }
 
 constexpr int kPanelW = 64;
@@ -507,7 +520,7 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
     cudaStreamSynchronize(st);  // previous staging copy may still read the buffer
     if (!gauss || gauss(gauss_user, D.seed, 1000 + (uint64_t)swaps, D.d, L1, t_host.pinned) != 0)
       return fail(ctx, FFB_ERR_ARGUMENT, "gauss callback failed");
-    e.ok(cudaMemcpyAsync(w.g2om, t_host.pinned, cnt * sizeof(double), cudaMemcpyHostToDevice, st));
+    e.ok(launch_copy_bytes(st, t_host.pinned, w.g2om, cnt * sizeof(double)));   // reads pinned host memory (UVA)
     return FFB_OK;
   };
   if (mode != FFB_MODE_TRQRCP) {
@@ -569,17 +582,17 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
 
   auto outputs_common = [&]() {
     if (out->perm)
-      e.ok(cudaMemcpyAsync(out->perm, w.arr, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, st));
+      e.ok(d2d(out->perm, w.arr, sizeof(int64_t) * n, st));
     if (out->R) e.ok(launch_r_arranged(st, w.R, L1, w.arr, l, n, out->R, out->ldr, l));
     if (out->B) e.ok(launch_gather_cols(st, w.B, s, s, w.arr, n, out->B, out->ldb));
     if (out->pivot_gap)
-      e.ok(cudaMemcpyAsync(out->pivot_gap, w.gap, sizeof(double) * l, cudaMemcpyDeviceToDevice, st));
+      e.ok(d2d(out->pivot_gap, w.gap, sizeof(double) * l, st));
   };
 
   if (mode == FFB_MODE_TRQRCP) {
     outputs_common();
-    if (out->Y) e.ok(cudaMemcpy2DAsync(out->Y, out->ldy * 8, w.Y, m * 8, m * 8, l, cudaMemcpyDeviceToDevice, st));
-    if (out->T) e.ok(cudaMemcpy2DAsync(out->T, out->ldt * 8, w.T, l * 8, l * 8, l, cudaMemcpyDeviceToDevice, st));
+    if (out->Y) e.ok(launch_copy_rows(st, w.Y, m, m, l, out->Y, out->ldy));
+    if (out->T) e.ok(launch_copy_rows(st, w.T, l, l, l, out->T, out->ldt));
     cudaError_t se = cudaStreamSynchronize(st);
     if (e.cerr != cudaSuccess) return cuda_fail(ctx, e.cerr, "trqrcp launch");
     if (se != cudaSuccess) return cuda_fail(ctx, se, "trqrcp");
@@ -612,7 +625,7 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
   auto pack_and_outputs = [&]() {
     e.ok(launch_pack(st, w.R, L1, w.arr, w.colsq, l, n, w.part, 0, w.sc));
     outputs_common();
-    if (out->Q) e.ok(cudaMemcpy2DAsync(out->Q, out->ldq * 8, w.Q, m * 8, m * 8, L1, cudaMemcpyDeviceToDevice, st));
+    if (out->Q) e.ok(launch_copy_rows(st, w.Q, m, m, L1, out->Q, out->ldq));
     if (out->rtilde) e.ok(launch_r_arranged(st, w.R, L1, w.arr, L1, L1, out->rtilde, L1, L1));
   };
 
@@ -641,8 +654,8 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
     e.gemm(m, k, l, -1.0, w.Yt, m, false, w.W2, l, true, 0.0, out->u, out->ldu);
     e.ok(launch_add_top(st, out->u, out->ldu, w.Us, l, l, k));
     e.gemm(n, k, l, 1.0, w.Yh, n, false, w.Vo, l, true, 0.0, out->v, out->ldv);
-    e.ok(cudaMemcpyAsync(out->s, w.sig, sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
-    if (out->sv_all) e.ok(cudaMemcpyAsync(out->sv_all, w.sig, sizeof(double) * l, cudaMemcpyDeviceToDevice, st));
+    e.ok(d2d(out->s, w.sig, sizeof(double) * k, st));
+    if (out->sv_all) e.ok(d2d(out->sv_all, w.sig, sizeof(double) * l, st));
   };
 
   pack_and_outputs();
@@ -650,7 +663,7 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
 
   auto read_sc = [&]() -> cudaError_t {
     if (!t_host.sc) cudaMallocHost(&t_host.sc, sizeof(SrqrScalars));
-    e.ok(cudaMemcpyAsync(t_host.sc, w.sc, sizeof(SrqrScalars), cudaMemcpyDeviceToHost, st));
+    e.ok(launch_copy_bytes(st, w.sc, t_host.sc, sizeof(SrqrScalars)));   // writes pinned host memory (UVA)
     return cudaStreamSynchronize(st);
   };
   cudaError_t se = read_sc();
@@ -817,7 +830,7 @@ extern "C" int ffb_rsisvd(ffb_ctx* ctx, void* stream, const double* A, int64_t m
   e.gemm(r, k, r, 1.0, w.Tl, r, false, w.W1, r, true, 0.0, w.W2, r);
   e.gemm(n, k, r, -1.0, w.Yl, n, false, w.W2, r, true, 0.0, v, ldv);
   e.ok(launch_add_top(st, v, ldv, w.Us, r, r, k));
-  e.ok(cudaMemcpyAsync(s, w.sig, sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
+  e.ok(d2d(s, w.sig, sizeof(double) * k, st));
   int sw = 0;
   uint32_t stw = 0;
   cudaError_t se = cudaSuccess;

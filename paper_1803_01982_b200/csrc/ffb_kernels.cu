@@ -684,6 +684,35 @@ cudaError_t launch_copy_rows(cudaStream_t st, const double* src, int64_t ld_src,
   FFB_LAUNCH_CHECK();
 }
 
+// Byte copy on the SMs (8-byte words + tail).  Used for every small transfer and
+// device-to-device copy on the engine's stream, with pinned host buffers
+// addressed directly (UVA), so no copy-engine queue -- where another stream's
+// large H2D/D2H may be in flight -- sits on a factorization's critical path.
+__global__ void copy_bytes_kernel(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst,
+                                  size_t bytes) {
+  const size_t nw = bytes >> 3;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t t0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if ((((uintptr_t)src | (uintptr_t)dst) & 7) == 0) {
+    const unsigned long long* s8 = reinterpret_cast<const unsigned long long*>(src);
+    unsigned long long* d8 = reinterpret_cast<unsigned long long*>(dst);
+    for (size_t t = t0; t < nw; t += stride) d8[t] = s8[t];
+    for (size_t t = (nw << 3) + t0; t < bytes; t += stride) dst[t] = src[t];
+  } else {
+    for (size_t t = t0; t < bytes; t += stride) dst[t] = src[t];
+  }
+}
+
+cudaError_t launch_copy_bytes(cudaStream_t st, const void* src, void* dst, size_t bytes) {
+  if (bytes == 0) return cudaSuccess;
+  size_t g = ((bytes >> 3) + 255) / 256;
+  if (g < 1) g = 1;
+  if (g > 2048) g = 2048;
+  copy_bytes_kernel<<<(unsigned)g, 256, 0, st>>>(static_cast<const unsigned char*>(src),
+                                                 static_cast<unsigned char*>(dst), bytes);
+  FFB_LAUNCH_CHECK();
+}
+
 __global__ void fill_kernel(double* p, size_t count, double v) {
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < count;
        t += (size_t)gridDim.x * blockDim.x)

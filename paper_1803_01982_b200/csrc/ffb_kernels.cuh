@@ -63,6 +63,7 @@ cudaError_t launch_gather_cols(cudaStream_t st, const double* src, int64_t ld_sr
                                const int64_t* idx, int64_t ncols, double* dst, int64_t ld_dst);
 cudaError_t launch_scatter_rows(cudaStream_t st, const double* src, int64_t ld_src, int64_t nrows,
                                 int64_t ncols, const int64_t* idx, double* dst, int64_t ld_dst);
+cudaError_t launch_copy_bytes(cudaStream_t st, const void* src, void* dst, size_t bytes);
 cudaError_t launch_copy_rows(cudaStream_t st, const double* src, int64_t ld_src, int64_t rows,
                              int64_t cols, double* dst, int64_t ld_dst);
 cudaError_t launch_fill(cudaStream_t st, double* p, size_t count, double v);
