@@ -598,6 +598,7 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
     if (se != cudaSuccess) return cuda_fail(ctx, se, "trqrcp");
     uint32_t stw = 0;
     d2h(&stw, w.status, sizeof(stw), st);
+    ++e.launches;   // d2h's copy kernel
     out->status_bits = stw;
     out->flops = e.gc.flops;
     out->kernels = e.gc.launches + e.launches;
@@ -672,6 +673,7 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
   SrqrScalars sc = *t_host.sc;
   uint32_t stw = 0;
   d2h(&stw, w.status, sizeof(stw), st);
+  ++e.launches;
   stw |= sc.status;
   out->status_bits = stw;
   if (stw & kStNonFinite) return fail(ctx, FFB_ERR_NUMERICAL, "non-finite values in input or factors");
@@ -719,6 +721,7 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
   if (mode == FFB_MODE_FLIPFLOP) {
     int sweeps = 0;
     d2h(&sweeps, w.jsweeps, sizeof(int), st);
+    ++e.launches;
     out->svd_sweeps = sweeps;
     if (sweeps >= kMaxSweeps) return fail(ctx, FFB_ERR_NUMERICAL, "small SVD did not converge");
   }
@@ -836,6 +839,7 @@ extern "C" int ffb_rsisvd(ffb_ctx* ctx, void* stream, const double* A, int64_t m
   cudaError_t se = cudaSuccess;
   if (e.cerr == cudaSuccess) se = d2h(&sw, w.jsweeps, sizeof(int), st);
   if (e.cerr == cudaSuccess && se == cudaSuccess) se = d2h(&stw, w.status, sizeof(stw), st);
+  e.launches += 2;   // the two d2h copy kernels
   if (e.cerr != cudaSuccess) return cuda_fail(ctx, e.cerr, "rsisvd launch");
   if (se != cudaSuccess) return cuda_fail(ctx, se, "rsisvd");
   if (flops) *flops = e.gc.flops;
