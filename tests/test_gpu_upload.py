@@ -1,0 +1,28 @@
+"""numpy inputs above the staging threshold go through the pinned ring upload
+(engine._upload_bytes): results must be bitwise those of the same matrix passed
+as a CUDA tensor, for F- and C-ordered arrays with a ragged last chunk."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.mark.parametrize("order", ["F", "C"])
+def test_staged_upload_matches_device_input(order):
+    import paper_1803_01982_b200 as ffb
+    from paper_1803_01982_b200 import engine
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    rs = np.random.default_rng(11)
+    m, n = 3001, 2999                         # 72 MB: > 2 staging chunks, ragged tail
+    assert m * n * 8 >= 2 * engine._STAGE_CHUNK
+    A = rs.standard_normal((m, n))
+    A = np.asfortranarray(A) if order == "F" else np.ascontiguousarray(A)
+    ap_np = ffb.flip_flop_srqr(A, 20, l=40, b=16, p=4, seed=3)
+    Ad = torch.from_numpy(np.asfortranarray(A).T).cuda().t()
+    ap_dev = ffb.flip_flop_srqr(Ad, 20, l=40, b=16, p=4, seed=3)
+    assert np.array_equal(np.asarray(ap_np.s), ap_dev.s.cpu().numpy())
+    assert np.array_equal(np.asarray(ap_np.u), ap_dev.u.cpu().numpy())
+    assert np.array_equal(ap_np.meta["srqr"].fact.perm, ap_dev.meta["srqr"].fact.perm.cpu().numpy())
