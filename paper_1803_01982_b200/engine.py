@@ -92,14 +92,7 @@ def _upload_bytes(torch, a, device):
         dst.copy_(torch.from_numpy(a.reshape(-1)))
         return dst
     st = torch.cuda.current_stream(device)
-    ring = getattr(_tls, "stage", None)
-    if ring is None or ring[0] != dst.device:
-        ring = _tls.stage = (
-            dst.device,
-            [torch.empty(_STAGE_CHUNK // 8, dtype=torch.float64, pin_memory=True) for _ in range(_STAGE_SLOTS)],
-            [torch.cuda.Event() for _ in range(_STAGE_SLOTS)],
-            [False] * _STAGE_SLOTS)
-    _, slots, events, used = ring
+    _, slots, events, used = _stage_ring(torch, dst.device)
     src = a.reshape(-1)
     pool = _copy_pool()
     nw = pool._max_workers
@@ -119,6 +112,62 @@ def _upload_bytes(torch, a, device):
         events[j].record(st)
         used[j] = True
     return dst
+
+
+def _stage_ring(torch, device):
+    ring = getattr(_tls, "stage", None)
+    if ring is None or ring[0] != device:
+        ring = _tls.stage = (
+            device,
+            [torch.empty(_STAGE_CHUNK // 8, dtype=torch.float64, pin_memory=True) for _ in range(_STAGE_SLOTS)],
+            [torch.cuda.Event() for _ in range(_STAGE_SLOTS)],
+            [False] * _STAGE_SLOTS)
+    return ring
+
+
+def _download(torch, x):
+    """CUDA float64 tensor -> numpy array of the same shape and strides kind,
+    through the pinned ring (the mirror of _upload_bytes)."""
+    if x.numel() * 8 < 2 * _STAGE_CHUNK or x.dtype != torch.float64:
+        return x.detach().cpu().numpy()
+    if x.is_contiguous():
+        flat, finish = x.reshape(-1), (lambda a: a.reshape(tuple(x.shape)))
+    elif x.dim() == 2 and x.t().is_contiguous():
+        flat, finish = x.t().reshape(-1), (lambda a: a.reshape(tuple(x.shape[::-1])).T)
+    else:
+        return x.detach().cpu().numpy()
+    st = torch.cuda.current_stream(x.device)
+    _, slots, events, used = _stage_ring(torch, x.device)
+    out = np.empty(flat.numel())
+    pool = _copy_pool()
+    nw = pool._max_workers
+    per = _STAGE_CHUNK // 8
+    offs = list(range(0, flat.numel(), per))
+
+    def issue(i):
+        j = i % _STAGE_SLOTS
+        if used[j]:
+            st.wait_event(events[j])
+        cnt = min(per, flat.numel() - offs[i])
+        slots[j][:cnt].copy_(flat[offs[i]:offs[i] + cnt], non_blocking=True)
+        events[j].record(st)
+        used[j] = True
+
+    for i in range(min(_STAGE_SLOTS, len(offs))):
+        issue(i)
+    for i, off in enumerate(offs):
+        j = i % _STAGE_SLOTS
+        cnt = min(per, flat.numel() - off)
+        events[j].synchronize()
+        hv = slots[j].numpy()
+        part = (cnt + nw - 1) // nw
+        futs = [pool.submit(np.copyto, out[off + q:off + min(cnt, q + part)], hv[q:min(cnt, q + part)])
+                for q in range(0, cnt, part)]
+        for f in futs:
+            f.result()
+        if i + _STAGE_SLOTS < len(offs):
+            issue(i + _STAGE_SLOTS)
+    return finish(out)
 
 
 def _to_device_colmajor(A, device):
@@ -290,7 +339,7 @@ def run(A, params: SketchParams, mode, device=None, trace_gaps=False):
 def _conv(x, as_np):
     if not as_np:
         return x
-    return x.detach().cpu().numpy()
+    return _download(_torch(), x)
 
 
 def _srqr_result(out):

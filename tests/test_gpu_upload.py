@@ -26,3 +26,18 @@ def test_staged_upload_matches_device_input(order):
     assert np.array_equal(np.asarray(ap_np.s), ap_dev.s.cpu().numpy())
     assert np.array_equal(np.asarray(ap_np.u), ap_dev.u.cpu().numpy())
     assert np.array_equal(ap_np.meta["srqr"].fact.perm, ap_dev.meta["srqr"].fact.perm.cpu().numpy())
+
+
+@pytest.mark.parametrize("layout", ["row", "col"])
+def test_staged_download_matches_cpu_copy(layout):
+    from paper_1803_01982_b200 import engine
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    g = torch.Generator(device="cuda").manual_seed(5)
+    base = torch.randn(3003, 2999, generator=g, dtype=torch.float64, device="cuda")
+    x = base if layout == "row" else base.t()      # contiguous / column-major view
+    got = engine._download(torch, x)
+    ref = x.cpu().numpy()
+    assert got.shape == ref.shape
+    assert np.array_equal(got, ref)
