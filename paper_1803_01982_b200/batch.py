@@ -68,6 +68,77 @@ def run_streams(problems, solve, n_streams=4, device=None):
     return list(ex.map(_one, problems))
 
 
+def run_host_pipeline(host_inputs, solve, n_streams=3, prefetch=2, device=None):
+    """Host-resident inputs -> `solve(i, device_tensor)` on `n_streams` compute streams,
+    with every upload issued ahead by one copy thread on its own stream.
+
+    With uploads inside each call (``run_streams``), a stream's next upload waits
+    for its previous factorization, so the copy engine idles whenever all streams
+    compute.  Here the copy engine runs back to back, at most
+    ``n_streams + prefetch`` inputs resident on the device at a time.  Inputs
+    should be pinned CPU tensors (any strides; the device copy keeps them).
+    Results keep input order.
+    """
+    import queue
+
+    import torch
+
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    streams, ex, lock, free = _pool(dev, max(1, n_streams))
+    key = (dev.index, "copy")
+    with _pools_lock:
+        if key not in _pools:
+            _pools[key] = torch.cuda.Stream(device=dev)
+        cst = _pools[key]
+    q = queue.Queue(maxsize=max(1, n_streams + prefetch))
+    err = []
+
+    def _uploader():
+        try:
+            with torch.cuda.device(dev), torch.cuda.stream(cst):
+                for i, h in enumerate(host_inputs):
+                    d = torch.empty_strided(tuple(h.shape), tuple(h.stride()), dtype=h.dtype, device=dev)
+                    d.copy_(h, non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(cst)
+                    q.put((i, d, ev))
+        except BaseException as e:   # surfaced by the consumers
+            err.append(e)
+            q.put(None)
+
+    up = threading.Thread(target=_uploader, name="ffb-uploader", daemon=True)
+    up.start()
+
+    def _one(_):
+        item = q.get()
+        if item is None:
+            q.put(None)
+            raise RuntimeError("upload failed") from (err[0] if err else None)
+        i, d, ev = item
+        with lock:
+            sid = free.pop()
+        try:
+            s_ = streams[sid]
+            with torch.cuda.device(dev), torch.cuda.stream(s_):
+                s_.wait_event(ev)
+                d.record_stream(s_)
+                out = solve(i, d)
+                s_.synchronize()
+                return i, out
+        finally:
+            with lock:
+                free.append(sid)
+
+    res = list(ex.map(_one, range(len(host_inputs))))
+    up.join()
+    if err:
+        raise err[0]
+    res.sort(key=lambda t: t[0])
+    return [r for _, r in res]
+
+
 def gather_slots(local_slots, n_problems, slot_shape, rank, world, device, dtype=None):
     """Gather fixed-size per-problem result slots to rank 0.
 

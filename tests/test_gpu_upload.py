@@ -41,3 +41,26 @@ def test_staged_download_matches_cpu_copy(layout):
     ref = x.cpu().numpy()
     assert got.shape == ref.shape
     assert np.array_equal(got, ref)
+
+
+def test_host_pipeline_matches_direct_calls():
+    """batch.run_host_pipeline (uploads on a copy stream, compute on a stream pool)
+    returns, in input order, exactly what one-at-a-time calls return."""
+    import paper_1803_01982_b200 as ffb
+    from paper_1803_01982_b200 import batch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    rs = np.random.default_rng(21)
+    hosts = []
+    for i in range(7):
+        A = rs.standard_normal((400 + 10 * i, 300))
+        h = torch.empty((300, 400 + 10 * i), dtype=torch.float64, pin_memory=True)
+        h.copy_(torch.from_numpy(A.T))
+        hosts.append(h.t())                       # column-major pinned view
+    got = batch.run_host_pipeline(
+        hosts, lambda i, Ad: ffb.flip_flop_srqr(Ad, 10, l=24, b=8, p=4, seed=i).s.cpu().numpy(),
+        n_streams=3, prefetch=1)
+    for i, h in enumerate(hosts):
+        ref = ffb.flip_flop_srqr(h.cuda(), 10, l=24, b=8, p=4, seed=i).s.cpu().numpy()
+        assert np.array_equal(got[i], ref)
