@@ -60,7 +60,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -71,26 +71,38 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.samples.append([x.strip() for x in line.split(",")])
 
-    def stop(self):
+    def ready(self, timeout=10.0):
+        """Block until nvidia-smi delivers its first sample (its start-up can
+        outlast a short timed region); returns the index the region starts at."""
+        t0 = time.time()
+        while self.proc is not None and not self.samples and time.time() - t0 < timeout:
+            time.sleep(0.01)
+        return len(self.samples)
+
+    def stop(self, since=0):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t0 = time.time()   # a region shorter than the 50 ms period: take the next sample
+        while len(self.samples) <= since and time.time() - t0 < 1.0:
+            time.sleep(0.005)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
         self.thread.join(timeout=2)
-        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
+        region = self.samples[since:]
+        sm = [float(s[0]) for s in region if s and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in region if len(s) > 1 and s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for s in self.samples:
+        for s in region:
             for i, nm in enumerate(names):
                 if len(s) > 3 + i and s[3 + i].lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.samples)}
+                "samples": len(region)}
 
 
 def dist_init():
@@ -184,6 +196,7 @@ def run_batched(args):
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
+    i0 = clocks.ready()
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
@@ -191,7 +204,7 @@ def run_batched(args):
         gathered = step()
     e1.record(st)
     torch.cuda.synchronize()
-    clk = clocks.stop()
+    clk = clocks.stop(i0)
     ms = e0.elapsed_time(e1) / args.steps
     if ws > 1:
         t = torch.tensor([ms], device=dev)
@@ -321,6 +334,7 @@ def main():
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
+    i0 = clocks.ready()
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
@@ -328,7 +342,7 @@ def main():
         ap_ = step()
     e1.record(st)
     torch.cuda.synchronize()
-    clk = clocks.stop()
+    clk = clocks.stop(i0)
     ms = e0.elapsed_time(e1) / args.steps
     if ws > 1:
         t = torch.tensor([ms], device=dev)
