@@ -16,6 +16,7 @@ from .ffsrqr_oracle import (  # noqa: F401
     OracleApprox,
     OracleSrqr,
     OracleTrqrcp,
+    check_theorem_bounds,
     flip_flop,
     flip_flop_flops,
     gaussian,

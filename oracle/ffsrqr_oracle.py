@@ -464,3 +464,43 @@ def flip_flop(A, k, l=None, b=32, p=5, epsilon=0.5, g=2.0, d=None, seed=0):
 def flip_flop_flops(m, n, l, b, p):
     """Paper flop budget 4mnl + 2(b+p)mn — ffsrqr/svd.py:258-260."""
     return 4 * m * n * l + 2 * (b + p) * m * n
+
+
+def check_theorem_bounds(A, perm, R, Q, rtilde, u, s, v, l, slack=1e-8):
+    """Restatement of ``ffsrqr/svd.py:174-255`` on explicit factors (the true
+    SRQR ``R`` l x n, ``Q`` m x l, ``rtilde`` (l+1) x (l+1)).  Returns a dict
+    with the report's scalars and flags."""
+    A = np.asarray(A, dtype=float)
+    k = s.shape[0]
+    sig = np.linalg.svd(A, compute_uv=False)
+    sig_l1 = float(sig[l]) if l < sig.size else 0.0
+    sig_k1 = float(sig[k]) if k < sig.size else 0.0
+    alpha = abs(float(rtilde[l, l]))
+    if sig_l1 <= 1e-12 * max(float(sig[0]), 1e-300) or alpha == 0.0:
+        return {"degenerate": True, "sv_upper_ok": bool(np.all(s <= sig[:k] * (1 + slack))),
+                "all_ok": bool(np.all(s <= sig[:k] * (1 + slack)))}
+
+    def inv_rows(T):                                   # svd.py:146-149
+        inv = scipy.linalg.solve_triangular(T, np.eye(T.shape[0]))
+        return float(np.sqrt(np.max(np.einsum("ij,ij->i", inv, inv))))
+
+    M = A[:, perm] - Q[:, :l] @ R[:l]
+    r22_2 = float(scipy.linalg.svdvals(M)[0])
+    r22_12 = math.sqrt(float(np.max(np.einsum("ij,ij->j", M, M))))
+    inv_rt, inv_r11 = inv_rows(rtilde), inv_rows(R[:l, :l])
+    g1, g2 = r22_12 / alpha, alpha * inv_rt
+    tau = g1 * g2 * (r22_2 / r22_12) / inv_rt / sig_l1
+    tau_hat = g1 * g2 * (r22_2 / r22_12) / inv_r11 / float(s[k - 1])
+    up, dn = 1 + slack, 1 - slack
+    upper = bool(np.all(s <= sig[:k] * up))
+    aux_lower = bool(np.all(s >= sig[:k] / np.power(1 + 2 * r22_2 ** 4 / s ** 4, 0.25) * dn))
+    cap = np.minimum(2 * tau_hat ** 4, tau ** 4 * (2 + 4 * tau_hat ** 4) * (sig_l1 / sig[:k]) ** 4)
+    lower = bool(np.all(s >= sig[:k] / np.power(1 + cap, 0.25) * dn))
+    resid2 = float(scipy.linalg.svdvals(A - (u * s) @ v.T)[0])
+    aux_budget = sig_k1 * (1 + 2 * (r22_2 / sig_k1) ** 4) ** 0.25 if sig_k1 > 0 else resid2
+    budget2 = sig_k1 * (1 + 2 * tau ** 4 * (sig_l1 / sig_k1) ** 4) ** 0.25 if sig_k1 > 0 else resid2
+    flags = dict(aux_lower_ok=aux_lower, sv_lower_ok=lower, sv_upper_ok=upper,
+                 aux_residual_ok=bool(resid2 <= aux_budget * up),
+                 residual_ok=bool(resid2 <= budget2 * up))
+    return dict(degenerate=False, tau=tau, tau_hat=tau_hat, g1=g1, g2=g2, r22_2=r22_2,
+                r22_12=r22_12, resid2=resid2, all_ok=all(flags.values()), **flags)

@@ -10,13 +10,14 @@ from .errors import (CertificationError, DimensionError, EngineUnavailable, NonF
 from .results import (ApproxSvd, PartialFactorization, SketchParams, SrqrCertificate, SrqrResult,
                       WYFactor, flip_flop_flop_formula)
 from .engine import flip_flop_srqr, rsisvd, srqr, trqrcp
+from .bounds import BoundReport, check_theorem_bounds
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "ApproxSvd", "CertificationError", "DimensionError", "EngineUnavailable", "NonFiniteInputError",
+    "ApproxSvd", "BoundReport", "CertificationError", "DimensionError", "EngineUnavailable", "NonFiniteInputError",
     "NumericalError",
     "PartialFactorization", "SingularTrailingBlockError", "SketchParams", "SrqrCertificate",
-    "SrqrResult", "WYFactor", "flip_flop_flop_formula", "flip_flop_srqr", "rsisvd", "srqr",
+    "SrqrResult", "WYFactor", "check_theorem_bounds", "flip_flop_flop_formula", "flip_flop_srqr", "rsisvd", "srqr",
     "trqrcp",
 ]
