@@ -72,3 +72,49 @@ def test_device_bounds_match_reference(name):
             assert _close(getattr(rep, key), float(c[key])), (key, getattr(rep, key))
         for key in ("r22_2", "r22_12", "resid2", "g1", "g2"):
             assert _close(rep.detail[key], float(c[key])), (key, rep.detail[key], float(c[key]))
+
+
+def _gen_type1(m, n, s, seed):
+    """Test-side restatement of ffsrqr/generators.py:17-28 (U D V^T + 1e-4 E,
+    D geometric 1 -> 1e-3 over s planted values, Philox stream 3e6)."""
+    from paper_1803_01982_b200 import rng
+
+    rs = rng.philox(seed, rng.STREAM_GEN)
+    U, _ = np.linalg.qr(rs.standard_normal((m, s)))
+    V, _ = np.linalg.qr(rs.standard_normal((n, s)))
+    return (U * np.geomspace(1.0, 1e-3, s)) @ V.T + 1e-4 * rs.standard_normal((m, n))
+
+
+def test_gen_type1_matches_golden():
+    c = _load("bounds_type1_300_s3")
+    np.testing.assert_array_equal(_gen_type1(300, 300, 100, 3), c["A"])
+
+
+@pytest.mark.gpu
+def test_device_bound_suite_acceptance():
+    """The reference's acceptance item 3 (tests/test_acceptance.py:101-110) and
+    TestBounds.test_hold_on_decaying_spectrum (tests/test_svd.py:81-87): every
+    bound holds, zero violations, and tau obeys the dimensional budget
+    (tests/test_svd.py:89-95)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1803_01982_b200 as ffb
+
+    violations = []
+    for seed in range(20):
+        A = torch.as_tensor(_gen_type1(300, 300, 100, seed), device="cuda")
+        rep = ffb.check_theorem_bounds(A, ffb.flip_flop_srqr(A, 20, l=25, seed=seed), slack=1e-8)
+        if not rep.all_ok:
+            violations.append(seed)
+    for seed in range(3):
+        A = torch.as_tensor(_gen_type1(120, 120, 50, seed), device="cuda")
+        rep = ffb.check_theorem_bounds(A, ffb.flip_flop_srqr(A, 10, l=15, seed=seed))
+        if not (rep.all_ok and rep.tau >= 0 and rep.tau_hat >= 0):
+            violations.append(("120", seed))
+    assert violations == []
+    A = _gen_type1(100, 100, 40, 7)
+    ap = ffb.flip_flop_srqr(A, 10, l=15, seed=1)
+    rep = ffb.check_theorem_bounds(A, ap)
+    cert = ap.meta["srqr"].cert
+    assert rep.tau <= cert.g1 * cert.g2 * np.sqrt((rep.l + 1) * (100 - rep.l)) + 1e-8
