@@ -169,7 +169,7 @@ def run_batched(args):
         seed_of = lambda i: i
     m, n = cfg.m, cfg.n
     if args.streams <= 0:
-        args.streams = 12 if args.workload == "cfg5" else 1
+        args.streams = 8 if args.workload == "cfg5" else 1
     # Omega for every local problem, generated on host threads (the reference RNG)
     # before the warm-up; SVT iterations reuse a fixed seed, so steady state
     # sees cached sketches
@@ -299,7 +299,7 @@ def main():
     ap.add_argument("--ref-budget-s", type=float, default=120.0)
     ap.add_argument("--streams", type=int, default=0,
                     help="batched workloads: problems in flight per GPU (CUDA streams); "
-                         "0 = default (cfg5: 12, cfg4: 1)")
+                         "0 = default (cfg5: 8, cfg4: 1)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
