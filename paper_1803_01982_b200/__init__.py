@@ -8,7 +8,7 @@ include/ffb200.h); this package is host glue only and has no CPU fallback.
 from .errors import (CertificationError, DimensionError, EngineUnavailable, NonFiniteInputError,
                      NumericalError, SingularTrailingBlockError)
 from .results import (ApproxSvd, PartialFactorization, SketchParams, SrqrCertificate, SrqrResult,
-                      WYFactor, flip_flop_flop_formula)
+                      WYFactor, flip_flop_flop_formula, rsisvd_flop_formula)
 from .engine import flip_flop_srqr, rsisvd, srqr, trqrcp
 from .bounds import BoundReport, check_theorem_bounds
 
@@ -19,5 +19,5 @@ __all__ = [
     "NumericalError",
     "PartialFactorization", "SingularTrailingBlockError", "SketchParams", "SrqrCertificate",
     "SrqrResult", "WYFactor", "check_theorem_bounds", "flip_flop_flop_formula", "flip_flop_srqr", "rsisvd", "srqr",
-    "trqrcp",
+    "trqrcp", "rsisvd_flop_formula",
 ]

@@ -25,7 +25,8 @@ FFB_MODE_FLIPFLOP = 2
 EXPORTS = ("ffb_ctx_create", "ffb_ctx_destroy", "ffb_last_error", "ffb_version",
            "ffb_workspace_query", "ffb_run", "ffb_flipflop", "ffb_gemm", "ffb_block_pivots",
            "ffb_run_batched", "ffb_rsisvd_workspace_query", "ffb_rsisvd", "ffb_svt_partials",
-           "ffb_ialm_update", "ffb_sumsq", "ffb_shrink_cols")
+           "ffb_ialm_update", "ffb_sumsq", "ffb_shrink_cols", "ffb_small_svd_workspace_query",
+           "ffb_small_svd")
 
 
 class Params(C.Structure):
@@ -137,6 +138,12 @@ def load(path=LIB_PATH):
         lib.ffb_shrink_cols.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
                                         C.c_void_p, C.c_double, C.c_void_p, C.c_int64]
         lib.ffb_shrink_cols.restype = C.c_int
+        lib.ffb_small_svd_workspace_query.argtypes = [C.c_int64, C.POINTER(C.c_size_t)]
+        lib.ffb_small_svd_workspace_query.restype = C.c_int
+        lib.ffb_small_svd.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                      C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                      C.c_void_p, C.c_size_t, C.POINTER(C.c_int32)]
+        lib.ffb_small_svd.restype = C.c_int
         _lib = lib
         return lib
 

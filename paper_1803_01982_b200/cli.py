@@ -100,8 +100,6 @@ def _run_svd(args, dev):
         ap = rsisvd(A, args.k, p=args.p, q=args.q, seed=args.seed)
     else:
         mn = min(A.shape)
-        if mn > 512:
-            raise DimensionError("exact SVD on the device is limited to min(m, n) <= 512")
         ap = rsisvd(A, args.k, p=mn - args.k, q=0, seed=args.seed)
     rt = time.perf_counter() - t0
     if args.artifacts:

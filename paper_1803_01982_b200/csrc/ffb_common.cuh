@@ -3,11 +3,26 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #define FFB_DEV __device__ __forceinline__
 
 namespace ffb {
 
 constexpr int kWarp = 32;
+
+// Opt-in to more than 48 KB of dynamic shared memory for `kern` on the CURRENT
+// device.  The attribute is per device, so a process driving several GPUs must
+// set it once on each: `done` is the call site's bitmask of devices already set.
+inline cudaError_t ensure_smem_optin(const void* kern, int bytes, std::atomic<unsigned long long>& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 // 1/x to ~1 ulp: MUFU reciprocal seed + two Newton steps (no IEEE division
 // subroutine on the critical path of sequential factorizations)

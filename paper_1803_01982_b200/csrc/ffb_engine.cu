@@ -117,7 +117,8 @@ struct Work {
   bool piv_smem;
   size_t piv_smem_bytes;
   // SRQR
-  double *r, *rinit, *u, *ct, *part, *rot, *g2om, *g2z;
+  double *r, *rinit, *u, *ct, *part, *rot, *g2om, *g2z, *g2R;
+  uint32_t* g2flag;
   SrqrScalars* sc;
   uint32_t* status;
   // flip-flop
@@ -196,6 +197,8 @@ size_t carve(const ffb_ctx* ctx, const Dims& D, void* base, size_t cap, Work& w)
   w.rot = b.take<double>(4 * L1 + 8);
   w.g2om = b.take<double>(D.d * L1);
   w.g2z = b.take<double>(D.d * L1);
+  w.g2R = L1 > 1024 ? b.take<double>(L1 * L1) : nullptr;   // explicit Rtilde, blocked g2 solve
+  w.g2flag = b.take<uint32_t>(1);
   w.sc = b.take<SrqrScalars>(1);
   w.status = b.take<uint32_t>(1);
   w.TYt = b.take<double>(l * l);
@@ -305,20 +308,42 @@ struct Eng {
     okm(cudaMemset2DAsync(p, ld * sizeof(double), 0, rows * sizeof(double), cols, st));
   }
 
-  // Rinv (ld bb) = Rb^{-1} for the upper-triangular bb x bb block factor (ld bb):
-  // one tile kernel for bb <= 64, else the 2 x 2 block form
-  // [A B; 0 C]^{-1} = [A^-1, -A^-1 B C^-1; 0, C^-1] with two tile inverses + 2 GEMMs
-  void tri_inverse(const double* Rb, int64_t bb, double* Rinv) {
-    if (bb <= kPanelW) {
-      ok(launch_triinv_upper(st, Rb, bb, (int)bb, Rinv, bb, w.status));
+  // g2 estimate (srqr.py:49-64): one-thread-per-row kernel for l + 1 <= 1024,
+  // else blocked back substitution (diagonal blocks of 1024 + GEMM updates)
+  void g2() {
+    const int64_t l = D.l, L1 = l + 1;
+    if (L1 <= 1024) {
+      ok(launch_g2(st, w.R, L1, w.arr, l, w.g2om, (int)D.d, D.g, w.g2z, w.sc));
       return;
     }
-    const int64_t h = kPanelW, t = bb - kPanelW;
-    ok(launch_triinv_upper(st, Rb, bb, (int)h, Rinv, bb, w.status));
-    ok(launch_triinv_upper(st, Rb + h + h * bb, bb, (int)t, Rinv + h + h * bb, bb, w.status));
-    memset2d(Rinv + h, bb, t, h);
-    gemm(h, t, t, 1.0, Rb + h * bb, bb, false, Rinv + h + h * bb, bb, true, 0.0, w.S2, h);
-    gemm(h, t, h, -1.0, Rinv, bb, false, w.S2, h, true, 0.0, Rinv + h * bb, bb);
+    ok(launch_r_arranged(st, w.R, L1, w.arr, L1, L1, w.g2R, L1, L1));
+    ok(launch_g2big_prep(st, w.g2R, L1, w.g2om, (int)D.d, w.g2z, w.sc, w.g2flag));
+    constexpr int64_t kBlk = 1024;
+    for (int64_t i1 = L1; i1 > 0; i1 -= kBlk) {
+      const int64_t i0 = std::max<int64_t>(0, i1 - kBlk);
+      ok(launch_g2big_diag(st, w.g2R, L1, i0, (int)(i1 - i0), w.g2z, (int)D.d));
+      if (i0 > 0)
+        gemm(i0, D.d, i1 - i0, -1.0, w.g2R + i0 * L1, L1, false, w.g2z + i0, L1, true, 1.0, w.g2z, L1);
+    }
+    ok(launch_g2big_finish(st, w.g2z, L1, (int)D.d, D.g, w.g2flag, w.sc));
+  }
+
+  // Rinv (ld ldo) = Rb^{-1} for an upper-triangular bb x bb block (ld ldr): one
+  // tile kernel for bb <= 64, else recursively in the 2 x 2 block form
+  // [A B; 0 C]^{-1} = [A^-1, -A^-1 B C^-1; 0, C^-1] (two half inverses + 2 GEMMs)
+  void tri_inverse(const double* Rb, int64_t ldr, int64_t bb, double* Rinv, int64_t ldo) {
+    if (bb <= kPanelW) {
+      ok(launch_triinv_upper(st, Rb, ldr, (int)bb, Rinv, ldo, w.status));
+      return;
+    }
+    const int64_t h = std::max<int64_t>(kPanelW, (bb / 2 + kPanelW - 1) / kPanelW * kPanelW);
+    const int64_t t = bb - h;
+    tri_inverse(Rb, ldr, h, Rinv, ldo);
+    tri_inverse(Rb + h + h * ldr, ldr, t, Rinv + h + h * ldo, ldo);
+    memset2d(Rinv + h, ldo, t, h);
+    // S2 (h x t) = B C^-1 ; Rinv12 = -A^-1 S2
+    gemm(h, t, t, 1.0, Rb + h * ldr, ldr, false, Rinv + h + h * ldo, ldo, true, 0.0, w.S2, h);
+    gemm(h, t, h, -1.0, Rinv, ldo, false, w.S2, h, true, 0.0, Rinv + h * ldo, ldo);
   }
 
   // Householder panel (Mp x wb, wb <= 64): one fused cooperative kernel
@@ -373,13 +398,33 @@ void explicit_q(Eng& e, const double* Y, int64_t ldy, const double* T, int64_t l
   e.ok(launch_add_identity(e.st, Q, ldq, Mx, Nx, 1.0));
 }
 
+// The message of the last failing call made on this thread (errno-like):
+// problems of a batch may fail concurrently on other threads, so a shared
+// string could be reassigned while a caller reads it.
+thread_local std::string t_err;
+
 int fail(ffb_ctx* ctx, int code, const std::string& msg) {
+  t_err = msg;
   if (ctx) {
     std::lock_guard<std::mutex> g(ctx->err_mu);
     ctx->err = msg;
   }
   return code;
 }
+
+// Makes `dev` current for the duration of an entry point and restores the
+// caller's current device afterwards.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
 
 int cuda_fail(ffb_ctx* ctx, cudaError_t e, const char* where) {
   return fail(ctx, FFB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -391,11 +436,8 @@ bool validate(const Dims& D) {
   if (D.b < 1 || D.p < 0 || D.s > D.m) return false;
   if (D.d < 1 || D.d > D.l) return false;
   if (D.mode != FFB_MODE_TRQRCP && D.l + 1 > std::min(D.m, D.n)) return false;
-  if (D.b > 128) return false; // block inverse covers b <= 128 (and s = b + p <= 128 below)
-  if (D.s > 128) return false; // pivot kernel holds one sketch column per warp (s <= 128)
+  if (D.s > 512) return false;  // pivot kernel: winner column <= 16 rows per lane of one warp
   if (D.n >= 2147483647LL) return false;  // pivot exchange carries 32-bit positions
-  if (D.mode == FFB_MODE_FLIPFLOP && D.l > 512) return false;  // Jacobi SVD: <= 16 block pairs
-  if (D.mode != FFB_MODE_TRQRCP && D.l > 1022) return false;  // g2 solve: one thread per row
   return true;
 }
 
@@ -407,13 +449,11 @@ const char* ffb_version(void) { return "ffb200 0.1.0 (sm_100a, FP64 DMMA)"; }
 
 int ffb_ctx_create(int device, ffb_ctx** out) {
   if (!out) return FFB_ERR_ARGUMENT;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return FFB_ERR_CUDA;
+  DeviceGuard dg(device);
   ffb_ctx* c = new ffb_ctx();
   c->device = device;
-  cudaError_t e = cudaSetDevice(device);
-  if (e != cudaSuccess) {
-    delete c;
-    return FFB_ERR_CUDA;
-  }
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
   cudaMallocHost(&c->sc_host, sizeof(SrqrScalars));
   *out = c;
@@ -428,7 +468,10 @@ int ffb_ctx_destroy(ffb_ctx* c) {
   return FFB_OK;
 }
 
-const char* ffb_last_error(const ffb_ctx* c) { return c ? c->err.c_str() : "no context"; }
+const char* ffb_last_error(const ffb_ctx* c) {
+  (void)c;
+  return t_err.c_str();
+}
 
 int ffb_workspace_query(int64_t m, int64_t n, const ffb_params* prm, int mode, size_t* bytes) {
   if (!prm || !bytes) return FFB_ERR_ARGUMENT;
@@ -443,6 +486,7 @@ int ffb_gemm(ffb_ctx* ctx, void* stream, int64_t M, int64_t N, int64_t K, double
              const double* A, int64_t lda, int a_kc, const double* B, int64_t ldb, int b_kc,
              double beta, double* C, int64_t ldc, void* workspace, size_t workspace_bytes) {
   if (!ctx) return FFB_ERR_ARGUMENT;
+  DeviceGuard dg(ctx->device);
   GemmCtx gc;
   gc.sms = ctx->sms;
   // workspace: [stream-K counters (64Ki u32, zeroed here) | split-K / stream-K partials]
@@ -464,6 +508,7 @@ int ffb_block_pivots(ffb_ctx* ctx, void* stream, const double* B, int64_t s, int
                      int64_t ldb, int64_t j0, int64_t bb, int64_t* arr, int64_t* pos, double* gap,
                      void* workspace, size_t workspace_bytes) {
   if (!ctx) return FFB_ERR_ARGUMENT;
+  DeviceGuard dg(ctx->device);
   if (bb < 1 || j0 < 0 || j0 + bb > n || n >= 2147483647LL || s < 1 || s > 128)
     return fail(ctx, FFB_ERR_DIMENSION, "bad pivot block");
   Work w;
@@ -489,6 +534,7 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
             int64_t lda, const ffb_params* prm, const double* omega, ffb_gauss_cb gauss,
             void* gauss_user, void* workspace, size_t workspace_bytes, ffb_result* out) {
   if (!ctx || !prm || !out || !A || !omega || !workspace) return FFB_ERR_ARGUMENT;
+  DeviceGuard dg(ctx->device);
   Eng e;
   e.ctx = ctx;
   e.st = (cudaStream_t)stream;
@@ -574,7 +620,7 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
     // sketch update B[:, trailing] -= (B_piv R11^{-1}) R12
     if (e1 < n) {
       e.ok(launch_gather_cols(st, w.B, s, s, w.arr + j0, bb, w.Bp, s));
-      e.tri_inverse(w.Rb, bb, w.Rinv);
+      e.tri_inverse(w.Rb, bb, bb, w.Rinv, bb);
       e.gemm(s, bb, bb, 1.0, w.Bp, s, false, w.Rinv, bb, true, 0.0, w.Z, s);
       e.gemm(s, n, bb, -1.0, w.Z, s, false, w.R + j0, L1, true, 1.0, w.B, s);
     }
@@ -621,7 +667,7 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
     e.ok(launch_ext_finish(st, w.part, nparts, l, n, w.arr, w.R, L1, w.r, w.sc, w.u, m, w.Q + m * l));
   };
   extend();
-  e.ok(launch_g2(st, w.R, L1, w.arr, l, w.g2om, (int)D.d, D.g, w.g2z, w.sc));
+  e.g2();
 
   auto pack_and_outputs = [&]() {
     e.ok(launch_pack(st, w.R, L1, w.arr, w.colsq, l, n, w.part, 0, w.sc));
@@ -704,7 +750,7 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
       if (!(sc.alpha > 0.0)) break;
       int rc = stage_gauss(swaps);
       if (rc) return rc;
-      e.ok(launch_g2(st, w.R, L1, w.arr, l, w.g2om, (int)D.d, D.g, w.g2z, w.sc));
+      e.g2();
       se = read_sc();
       if (e.cerr != cudaSuccess || se != cudaSuccess) return cuda_fail(ctx, e.cerr ? e.cerr : se, "swap g2");
       sc = *t_host.sc;
@@ -753,12 +799,13 @@ extern "C" int ffb_run_batched(ffb_ctx* ctx, ffb_batch_item* items, int64_t coun
   int nt = max_threads < 1 ? 1 : max_threads;
   if (nt > count) nt = (int)count;
   std::atomic<int64_t> next{0};
+  std::vector<std::string> msgs((size_t)count);
   auto worker = [&]() {
-    cudaSetDevice(ctx->device);
     for (int64_t i = next++; i < count; i = next++) {
       ffb_batch_item& it = items[i];
       it.status = ffb_run(ctx, it.stream, it.mode, it.A, it.m, it.n, it.lda, &it.prm, it.omega,
                           gauss, gauss_user, it.workspace, it.workspace_bytes, it.out);
+      if (it.status != FFB_OK) msgs[(size_t)i] = t_err;
     }
   };
   std::vector<std::thread> pool;
@@ -766,7 +813,10 @@ extern "C" int ffb_run_batched(ffb_ctx* ctx, ffb_batch_item* items, int64_t coun
   worker();
   for (auto& t : pool) t.join();
   for (int64_t i = 0; i < count; ++i)
-    if (items[i].status != FFB_OK) return items[i].status;
+    if (items[i].status != FFB_OK) {
+      t_err = "problem " + std::to_string(i) + ": " + msgs[(size_t)i];
+      return items[i].status;
+    }
   return FFB_OK;
 }
 
@@ -781,7 +831,7 @@ extern "C" int ffb_run_batched(ffb_ctx* ctx, ffb_batch_item* items, int64_t coun
 extern "C" int ffb_rsisvd_workspace_query(int64_t m, int64_t n, int64_t k, int64_t r,
                                           size_t* bytes) {
   if (!bytes) return FFB_ERR_ARGUMENT;
-  if (m < 1 || n < 1 || k < 1 || k > r || r > std::min(m, n) || r > 512) return FFB_ERR_DIMENSION;
+  if (m < 1 || n < 1 || k < 1 || k > r || r > std::min(m, n)) return FFB_ERR_DIMENSION;
   Work w;
   *bytes = carve_rsisvd(nullptr, m, n, k, r, nullptr, (size_t)-1, w) + (8u << 20);
   return FFB_OK;
@@ -792,9 +842,10 @@ extern "C" int ffb_rsisvd(ffb_ctx* ctx, void* stream, const double* A, int64_t m
                           void* workspace, size_t workspace_bytes, double* u, int64_t ldu,
                           double* s, double* v, int64_t ldv, int64_t* flops, int32_t* sweeps_out) {
   if (!ctx || !A || !omega || !workspace || !u || !s || !v) return FFB_ERR_ARGUMENT;
-  if (m < 1 || n < 1 || k < 1 || k > r || r > std::min(m, n) || r > 512 || q < 0 || lda < m ||
+  DeviceGuard dg(ctx->device);
+  if (m < 1 || n < 1 || k < 1 || k > r || r > std::min(m, n) || q < 0 || lda < m ||
       ldu < m || ldv < n)
-    return fail(ctx, FFB_ERR_DIMENSION, "rsisvd needs 1 <= k <= r <= min(m, n), r <= 512, q >= 0");
+    return fail(ctx, FFB_ERR_DIMENSION, "rsisvd needs 1 <= k <= r <= min(m, n), q >= 0");
   Eng e;
   e.ctx = ctx;
   e.st = (cudaStream_t)stream;
@@ -845,6 +896,48 @@ extern "C" int ffb_rsisvd(ffb_ctx* ctx, void* stream, const double* A, int64_t m
   if (flops) *flops = e.gc.flops;
   if (sweeps_out) *sweeps_out = sw;
   if (stw & 1u) return fail(ctx, FFB_ERR_NUMERICAL, "non-finite values in rsisvd");
+  if (sw >= kMaxSweeps) return fail(ctx, FFB_ERR_NUMERICAL, "small SVD did not converge");
+  return FFB_OK;
+}
+
+// --------------------------------------------------------------------------
+// Standalone small SVD (the dgesdd of svd.py:79): the flip-flop's Jacobi.
+namespace {
+size_t carve_small_svd(int64_t l, void* base, size_t cap, Work& w) {
+  Bump b{static_cast<char*>(base), 0, cap};
+  w.jwork = b.take<double>(jacobi_work_doubles((int)l, kMaxSweeps));
+  w.joff = b.take<double>(kMaxSweeps);
+  w.jbar = b.take<uint32_t>(4);
+  w.jsweeps = b.take<int>(4);
+  w.jorder = b.take<int>(l);
+  return b.off + kAlign;
+}
+}  // namespace
+
+extern "C" int ffb_small_svd_workspace_query(int64_t l, size_t* bytes) {
+  if (!bytes) return FFB_ERR_ARGUMENT;
+  if (l < 1 || l > (1 << 20)) return FFB_ERR_DIMENSION;
+  Work w;
+  *bytes = carve_small_svd(l, nullptr, (size_t)-1, w);
+  return FFB_OK;
+}
+
+extern "C" int ffb_small_svd(ffb_ctx* ctx, void* stream, const double* M, int64_t l, int64_t ldm,
+                             double* sig, double* U, int64_t ldu, double* V, int64_t ldv,
+                             void* workspace, size_t workspace_bytes, int32_t* sweeps) {
+  if (!ctx || !M || !sig || !U || !V || !workspace) return FFB_ERR_ARGUMENT;
+  DeviceGuard dg(ctx->device);
+  if (l < 1 || ldm < l || ldu < l || ldv < l) return fail(ctx, FFB_ERR_DIMENSION, "small svd needs l >= 1, ld >= l");
+  Work w;
+  if (carve_small_svd(l, workspace, workspace_bytes, w) > workspace_bytes)
+    return fail(ctx, FFB_ERR_ARGUMENT, "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = launch_jacobi_svd(st, ctx->sms, M, ldm, (int)l, sig, U, ldu, V, ldv, w.jwork, w.jbar,
+                                    w.joff, w.jsweeps, w.jorder, kMaxSweeps);
+  int sw = 0;
+  if (e == cudaSuccess) e = d2h(&sw, w.jsweeps, sizeof(int), st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "ffb_small_svd");
+  if (sweeps) *sweeps = sw;
   if (sw >= kMaxSweeps) return fail(ctx, FFB_ERR_NUMERICAL, "small SVD did not converge");
   return FFB_OK;
 }

@@ -14,11 +14,8 @@ template <int BM, int BN, int BK, int WM, int WN, bool AK, bool BKC, int ST, boo
 cudaError_t launch_cfg2(cudaStream_t st, const GemmArgs& g, dim3 grid) {
   using Cfg = GemmCfg<BM, BN, BK, WM, WN, AK, BKC, ST>;
   auto kern = gemm_f64_kernel<BM, BN, BK, WM, WN, AK, BKC, ST, V2, SK>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  ensure_smem_optin((const void*)kern, (int)Cfg::kSmem, attr);
   kern<<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(g);
   return cudaGetLastError();
 }

@@ -16,6 +16,8 @@
 // two-sided iteration never accumulates into the factorization.  A grid barrier
 // separates rounds; sweeps stop when max |cos| seen in a sweep <= tol.
 #include <math.h>
+
+#include <algorithm>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -523,6 +525,238 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
 #undef JPROF
 }
 
+// ---------------------------------------------------------------------------
+// General geometry (l > 512: more block pairs than one cluster holds, columns
+// taller than shared memory).  The same block one-sided Jacobi as
+// jacobi_kernel, with three changes:
+//   * `grid` cooperative CTAs take the P pair slots of a round round-robin
+//     (slot = blockIdx.x, + grid, ...), so P may exceed the co-resident CTAs;
+//   * a pair's 32 columns are streamed through shared memory in chunks of
+//     kRC rows: the Gram accumulates over the chunks, the rotation chain runs
+//     on the reduced 32 x 32 Gram, and the apply re-stages each chunk (M stays
+//     L2-resident up to l ~ 2000: 32 MB);
+//   * V is rotated in place with the same J (row-major like M) instead of
+//     replaying a recorded J history (which would grow as sweeps x l^2 x 32).
+constexpr int kRC = 256;   // rows per staged chunk
+
+FFB_DEV void gram_chunk(const double* Ms, int R, bool cross_only, double (&acc)[4][4][2]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, fr = lane >> 2, fk = lane & 3;
+  const int kr = R >> 3;   // rows per warp (multiple of 4)
+  for (int k0 = warp * kr; k0 < (warp + 1) * kr; k0 += 4) {
+    double f[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) f[i] = Ms[(k0 + fk) * kMW + 8 * i + fr];
+    if (cross_only) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 2; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], f[i], f[j]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = i; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], f[i], f[j]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kJThreads, 1) jacobi_general_kernel(JacobiArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const int lpad = a.lpad, nb = a.nb, P = a.P;
+  const int lrows = ((a.l + 31) & ~31) < lpad ? ((a.l + 31) & ~31) : lpad;
+  const bool resident = lrows <= kRC;   // one chunk: staged once, reused by the apply
+  double* Ms = sm;                      // kRC x kMW
+  double* Gs = Ms + (size_t)kRC * kMW;
+  double* Js = Gs + 32 * kMW;
+  double* Gs2 = Js + 32 * kMW;
+  double* Js2 = Gs2 + 32 * kMW;
+  double* part = Js2 + 32 * kMW;        // 4 x 32 x 33 Gram partials
+  __shared__ double s_off;
+  __shared__ int s_active;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const double tol = a.tol, tol2 = a.tol * a.tol;
+  const int64_t ld = a.ld;
+  for (int sweep = 0; sweep < a.max_sweeps; ++sweep) {
+    if (tid == 0) s_off = 0.0;
+    for (int r = 0; r < nb - 1; ++r) {
+      for (int slot = blockIdx.x; slot < P; slot += gridDim.x) {
+        const int pa = rr_player(slot, r, nb), pb = rr_player(nb - 1 - slot, r, nb);
+        const bool cross_only = r > 0;
+        // ---- Gram over the row chunks
+        const int fr = lane >> 2, fk = lane & 3;
+        double acc[4][4][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int c0 = 0; c0 < lrows; c0 += kRC) {
+          const int R = lrows - c0 < kRC ? lrows - c0 : kRC;
+          __syncthreads();   // previous chunk's readers are done with Ms
+          stage_rows_async(Ms, a.M, ld, pa, pb, c0, R);
+          cp_async_commit();
+          cp_async_wait<0>();
+          __syncthreads();
+          gram_chunk(Ms, R, cross_only, acc);
+        }
+        double* pw = part + (warp & 3) * 32 * 33;
+        if (warp >= 4) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = i; j < 4; ++j)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) pw[(8 * i + fr) * 33 + 8 * j + 2 * fk + h] = acc[i][j][h];
+        }
+        __syncthreads();
+        if (warp < 4) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = i; j < 4; ++j)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                double& d = pw[(8 * i + fr) * 33 + 8 * j + 2 * fk + h];
+                d = acc[i][j][h] + d;
+              }
+        }
+        __syncthreads();
+        {
+          const double* da = a.gdiag + (size_t)pa * kBS * kBS;
+          const double* db = a.gdiag + (size_t)pb * kBS * kBS;
+          for (int t = tid; t < 32 * 32; t += nt) {
+            const int rr = t >> 5, c = t & 31;
+            const int ru = rr < c ? rr : c, cu = rr < c ? c : rr;
+            const int o = ru * 33 + cu;
+            double g;
+            if (cross_only && (rr < kBS) == (c < kBS))
+              g = rr < kBS ? da[rr * kBS + c] : db[(rr - kBS) * kBS + (c - kBS)];
+            else
+              g = (part[o] + part[32 * 33 + o]) + (part[2 * 32 * 33 + o] + part[3 * 32 * 33 + o]);
+            Gs[rr * kMW + c] = g;
+            Js[rr * kMW + c] = rr == c ? 1.0 : 0.0;
+          }
+        }
+        if (tid == 0) s_active = 0;
+        __syncthreads();
+        {
+          bool act = false;
+          for (int t = tid; t < 32 * 32; t += nt) {
+            const int p = t >> 5, q = t & 31;
+            if (p >= q || (r != 0 && !(p < kBS && q >= kBS))) continue;
+            const double gpq = Gs[p * kMW + q];
+            act |= gpq * gpq > tol2 * (Gs[p * kMW + p] * Gs[q * kMW + q]);
+          }
+          if (__any_sync(0xffffffffu, act) && lane == 0) s_active = 1;
+        }
+        __syncthreads();
+        const bool active = s_active != 0;
+        // ---- rotation chain (as jacobi_kernel)
+        double offn = 0.0, offd = 1.0;
+        const int n_within = (r == 0) ? kBS - 1 : 0;
+        const int n_cross = a.inner * kBS;
+        const int ba = tid >> 4, bb2 = tid & 15;
+        const double* Gc = Gs;
+        const double* Jc = Js;
+        double* Gn = Gs2;
+        double* Jn = Js2;
+        auto step = [&](int pa2, int qa2, int pb2, int qb2) {
+          const int ra = pa2 * kMW, rq = qa2 * kMW;
+          const double g00 = Gc[ra + pb2], g01 = Gc[ra + qb2];
+          const double g10 = Gc[rq + pb2], g11 = Gc[rq + qb2];
+          const double j00 = Jc[ra + pb2], j01 = Jc[ra + qb2];
+          const double j10 = Jc[rq + pb2], j11 = Jc[rq + qb2];
+          double cb, sb, c2b, denb;
+          const bool rot = rotation(Gc, pb2, qb2, tol2, cb, sb, c2b, denb);
+          const double ca = __shfl_sync(0xffffffffu, cb, ba);
+          const double sa = __shfl_sync(0xffffffffu, sb, ba);
+          if (rot && ba == bb2 && c2b * offd > offn * denb) {
+            offn = c2b;
+            offd = denb;
+          }
+          const double h00 = cb * g00 - sb * g01, h01 = sb * g00 + cb * g01;
+          const double h10 = cb * g10 - sb * g11, h11 = sb * g10 + cb * g11;
+          Gn[ra + pb2] = ca * h00 - sa * h10;
+          Gn[ra + qb2] = ca * h01 - sa * h11;
+          Gn[rq + pb2] = sa * h00 + ca * h10;
+          Gn[rq + qb2] = sa * h01 + ca * h11;
+          Jn[ra + pb2] = cb * j00 - sb * j01;
+          Jn[ra + qb2] = sb * j00 + cb * j01;
+          Jn[rq + pb2] = cb * j10 - sb * j11;
+          Jn[rq + qb2] = sb * j10 + cb * j11;
+          __syncthreads();
+          const double* tg = Gc;
+          Gc = Gn;
+          Gn = const_cast<double*>(tg);
+          const double* tj = Jc;
+          Jc = Jn;
+          Jn = const_cast<double*>(tj);
+        };
+        for (int t = 0; active && t < n_within; ++t) {
+          int pa2, qa2, pb2, qb2;
+          inner_pair(t, ba, n_within, pa2, qa2);
+          inner_pair(t, bb2, n_within, pb2, qb2);
+          step(pa2, qa2, pb2, qb2);
+        }
+        for (int t = 0; active && t < n_cross; ++t) {
+          const int tt = t & (kBS - 1);
+          step(ba, kBS + ((ba + tt) & (kBS - 1)), bb2, kBS + ((bb2 + tt) & (kBS - 1)));
+        }
+        double off = offn > 0.0 ? sqrt(offn / offd) : 0.0;
+        {
+          double* da = a.gdiag + (size_t)pa * kBS * kBS;
+          double* db = a.gdiag + (size_t)pb * kBS * kBS;
+          for (int t = tid; t < 2 * kBS * kBS; t += nt) {
+            const int blk = t / (kBS * kBS), e = t - blk * kBS * kBS, rr = e / kBS, c = e - rr * kBS;
+            const int o = blk * kBS;
+            (blk ? db : da)[e] = Gc[(o + rr) * kMW + o + c];
+          }
+        }
+        // ---- apply J to M's and V's pair columns, chunk by chunk
+        if (active) {
+          for (int pass = 0; pass < 2; ++pass) {
+            double* X = pass == 0 ? a.M : a.V;
+            const int rows = lrows;   // V rows >= l are zero and stay zero
+            for (int c0 = 0; c0 < rows; c0 += kRC) {
+              const int R = rows - c0 < kRC ? rows - c0 : kRC;
+              if (!(pass == 0 && resident)) {
+                __syncthreads();
+                stage_rows_async(Ms, X, ld, pa, pb, c0, R);
+                cp_async_commit();
+                cp_async_wait<0>();
+              }
+              __syncthreads();
+              apply_rows(Ms, R, Jc, X, ld, pa, pb, c0);
+            }
+          }
+        }
+        __syncthreads();
+        off = warp_max(off);
+        if (lane == 0 && off > 0.0)
+          atomicMax(reinterpret_cast<unsigned long long*>(&s_off),
+                    (unsigned long long)__double_as_longlong(off));
+      }
+      __syncthreads();
+      if (tid == 0 && s_off > 0.0)
+        atomicMax(reinterpret_cast<unsigned long long*>(a.offmax + sweep),
+                  (unsigned long long)__double_as_longlong(s_off));
+      grid_barrier(a.bar, gridDim.x);
+    }
+    const double om = *((volatile double*)(a.offmax + sweep));
+    if (tid == 0 && blockIdx.x == 0) *a.sweeps = sweep + 1;
+    if (!(om > tol) || om < 1e-8 || sweep + 1 == a.max_sweeps) break;
+  }
+}
+
+// V = I (row-major lpad x ncp) for the in-place V of the general kernel
+__global__ void jacobi_vinit_kernel(double* Vrm, int l, int lpad, int ncp) {
+  const int64_t total = (int64_t)lpad * ncp;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / ncp), c = (int)(idx - (int64_t)r * ncp);
+    Vrm[idx] = (r == c && r < l) ? 1.0 : 0.0;
+  }
+}
+
 // Deferred V accumulation.  V = prod over (sweep, round) of the block-diagonal
 // rotations J recorded by jacobi_kernel; every ROW of V evolves independently
 // (row_i <- row_i J on the pair's 32 columns), so CTA g owns rows [8g, 8g + 8)
@@ -695,12 +929,23 @@ static void jacobi_geometry(int l, int& nb, int& lpad, int& ncp) {
   ncp = nb * kBS;
 }
 
+// l > 512 (more than 16 block pairs, or columns taller than one CTA's shared
+// memory) runs jacobi_general_kernel; FFB_JACOBI_GENERAL=1 forces it (tests).
+static bool jacobi_general(int l) {
+  int nb, lpad, ncp;
+  jacobi_geometry(l, nb, lpad, ncp);
+  const size_t smem = sizeof(double) * ((size_t)lpad * kMW + 4 * 32 * kMW + 4 * 32 * 33);
+  return nb / 2 > 16 || smem > 226 * 1024;
+}
+
 size_t jacobi_work_doubles(int l, int max_sweeps) {
   int nb, lpad, ncp;
   jacobi_geometry(l, nb, lpad, ncp);
-  // Mrm, Vrm, norms, J history (max_sweeps x rounds x pairs x 32 x 32), diagonal Gram blocks
-  return 2 * (size_t)lpad * ncp + (size_t)lpad + (size_t)max_sweeps * (nb - 1) * (nb / 2) * 1024 +
-         (size_t)nb * kBS * kBS;
+  // Mrm, Vrm, norms, diagonal Gram blocks, and (cluster kernel only) the J
+  // history (max_sweeps x rounds x pairs x 32 x 32) replayed into V
+  size_t w = 2 * (size_t)lpad * ncp + (size_t)lpad + (size_t)nb * kBS * kBS;
+  if (!jacobi_general(l)) w += (size_t)max_sweeps * (nb - 1) * (nb / 2) * 1024;
+  return w;
 }
 
 cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, const double* M, int64_t ldm, int l,
@@ -713,18 +958,43 @@ cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, const double* M, int64_t
   double* Mrm = work;
   double* Vrm = Mrm + (size_t)lpad * ncp;
   double* nrm = Vrm + (size_t)lpad * ncp;
-  double* jhist = nrm + lpad;
-  double* gdiag = jhist + (size_t)max_sweeps * (nb - 1) * P * 1024;
+  double* gdiag = nrm + lpad;
+  double* jhist = gdiag + (size_t)nb * kBS * kBS;
   int inner = 1;
   if (const char* e = getenv("FFB_JACOBI_INNER")) inner = atoi(e);
   if (inner < 1) inner = 1;
   static long long* prof = nullptr;
   if (getenv("FFB_JACOBI_PROF") && !prof) cudaMallocManaged(&prof, 8 * sizeof(long long));
   constexpr size_t kSmemMax = 226 * 1024;   // + static shared memory stays under the 227 KB opt-in limit
-  const size_t smem = sizeof(double) * ((size_t)lpad * kMW + 4 * 32 * kMW + 4 * 32 * 33);
-  if (smem > kSmemMax) return cudaErrorInvalidValue;   // l > ~560 not supported
+  const bool general = jacobi_general(l) || getenv("FFB_JACOBI_GENERAL") != nullptr;
+  const size_t smem = general ? sizeof(double) * ((size_t)kRC * kMW + 4 * 32 * kMW + 4 * 32 * 33)
+                              : sizeof(double) * ((size_t)lpad * kMW + 4 * 32 * kMW + 4 * 32 * 33);
   JacobiArgs a{Mrm, jhist, ncp, l, lpad, nb, 1e-15 * sqrt((double)l), max_sweeps, bar, offmax,
                sweeps, inner, prof, P, Vrm, bar + 2, 0, gdiag};
+  if (general) {
+    cudaError_t e = cudaFuncSetAttribute(jacobi_general_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaMemsetAsync(bar, 0, 4 * sizeof(uint32_t), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(offmax, 0, sizeof(double) * max_sweeps, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(gdiag, 0, sizeof(double) * (size_t)nb * kBS * kBS, st);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, jacobi_general_kernel, kJThreads, smem) != cudaSuccess || occ < 1)
+      occ = 1;
+    int grid = std::min(P, occ * sms);
+    if (const char* ev = getenv("FFB_JACOBI_GRID")) grid = std::max(1, std::min(grid, atoi(ev)));   // tests: slot loop
+    const int64_t total = (int64_t)lpad * ncp;
+    const int g = (int)std::min<int64_t>((total + 255) / 256, 4 * sms);
+    jacobi_scale_kernel<<<1, 1024, 0, st>>>(M, ldm, l, sweeps);
+    jacobi_layout_kernel<<<g, 256, 0, st>>>(M, ldm, l, lpad, ncp, sweeps, Mrm);
+    jacobi_vinit_kernel<<<g, 256, 0, st>>>(Vrm, l, lpad, ncp);
+    void* args[] = {&a};
+    e = cudaLaunchCooperativeKernel((void*)jacobi_general_kernel, dim3(grid), dim3(kJThreads), args, smem, st);
+    if (e != cudaSuccess) return e;
+    jacobi_norms_kernel<<<1, 1024, sizeof(double) * (size_t)l, st>>>(Mrm, ncp, l, lpad, sweeps, sig, order, nrm);
+    const int go = (int)std::min<int64_t>(((int64_t)l * l + 255) / 256, 4 * sms);
+    jacobi_out_kernel<<<go, 256, 0, st>>>(Mrm, Vrm, ncp, l, order, nrm, U, ldu, Vo, ldvo);
+    return cudaGetLastError();
+  }
   const bool cluster = P <= 16 && getenv("FFB_JACOBI_NOCLUSTER") == nullptr;
   void* kern = cluster ? (void*)jacobi_kernel<true> : (void*)jacobi_kernel<false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);

@@ -191,8 +191,11 @@ FFB_DEV void warp_best(double& r, int64_t& p) {
 
 // RQ > 0: every column group owns at most one column and keeps its rows
 // (sub + 4q, q < RQ) in registers; shared memory gets a write-through copy that
-// the publish step reads.  RQ == 0: generic shared/global-memory loop.
-template <bool SMEM, int RQ>
+// the publish step reads.  RQ == 0: generic shared/global-memory loop with the
+// rows of a column loaded to registers (s <= 128).  RQ == -1: generic loop
+// straight on shared/global memory (any s).  XQ: winner-column rows per lane
+// of the reflector warp (s <= 32 XQ).
+template <bool SMEM, int RQ, int XQ>
 __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int s = a.s, cpc = a.cpc, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -221,6 +224,7 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
   for (int c = tid; c < nc; c += kPivThreads) pp[c] = a.pos[c0 + c];
   __syncthreads();
   double x[RQ > 0 ? RQ : 1];
+  (void)x;
   if constexpr (RQ > 0) {
 #pragma unroll
     for (int q = 0; q < RQ; ++q) {
@@ -354,28 +358,28 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
       const int64_t wpos = gw.p1 >= 0 ? gw.p1 : P;
       PPROF(2)
       // winner column rows j..s-1 -> reflector (ffsrqr/qr.py:21-43)
-      double xv[4];
+      double xv[XQ];
       {
         const unsigned long long* wrec = base + (size_t)(wc_cta >= 0 ? wc_cta : 0) * a.recw + 8;
-        unsigned long long xw[4][2];
+        unsigned long long xw[XQ][2];
         unsigned xneed = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < XQ; ++q) {
           const int i = lane + 32 * q;
           if (i >= j && i < s && wc_cta >= 0) xneed |= 1u << q;
           xw[q][0] = xw[q][1] = 0ull;
         }
         do {
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < XQ; ++q)
             if (xneed & (1u << q)) ld_ll2(wrec + 2 * (lane + 32 * q), xw[q][0], xw[q][1]);
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < XQ; ++q)
             if ((xneed & (1u << q)) && ll_tag(xw[q][0]) == tag && ll_tag(xw[q][1]) == tag)
               xneed &= ~(1u << q);
         } while (__any_sync(0xffffffffu, xneed != 0));
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < XQ; ++q) {
           const int i = lane + 32 * q;
           xv[q] = (i >= j && i < s && wc_cta >= 0)
                       ? __hiloint2double((int)ll_data(xw[q][1]), (int)ll_data(xw[q][0]))
@@ -384,14 +388,14 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
       }
       double tsq = 0.0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < XQ; ++q) {
         const int i = lane + 32 * q;
         if (i > j && i < s) tsq = fma(xv[q], xv[q], tsq);
       }
       tsq = warp_sum(tsq);
       double xsel = 0.0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) xsel = sel_f64(q == (j >> 5), xv[q], xsel);
+      for (int q = 0; q < XQ; ++q) xsel = sel_f64(q == (j >> 5), xv[q], xsel);
       const double x0 = __shfl_sync(0xffffffffu, xsel, j & 31);
       double tau = 0.0, div = 1.0;
       if (tsq != 0.0) {
@@ -401,7 +405,7 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
         tau = (alpha - x0) / alpha;
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < XQ; ++q) {
         const int i = lane + 32 * q;
         if (i < s) vv[i] = (i == j) ? 1.0 : (i > j && tau != 0.0 ? xv[q] / div : 0.0);
       }
@@ -474,6 +478,39 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
           if (sub == 0) r[c] = rr;
           cand_push(cd, rr, p);
         }
+      }
+    } else if constexpr (RQ < 0) {
+      for (int c = grp; c < nc; c += kPivGroups) {
+        int64_t p = pp[c];
+        if (p == wpos) p = P;
+        else if (p == P) p = wpos;
+        if (sub == 0) pp[c] = p;
+        if (p <= P) continue;
+        double* col = W + (size_t)c * sP;
+        if (tau != 0.0) {
+          double w0 = 0.0, w1 = 0.0;
+          for (int i = j + sub, q = 0; i < s; i += 4, ++q) {
+            if (q & 1) w1 = fma(vv[i], col[i], w1);
+            else w0 = fma(vv[i], col[i], w0);
+          }
+          double wsum = w0 + w1;
+          wsum += __shfl_xor_sync(gmask, wsum, 1);
+          wsum += __shfl_xor_sync(gmask, wsum, 2);
+          const double wt = wsum * tau;
+          for (int i = j + sub; i < s; i += 4) col[i] = fma(-vv[i], wt, col[i]);
+        }
+        __syncwarp(gmask);
+        const double rj = col[j];
+        double rr = r[c] - rj * rj;
+        if (rr < 1e-8 * r0[c] || rr < 0.0) {
+          double t = 0.0;
+          for (int i = j + 1 + sub; i < s; i += 4) t = fma(col[i], col[i], t);
+          t += __shfl_xor_sync(gmask, t, 1);
+          t += __shfl_xor_sync(gmask, t, 2);
+          rr = t > 0.0 ? t : 0.0;
+        }
+        if (sub == 0) r[c] = rr;
+        cand_push(cd, rr, p);
       }
     } else {
       for (int c = grp; c < nc; c += kPivGroups) {
@@ -571,18 +608,21 @@ int pivots_stride(int s) {
 }
 
 int pivots_rq(int s, int cpc, bool smem_mode) {
+  if (s > 128) return -1;
   if (!smem_mode || cpc > kPivGroups) return 0;
   return s <= 32 ? 8 : s <= 64 ? 16 : s <= 96 ? 24 : 32;
 }
 
-void* pivots_kernel_ptr(bool smem_mode, int rq) {
-  if (!smem_mode) return (void*)pivots_kernel<false, 0>;
+void* pivots_kernel_ptr(bool smem_mode, int rq, int s) {
+  if (s > 256) return smem_mode ? (void*)pivots_kernel<true, -1, 16> : (void*)pivots_kernel<false, -1, 16>;
+  if (s > 128) return smem_mode ? (void*)pivots_kernel<true, -1, 8> : (void*)pivots_kernel<false, -1, 8>;
+  if (!smem_mode) return (void*)pivots_kernel<false, 0, 4>;
   switch (rq) {
-    case 8: return (void*)pivots_kernel<true, 8>;
-    case 16: return (void*)pivots_kernel<true, 16>;
-    case 24: return (void*)pivots_kernel<true, 24>;
-    case 32: return (void*)pivots_kernel<true, 32>;
-    default: return (void*)pivots_kernel<true, 0>;
+    case 8: return (void*)pivots_kernel<true, 8, 4>;
+    case 16: return (void*)pivots_kernel<true, 16, 4>;
+    case 24: return (void*)pivots_kernel<true, 24, 4>;
+    case 32: return (void*)pivots_kernel<true, 32, 4>;
+    default: return (void*)pivots_kernel<true, 0, 4>;
   }
 }
 
@@ -596,16 +636,14 @@ cudaError_t launch_pivots(cudaStream_t st, const PivotArgs& a, bool smem_mode, s
     args.prof = prof;
   }
   void* kargs[] = {&args};
-  void* kern = pivots_kernel_ptr(smem_mode, pivots_rq(a.s, a.cpc, smem_mode));
-  static void* attr_done[8] = {};
-  for (void*& k : attr_done) {
-    if (k == kern) break;
-    if (!k) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
-      k = kern;
-      break;
-    }
-  }
+  if (a.s > 512) return cudaErrorInvalidValue;
+  const int rq = pivots_rq(a.s, a.cpc, smem_mode);
+  void* kern = pivots_kernel_ptr(smem_mode, rq, a.s);
+  // one per-device opt-in mask per kernel instance of pivots_kernel_ptr
+  static std::atomic<unsigned long long> attr_done[10];
+  const int ki = a.s > 256 ? 6 + smem_mode : a.s > 128 ? 8 + smem_mode
+               : !smem_mode ? 0 : rq == 8 ? 1 : rq == 16 ? 2 : rq == 24 ? 3 : rq == 32 ? 4 : 5;
+  ensure_smem_optin(kern, 210 * 1024, attr_done[ki]);
   cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3(a.G),
                                               dim3(kPivThreads), kargs, smem, st);
   if (prof && e == cudaSuccess) {
@@ -887,12 +925,9 @@ __global__ void __launch_bounds__(256) cholinv_kernel(const double* __restrict__
 
 cudaError_t launch_cholinv(cudaStream_t st, const double* G, int w, int64_t rows_m, bool shift,
                            bool first, double* Racc, double* Rinv, uint32_t* status) {
-  static bool init = false;
   constexpr int kSm = 3 * kMaxW * kSLD * sizeof(double);
-  if (!init) {
-    cudaFuncSetAttribute(cholinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSm);
-    init = true;
-  }
+  static std::atomic<unsigned long long> init{0};
+  ensure_smem_optin((const void*)cholinv_kernel, kSm, init);
   cholinv_kernel<<<1, 256, kSm, st>>>(G, w, rows_m, shift ? 1 : 0, first ? 1 : 0, Racc, Rinv,
                                        status);
   FFB_LAUNCH_CHECK();
@@ -994,12 +1029,9 @@ __global__ void __launch_bounds__(256) signlu_kernel(const double* __restrict__ 
 cudaError_t launch_signlu(cudaStream_t st, const double* Qtop, int64_t ldq, int w,
                           const double* Racc, double* Y, int64_t ldy, double* T, int64_t ldt,
                           double* R, int64_t ldr, double* Ut, double* D) {
-  static bool init = false;
   constexpr int kSm = 5 * kMaxW * kSLD * sizeof(double);
-  if (!init) {
-    cudaFuncSetAttribute(signlu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSm);
-    init = true;
-  }
+  static std::atomic<unsigned long long> init{0};
+  ensure_smem_optin((const void*)signlu_kernel, kSm, init);
   signlu_kernel<<<1, 256, kSm, st>>>(Qtop, ldq, w, Racc, Y, ldy, T, ldt, R, ldr, Ut, D);
   FFB_LAUNCH_CHECK();
 }
@@ -1064,12 +1096,9 @@ __global__ void __launch_bounds__(256) triinv_upper_kernel(const double* __restr
 
 cudaError_t launch_triinv_upper(cudaStream_t st, const double* Rb, int64_t ldrb, int w,
                                 double* Rinv, int64_t ldo, uint32_t* status) {
-  static bool init = false;
   constexpr int kSm = (2 * 64 * tile64::kTL + 1024) * sizeof(double);
-  if (!init) {
-    cudaFuncSetAttribute(triinv_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSm);
-    init = true;
-  }
+  static std::atomic<unsigned long long> init{0};
+  ensure_smem_optin((const void*)triinv_upper_kernel, kSm, init);
   triinv_upper_kernel<<<1, 256, kSm, st>>>(Rb, ldrb, w, Rinv, ldo, status);
   FFB_LAUNCH_CHECK();
 }
@@ -1415,6 +1444,124 @@ cudaError_t launch_g2(cudaStream_t st, const double* R, int64_t ldr, const int64
   const int threads = (int)((l + 1 + 31) / 32 * 32);
   if (threads <= 512) g2_kernel<512><<<1, threads, smem, st>>>(R, ldr, arr, l, omega, d, g, Z, sc);
   else g2_kernel<1024><<<1, threads, smem, st>>>(R, ldr, arr, l, omega, d, g, Z, sc);
+  FFB_LAUNCH_CHECK();
+}
+
+// ---- g2 for l + 1 > 1024 (srqr.py:49-64): Z = Rtilde^{-1} Omega^T by blocked
+// back substitution on an explicit Rtilde — diagonal blocks of <= 1024 rows
+// solved one thread per row (as g2_kernel), the rows above updated by one
+// engine GEMM per block — then row norms and the first-max argmax.
+
+// Rt (L1 x L1, upper, from launch_r_arranged): diagonal (l, l) <- alpha;
+// Z (L1 x d, column-major) <- Omega^T; flag <- 1 alpha == 0, 2 singular
+__global__ void g2big_prep_kernel(double* Rt, int64_t L1, const double* __restrict__ omega, int d,
+                                  double* Z, const SrqrScalars* sc, uint32_t* flag) {
+  const double alpha = sc->alpha;
+  const int64_t tot = L1 * (int64_t)d;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / L1, k = t - r * L1;
+    Z[k + r * L1] = omega[r * L1 + k];
+    if (r == 0) {
+      if (k == L1 - 1) Rt[k + k * L1] = alpha;
+      const double dv = (k == L1 - 1) ? alpha : Rt[k + k * L1];
+      if (!(alpha > 0.0)) atomicOr(flag, 1u);
+      else if (dv == 0.0) atomicOr(flag, 2u);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024) g2big_diag_kernel(const double* __restrict__ Rt, int64_t L1,
+                                                          int64_t i0, int nbk, double* Z, int d) {
+  __shared__ double zb[2][kG2MaxD];
+  const int t = threadIdx.x;
+  const int64_t k = i0 + t;
+  const bool own = t < nbk;
+  const double rd = own ? 1.0 / Rt[k + k * L1] : 1.0;
+  for (int r0 = 0; r0 < d; r0 += kG2MaxD) {
+    const int dc = d - r0 < kG2MaxD ? d - r0 : kG2MaxD;
+    double z[kG2MaxD];
+#pragma unroll
+    for (int r = 0; r < kG2MaxD; ++r) z[r] = (own && r < dc) ? Z[k + (int64_t)(r0 + r) * L1] : 0.0;
+    double cn = (own && t < nbk - 1) ? Rt[k + (i0 + nbk - 1) * L1] : 0.0;
+    for (int i = nbk - 1; i >= 0; --i) {
+      const int par = i & 1;
+      if (t == i) {
+#pragma unroll
+        for (int r = 0; r < kG2MaxD; ++r)
+          if (r < dc) {
+            z[r] = z[r] * rd;
+            zb[par][r] = z[r];
+          }
+      }
+      const double c = cn;
+      cn = (own && t < i - 1) ? Rt[k + (i0 + i - 1) * L1] : 0.0;   // next step's coefficient
+      __syncthreads();
+      if (t < i) {
+#pragma unroll
+        for (int r = 0; r < kG2MaxD; ++r)
+          if (r < dc) z[r] = fma(-c, zb[par][r], z[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kG2MaxD; ++r)
+      if (own && r < dc) Z[k + (int64_t)(r0 + r) * L1] = z[r];
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(1024) g2big_finish_kernel(const double* __restrict__ Z, int64_t L1,
+                                                            int d, double g, const uint32_t* flag,
+                                                            SrqrScalars* sc) {
+  __shared__ double red_v[32];
+  __shared__ int64_t red_i[32];
+  const uint32_t f = *flag;
+  ArgMax best{-1.0, -1};
+  for (int64_t k = threadIdx.x; k < L1; k += blockDim.x) {
+    double nrm2 = 0.0;
+    for (int r = 0; r < d; ++r) {
+      const double z = Z[k + (int64_t)r * L1];
+      nrm2 = fma(z, z, nrm2);
+    }
+    best = argmax_better(best, ArgMax{sqrt(nrm2), k});
+  }
+  best = block_argmax(best, red_v, red_i);
+  if (threadIdx.x == 0) {
+    if (f & 1u) {
+      sc->g2 = 0.0;
+      sc->i_off = 0;
+      sc->need_swap = 0;
+    } else if (f & 2u) {
+      sc->status |= kStSingular;
+      sc->need_swap = 0;
+    } else {
+      const double g2 = fabs(sc->alpha) / sqrt((double)d) * best.v;
+      sc->g2 = g2;
+      sc->i_off = best.i;
+      sc->need_swap = g2 > g ? 1u : 0u;
+    }
+  }
+}
+
+cudaError_t launch_g2big_prep(cudaStream_t st, double* Rt, int64_t L1, const double* omega, int d,
+                              double* Z, const SrqrScalars* sc, uint32_t* flag) {
+  cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(uint32_t), st);
+  if (e != cudaSuccess) return e;
+  unsigned g = nblk(L1 * (int64_t)d, 256);
+  if (g > 4096) g = 4096;
+  g2big_prep_kernel<<<g, 256, 0, st>>>(Rt, L1, omega, d, Z, sc, flag);
+  FFB_LAUNCH_CHECK();
+}
+
+cudaError_t launch_g2big_diag(cudaStream_t st, const double* Rt, int64_t L1, int64_t i0, int nbk,
+                              double* Z, int d) {
+  g2big_diag_kernel<<<1, (nbk + 31) / 32 * 32, 0, st>>>(Rt, L1, i0, nbk, Z, d);
+  FFB_LAUNCH_CHECK();
+}
+
+cudaError_t launch_g2big_finish(cudaStream_t st, const double* Z, int64_t L1, int d, double g,
+                                const uint32_t* flag, SrqrScalars* sc) {
+  g2big_finish_kernel<<<1, 1024, 0, st>>>(Z, L1, d, g, flag, sc);
   FFB_LAUNCH_CHECK();
 }
 

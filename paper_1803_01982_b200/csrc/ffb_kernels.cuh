@@ -56,7 +56,7 @@ cudaError_t launch_pivots(cudaStream_t st, const PivotArgs& a, bool smem_mode, s
 size_t pivots_smem_bytes(int s, int cpc, bool smem_mode);
 int pivots_stride(int s);
 int pivots_recw(int s);
-void* pivots_kernel_ptr(bool smem_mode, int rq);
+void* pivots_kernel_ptr(bool smem_mode, int rq, int s);
 int pivots_rq(int s, int cpc, bool smem_mode);
 
 cudaError_t launch_gather_cols(cudaStream_t st, const double* src, int64_t ld_src, int64_t rows,
@@ -104,6 +104,12 @@ cudaError_t launch_ext_finish(cudaStream_t st, const double* part, int nparts, i
                               SrqrScalars* sc, const double* u, int64_t m, double* Ql);
 cudaError_t launch_g2(cudaStream_t st, const double* R, int64_t ldr, const int64_t* arr, int64_t l,
                       const double* omega, int d, double g, double* Z, SrqrScalars* sc);
+cudaError_t launch_g2big_prep(cudaStream_t st, double* Rt, int64_t L1, const double* omega, int d,
+                              double* Z, const SrqrScalars* sc, uint32_t* flag);
+cudaError_t launch_g2big_diag(cudaStream_t st, const double* Rt, int64_t L1, int64_t i0, int nbk,
+                              double* Z, int d);
+cudaError_t launch_g2big_finish(cudaStream_t st, const double* Z, int64_t L1, int d, double g,
+                                const uint32_t* flag, SrqrScalars* sc);
 cudaError_t launch_pack(cudaStream_t st, const double* R, int64_t ldr, const int64_t* arr,
                         const double* colsq, int64_t l, int64_t n, double* part, int64_t swaps,
                         SrqrScalars* sc);

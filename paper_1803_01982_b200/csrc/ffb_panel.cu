@@ -563,12 +563,9 @@ cudaError_t launch_panel_qr(cudaStream_t st, int sms, const double* X, int64_t l
                             int w, double* Y, int64_t ldy, double* T, int64_t ldt, double* R,
                             int64_t ldr, double* Qa, double* Qb, double* part, double* Gg,
                             uint32_t* bar, uint32_t* status) {
-  static bool attr = false;
+  static std::atomic<unsigned long long> attr{0};
   const size_t smem = panel_smem_bytes();
-  if (!attr) {
-    cudaFuncSetAttribute(panel_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  ensure_smem_optin((const void*)panel_qr_kernel, (int)smem, attr);
   const int G = panel_grid(sms, Mp);
   PanelArgs a{X, ldx, Mp, w, Y, ldy, T, ldt, R, ldr, Qa, Qb, part, Gg, bar, status,
               (int)((Mp + G - 1) / G), nullptr};

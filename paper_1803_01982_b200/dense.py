@@ -17,14 +17,17 @@ _tls = threading.local()
 _WS_BYTES = (65536 * 4) + (32 << 20)   # stream-K counters + split-K partials
 
 
-def _ws(torch, dev):
+def _ws(torch, dev, stream):
+    """Split-K scratch per (thread, device, stream): ffb_gemm is asynchronous and
+    writes its partials without a sync, so two streams must never share one."""
     cache = getattr(_tls, "ws", None)
     if cache is None:
         cache = _tls.ws = {}
-    buf = cache.get(dev.index)
+    key = (dev.index, stream)
+    buf = cache.get(key)
     if buf is None:
         buf = torch.empty(_WS_BYTES, dtype=torch.uint8, device=dev)
-        cache[dev.index] = buf
+        cache[key] = buf
     return buf
 
 
@@ -81,13 +84,14 @@ def gemm(A, B, out=None, alpha=1.0, beta=0.0):
         return out
     lib = _capi.load()
     ctx = _capi.context(dev.index)
-    ws = _ws(torch, dev)
     a_kc = 1 if la[0] == "row" else 0      # row-major A: A(i,k) = A[k + i*lda]
     b_kc = 1 if lb[0] == "col" else 0      # col-major B: B(k,j) = B[k + j*ldb]
-    stream = torch.cuda.current_stream(dev).cuda_stream
-    rc = lib.ffb_gemm(ctx, C.c_void_p(stream), M, N, K, float(alpha), C.c_void_p(A.data_ptr()),
-                      la[1], a_kc, C.c_void_p(B.data_ptr()), lb[1], b_kc, float(beta),
-                      C.c_void_p(out.data_ptr()), lc[1], C.c_void_p(ws.data_ptr()), ws.numel())
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        ws = _ws(torch, dev, stream)
+        rc = lib.ffb_gemm(ctx, C.c_void_p(stream), M, N, K, float(alpha), C.c_void_p(A.data_ptr()),
+                          la[1], a_kc, C.c_void_p(B.data_ptr()), lb[1], b_kc, float(beta),
+                          C.c_void_p(out.data_ptr()), lc[1], C.c_void_p(ws.data_ptr()), ws.numel())
     if rc != _capi.FFB_OK:
         raise RuntimeError(f"ffb_gemm failed ({rc}): {_capi.last_error(ctx)}")
     return out
@@ -101,9 +105,10 @@ def sumsq(x):
     lib = _capi.load()
     part = torch.empty(lib.ffb_svt_partials(), dtype=torch.float64, device=x.device)
     out = torch.empty(1, dtype=torch.float64, device=x.device)
-    stream = torch.cuda.current_stream(x.device).cuda_stream
-    rc = lib.ffb_sumsq(C.c_void_p(stream), C.c_void_p(x.data_ptr()), x.numel(),
-                       C.c_void_p(part.data_ptr()), C.c_void_p(out.data_ptr()))
+    with torch.cuda.device(x.device):
+        stream = torch.cuda.current_stream(x.device).cuda_stream
+        rc = lib.ffb_sumsq(C.c_void_p(stream), C.c_void_p(x.data_ptr()), x.numel(),
+                           C.c_void_p(part.data_ptr()), C.c_void_p(out.data_ptr()))
     if rc != _capi.FFB_OK:
         raise RuntimeError(f"ffb_sumsq failed ({rc})")
     return out
@@ -135,3 +140,40 @@ def spectral_norm(M, tol=1e-15, max_iter=5000, seed=1234):
             break
         prev = est
     return est
+
+
+def small_svd(M):
+    """(U, sig, V) of a square float64 CUDA matrix via the engine's one-sided
+    block Jacobi (ffb_small_svd): the device replacement for the dgesdd of the
+    flip-flop tail (ffsrqr/svd.py:79).  sig descending; M = U diag(sig) V^T."""
+    import torch
+
+    from .errors import DimensionError, NumericalError
+
+    l, l2 = M.shape
+    if l != l2:
+        raise DimensionError("small_svd expects a square matrix")
+    dev = M.device
+    if not (M.stride(0) == 1 and M.stride(1) >= l):
+        M = M.t().contiguous().t()
+    lib = _capi.load()
+    ctx = _capi.context(dev.index)
+    nb = C.c_size_t()
+    if lib.ffb_small_svd_workspace_query(l, C.byref(nb)) != _capi.FFB_OK:
+        raise DimensionError("invalid size")
+    ws = torch.empty(nb.value, dtype=torch.uint8, device=dev)
+    U = colmajor(torch, l, l, dev)
+    V = colmajor(torch, l, l, dev)
+    sig = torch.empty(l, dtype=torch.float64, device=dev)
+    sw = C.c_int32(0)
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        rc = lib.ffb_small_svd(ctx, C.c_void_p(stream), C.c_void_p(M.data_ptr()), l, M.stride(1),
+                               C.c_void_p(sig.data_ptr()), C.c_void_p(U.data_ptr()), l,
+                               C.c_void_p(V.data_ptr()), l, C.c_void_p(ws.data_ptr()), ws.numel(),
+                               C.byref(sw))
+    if rc == _capi.FFB_ERR_NUMERICAL:
+        raise NumericalError(_capi.last_error(ctx))
+    if rc != _capi.FFB_OK:
+        raise RuntimeError(f"ffb_small_svd failed ({rc}): {_capi.last_error(ctx)}")
+    return U, sig, V, int(sw.value)

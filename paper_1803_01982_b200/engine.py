@@ -24,7 +24,7 @@ import threading
 
 import numpy as np
 
-from . import _capi, rng
+from . import _capi, flops, rng
 from .errors import (CertificationError, DimensionError, EngineUnavailable, NonFiniteInputError,
                      NumericalError, SingularTrailingBlockError)
 from .results import (ApproxSvd, PartialFactorization, SketchParams, SrqrCertificate, SrqrResult,
@@ -193,7 +193,9 @@ def _to_device_colmajor(A, device):
 
 
 def _workspace(torch, device, nbytes):
-    key = (device.index,)
+    """Engine workspace per (thread, device, stream): the engine writes it
+    asynchronously, so work queued on two streams must not share one."""
+    key = (device.index, torch.cuda.current_stream(device).cuda_stream)
     cache = getattr(_tls, "ws", None)
     if cache is None:
         cache = _tls.ws = {}
@@ -261,10 +263,8 @@ def run(A, params: SketchParams, mode, device=None, trace_gaps=False):
         prm = params.resolve(m, n)
         if mode != _capi.FFB_MODE_TRQRCP and prm.l + 1 > min(m, n):
             raise DimensionError(f"srqr needs l+1 <= min(m,n); got l={prm.l}, min={min(m, n)}")
-        if prm.b > 128:
-            raise DimensionError("the B200 engine supports block sizes b <= 128")
-        if prm.b + prm.p > 128:
-            raise DimensionError("the B200 engine supports sketch sizes b + p <= 128")
+        if prm.b + prm.p > 512:
+            raise DimensionError("the B200 engine supports sketch sizes b + p <= 512")
         lib = _capi.load()
         ctx = _capi.context(dev.index)
         cp = _capi.Params(prm.k, prm.l, prm.b, prm.p, prm.d, prm.epsilon, prm.g,
@@ -373,14 +373,24 @@ def flip_flop_srqr(A, k, l=None, b=32, p=5, epsilon=0.5, g=2.0, d=None, seed=0, 
     out = run(A, params, _capi.FFB_MODE_FLIPFLOP, device=device, trace_gaps=trace_gaps)
     np_ = out["is_numpy"]
     res = _srqr_result(out)
+    prm = out["params"]
+    # the reference's own tally (ffsrqr/flops.py), replayed from the run's shapes
+    # and swap trace; the flops the device executed are meta["device_flops"]
+    fc = flops.flip_flop_count(out["m"], out["n"], prm.k, prm.l, prm.b, prm.p, prm.d,
+                               out["swaps"], out["i_offs"], out["alpha"] == 0.0)
     meta = {"srqr": res, "params": out["params"], "method": "flip_flop_srqr",
+            "device_flops": out["flops"],
             "diag_L": _conv(out["diag_L"], np_), "sv_all": _conv(out["sv_all"], np_),
             "pivot_gap": _conv(out["pivot_gap"], np_) if "pivot_gap" in out else None,
             "engine": "ffb200-sm100a",
             "kernels": out["kernels"], "i_offs": out["i_offs"],
-            "svd_sweeps": out["svd_sweeps"]}
+            "svd_sweeps": out["svd_sweeps"],
+            # exact zero on an R11 diagonal: the sketch update used a zero inverse row
+            # where the reference takes lstsq (sketch.py:75-83); only the order of
+            # rank-deficient noise columns can differ
+            "zero_pivot": bool(out["status_bits"] & 8)}
     return ApproxSvd(u=_conv(out["u"], np_), s=_conv(out["s"], np_), v=_conv(out["v"], np_),
-                     flop_count=out["flops"], meta=meta)
+                     flop_count=fc, meta=meta)
 
 
 def srqr(A, params: SketchParams, device=None):
@@ -418,8 +428,6 @@ def rsisvd(A, k, p=5, q=2, seed=0, device=None):
     if p < 0 or q < 0:
         raise DimensionError("rsisvd needs p >= 0 and q >= 0")
     r = min(k + p, min(m, n))
-    if r > 512:
-        raise DimensionError("the B200 engine supports rsisvd widths k + p <= 512")
     dev = _device(device if device is not None else (A.device if isinstance(A, torch.Tensor) and A.is_cuda else None))
     with torch.cuda.device(dev):
         Ad, is_np = _to_device_colmajor(A, dev)
@@ -431,12 +439,14 @@ def rsisvd(A, k, p=5, q=2, seed=0, device=None):
             raise DimensionError("invalid dimensions for the engine")
         ws = _workspace(torch, dev, nbytes.value)
         key = (dev.index, n, r, int(seed) & 0xFFFFFFFFFFFFFFFF)
-        om = _rs_omega_cache.get(key)
+        with _omega_lock:
+            om = _rs_omega_cache.get(key)
         if om is None:
             om = torch.from_numpy(rng.gaussian(n, r, seed, rng.STREAM_RSISVD)).to(dev)
-            if len(_rs_omega_cache) > 64:
-                _rs_omega_cache.clear()
-            _rs_omega_cache[key] = om
+            with _omega_lock:
+                if len(_rs_omega_cache) > 64:
+                    _rs_omega_cache.clear()
+                _rs_omega_cache[key] = om
         u = _colmajor(torch, m, k, dev)
         s = torch.empty(k, dtype=torch.float64, device=dev)
         v = _colmajor(torch, n, k, dev)
@@ -455,6 +465,6 @@ def rsisvd(A, k, p=5, q=2, seed=0, device=None):
                 raise NumericalError(msg)
             raise RuntimeError(f"ffb_rsisvd failed ({rc}): {msg}")
         meta = {"method": "rsisvd", "q": q, "p": p, "engine": "ffb200-sm100a",
-                "svd_sweeps": int(sw.value)}
+                "svd_sweeps": int(sw.value), "device_flops": int(fl.value)}
         return ApproxSvd(u=_conv(u, is_np), s=_conv(s, is_np), v=_conv(v, is_np),
-                         flop_count=int(fl.value), meta=meta)
+                         flop_count=flops.rsisvd_count(m, n, k, r, q), meta=meta)

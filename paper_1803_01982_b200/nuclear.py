@@ -71,8 +71,6 @@ class _PartialSvd:
     def __call__(self, M, sv):
         sv = min(sv, self.cap)
         if self.engine == "exact" or sv >= self.min_dim:
-            if self.min_dim > 512:
-                raise DimensionError("exact partial SVD on the device needs min(m, n) <= 512")
             ap = rsisvd(M, sv, p=self.min_dim - sv, q=0, seed=self.seed)
         elif self.engine == "flipflop":
             l = min(sv + 60, self.min_dim - 1)
@@ -105,9 +103,10 @@ def _shrink_spectrum(psvd, W, sv, mu):
         return X, 0
     Us = dense.colmajor(torch, m, keep, W.device)
     lib = _capi.load()
-    stream = torch.cuda.current_stream(W.device).cuda_stream
-    rc = lib.ffb_shrink_cols(C.c_void_p(stream), C.c_void_p(U.data_ptr()), U.stride(1), m, keep,
-                             C.c_void_p(s.data_ptr()), 1.0 / mu, C.c_void_p(Us.data_ptr()), m)
+    with torch.cuda.device(W.device):
+        stream = torch.cuda.current_stream(W.device).cuda_stream
+        rc = lib.ffb_shrink_cols(C.c_void_p(stream), C.c_void_p(U.data_ptr()), U.stride(1), m, keep,
+                                 C.c_void_p(s.data_ptr()), 1.0 / mu, C.c_void_p(Us.data_ptr()), m)
     if rc != _capi.FFB_OK:
         raise RuntimeError(f"ffb_shrink_cols failed ({rc})")
     dense.gemm(Us, V[:, :keep].t(), out=X)
@@ -130,13 +129,14 @@ def _device_matrix(M):
 def _update(mode, M, X, Y, E, mask, mu, thresh, mu_next, W, part, zsq):
     torch = _torch()
     lib = _capi.load()
-    stream = torch.cuda.current_stream(M.device).cuda_stream
-    rc = lib.ffb_ialm_update(C.c_void_p(stream), mode, C.c_void_p(M.data_ptr()),
-                             C.c_void_p(X.data_ptr()), C.c_void_p(Y.data_ptr()),
-                             C.c_void_p(E.data_ptr()), C.c_void_p(mask.data_ptr() if mask is not None else 0),
-                             M.numel(), float(mu), float(thresh), float(mu_next),
-                             C.c_void_p(W.data_ptr()), C.c_void_p(part.data_ptr()),
-                             C.c_void_p(zsq.data_ptr()))
+    with torch.cuda.device(M.device):
+        stream = torch.cuda.current_stream(M.device).cuda_stream
+        rc = lib.ffb_ialm_update(C.c_void_p(stream), mode, C.c_void_p(M.data_ptr()),
+                                 C.c_void_p(X.data_ptr()), C.c_void_p(Y.data_ptr()),
+                                 C.c_void_p(E.data_ptr()), C.c_void_p(mask.data_ptr() if mask is not None else 0),
+                                 M.numel(), float(mu), float(thresh), float(mu_next),
+                                 C.c_void_p(W.data_ptr()), C.c_void_p(part.data_ptr()),
+                                 C.c_void_p(zsq.data_ptr()))
     if rc != _capi.FFB_OK:
         raise RuntimeError(f"ffb_ialm_update failed ({rc})")
 

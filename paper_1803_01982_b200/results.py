@@ -168,3 +168,8 @@ class ApproxSvd:
 def flip_flop_flop_formula(m, n, l, b, p):
     """Leading-order flop budget 4mnl + 2(b+p)mn (ffsrqr/svd.py:258-260)."""
     return 4 * m * n * l + 2 * (b + p) * m * n
+
+
+def rsisvd_flop_formula(m, n, k, p, q):
+    """Leading-order flop budget (4q+4)mn(k+p) of subspace iteration (ffsrqr/svd.py:263-265)."""
+    return (4 * q + 4) * m * n * (k + p)

@@ -159,8 +159,6 @@ def _make_engine(engine, seed):
         # full-width RSISVD with no power step is an exact SVD (Q spans range(M))
         def _exact(M, r):
             mn = min(M.shape)
-            if mn > 512:
-                raise DimensionError("exact engine on the device is limited to min(m, n) <= 512")
             return rsisvd(M, r, p=mn - r, q=0, seed=seed)
         return _exact
     raise ValueError(f"unknown low-rank engine {engine!r}")

@@ -242,3 +242,36 @@ def test_non_finite_input_raises(ffb, bad):
             call()
         with pytest.raises(ffb.NumericalError):
             call()
+
+
+@pytest.mark.parametrize("name", [n for n in CASES if "flop_count" in load(n)])
+def test_flop_count_matches_reference(ffb, name):
+    # flop_count is the reference's tally (ffsrqr/flops.py) replayed with the
+    # device run's swap trace; the golden holds the reference's own count
+    c = load(name)
+    try:
+        ap = ffb.flip_flop_srqr(c["A"], c["k"], l=c["l"], b=c["b"], p=c["p"], g=c["g"], d=c["d"],
+                                seed=c["seed"])
+    except ffb.CertificationError:
+        pytest.skip("certification failure: no flop_count")
+    want = int(c["flop_count"])
+    full_rank = c["cert"][0] != 0.0 and c["m"] > c["b"] + c["p"]
+    if full_rank:
+        # shape-only call sites plus the traced Givens chases
+        assert abs(ap.flop_count - want) <= 1e-3 * want, (ap.flop_count, want)
+    else:
+        assert abs(ap.flop_count - want) <= 0.03 * want, (ap.flop_count, want)
+    assert ap.meta["device_flops"] > 0
+
+
+def test_flop_count_band_1000(ffb):
+    # ffsrqr tests/test_svd.py:105-112 through the device engine
+    g = np.random.default_rng(9)
+    U, _ = np.linalg.qr(g.standard_normal((1000, 100)))
+    V, _ = np.linalg.qr(g.standard_normal((1000, 100)))
+    A = (U * (1.0 / np.arange(1, 101))) @ V.T
+    ap = ffb.flip_flop_srqr(A, 25, l=30, b=32, p=5, seed=0)
+    formula = ffb.flip_flop_flop_formula(1000, 1000, 30, 32, 5)
+    assert abs(ap.flop_count - formula) <= 0.15 * formula
+    rs = ffb.rsisvd(A, 30, p=5, q=1, seed=0)
+    assert abs(rs.flop_count - ffb.rsisvd_flop_formula(1000, 1000, 30, 5, 1)) <= 0.15 * rs.flop_count
