@@ -11,9 +11,15 @@ flip_flop_srqr factorization of the device-resident matrix through the engine
 (sketch, TRQRCP, SRQR certificate, partial LQ, A*Qhat, small SVD, back-map).
 A (537 MB) exceeds the 126 MB L2, so no flush is needed between steps.
 
-Multi-GPU (torchrun, one rank per GPU): every rank factorizes its own matrix
-(seed = rank) — weak scaling, no collective on the data path; the per-step
-time is the max over ranks (NCCL all-reduce of CUDA-event times).
+Multi-GPU: one rank per GPU.  ``--gpus N`` without a torchrun environment
+re-launches itself under ``torch.distributed.run`` with N ranks (127.0.0.1).
+cfg1-3 run replicas (every rank factorizes its own matrix: weak scaling, no
+collective on the data path); cfg4/cfg5 partition their independent problems
+contiguously over the ranks (strong scaling) and gather every problem's
+result slot (U, s, V, perm, certificate; cfg4: U, s, perm) to rank 0 with
+NCCL on a dedicated stream while the remaining problems compute.  Times are
+CUDA events, max over ranks.  ``--dry`` runs the partition + gather logic on
+CPU with gloo (placeholder slots) for the CPU test suite.
 
 --impl reference: times the CPU oracle port of the reference algorithm
 (oracle/, numpy + OpenBLAS on all host cores) on the same workload, rank 0 only.
@@ -21,6 +27,7 @@ time is the max over ranks (NCCL all-reduce of CUDA-event times).
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,15 +40,31 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP64_PEAK_TFLOPS = 37.0   # measured DMMA peak on this pool's B200 (profiles/r01_fp64_peak.md)
+FP64_PEAK_SOURCE = "measured DMMA peak, profiles/r01_fp64_peak.md (MEASURED_PEAKS.json has no FP64 entry)"
 METRIC = "flip_flop_srqr_factorizations_per_s"
+L2_BYTES = 126 * 2 ** 20
 
 
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return json.load(f)
-    except OSError:
+    except (OSError, ValueError):
         return {}
+
+
+def hbm_peak():
+    """(GB/s, source): MEASURED_PEAKS.json's HBM copy bandwidth, else the recipe's fallback."""
+    pk = _peaks()
+    for key in ("hbm_gbps", "hbm_GBps", "hbm_bw_gbps", "copy_gbps"):
+        if isinstance(pk.get(key), (int, float)):
+            return float(pk[key]), f"MEASURED_PEAKS.json:{key}"
+    for v in pk.values():
+        if isinstance(v, dict):
+            for key in ("hbm_gbps", "copy_gbps", "GB/s"):
+                if isinstance(v.get(key), (int, float)):
+                    return float(v[key]), "MEASURED_PEAKS.json"
+    return 6546.9, "MEASURED_PEAKS.json value recorded in DESIGN.md (file absent)"
 
 
 class ClockSampler:
@@ -112,6 +135,41 @@ def dist_init():
     return ws, rank, local
 
 
+def maybe_spawn(args):
+    """`--gpus N` outside torchrun: re-launch this script with N ranks."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def workload_config(args, ws):
+    """The config dict both arms print (the driver compares them)."""
+    from paper_1803_01982_b200 import workloads
+
+    cfg = workloads.CONFIGS[args.workload]
+    a_bytes = cfg.m * cfg.n * 8
+    d = {"workload": args.workload, "m": cfg.m, "n": cfg.n, "k": cfg.k, "p": cfg.p, "b": cfg.b,
+         "l": cfg.l, "batch": cfg.batch,
+         "l2_flush": (f"input A {a_bytes / 1e6:.0f} MB per problem > {L2_BYTES / 1e6:.0f} MB L2 "
+                      "(no explicit flush)") if a_bytes > L2_BYTES else
+                     (f"per-problem A {a_bytes / 1e6:.0f} MB; the {cfg.batch}-problem batch "
+                      f"({cfg.batch * a_bytes / 1e9:.1f} GB) streams through the "
+                      f"{L2_BYTES / 1e6:.0f} MB L2 (no explicit flush)") if cfg.batch * a_bytes > 2 * L2_BYTES else
+                     f"input A {a_bytes / 1e6:.0f} MB fits L2: a 512 MB buffer is written between "
+                     "timed steps (per-step CUDA events, flush outside them)"}
+    if cfg.batch > 1:
+        d["parallelism"] = f"partitioned x{ws} (contiguous)" if ws > 1 else "single GPU, all problems"
+    else:
+        d["parallelism"] = f"replicas x{ws}" if ws > 1 else "single"
+    return d
+
+
 def make_workload(name, seed, device):
     from paper_1803_01982_b200 import workloads
 
@@ -123,44 +181,252 @@ def make_workload(name, seed, device):
     return cfg, A
 
 
-def k13_traffic(workload):
-    """DRAM bytes per launch of the roofline kernel from the committed ncu capture
-    (profiles/*_k13_ncu.json, `ncu --set full`), or None."""
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the newest committed ncu --set full
+    summary (profiles/*_traffic.json: {kernel: {"dram_bytes": .., "source": ..}})."""
     import glob
 
-    best, src = None, None
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_k13_ncu.json"))):
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json"))):
         try:
             with open(path) as f:
                 d = json.load(f)
         except (OSError, ValueError):
             continue
-        if d.get("workload") == workload:
-            best, src = d, os.path.relpath(path, ROOT)
-    if best is None:
-        return None, None
-    return best["dram_bytes_read"] + best["dram_bytes_write"], src
+        if kernel in d:
+            best = (d[kernel]["dram_bytes"], os.path.relpath(path, ROOT) + ": " + d[kernel].get("source", ""))
+    return best if best else (None, None)
+
+
+# --------------------------------------------------------------------- stages
+def kernel_family(name):
+    import re
+
+    n = re.sub(r"\(.*", "", name).replace("void ", "")
+    n = re.sub(r"<.*", "", n)
+    return n.split("::")[-1]
+
+
+def panel_bytes(m, n, l, b):
+    """Algorithmic bytes of every panel_qr launch of one factorization: each
+    Mp x wb panel read once and its reflectors written once (2 * 8 Mp wb)."""
+    tot = 0
+    j0 = 0
+    while j0 < l:                                 # TRQRCP blocks: (m - j0) x bb, 64-wide panels
+        bb = min(b, l - j0)
+        for c0 in range(0, bb, 64):
+            tot += 2 * 8 * (m - j0 - c0) * min(64, bb - c0)
+        j0 += bb
+    for rows in (n, m):                           # partial LQ of R^T (n x l), QR of tmp (m x l)
+        for c0 in range(0, l, 64):
+            tot += 2 * 8 * (rows - c0) * min(64, l - c0)
+    return tot
+
+
+def pivot_bytes(n, l, b, p):
+    """sum over blocks of bb * 8 * s * (n - j0)."""
+    s = b + p
+    tot, j0 = 0, 0
+    while j0 < l:
+        bb = min(b, l - j0)
+        tot += bb * 8 * s * (n - j0)
+        j0 += bb
+    return tot
+
+
+def stage_table(cfg, kern_times, counts, step_ms, hbm_gbps):
+    """Top kernel families of one factorization: share of the step, algorithmic
+    work, achieved rate and roofline fraction."""
+    from paper_1803_01982_b200 import flip_flop_flop_formula
+
+    m, n, l, b, p = cfg.m, cfg.n, cfg.l, cfg.b, cfg.p
+    algo = {
+        "gemm_f64_kernel": ("tensor", flip_flop_flop_formula(m, n, l, b, p), "flop",
+                            "sketch + WT + A*Qhat GEMMs: 4mnl + 2(b+p)mn (svd.py:258-260)"),
+        "jacobi_kernel": ("tensor", 6 * l ** 3, "flop",
+                          "count_svd(l, l) = 6 l^3 (flops.py:49-52) of the l x l SVD"),
+        "jacobi_general_kernel": ("tensor", 6 * l ** 3, "flop", "count_svd(l, l) = 6 l^3"),
+        "panel_qr_kernel": ("hbm", panel_bytes(m, n, l, b), "byte",
+                            "each Mp x wb panel read once + reflectors written once"),
+        "pivots_kernel": ("hbm", pivot_bytes(n, l, b, p), "byte",
+                          "SURVEY 8(d) K2: sum_blocks bb * 8 s (n - j0)"),
+    }
+    tot = sum(kern_times.values())
+    rows = []
+    for fam, t_ms in sorted(kern_times.items(), key=lambda kv: -kv[1])[:6]:
+        ent = {"kernel": fam, "launches": counts[fam], "ms": round(t_ms, 4),
+               "share_of_kernel_time": round(t_ms / tot, 4) if tot else None,
+               "share_of_step": round(t_ms / step_ms, 4)}
+        if fam in algo:
+            bound, work, unit, note = algo[fam]
+            if unit == "flop":
+                ach = work / (t_ms * 1e-3) / 1e12
+                ent.update(bound=bound, algorithmic_flop=work, achieved=ach, unit="TFLOP/s",
+                           peak=FP64_PEAK_TFLOPS, frac=ach / FP64_PEAK_TFLOPS, algorithm=note)
+            else:
+                ach = work / (t_ms * 1e-3) / 1e9
+                ent.update(bound=bound, algorithmic_bytes=work, achieved=ach, unit="GB/s",
+                           peak=hbm_gbps, frac=ach / hbm_gbps, algorithm=note)
+        else:
+            ent.update(bound="latency", note="small kernels: launch/latency bound")
+        rows.append(ent)
+    return rows
+
+
+def profile_kernels(step):
+    """Per-family device time of one step from CUPTI activity records
+    (torch.profiler) — the share table; the headline numbers are CUDA events."""
+    from collections import defaultdict
+
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    times, counts = defaultdict(float), defaultdict(int)
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        step()
+        torch.cuda.synchronize()
+    for ev in prof.events():
+        dt = getattr(ev, "device_type", None)
+        if dt is None or "CUDA" not in str(dt):
+            continue
+        us = getattr(ev, "device_time", None)
+        if us is None:
+            us = getattr(ev, "cuda_time", 0.0)
+        fam = kernel_family(ev.name)
+        if fam.startswith("Memset") or fam.startswith("Memcpy") or "memset" in fam.lower():
+            continue
+        times[fam] += us / 1e3
+        counts[fam] += 1
+    return dict(times), dict(counts)
+
+
+def time_top_kernel(fam, cfg, A, st, dev, ctx, lib):
+    """CUDA-event time of one launch of the step's dominant kernel family, run
+    standalone on the bench stream with the step's shapes."""
+    import ctypes as C
+
+    import torch
+
+    m, n, l = cfg.m, cfg.n, cfg.l
+    if fam == "gemm_f64_kernel":
+        # K13 A*Yhat (m x l x n), the largest GEMM of the step
+        Yh = torch.randn(n, l, dtype=torch.float64, device=dev).t().contiguous().t()
+        out = torch.empty((l, m), dtype=torch.float64, device=dev).t()
+        wsb = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
+
+        def launch():
+            lib.ffb_gemm(ctx, C.c_void_p(st.cuda_stream), m, l, n, 1.0, C.c_void_p(A.data_ptr()),
+                         A.stride(1), 0, C.c_void_p(Yh.data_ptr()), n, 1, 0.0,
+                         C.c_void_p(out.data_ptr()), m, C.c_void_p(wsb.data_ptr()), wsb.numel())
+        work, unit, note = 2.0 * m * n * l, "flop", "K13 A*Qhat (m x l x n): 2mnl flop"
+    elif fam in ("jacobi_kernel", "jacobi_general_kernel"):
+        # the l x l SVD on an R_t with the workload's leading spectrum
+        from paper_1803_01982_b200 import workloads
+
+        g = np.random.default_rng(0)
+        U0, _ = np.linalg.qr(g.standard_normal((l, l)))
+        V0, _ = np.linalg.qr(g.standard_normal((l, l)))
+        s0 = workloads.spectrum(cfg.name if cfg.name != "cfg4" else "cfg5", l)
+        R = np.linalg.qr((U0 * s0) @ V0.T, mode="r")
+        Rd = torch.from_numpy(np.asfortranarray(R)).to(dev)
+        nb = C.c_size_t()
+        lib.ffb_small_svd_workspace_query(l, C.byref(nb))
+        wsb = torch.empty(nb.value, dtype=torch.uint8, device=dev)
+        U = torch.empty((l, l), dtype=torch.float64, device=dev)
+        V = torch.empty((l, l), dtype=torch.float64, device=dev)
+        sg = torch.empty(l, dtype=torch.float64, device=dev)
+        sw = C.c_int32(0)
+
+        def launch():
+            lib.ffb_small_svd(ctx, C.c_void_p(st.cuda_stream), C.c_void_p(Rd.data_ptr()), l, l,
+                              C.c_void_p(sg.data_ptr()), C.c_void_p(U.data_ptr()), l,
+                              C.c_void_p(V.data_ptr()), l, C.c_void_p(wsb.data_ptr()), wsb.numel(),
+                              C.byref(sw))
+        work, unit, note = 6.0 * l ** 3, "flop", "count_svd(l, l) = 6 l^3 (l x l SVD with vectors)"
+    else:
+        return None
+    for _ in range(3):
+        launch()
+    torch.cuda.synchronize()
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    g0.record(st)
+    for _ in range(reps):
+        launch()
+    g1.record(st)
+    torch.cuda.synchronize()
+    ms = g0.elapsed_time(g1) / reps
+    return ms, work, unit, note
+
+
+# ------------------------------------------------------------------- batched
+def slot_layout(cfg, workload):
+    """Per-problem result slot (float64 words): U (m k), s (k), [V (n k)], perm (n,
+    int64 bits), certificate (8)."""
+    parts = [("u", cfg.m * cfg.k), ("s", cfg.k)]
+    if workload != "cfg4":              # HOSVD ignores V (tensor.py:114)
+        parts.append(("v", cfg.n * cfg.k))
+    parts += [("perm", cfg.n), ("cert", 8)]
+    return parts
+
+
+def pack_slot(res, parts, out):
+    """Flatten one ApproxSvd into its slot row (device copies on the current stream)."""
+    import torch
+
+    off = 0
+    for name, cnt in parts:
+        dst = out[off:off + cnt]
+        if name == "u":
+            dst.view(res.u.shape[1], res.u.shape[0]).copy_(res.u.t())
+        elif name == "v":
+            dst.view(res.v.shape[1], res.v.shape[0]).copy_(res.v.t())
+        elif name == "s":
+            dst.copy_(res.s)
+        elif name == "perm":
+            dst.copy_(res.meta["srqr"].fact.perm.view(torch.float64))
+        else:
+            c = res.meta["srqr"].cert
+            dst.copy_(torch.tensor([c.alpha, c.g1, c.g2, c.swaps, c.tau_bound, c.tau_hat_bound,
+                                    res.meta["srqr"].r22_norm_estimate, 0.0], dtype=torch.float64))
+        off += cnt
 
 
 def run_batched(args):
     """cfg4 / cfg5: independent problems partitioned contiguously over the ranks
-    (paper_1803_01982_b200.batch.partition); each rank factorizes its share, then
-    the singular values and certificates are gathered to rank 0 (the only
-    collective).  Strong scaling: the total number of problems is fixed."""
+    (batch.partition); each rank factorizes its share on several streams, with
+    Omega generated on the host inside the timed region (every matrix of cfg5
+    has its own seed), and each finished chunk of result slots is all-gathered
+    to rank 0 on a dedicated NCCL stream while the next chunk computes."""
     import torch
     import torch.distributed as dist
 
     import paper_1803_01982_b200 as ffb
-    from paper_1803_01982_b200 import batch, workloads
+    from paper_1803_01982_b200 import batch, engine, workloads
 
     ws, rank, local = dist_init()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dry = args.dry
+    dev = torch.device("cpu") if dry else torch.device("cuda", local)
+    if not dry:
+        torch.cuda.set_device(local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if dry:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     cfg = workloads.CONFIGS[args.workload]
     mine = list(batch.partition(cfg.batch, ws, rank))
-    if args.workload == "cfg4":
+    shares = [len(batch.partition(cfg.batch, ws, r)) for r in range(ws)]
+    pad = max(shares)
+    parts = slot_layout(cfg, args.workload)
+    slot_len = sum(c for _, c in parts)
+    if args.streams <= 0:
+        args.streams = 8 if args.workload == "cfg5" else 1
+    chunk = max(1, args.streams)
+    if dry:
+        probs = {i: None for i in mine}
+        seed_of = lambda i: i
+    elif args.workload == "cfg4":
         unf = workloads.torch_tensor_unfoldings(seed=0, device=dev)
         probs = {i: unf[i] for i in mine}
         seed_of = lambda i: 0
@@ -168,104 +434,165 @@ def run_batched(args):
         probs = {i: workloads.torch_matrix("cfg5", seed=i, device=dev) for i in mine}
         seed_of = lambda i: i
     m, n = cfg.m, cfg.n
-    if args.streams <= 0:
-        args.streams = 8 if args.workload == "cfg5" else 1
-    # Omega for every local problem, generated on host threads (the reference RNG)
-    # before the warm-up; SVT iterations reuse a fixed seed, so steady state
-    # sees cached sketches
-    from paper_1803_01982_b200 import engine
-    engine.prefetch_omega([(cfg.b + cfg.p, m, seed_of(i)) for i in mine], device=dev,
-                          threads=min(16, len(os.sched_getaffinity(0))))
+    local_slots = torch.zeros((pad, slot_len), dtype=torch.float64, device=dev) if (ws > 1 or dry) else None
+    gathered = torch.zeros((ws, pad, slot_len), dtype=torch.float64, device=dev) if ws > 1 else None
+    comm = None if dry else torch.cuda.Stream(device=dev)
 
     def solve(i):
-        return ffb.flip_flop_srqr(probs[i], cfg.k, l=cfg.l, b=cfg.b, p=cfg.p, seed=seed_of(i))
+        if dry:
+            return None
+        r = ffb.flip_flop_srqr(probs[i], cfg.k, l=cfg.l, b=cfg.b, p=cfg.p, seed=seed_of(i))
+        if ws > 1:
+            pack_slot(r, parts, local_slots[i - mine[0]])
+        return r
 
-    def step():
-        if args.streams > 1:
-            res = batch.run_streams(mine, solve, n_streams=args.streams, device=dev)
-        else:
-            res = [solve(i) for i in mine]
-        local_s = torch.stack([r.s for r in res]) if res else torch.zeros((0, cfg.k), dtype=torch.float64, device=dev)
-        return batch.gather_slots(local_s, cfg.batch, (cfg.k,), rank, ws, dev)
+    def step(fresh_omega=True):
+        if fresh_omega and not dry:
+            engine.clear_omega_cache()       # every step generates its sketches on the host
+        works = []
+        for c0 in range(0, pad, chunk):
+            ids = [mine[j] for j in range(c0, min(c0 + chunk, len(mine)))]
+            if dry:
+                for i in ids:
+                    local_slots[i - mine[0]].fill_(float(i))
+            elif len(ids) > 1:
+                batch.run_streams(ids, solve, n_streams=args.streams, device=dev)
+            else:
+                for i in ids:
+                    solve(i)
+            if ws > 1:
+                seg = local_slots[c0:c0 + chunk]
+                outs = [gathered[r, c0:c0 + chunk] for r in range(ws)]
+                if dry:
+                    dist.all_gather(outs, seg.contiguous())
+                else:
+                    ev = torch.cuda.Event()
+                    ev.record(torch.cuda.current_stream(dev))
+                    comm.wait_event(ev)
+                    with torch.cuda.stream(comm):
+                        works.append(dist.all_gather(outs, seg, async_op=True))
+        for w in works:
+            w.wait()
+        if not dry:
+            torch.cuda.current_stream(dev).wait_stream(comm)
 
+    # host Omega generation cost for this rank's problems (reported separately too)
+    om_ms = None
+    if not dry:
+        engine.clear_omega_cache()
+        t0 = time.perf_counter()
+        engine.prefetch_omega([(cfg.b + cfg.p, m, seed_of(i)) for i in mine], device=dev, threads=1)
+        torch.cuda.synchronize()
+        om_ms = (time.perf_counter() - t0) * 1e3
     for _ in range(max(args.warmup, 3)):
         step()
-    torch.cuda.synchronize()
+    if not dry:
+        torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
-    torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    clocks.start()
-    i0 = clocks.ready()
-    st = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    for _ in range(args.steps):
-        gathered = step()
-    e1.record(st)
-    torch.cuda.synchronize()
-    clk = clocks.stop(i0)
-    ms = e0.elapsed_time(e1) / args.steps
+    if dry:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step()
+        ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        clk = {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["dry run: no GPU"]}
+    else:
+        torch.cuda.synchronize()
+        clocks = ClockSampler(local)
+        clocks.start()
+        i0 = clocks.ready()
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(args.steps):
+            step()
+        e1.record(st)
+        torch.cuda.synchronize()
+        clk = clocks.stop(i0)
+        ms = e0.elapsed_time(e1) / args.steps
     if ws > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    ok = True
+    if ws > 1 and rank == 0:
+        # every problem's slot reached rank 0 (singular values positive / dry markers)
+        for r in range(ws):
+            for j in range(shares[r]):
+                i = sum(shares[:r]) + j
+                row = gathered[r, j]
+                ok &= bool(row[0].item() == float(i)) if dry else bool(row[m * cfg.k].item() > 0)
     if rank == 0:
         flop_alg = ffb.flip_flop_flop_formula(m, n, cfg.l, cfg.b, cfg.p) * cfg.batch
         achieved = flop_alg / (ms * 1e-3) / 1e12
+        slot_bytes = slot_len * 8
         line = {
             "metric": METRIC, "value": cfg.batch * 1000.0 / ms, "unit": "factorizations/s",
             "n_gpus": ws, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Haar factors / Tucker tensor, BASELINE spectra, device-generated)",
-            "config": {"workload": args.workload, "m": m, "n": n, "k": cfg.k, "p": cfg.p, "b": cfg.b,
-                       "l": cfg.l, "batch": cfg.batch,
-                       "parallelism": f"partitioned x{ws} (contiguous), {args.streams} streams/GPU, "
-                                      "NCCL gather of s to rank 0",
-                       "l2_flush": "per-problem A %d MB, batch >> L2" % (m * n * 8 // 2**20)},
+            "config": workload_config(args, ws),
             "step_roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                               "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
-                              "flop_alg": flop_alg},
+                              "flop_alg": flop_alg, "peak_source": FP64_PEAK_SOURCE},
+            "streams_per_gpu": args.streams,
+            "omega": {"inside_timed_region": True,
+                      "host_ms_per_step_rank0": om_ms,
+                      "note": "engine Omega cache cleared every step: each problem's "
+                              "gaussian(b+p, m, seed, 0) is generated on a host thread inside its call"},
+            "gather": {"slot": [nm for nm, _ in parts], "bytes_per_problem": slot_bytes,
+                       "bytes_per_step": slot_bytes * cfg.batch if ws > 1 else 0,
+                       "collective": "NCCL all_gather per chunk of %d problems on a dedicated stream" % chunk
+                       if ws > 1 else "none (1 GPU)", "complete": ok},
             "clocks": clk,
-            "gathered": list(gathered.shape) if gathered is not None else None,
         }
+        if dry:
+            line["dry"] = True
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
-    return 0
+    return 0 if ok else 1
 
 
-def cpu_oracle_sample(A_host, cfg, budget_s=30.0):
+# ------------------------------------------------------------- reference arm
+def cpu_oracle_sample(A_host, cfg):
     """Time the CPU oracle (reference algorithm port) on the same matrix."""
     import oracle
 
     t0 = time.perf_counter()
     oracle.flip_flop(A_host, cfg.k, l=cfg.l, b=cfg.b, p=cfg.p, seed=0)
-    t = time.perf_counter() - t0
-    return t
+    return time.perf_counter() - t0
+
+
+def reference_matrix(args):
+    import torch
+
+    from paper_1803_01982_b200 import workloads
+
+    cfg = workloads.CONFIGS[args.workload]
+    if args.workload == "cfg5" or args.workload == "cfg4":
+        # one problem of the batch (the unit of the metric)
+        dev = "cuda:0" if torch.cuda.is_available() else "cpu"
+        _, A = make_workload(args.workload, 0, dev)
+        return cfg, np.asfortranarray(A.cpu().numpy())
+    dev = "cuda:0" if torch.cuda.is_available() else "cpu"
+    _, A = make_workload(args.workload, 0, dev)
+    return cfg, np.asfortranarray(A.cpu().numpy())
 
 
 def run_reference(args):
     ws, rank, local = dist_init()
     if rank != 0:
         return 0
-    import torch
-
-    from paper_1803_01982_b200 import workloads
-
-    cfg = workloads.CONFIGS[args.workload]
-    dev = "cuda:0" if torch.cuda.is_available() else "cpu"
-    _, A = make_workload(args.workload, 0, dev)
-    A_host = np.asfortranarray(A.cpu().numpy())
-    del A
+    cfg, A_host = reference_matrix(args)
     cores = len(os.sched_getaffinity(0))
     warm = min(args.warmup, 1)
     times = []
     for _ in range(warm):
         cpu_oracle_sample(A_host, cfg)
     t_start = time.perf_counter()
-    for i in range(max(1, args.steps)):
+    for _ in range(max(1, args.steps)):
         times.append(cpu_oracle_sample(A_host, cfg))
         if time.perf_counter() - t_start > args.ref_budget_s:
             break
@@ -274,13 +601,15 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "factorizations/s",
         "n_gpus": ws, "steps": len(times), "warmup": warm, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded Haar factors, BASELINE spectrum)",
-        "config": {"workload": args.workload, "m": cfg.m, "n": cfg.n, "k": cfg.k, "p": cfg.p,
-                   "b": cfg.b, "l": cfg.l},
+        "higher_is_better": True, "scaling": "strong" if cfg.batch > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Haar factors / Tucker tensor, BASELINE spectra, device-generated)",
+        "config": workload_config(args, ws),
         "cpu_baseline": {"value": v, "unit": "factorizations/s", "cores": cores, "kind": "port",
-                         "sample": f"{len(times)} full {args.workload} factorization(s) by the "
-                                   "numpy oracle port (oracle/ffsrqr_oracle.py), OpenBLAS threads=all"},
+                         "sample": f"{len(times)} full {args.workload} factorization(s) of one problem "
+                                   "by the numpy oracle port (oracle/ffsrqr_oracle.py), OpenBLAS "
+                                   "threads=all; calibration against the numba reference: "
+                                   "profiles/r04_cpu_calibration.json"},
         "e2e": {"value": v, "unit": "factorizations/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -288,29 +617,15 @@ def run_reference(args):
     return 0
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-budget-s", type=float, default=120.0)
-    ap.add_argument("--streams", type=int, default=0,
-                    help="batched workloads: problems in flight per GPU (CUDA streams); "
-                         "0 = default (cfg5: 8, cfg4: 1)")
-    args = ap.parse_args()
-    if args.impl == "reference":
-        return run_reference(args)
-    if args.workload in ("cfg4", "cfg5"):
-        return run_batched(args)
+# ----------------------------------------------------------------- single
+def run_single(args):
+    import ctypes as C
 
     import torch
     import torch.distributed as dist
 
     import paper_1803_01982_b200 as ffb
-    from paper_1803_01982_b200 import _capi, engine
+    from paper_1803_01982_b200 import _capi, engine, rng
 
     ws, rank, local = dist_init()
     torch.cuda.set_device(local)
@@ -321,9 +636,15 @@ def main():
     m, n = A.shape
     k, l, b, p = cfg.k, cfg.l, cfg.b, cfg.p
     flop_alg = ffb.flip_flop_flop_formula(m, n, l, b, p)
+    hbm_gbps, hbm_src = hbm_peak()
 
     def step():
         return ffb.flip_flop_srqr(A, k, l=l, b=b, p=p, seed=0)
+
+    # host generation of Omega = gaussian(b+p, m, 0, 0) (reported; cached per (seed, s, m))
+    t0 = time.perf_counter()
+    rng.gaussian(b + p, m, 0, rng.STREAM_SKETCH)
+    omega_ms = (time.perf_counter() - t0) * 1e3
 
     for _ in range(max(args.warmup, 3)):
         ap_ = step()
@@ -336,52 +657,78 @@ def main():
     clocks.start()
     i0 = clocks.ready()
     st = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    for _ in range(args.steps):
-        ap_ = step()
-    e1.record(st)
-    torch.cuda.synchronize()
+    if m * n * 8 > L2_BYTES:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(args.steps):
+            ap_ = step()
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+    else:
+        # A fits L2: flush (write 512 MB) between steps, outside each step's events
+        flush = torch.empty(64 << 20, dtype=torch.float64, device=dev)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        for a0, a1 in evs:
+            flush.fill_(1.0)
+            a0.record(st)
+            ap_ = step()
+            a1.record(st)
+        torch.cuda.synchronize()
+        ms = sum(a0.elapsed_time(a1) for a0, a1 in evs) / args.steps
+        del flush
     clk = clocks.stop(i0)
-    ms = e0.elapsed_time(e1) / args.steps
     if ws > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = ws * 1000.0 / ms
 
-    # dominant kernel live timing: the A*Qhat GEMM (K13, m x l x n), same shape as in the step
     lib = _capi.load()
-    import ctypes as C
-
-    Yh = torch.randn(n, l, dtype=torch.float64, device=dev).t().contiguous().t()
-    out = torch.empty((l, m), dtype=torch.float64, device=dev).t()
-    wsb = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
     ctx = _capi.context(local)
-    def kgemm():
-        lib.ffb_gemm(ctx, C.c_void_p(st.cuda_stream), m, l, n, 1.0, C.c_void_p(A.data_ptr()),
-                     A.stride(1), 0, C.c_void_p(Yh.data_ptr()), n, 1, 0.0,
-                     C.c_void_p(out.data_ptr()), m, C.c_void_p(wsb.data_ptr()), wsb.numel())
-    for _ in range(3):
-        kgemm()
-    torch.cuda.synchronize()
-    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    g0.record(st)
-    for _ in range(5):
-        kgemm()
-    g1.record(st)
-    torch.cuda.synchronize()
-    gms = g0.elapsed_time(g1) / 5
-    g_tflops = 2.0 * m * n * l / (gms * 1e-3) / 1e12
+
+    # stage table (CUPTI shares of one extra step) and the dominant kernel timed
+    # standalone with CUDA events
+    stages, roof = None, None
+    if rank == 0:
+        try:
+            ktimes, kcounts = profile_kernels(step)
+            stages = stage_table(cfg, ktimes, kcounts, ms, hbm_gbps)
+        except Exception as e:   # pragma: no cover - profiler unavailable
+            stages = [{"error": f"profiler unavailable: {e!r}"}]
+        top = stages[0]["kernel"] if stages and "kernel" in stages[0] else "gemm_f64_kernel"
+        timed = time_top_kernel(top, cfg, A, st, dev, ctx, lib)
+        if timed is None:          # no standalone launcher: the profiler's average
+            ent = stages[0]
+            timed = (ent["ms"] / ent["launches"], ent.get("algorithmic_bytes", 0) / ent["launches"],
+                     "byte", ent.get("algorithm", ""))
+        kms, work, unit, note = timed
+        traffic, tsrc = ncu_traffic(top)
+        if unit == "flop":
+            ach = work / (kms * 1e-3) / 1e12
+            roof = {"bound": "tensor", "kernel": top, "achieved": ach, "peak": FP64_PEAK_TFLOPS,
+                    "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "traffic": traffic,
+                    "traffic_source": tsrc, "ms_per_launch": kms, "algorithmic": note,
+                    "peak_source": FP64_PEAK_SOURCE,
+                    "timing": "CUDA events on the bench stream, standalone launches with the step's shapes"}
+        else:
+            ach = work / (kms * 1e-3) / 1e9
+            roof = {"bound": "hbm", "kernel": top, "achieved": ach, "peak": hbm_gbps, "unit": "GB/s",
+                    "frac": ach / hbm_gbps, "traffic": traffic, "traffic_source": tsrc,
+                    "ms_per_launch": kms, "algorithmic": note, "peak_source": hbm_src,
+                    "timing": "CUPTI average per launch (no standalone launcher)"}
 
     # e2e through the public API with host buffers (pinned), H2D + D2H in the timed region
-    A_host = None
     e2e = None
     if rank == 0 or ws > 1:
+        from paper_1803_01982_b200 import batch
+
         A_host = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
         A_host.copy_(A.t())
         A_host_cm = A_host.t()            # column-major (m, n) host view
-        # pinned host destinations of the step's result (u, s, v, perm)
+        h2d = m * n * 8                    # A; Omega is cached on the device per (seed, s, m)
+        d2h = (m + n) * k * 8 + k * 8 + n * 8   # u, v, s, perm
         u_h = torch.empty((k, m), dtype=torch.float64, pin_memory=True).t()
         v_h = torch.empty((k, n), dtype=torch.float64, pin_memory=True).t()
         s_h = torch.empty(k, dtype=torch.float64, pin_memory=True)
@@ -395,26 +742,20 @@ def main():
             p_h.copy_(r.meta["srqr"].fact.perm, non_blocking=True)
             st.synchronize()
             return r
-        r = e2e_step()
+        e2e_step()
         torch.cuda.synchronize()
         es = max(1, min(args.steps, 5))
-        t0 = time.perf_counter()
         x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         x0.record(st)
         for _ in range(es):
-            r = e2e_step()
+            e2e_step()
         x1.record(st)
         torch.cuda.synchronize()
         ems = x0.elapsed_time(x1) / es
-        h2d = m * n * 8                    # A; Omega is cached on the device per (seed, s, m)
-        d2h = (m + n) * k * 8 + k * 8 + n * 8   # u, v, s, perm
-        # the same calls pipelined through the public batch driver
-        # (batch.run_host_pipeline): one copy thread uploads every step's A from
-        # pinned host memory back to back on its own stream, three compute streams
-        # factorize; every step still uploads its own A and reads back its own
-        # u, s, v, perm into pinned host memory
-        from paper_1803_01982_b200 import batch
 
+        # the same calls pipelined through the public batch driver
+        # (batch.run_host_pipeline): uploads on a copy stream, 3 compute streams;
+        # every call still uploads its own A and reads back its own u, s, v, perm
         npipe = 12
         outs = [(torch.empty((k, m), dtype=torch.float64, pin_memory=True).t(),
                  torch.empty((k, n), dtype=torch.float64, pin_memory=True).t(),
@@ -439,17 +780,35 @@ def main():
         y1.record(st)
         torch.cuda.synchronize()
         pms = y0.elapsed_time(y1) / npipe
-        e2e = {"value": 1000.0 / pms * (ws if ws > 1 else 1), "unit": "factorizations/s",
+
+        # the reference's own signature: numpy in, numpy out, one call at a time
+        # (svd.py:43); Omega generated on the host inside every call
+        A_np = np.asfortranarray(A_host_cm.numpy())
+
+        def np_step():
+            engine.clear_omega_cache()
+            r = ffb.flip_flop_srqr(A_np, k, l=l, b=b, p=p, seed=0)
+            return r.u, r.s, r.v, r.meta["srqr"].fact.perm
+        np_step()
+        nn = max(1, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(nn):
+            np_step()
+        nms = (time.perf_counter() - t0) * 1e3 / nn
+        e2e = {"value": 1000.0 / pms * ws, "unit": "factorizations/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": pms,
                "path": "paper_1803_01982_b200.flip_flop_srqr on pinned host tensors, "
                        f"{npipe} calls: uploads on a copy stream, 3 compute streams "
                        "(batch.run_host_pipeline)",
-               "serial": {"value": 1000.0 / ems * (ws if ws > 1 else 1), "ms_per_step": ems,
-                          "path": "one paper_1803_01982_b200.flip_flop_srqr call at a time"}}
+               "serial": {"value": 1000.0 / ems * ws, "ms_per_step": ems,
+                          "path": "one flip_flop_srqr call at a time on pinned host tensors"},
+               "numpy": {"value": 1000.0 / nms * ws, "ms_per_step": nms,
+                         "path": "reference signature: numpy F-order A in, numpy u, s, v, perm out, "
+                                 "one call at a time, Omega generated on the host inside each call "
+                                 "(wall clock, host-synchronous API)"}}
+        del A_host, A_np
 
-    # capacity: independent factorizations of the resident matrix in flight on 3
-    # streams (the latency-bound stages leave SMs idle); reported beside `value`,
-    # which stays one factorization at a time
+    # capacity: independent factorizations of the resident matrix on 3 streams
     conc = None
     if rank == 0 or ws > 1:
         from paper_1803_01982_b200 import batch as _batch
@@ -470,8 +829,7 @@ def main():
         conc = {"value": 1000.0 / cms * ws, "unit": "factorizations/s", "ms_per_factorization": cms,
                 "streams": 3, "factorizations": nconc}
 
-    # the paper's competitor on the same device kernels: RSISVD,
-    # rank k, oversampling p, q = 2 power steps (ffsrqr/svd.py:101-133)
+    # the paper's competitor on the same device kernels
     rsi = None
     if rank == 0 and ws == 1:
         def rs_step():
@@ -492,50 +850,70 @@ def main():
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        A_np = A_host.t().numpy() if A_host is not None else A.cpu().numpy()
-        A_np = np.asfortranarray(A_np)
+        A_np = np.asfortranarray(A.cpu().numpy())
         t_cpu = cpu_oracle_sample(A_np, cfg)
         cpu = {"value": 1.0 / t_cpu, "unit": "factorizations/s",
                "cores": len(os.sched_getaffinity(0)), "kind": "port",
                "sample": f"1 full {args.workload} factorization by the numpy oracle port "
-                         f"(oracle/ffsrqr_oracle.py) on the same matrix, {t_cpu:.2f} s"}
+                         f"(oracle/ffsrqr_oracle.py) on the same matrix, {t_cpu:.2f} s; calibration "
+                         "against the numba reference: profiles/r04_cpu_calibration.json"}
 
     if rank == 0:
         achieved = flop_alg / (ms * 1e-3) / 1e12
-        traffic, traffic_src = k13_traffic(args.workload)
         line = {
             "metric": METRIC, "value": value, "unit": "factorizations/s", "n_gpus": ws,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded Haar factors, BASELINE spectrum, device-generated)",
-            "config": {"workload": args.workload, "m": m, "n": n, "k": k, "p": p, "b": b, "l": l,
-                       "l2_flush": "input 537 MB > 126 MB L2" if m * n * 8 > 126e6 else "none",
-                       "parallelism": f"replicas x{ws}" if ws > 1 else "single"},
+            "data": "synthetic (seeded Haar factors / Tucker tensor, BASELINE spectra, device-generated)",
+            "config": workload_config(args, ws),
             "achieved_tflops": achieved,
             "step_roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                               "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
-                              "flop_alg": flop_alg,
-                              "peak_source": "measured DMMA peak, profiles/r01_fp64_peak.md"},
-            "roofline": {"bound": "tensor", "kernel": "K13 A*Qhat DMMA GEMM (m x l x n)",
-                         "achieved": g_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": g_tflops / FP64_PEAK_TFLOPS, "traffic": traffic,
-                         "traffic_source": traffic_src,
-                         "algorithmic_bytes": 8 * (m * n + n * l + m * l),
-                         "ms_per_launch": gms,
-                         "peak_source": "measured DMMA peak (MEASURED_PEAKS.json has no FP64)"},
+                              "flop_alg": flop_alg, "peak_source": FP64_PEAK_SOURCE},
+            "roofline": roof,
+            "stages": stages,
             "gpu_launches": kernels * args.steps,
             "clocks": clk,
+            "omega_host_ms": omega_ms,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "rsisvd_same_device": rsi,
             "concurrent": conc,
-            "certificate": {"swaps": ap_.meta["srqr"].cert.swaps, "g2": ap_.meta["srqr"].cert.g2},
+            "certificate": {"swaps": ap_.meta["srqr"].cert.swaps, "g2": ap_.meta["srqr"].cert.g2,
+                            "svd_sweeps": ap_.meta["svd_sweeps"]},
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget-s", type=float, default=120.0)
+    ap.add_argument("--streams", type=int, default=0,
+                    help="batched workloads: problems in flight per GPU (CUDA streams); "
+                         "0 = default (cfg5: 8, cfg4: 1)")
+    ap.add_argument("--dry", action="store_true",
+                    help="CPU/gloo run of the batched partition + gather logic (tests)")
+    args = ap.parse_args()
+    rc = maybe_spawn(args)
+    if rc is not None:
+        return rc
+    if args.impl == "reference":
+        return run_reference(args)
+    if args.workload in ("cfg4", "cfg5"):
+        return run_batched(args)
+    if args.dry:
+        raise SystemExit("--dry covers the batched workloads (cfg4, cfg5)")
+    return run_single(args)
 
 
 if __name__ == "__main__":

@@ -3,6 +3,10 @@
 #include <cstdlib>
 #include <cstdio>
 
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "ffb_gemm.h"
 #include "gemm_f64.cuh"
 
@@ -10,10 +14,11 @@ namespace ffb {
 
 namespace {
 
-template <int BM, int BN, int BK, int WM, int WN, bool AK, bool BKC, int ST, bool V2, bool SK>
+template <int BM, int BN, int BK, int WM, int WN, bool AK, bool BKC, int ST, bool V2, bool SK,
+          bool TMA = false>
 cudaError_t launch_cfg2(cudaStream_t st, const GemmArgs& g, dim3 grid) {
-  using Cfg = GemmCfg<BM, BN, BK, WM, WN, AK, BKC, ST>;
-  auto kern = gemm_f64_kernel<BM, BN, BK, WM, WN, AK, BKC, ST, V2, SK>;
+  using Cfg = GemmCfg<BM, BN, BK, WM, WN, AK, BKC, ST, TMA>;
+  auto kern = gemm_f64_kernel<BM, BN, BK, WM, WN, AK, BKC, ST, V2, SK, TMA>;
   static std::atomic<unsigned long long> attr{0};
   ensure_smem_optin((const void*)kern, (int)Cfg::kSmem, attr);
   kern<<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(g);
@@ -67,6 +72,53 @@ template <int BM, int BN, int BK, int WM, int WN, bool AK, bool BKC, int ST>
 cudaError_t launch_cfg(cudaStream_t st, const GemmArgs& g, dim3 grid) {
   if (vec2_ok(g)) return launch_cfg1<BM, BN, BK, WM, WN, AK, BKC, ST, true>(st, g, grid);
   return launch_cfg1<BM, BN, BK, WM, WN, AK, BKC, ST, false>(st, g, grid);
+}
+
+template <int BM, int BN, int WM, int WN, int ST>
+cudaError_t launch_tma_cfg(cudaStream_t st, const GemmArgs& g, dim3 grid) {
+  if (g.sk_per > 0) return launch_cfg2<BM, BN, 16, WM, WN, true, true, ST, true, true, true>(st, g, grid);
+  return launch_cfg2<BM, BN, 16, WM, WN, true, true, ST, true, false, true>(st, g, grid);
+}
+
+// TMA-staged tiles for the k-contiguous x k-contiguous products (the sketch
+// Omega A, the WT rows Y^T A): configs with a TMA instance
+bool tma_cfg(int cfg) { return cfg == 0 || cfg == 1 || cfg == 2 || cfg == 5 || cfg == 6 || cfg == 11; }
+
+cudaError_t launch_tma(int cfg, cudaStream_t st, const GemmArgs& g, dim3 grid) {
+  switch (cfg) {
+    case 0: return launch_tma_cfg<48, 64, 24, 32, 4>(st, g, grid);
+    case 1: return launch_tma_cfg<64, 64, 32, 32, 4>(st, g, grid);
+    case 2: return launch_tma_cfg<96, 64, 48, 32, 4>(st, g, grid);
+    case 5: return launch_tma_cfg<16, 64, 16, 16, 4>(st, g, grid);
+    case 6: return launch_tma_cfg<32, 64, 16, 32, 4>(st, g, grid);
+    default: return launch_tma_cfg<80, 64, 40, 32, 4>(st, g, grid);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// (K inner, rows) k-contiguous operand with leading dimension ld, box (16, box_rows)
+bool encode_kc(CUtensorMap* map, const double* base, int64_t K, int64_t rows, int64_t ld, int box_rows) {
+  auto enc = tma_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  cuuint32_t box[2] = {16u, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1u, 1u};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 struct Shape {
@@ -240,10 +292,22 @@ cudaError_t gemm_f64(GemmCtx& c, cudaStream_t st, int64_t M, int64_t N, int64_t 
       }
     }
   }
+  // TMA staging for k-contiguous x k-contiguous products (FFB_GEMM_TMA=0 disables)
+  static int tma_mode = -2;
+  if (tma_mode == -2) {
+    const char* e = getenv("FFB_GEMM_TMA");
+    tma_mode = e ? atoi(e) : 1;
+  }
+  auto al16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
+  const bool use_tma = tma_mode != 0 && akc && bkc && tma_cfg(cfg) && K >= 256 && al16(A) && al16(B) &&
+                       lda % 2 == 0 && ldb % 2 == 0 && M < (1LL << 31) && N < (1LL << 31) &&
+                       K < (1LL << 31) && encode_kc(&g.tmA, A, K, M, lda, sh.bm) &&
+                       encode_kc(&g.tmB, B, K, N, ldb, sh.bn);
   if (use_sk) {
     dim3 grid((unsigned)gx, 1, 1);
     cudaError_t e;
-    if (akc && bkc) e = launch_layout<true, true>(cfg, st, g, grid);
+    if (use_tma) e = launch_tma(cfg, st, g, grid);
+    else if (akc && bkc) e = launch_layout<true, true>(cfg, st, g, grid);
     else if (akc && !bkc) e = launch_layout<true, false>(cfg, st, g, grid);
     else if (!akc && bkc) e = launch_layout<false, true>(cfg, st, g, grid);
     else e = launch_layout<false, false>(cfg, st, g, grid);
@@ -253,7 +317,8 @@ cudaError_t gemm_f64(GemmCtx& c, cudaStream_t st, int64_t M, int64_t N, int64_t 
   }
   dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)g.splits);
   cudaError_t e;
-  if (akc && bkc) e = launch_layout<true, true>(cfg, st, g, grid);
+  if (use_tma) e = launch_tma(cfg, st, g, grid);
+  else if (akc && bkc) e = launch_layout<true, true>(cfg, st, g, grid);
   else if (akc && !bkc) e = launch_layout<true, false>(cfg, st, g, grid);
   else if (!akc && bkc) e = launch_layout<false, true>(cfg, st, g, grid);
   else e = launch_layout<false, false>(cfg, st, g, grid);

@@ -10,7 +10,17 @@
 // padded so that DMMA fragment loads are bank-conflict free.  Split-K writes
 // fp64 partial tiles that a second kernel reduces in fixed order, so results
 // are bitwise deterministic run to run.
+//
+// TMA variant (LOAD_TMA, both operands k-contiguous: the sketch B = Omega A and
+// the WT products Y^T A): one elected thread issues cp.async.bulk.tensor 2-D
+// loads of the (rows x 16) k-tiles into 128B-swizzled shared memory, completion
+// is tracked by one mbarrier per stage (expect_tx), and edges are zero-filled by
+// the TMA unit.  The 16-byte chunk c of tile row r sits at chunk c ^ (r & 7);
+// DMMA fragment rows are taken in the order 0,2,4,6 | 1,3,5,7 within each 8-row
+// group so that every half-warp's 16 doubles land on 16 distinct bank pairs.
 #pragma once
+#include <cuda.h>
+
 #include "ffb_common.cuh"
 
 namespace ffb {
@@ -36,7 +46,43 @@ struct GemmArgs {
   int sk_tiles_n;    // tiles along N (tile = ty * sk_tiles_n + tx)
   int64_t sk_kiters; // k-tiles per tile
   unsigned* sk_cnt;  // per-tile arrival counters (zero; reset by the last arriver)
+  CUtensorMap tmA;   // LOAD_TMA: A as (K inner, M rows), box (16, BM), 128B swizzle
+  CUtensorMap tmB;   // LOAD_TMA: B as (K inner, N rows), box (16, BN), 128B swizzle
 };
+
+// ---- TMA / mbarrier helpers (sm_90+ PTX; sm_100a here)
+FFB_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+FFB_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+FFB_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+FFB_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+FFB_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// fragment row q (0..7) -> row inside its 8-row group (bank-conflict-free order)
+FFB_DEV int tma_perm(int q) { return 2 * (q & 3) + (q >> 2); }
+// double index of element (r, k) of a 128B-swizzled (rows x 16) k-tile
+FFB_DEV int tma_idx(int r, int k) { return r * 16 + ((((k >> 1) ^ (r & 7))) << 1) + (k & 1); }
 
 template <int BM, int BK>
 struct APad {
@@ -46,16 +92,19 @@ struct APad {
   static constexpr int mc = BM + ((4 - BM % 16) + 16) % 16;
 };
 
-template <int BM, int BN, int BK, int WM, int WN, bool A_KC, bool B_KC, int STAGES>
+template <int BM, int BN, int BK, int WM, int WN, bool A_KC, bool B_KC, int STAGES, bool TMA = false>
 struct GemmCfg {
   static constexpr int kWarpsM = BM / WM, kWarpsN = BN / WN;
   static constexpr int kThreads = 32 * kWarpsM * kWarpsN;
   static constexpr int kTM = WM / 8, kTN = WN / 8;
-  static constexpr int kAStage = A_KC ? BM * APad<BM, BK>::kc : BK * APad<BM, BK>::mc;
-  static constexpr int kBStage = B_KC ? BN * APad<BN, BK>::kc : BK * APad<BN, BK>::mc;
+  // TMA: dense 128B-swizzled (rows x 16) tiles, 1024-byte aligned stages
+  static constexpr int kAStage = TMA ? (BM * 16 + 127) / 128 * 128
+                                     : (A_KC ? BM * APad<BM, BK>::kc : BK * APad<BM, BK>::mc);
+  static constexpr int kBStage = TMA ? (BN * 16 + 127) / 128 * 128
+                                     : (B_KC ? BN * APad<BN, BK>::kc : BK * APad<BN, BK>::mc);
   static constexpr size_t kStages = (size_t)STAGES * (kAStage + kBStage);
   static constexpr size_t kCTile = (size_t)(BM + 1) * BN;   // epilogue staging
-  static constexpr size_t kSmem = sizeof(double) * (kStages > kCTile ? kStages : kCTile);
+  static constexpr size_t kSmem = sizeof(double) * (kStages > kCTile ? kStages : kCTile) + (TMA ? 1024 : 0);
 };
 
 // Operand tile loader: each thread owns a fixed set of (row, k) slots of the
@@ -157,16 +206,28 @@ struct TileLoader {
 };
 
 template <int BM, int BN, int BK, int WM, int WN, bool A_KC, bool B_KC, int STAGES, bool VEC2,
-          bool SK>
-__global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES>::kThreads)
-    gemm_f64_kernel(GemmArgs g) {
-  using Cfg = GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES>;
+          bool SK, bool TMA = false>
+__global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES, TMA>::kThreads)
+    gemm_f64_kernel(const __grid_constant__ GemmArgs g) {
+  using Cfg = GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES, TMA>;
+  static_assert(!TMA || (A_KC && B_KC && BK == 16), "TMA path: k-contiguous operands, 16-wide k-tiles");
   constexpr int NT = Cfg::kThreads;
   constexpr int ALD = A_KC ? APad<BM, BK>::kc : APad<BM, BK>::mc;
   constexpr int BLD = B_KC ? APad<BN, BK>::kc : APad<BN, BK>::mc;
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(16) double smem_raw[];
+  double* smem = TMA ? reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023))
+                     : smem_raw;
   double* As = smem;
   double* Bs = smem + STAGES * Cfg::kAStage;
+  __shared__ __align__(8) uint64_t full_bar[TMA ? STAGES : 1];
+  uint32_t phases = 0;   // TMA: parity bit per stage of the next wait
+  if (TMA) {
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < STAGES; ++s) mbar_init(&full_bar[s], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+  }
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm0 = (warp / Cfg::kWarpsN) * WM, wn0 = (warp % Cfg::kWarpsN) * WN;
@@ -208,12 +269,15 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
     it = it_end;
   }
   const int nk = kbeg < kend ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+  if (TMA) fence_proxy_async_smem();   // epilogue's generic smem writes before the next TMA fills
   __syncthreads();   // previous segment's smem reads done before refilling
 
   TileLoader<BM, BK, A_KC, VEC2, NT> la;
   TileLoader<BN, BK, B_KC, VEC2, NT> lb;
-  la.init(g.A, g.lda, i0, g.M, kbeg, tid);
-  lb.init(g.B, g.ldb, j0, g.N, kbeg, tid);
+  if (!TMA) {
+    la.init(g.A, g.lda, i0, g.M, kbeg, tid);
+    lb.init(g.B, g.ldb, j0, g.N, kbeg, tid);
+  }
 
   double acc[Cfg::kTM][Cfg::kTN][2];
 #pragma unroll
@@ -223,6 +287,16 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
 
   int fetched = 0;
   auto fetch = [&](int stage) {
+    if constexpr (TMA) {
+      if (tid == 0) {
+        const int k0 = (int)(kbeg + (int64_t)fetched * BK);
+        mbar_expect_tx(&full_bar[stage], (uint32_t)((BM + BN) * BK * sizeof(double)));
+        tma_load_2d(As + stage * Cfg::kAStage, &g.tmA, &full_bar[stage], k0, (int)i0);
+        tma_load_2d(Bs + stage * Cfg::kBStage, &g.tmB, &full_bar[stage], k0, (int)j0);
+      }
+      ++fetched;
+      return;
+    }
     const int64_t k0 = kbeg + (int64_t)fetched * BK;
     const int64_t krem = kend - k0;
     const int kvalid = krem < BK ? (int)krem : BK;
@@ -243,17 +317,23 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
 #pragma unroll
   for (int st = 0; st < STAGES - 1; ++st) {
     if (st < nk) fetch(st);
-    cp_async_commit();
+    if (!TMA) cp_async_commit();
   }
 
   const int fr = lane >> 2, fk = lane & 3;
+  const int frp = TMA ? tma_perm(fr) : fr;   // fragment row -> tile row inside the 8-row group
   for (int kt = 0; kt < nk; ++kt) {
-    cp_async_wait<STAGES - 2>();
+    if (!TMA) cp_async_wait<STAGES - 2>();
     __syncthreads();
     {
       const int pf = kt + STAGES - 1;
       if (pf < nk) fetch(pf % STAGES);
-      cp_async_commit();
+      if (!TMA) cp_async_commit();
+    }
+    if (TMA) {
+      const int s_ = kt % STAGES;
+      mbar_wait(&full_bar[s_], (phases >> s_) & 1u);
+      phases ^= 1u << s_;
     }
     const double* as = As + (kt % STAGES) * Cfg::kAStage;
     const double* bs = Bs + (kt % STAGES) * Cfg::kBStage;
@@ -264,13 +344,13 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
     auto load_frag = [&](int k4, double (&a_)[Cfg::kTM], double (&b_)[Cfg::kTN]) {
 #pragma unroll
       for (int a = 0; a < Cfg::kTM; ++a) {
-        const int r = wm0 + a * 8 + fr, kk = k4 + fk;
-        a_[a] = A_KC ? as[r * ALD + kk] : as[kk * ALD + r];
+        const int r = wm0 + a * 8 + frp, kk = k4 + fk;
+        a_[a] = TMA ? as[tma_idx(r, kk)] : (A_KC ? as[r * ALD + kk] : as[kk * ALD + r]);
       }
 #pragma unroll
       for (int b = 0; b < Cfg::kTN; ++b) {
-        const int c = wn0 + b * 8 + fr, kk = k4 + fk;
-        b_[b] = B_KC ? bs[c * BLD + kk] : bs[kk * BLD + c];
+        const int c = wn0 + b * 8 + frp, kk = k4 + fk;
+        b_[b] = TMA ? bs[tma_idx(c, kk)] : (B_KC ? bs[c * BLD + kk] : bs[kk * BLD + c]);
       }
     };
     load_frag(0, af[0], bf[0]);
@@ -285,7 +365,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
           dmma_884(acc[a][b][0], acc[a][b][1], af[cur][a], bf[cur][b]);
     }
   }
-  cp_async_wait<0>();
+  if (!TMA) cp_async_wait<0>();
 
   // Epilogue: stage the accumulator tile in shared memory (column-major, ld
   // BM + 1), then one compact coalesced loop writes it out (C, a split-K slab
@@ -299,8 +379,10 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
 #pragma unroll
     for (int b = 0; b < Cfg::kTN; ++b)
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
-        Ct[(wm0 + a * 8 + fr) + (wn0 + b * 8 + 2 * fk + h) * CLD] = acc[a][b][h];
+      for (int h = 0; h < 2; ++h) {
+        const int cq = TMA ? tma_perm(2 * fk + h) : 2 * fk + h;
+        Ct[(wm0 + a * 8 + frp) + (wn0 + b * 8 + cq) * CLD] = acc[a][b][h];
+      }
   __syncthreads();
   {
     // destination: 0 = C (alpha, beta), 1 = partial slab (raw)

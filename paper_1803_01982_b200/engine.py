@@ -232,6 +232,13 @@ def _omega(torch, dev, s, m, seed):
     return om
 
 
+def clear_omega_cache():
+    """Drop every cached sketch matrix (the next call regenerates its Omega)."""
+    with _omega_lock:
+        _omega_cache.clear()
+        _rs_omega_cache.clear()
+
+
 def prefetch_omega(keys, device=None, threads=8):
     """Generate and cache Omega for many (s, m, seed) on host threads in parallel
     (numpy's Philox releases the GIL), e.g. before a batch of independent problems."""

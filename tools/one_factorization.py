@@ -21,9 +21,12 @@ A = workloads.torch_matrix(a.workload, seed=0) if a.workload != "cfg4" else \
 for _ in range(a.warmup):
     r = ffb.flip_flop_srqr(A, cfg.k, l=cfg.l, b=cfg.b, p=cfg.p, seed=0)
 torch.cuda.synchronize()
+# ncu --profile-from-start off: only the measured factorizations are captured
+torch.cuda.profiler.start()
 torch.cuda.nvtx.range_push("factor")
 for _ in range(a.reps):
     r = ffb.flip_flop_srqr(A, cfg.k, l=cfg.l, b=cfg.b, p=cfg.p, seed=0)
 torch.cuda.synchronize()
 torch.cuda.nvtx.range_pop()
+torch.cuda.profiler.stop()
 print("kernels per factorization:", r.meta["kernels"], "swaps:", r.meta["srqr"].cert.swaps, "svd_sweeps:", r.meta.get("svd_sweeps"))
