@@ -149,6 +149,17 @@ def qrnp_inplace(W, k):
     Returns taus; W holds R (upper) and reflector tails (strictly lower).
     """
     m, n = W.shape
+    if k == n and k <= m and W.flags.f_contiguous:
+        # all columns: LAPACK dgeqrf is the same factorization in the same
+        # storage (dlarfg: beta = -sign(x0) ||x||, tau = (beta - x0)/beta, tail
+        # scaled by 1/(x0 - beta), tau = 0 for a zero tail), blocked (BLAS-3)
+        from scipy.linalg import lapack
+
+        qr, taus, _, info = lapack.dgeqrf(W, overwrite_a=True)
+        if info == 0:
+            if qr is not W:
+                W[...] = qr
+            return np.asarray(taus[:k], dtype=float).copy()
     taus = np.zeros(k)
     for j in range(k):
         x0 = W[j, j]

@@ -299,7 +299,11 @@ cudaError_t gemm_f64(GemmCtx& c, cudaStream_t st, int64_t M, int64_t N, int64_t 
     tma_mode = e ? atoi(e) : 1;
   }
   auto al16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
-  const bool use_tma = tma_mode != 0 && akc && bkc && tma_cfg(cfg) && K >= 256 && al16(A) && al16(B) &&
+  // measured (tools/gemm_bench.py): TMA wins on the wide products (>= ~100 output
+  // tiles: cfg2 sketch 29.7 -> 31.1 TF, WT 25.8 -> 27.8 TF) and loses on the
+  // few-tile stream-K ones (cfg3 / cfg5 WT), which keep cp.async
+  const bool use_tma = tma_mode != 0 && akc && bkc && tma_cfg(cfg) && K >= 256 &&
+                       (tma_mode == 2 || tiles >= 96) && al16(A) && al16(B) &&
                        lda % 2 == 0 && ldb % 2 == 0 && M < (1LL << 31) && N < (1LL << 31) &&
                        K < (1LL << 31) && encode_kc(&g.tmA, A, K, M, lda, sh.bm) &&
                        encode_kc(&g.tmB, B, K, N, ldb, sh.bn);

@@ -322,6 +322,11 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
 
   const int fr = lane >> 2, fk = lane & 3;
   const int frp = TMA ? tma_perm(fr) : fr;   // fragment row -> tile row inside the 8-row group
+  // TMA: element (r, 4q + fk) of a swizzled tile sits at r*16 + (fk & 1) + (4q ^ c0)
+  // with c0 = ((fk >> 1) ^ (r & 7)) << 1 (r & 7 = frp for every fragment row)
+  const int tma_c0 = ((fk >> 1) ^ frp) << 1;
+  const int tma_a0 = (wm0 + frp) * 16 + (fk & 1);
+  const int tma_b0 = (wn0 + frp) * 16 + (fk & 1);
   for (int kt = 0; kt < nk; ++kt) {
     if (!TMA) cp_async_wait<STAGES - 2>();
     __syncthreads();
@@ -342,15 +347,25 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
     // no LDS overwrites a register an in-flight DMMA still reads
     double af[2][Cfg::kTM], bf[2][Cfg::kTN];
     auto load_frag = [&](int k4, double (&a_)[Cfg::kTM], double (&b_)[Cfg::kTN]) {
+      if constexpr (TMA) {
+        const int x = k4 ^ tma_c0;   // k4 = 4q is a compile-time constant
+        const double* pa = as + tma_a0 + x;
+        const double* pb = bs + tma_b0 + x;
+#pragma unroll
+        for (int a = 0; a < Cfg::kTM; ++a) a_[a] = pa[a * 128];   // 8 rows x 16 doubles per fragment
+#pragma unroll
+        for (int b = 0; b < Cfg::kTN; ++b) b_[b] = pb[b * 128];
+        return;
+      }
 #pragma unroll
       for (int a = 0; a < Cfg::kTM; ++a) {
         const int r = wm0 + a * 8 + frp, kk = k4 + fk;
-        a_[a] = TMA ? as[tma_idx(r, kk)] : (A_KC ? as[r * ALD + kk] : as[kk * ALD + r]);
+        a_[a] = A_KC ? as[r * ALD + kk] : as[kk * ALD + r];
       }
 #pragma unroll
       for (int b = 0; b < Cfg::kTN; ++b) {
         const int c = wn0 + b * 8 + frp, kk = k4 + fk;
-        b_[b] = TMA ? bs[tma_idx(c, kk)] : (B_KC ? bs[c * BLD + kk] : bs[kk * BLD + c]);
+        b_[b] = B_KC ? bs[c * BLD + kk] : bs[kk * BLD + c];
       }
     };
     load_frag(0, af[0], bf[0]);

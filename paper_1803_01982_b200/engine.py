@@ -212,24 +212,63 @@ _OMEGA_CACHE_MAX = 256              # entries
 _OMEGA_CACHE_BYTES = 1 << 30        # and bytes of device memory
 
 
+_omega_inflight = {}
+
+
 def _omega(torch, dev, s, m, seed):
     """Device copy of Omega = gaussian(s, m, seed, 0) (ffsrqr/sketch.py:108).
 
     Omega depends only on (seed, s, m), so repeated factorizations with the same
-    seed (IALM/SVT iterations, HOSVD modes of equal size, benchmarks) reuse it."""
+    seed (IALM/SVT iterations, HOSVD modes of equal size, benchmarks) reuse it.
+    A key another thread is generating right now is waited for, not redone."""
     key = (dev.index, int(s), int(m), int(seed) & 0xFFFFFFFFFFFFFFFF)
-    with _omega_lock:
-        om = _omega_cache.get(key)
-        if om is not None:
-            return om
-    om = torch.from_numpy(rng.gaussian(s, m, seed, rng.STREAM_SKETCH)).to(dev)
-    with _omega_lock:
-        while _omega_cache and (len(_omega_cache) >= _OMEGA_CACHE_MAX or
-                                sum(v.numel() * 8 for v in _omega_cache.values()) + om.numel() * 8
-                                > _OMEGA_CACHE_BYTES):
-            _omega_cache.pop(next(iter(_omega_cache)))
-        _omega_cache[key] = om
+    while True:
+        with _omega_lock:
+            om = _omega_cache.get(key)
+            if om is not None:
+                return om
+            ev = _omega_inflight.get(key)
+            if ev is None:
+                ev = _omega_inflight[key] = threading.Event()
+                break
+        ev.wait()
+    try:
+        om = torch.from_numpy(rng.gaussian(s, m, seed, rng.STREAM_SKETCH)).to(dev)
+        with _omega_lock:
+            while _omega_cache and (len(_omega_cache) >= _OMEGA_CACHE_MAX or
+                                    sum(v.numel() * 8 for v in _omega_cache.values()) + om.numel() * 8
+                                    > _OMEGA_CACHE_BYTES):
+                _omega_cache.pop(next(iter(_omega_cache)))
+            _omega_cache[key] = om
+    finally:
+        with _omega_lock:
+            _omega_inflight.pop(key, None)
+        ev.set()
     return om
+
+
+_prefetch_pool = None
+
+
+def prefetch_omega_async(keys, device=None, threads=8):
+    """Start generating Omega for (s, m, seed) keys on background host threads
+    (in order) and return at once; a factorization that needs one of them waits
+    for it.  Overlaps the host RNG of a batch with the device work of its first
+    problems."""
+    global _prefetch_pool
+    import torch
+    from concurrent.futures import ThreadPoolExecutor
+
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    with _omega_lock:
+        if _prefetch_pool is None or _prefetch_pool._max_workers != threads:
+            _prefetch_pool = ThreadPoolExecutor(max_workers=max(1, threads), thread_name_prefix="ffb-omega")
+        pool = _prefetch_pool
+
+    def gen(k):
+        with torch.cuda.device(dev):
+            return _omega(torch, dev, k[0], k[1], k[2])
+    return [pool.submit(gen, k) for k in keys]
 
 
 def clear_omega_cache():
