@@ -203,7 +203,8 @@ def ncu_traffic(kernel):
 def kernel_family(name):
     import re
 
-    n = re.sub(r"\(.*", "", name).replace("void ", "")
+    n = name.replace("(anonymous namespace)::", "").replace("void ", "")
+    n = re.sub(r"\(.*", "", n)
     n = re.sub(r"<.*", "", n)
     return n.split("::")[-1]
 
