@@ -21,6 +21,8 @@ FFB_ERR_ARGUMENT = 6
 FFB_MODE_TRQRCP = 0
 FFB_MODE_SRQR = 1
 FFB_MODE_FLIPFLOP = 2
+FFB_LAYOUT_COL = 0
+FFB_LAYOUT_ROW = 1
 
 EXPORTS = ("ffb_ctx_create", "ffb_ctx_destroy", "ffb_last_error", "ffb_version",
            "ffb_workspace_query", "ffb_run", "ffb_flipflop", "ffb_gemm", "ffb_block_pivots",
@@ -63,7 +65,8 @@ class Result(C.Structure):
 
 class BatchItem(C.Structure):
     _fields_ = [("stream", C.c_void_p), ("mode", C.c_int), ("A", C.c_void_p),
-                ("m", C.c_int64), ("n", C.c_int64), ("lda", C.c_int64), ("prm", Params),
+                ("m", C.c_int64), ("n", C.c_int64), ("lda", C.c_int64), ("a_layout", C.c_int),
+                ("prm", Params),
                 ("omega", C.c_void_p), ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
                 ("out", C.POINTER(Result)), ("status", C.c_int)]
 
@@ -99,11 +102,11 @@ def load(path=LIB_PATH):
                                             C.POINTER(C.c_size_t)]
         lib.ffb_workspace_query.restype = C.c_int
         lib.ffb_run.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_int64,
-                                C.c_int64, C.POINTER(Params), C.c_void_p, GAUSS_CB, C.c_void_p,
-                                C.c_void_p, C.c_size_t, C.POINTER(Result)]
+                                C.c_int64, C.c_int, C.POINTER(Params), C.c_void_p, GAUSS_CB,
+                                C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(Result)]
         lib.ffb_run.restype = C.c_int
         lib.ffb_flipflop.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
-                                     C.c_int64, C.POINTER(Params), C.c_void_p, GAUSS_CB,
+                                     C.c_int64, C.c_int, C.POINTER(Params), C.c_void_p, GAUSS_CB,
                                      C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(Result)]
         lib.ffb_flipflop.restype = C.c_int
         lib.ffb_run_batched.argtypes = [C.c_void_p, C.POINTER(BatchItem), C.c_int64, C.c_int,
@@ -122,7 +125,7 @@ def load(path=LIB_PATH):
                                                    C.POINTER(C.c_size_t)]
         lib.ffb_rsisvd_workspace_query.restype = C.c_int
         lib.ffb_rsisvd.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
-                                   C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
+                                   C.c_int64, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
                                    C.c_void_p, C.c_size_t, C.c_void_p, C.c_int64, C.c_void_p,
                                    C.c_void_p, C.c_int64, C.POINTER(C.c_int64),
                                    C.POINTER(C.c_int32)]

@@ -19,6 +19,7 @@
 #include <atomic>
 #include <mutex>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/ffb200.h"
@@ -29,6 +30,13 @@
 
 using namespace ffb;
 
+// A captured launch sequence (ffb_run's core) and the bookkeeping it adds.
+struct GraphEnt {
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches = 0, glaunches = 0, flops = 0;
+  uint64_t stamp = 0;
+};
+
 struct ffb_ctx {
   int device = 0;
   int sms = 148;
@@ -38,6 +46,10 @@ struct ffb_ctx {
   double* pinned = nullptr;        // host staging for g2 Gaussians
   size_t pinned_cap = 0;
   SrqrScalars* sc_host = nullptr;  // pinned
+  std::mutex gmu;                  // graph cache (several host threads per context)
+  std::unordered_map<std::string, GraphEnt> graphs;
+  std::vector<cudaGraphExec_t> retired;
+  uint64_t gstamp = 0;
 };
 
 namespace {
@@ -47,6 +59,7 @@ namespace {
 struct HostStage {
   double* pinned = nullptr;        // g2 Gaussians
   size_t cap = 0;
+  cudaStream_t capture[64] = {};   // per device: private stream the graph capture records on
   SrqrScalars* sc = nullptr;       // certificate scalars read back after the pipeline
   unsigned char* small = nullptr;  // 256 B: small read-backs (status words, sweep counts)
   ~HostStage() {
@@ -117,7 +130,7 @@ struct Work {
   bool piv_smem;
   size_t piv_smem_bytes;
   // SRQR
-  double *r, *rinit, *u, *ct, *part, *rot, *g2om, *g2z, *g2R;
+  double *r, *rinit, *u, *ct, *part, *rot, *g2om, *g2z, *g2R, *cpart;
   uint32_t* g2flag;
   SrqrScalars* sc;
   uint32_t* status;
@@ -158,6 +171,7 @@ size_t carve(const ffb_ctx* ctx, const Dims& D, void* base, size_t cap, Work& w)
   const int64_t mn = max_i(m, n);
   w.B = b.take<double>(s * n);
   w.colsq = b.take<double>(n);
+  w.cpart = b.take<double>(colsq_rm_part_doubles(n));   // row-major A: column-norm partials
   w.arr = b.take<int64_t>(n);
   w.pos = b.take<int64_t>(n);
   w.Y = b.take<double>(m * l);
@@ -273,6 +287,19 @@ size_t carve_rsisvd(const ffb_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t
   w.skcnt = b.take<unsigned>(65536);
   return b.off + kAlign;
 }
+
+// The input matrix A (m x n) in the caller's storage: column-major
+// (A(i, j) = p[i + j*ld]) or row-major (p[i*ld + j], FFB_LAYOUT_ROW).
+struct AView {
+  const double* p;
+  int64_t ld;
+  bool row;
+  const double* rows_from(int64_t i0) const { return row ? p + i0 * ld : p + i0; }
+  int64_t rs() const { return row ? ld : 1; }   // stride between rows
+  int64_t cs() const { return row ? 1 : ld; }   // stride between columns
+  bool kc_as_b() const { return !row; }          // as GEMM B operand with k = row index
+  bool kc_as_a() const { return row; }           // as GEMM A operand with k = column index
+};
 
 struct Eng {
   ffb_ctx* ctx;
@@ -430,6 +457,129 @@ int cuda_fail(ffb_ctx* ctx, cudaError_t e, const char* where) {
   return fail(ctx, FFB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
+// ---- CUDA graph cache of ffb_run's core (FFB_GRAPHS=0 disables it)
+constexpr size_t kMaxGraphs = 256;
+
+bool graphs_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FFB_GRAPHS");
+    // the FFB_*_PROF probes synchronise inside the sequence: no capture then
+    on = (e && atoi(e) == 0) || getenv("FFB_PIV_PROF") || getenv("FFB_PANEL_PROF") ||
+                 getenv("FFB_JACOBI_PROF")
+             ? 0
+             : 1;
+  }
+  return on == 1;
+}
+
+template <typename T>
+void key_put(std::string& k, const T& v) {
+  k.append(reinterpret_cast<const char*>(&v), sizeof(v));
+}
+
+std::string graph_key(int mode, const double* A, int64_t lda, bool arow, int64_t m, int64_t n,
+                      const Dims& D, const double* omega, const void* ws, size_t wsb,
+                      const ffb_result* out) {
+  std::string k;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  key_put(k, dev);
+  key_put(k, mode);
+  key_put(k, A);
+  key_put(k, lda);
+  key_put(k, arow);
+  key_put(k, m);
+  key_put(k, n);
+  key_put(k, D.k);
+  key_put(k, D.l);
+  key_put(k, D.b);
+  key_put(k, D.p);
+  key_put(k, D.d);
+  key_put(k, D.g);
+  key_put(k, omega);
+  key_put(k, ws);
+  key_put(k, wsb);
+  key_put(k, out->pivot_gap != nullptr);
+  return k;
+}
+
+// Run `core` (a stream-ordered launch sequence with no host synchronisation) on
+// `st`: replay its cached CUDA graph, or capture it on a private stream,
+// instantiate, cache and launch it; anything not capturable runs eagerly.
+template <class Eng_, class F>
+void run_core(ffb_ctx* ctx, Eng_& e, cudaStream_t& st, const std::string& key, F&& core) {
+  if (!graphs_enabled()) {
+    core();
+    return;
+  }
+  {
+    std::lock_guard<std::mutex> g(ctx->gmu);
+    auto it = ctx->graphs.find(key);
+    if (it != ctx->graphs.end()) {
+      GraphEnt& ge = it->second;
+      ge.stamp = ++ctx->gstamp;
+      e.okm(cudaGraphLaunch(ge.exec, st));
+      e.launches += ge.launches;
+      e.gc.launches += ge.glaunches;
+      e.gc.flops += ge.flops;
+      return;
+    }
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaStream_t& cap = t_host.capture[dev & 63];
+  if (!cap && cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess) {
+    cap = nullptr;
+    core();
+    return;
+  }
+  const cudaStream_t user = st;
+  const int64_t l0 = e.launches, gl0 = e.gc.launches, f0 = e.gc.flops;
+  st = e.st = cap;
+  cudaGraph_t graph = nullptr;
+  bool ok = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  if (ok) {
+    core();
+    const cudaError_t ce = cudaStreamEndCapture(cap, &graph);
+    ok = ce == cudaSuccess && graph != nullptr && e.cerr == cudaSuccess;
+  }
+  st = e.st = user;
+  cudaGraphExec_t exec = nullptr;
+  if (ok) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+  if (graph) cudaGraphDestroy(graph);
+  if (!ok) {   // not capturable here: run the sequence eagerly
+    (void)cudaGetLastError();
+    e.cerr = cudaSuccess;
+    e.launches = l0;
+    e.gc.launches = gl0;
+    e.gc.flops = f0;
+    core();
+    return;
+  }
+  GraphEnt ge;
+  ge.exec = exec;
+  ge.launches = e.launches - l0;
+  ge.glaunches = e.gc.launches - gl0;
+  ge.flops = e.gc.flops - f0;
+  e.okm(cudaGraphLaunch(exec, st));
+  std::lock_guard<std::mutex> g(ctx->gmu);
+  if (ctx->graphs.count(key)) {   // another thread captured the same key meanwhile
+    ctx->retired.push_back(exec);
+    return;
+  }
+  if (ctx->graphs.size() >= kMaxGraphs) {
+    auto old = ctx->graphs.begin();
+    for (auto it = ctx->graphs.begin(); it != ctx->graphs.end(); ++it)
+      if (it->second.stamp < old->second.stamp) old = it;
+    cudaDeviceSynchronize();   // the evicted graph may still run on another stream
+    cudaGraphExecDestroy(old->second.exec);
+    ctx->graphs.erase(old);
+  }
+  ge.stamp = ++ctx->gstamp;
+  ctx->graphs.emplace(key, ge);
+}
+
 bool validate(const Dims& D) {
   if (D.m < 1 || D.n < 1) return false;
   if (!(1 <= D.k && D.k <= D.l && D.l <= std::min(D.m, D.n))) return false;
@@ -462,6 +612,12 @@ int ffb_ctx_create(int device, ffb_ctx** out) {
 
 int ffb_ctx_destroy(ffb_ctx* c) {
   if (!c) return FFB_OK;
+  {
+    DeviceGuard dg(c->device);
+    cudaDeviceSynchronize();
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second.exec);
+    for (auto ex : c->retired) cudaGraphExecDestroy(ex);
+  }
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->sc_host) cudaFreeHost(c->sc_host);
   delete c;
@@ -531,16 +687,20 @@ int ffb_block_pivots(ffb_ctx* ctx, void* stream, const double* B, int64_t s, int
 }
 
 int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, int64_t n,
-            int64_t lda, const ffb_params* prm, const double* omega, ffb_gauss_cb gauss,
-            void* gauss_user, void* workspace, size_t workspace_bytes, ffb_result* out) {
+            int64_t lda, int a_layout, const ffb_params* prm, const double* omega,
+            ffb_gauss_cb gauss, void* gauss_user, void* workspace, size_t workspace_bytes,
+            ffb_result* out) {
   if (!ctx || !prm || !out || !A || !omega || !workspace) return FFB_ERR_ARGUMENT;
+  if (a_layout != FFB_LAYOUT_COL && a_layout != FFB_LAYOUT_ROW) return FFB_ERR_ARGUMENT;
+  const AView av{A, lda, a_layout == FFB_LAYOUT_ROW};
   DeviceGuard dg(ctx->device);
   Eng e;
   e.ctx = ctx;
   e.st = (cudaStream_t)stream;
   Dims& D = e.D;
   D = Dims{m, n, prm->k, prm->l, prm->b, prm->p, prm->b + prm->p, prm->d, prm->g, prm->seed, mode};
-  if (!validate(D) || lda < m) return fail(ctx, FFB_ERR_DIMENSION, "invalid dimensions/parameters");
+  if (!validate(D) || lda < (av.row ? n : m))
+    return fail(ctx, FFB_ERR_DIMENSION, "invalid dimensions/parameters");
   if (mode == FFB_MODE_FLIPFLOP && (!out->u || !out->s || !out->v))
     return fail(ctx, FFB_ERR_ARGUMENT, "u, s, v outputs are required");
   Work& w = e.w;
@@ -575,56 +735,61 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
   }
 
   // ---------------------------------------------------------------- TRQRCP
-  e.okm(cudaMemsetAsync(w.status, 0, sizeof(uint32_t), st));
-  e.okm(cudaMemsetAsync(w.skcnt, 0, sizeof(unsigned) * 65536, st));
-  // B = Omega * A (Omega row-major s x m: A-operand with contiguous k)
-  e.gemm(s, n, m, 1.0, omega, m, true, A, lda, true, 0.0, w.B, s);
-  e.ok(launch_colsq(st, A, lda, m, n, w.colsq));
-  e.ok(launch_finite_check(st, w.colsq, (size_t)n, w.status));   // NaN / Inf anywhere in A
-  e.ok(launch_iota2(st, w.arr, w.pos, n));
-  e.memset2d(w.Y, m, m, l);
-  e.memset2d(w.T, l, l, l);
-  e.memset2d(w.WT, l, l, n);
-  e.memset2d(w.R, L1, L1, n);
-  {
-  }
-  for (int64_t j0 = 0; j0 < l && e.cerr == cudaSuccess; j0 += D.b) {
-    const int64_t bb = std::min<int64_t>(D.b, l - j0), e1 = j0 + bb;
-    // (K2) pivots on the sketch
-    e.okm(cudaMemsetAsync(w.prec, 0, 16 * (size_t)w.G * pivots_recw((int)s), st));
-    PivotArgs pa{w.B, s, (int)s, n, j0, (int)bb, w.arr, w.pos, w.G, w.cpc, 0, w.pwork, w.prec,
-                 pivots_recw((int)s), w.hist, out->pivot_gap ? w.gap + j0 : nullptr};
-    e.ok(launch_pivots(st, pa, w.piv_smem, w.piv_smem_bytes));
-    // (K4) panel P = A[:, piv] - Y[:, :j0] WT[:j0, piv]
-    e.ok(launch_gather_cols(st, A, lda, m, w.arr + j0, bb, w.P, m));
-    if (j0 > 0) {
-      e.ok(launch_gather_cols(st, w.WT, l, j0, w.arr + j0, bb, w.WTg, j0));
-      e.gemm(m, bb, j0, -1.0, w.Y, m, false, w.WTg, j0, true, 1.0, w.P, m);
+  auto trqrcp_body = [&]() {
+    e.okm(cudaMemsetAsync(w.status, 0, sizeof(uint32_t), st));
+    e.okm(cudaMemsetAsync(w.skcnt, 0, sizeof(unsigned) * 65536, st));
+    // B = Omega * A (Omega row-major s x m: A-operand with contiguous k)
+    e.gemm(s, n, m, 1.0, omega, m, true, A, lda, av.kc_as_b(), 0.0, w.B, s);
+    if (av.row) e.ok(launch_colsq_rm(st, A, lda, m, n, w.cpart, w.colsq));
+    else e.ok(launch_colsq(st, A, lda, m, n, w.colsq));
+    e.ok(launch_finite_check(st, w.colsq, (size_t)n, w.status));   // NaN / Inf anywhere in A
+    e.ok(launch_iota2(st, w.arr, w.pos, n));
+    e.memset2d(w.Y, m, m, l);
+    e.memset2d(w.T, l, l, l);
+    e.memset2d(w.WT, l, l, n);
+    e.memset2d(w.R, L1, L1, n);
+    {
     }
-    // Householder QR of P[j0:, :] -> Y block, T block, Rb
-    e.hh_qr(w.P + j0, m - j0, bb, m, w.Y + j0 + j0 * m, m, w.T + j0 + j0 * l, l, w.Rb, bb, true);
-    // T12 = -T11 (Y1^T Y2) T22
-    if (j0 > 0) {
-      e.gemm(j0, bb, m - j0, 1.0, w.Y + j0, m, true, w.Y + j0 + j0 * m, m, true, 0.0, w.S1, j0);
-      e.gemm(j0, bb, bb, 1.0, w.S1, j0, false, w.T + j0 + j0 * l, l, true, 0.0, w.S2, j0);
-      e.gemm(j0, bb, j0, -1.0, w.T, l, false, w.S2, j0, true, 0.0, w.T + j0 * l, l);
+    for (int64_t j0 = 0; j0 < l && e.cerr == cudaSuccess; j0 += D.b) {
+      const int64_t bb = std::min<int64_t>(D.b, l - j0), e1 = j0 + bb;
+      // (K2) pivots on the sketch
+      e.okm(cudaMemsetAsync(w.prec, 0, 16 * (size_t)w.G * pivots_recw((int)s), st));
+      PivotArgs pa{w.B, s, (int)s, n, j0, (int)bb, w.arr, w.pos, w.G, w.cpc, 0, w.pwork, w.prec,
+                   pivots_recw((int)s), w.hist, out->pivot_gap ? w.gap + j0 : nullptr};
+      e.ok(launch_pivots(st, pa, w.piv_smem, w.piv_smem_bytes));
+      // (K4) panel P = A[:, piv] - Y[:, :j0] WT[:j0, piv]
+      e.ok(launch_gather_cols_strided(st, A, av.rs(), av.cs(), m, w.arr + j0, bb, w.P, m));
+      if (j0 > 0) {
+        e.ok(launch_gather_cols(st, w.WT, l, j0, w.arr + j0, bb, w.WTg, j0));
+        e.gemm(m, bb, j0, -1.0, w.Y, m, false, w.WTg, j0, true, 1.0, w.P, m);
+      }
+      // Householder QR of P[j0:, :] -> Y block, T block, Rb
+      e.hh_qr(w.P + j0, m - j0, bb, m, w.Y + j0 + j0 * m, m, w.T + j0 + j0 * l, l, w.Rb, bb, true);
+      // T12 = -T11 (Y1^T Y2) T22
+      if (j0 > 0) {
+        e.gemm(j0, bb, m - j0, 1.0, w.Y + j0, m, true, w.Y + j0 + j0 * m, m, true, 0.0, w.S1, j0);
+        e.gemm(j0, bb, bb, 1.0, w.S1, j0, false, w.T + j0 + j0 * l, l, true, 0.0, w.S2, j0);
+        e.gemm(j0, bb, j0, -1.0, w.T, l, false, w.S2, j0, true, 0.0, w.T + j0 * l, l);
+      }
+      // (K5) WT[j0:e, :] = T22^T (Y2^T A - (Y2^T Y1) WT[:j0, :])
+      e.gemm(bb, n, m - j0, 1.0, w.Y + j0 + j0 * m, m, true, av.rows_from(j0), lda, av.kc_as_b(), 0.0,
+             w.G1, bb);
+      if (j0 > 0) e.gemm(bb, n, j0, -1.0, w.S1, j0, true, w.WT, l, true, 1.0, w.G1, bb);
+      e.gemm(bb, n, bb, 1.0, w.T + j0 + j0 * l, l, true, w.G1, bb, true, 0.0, w.WT + j0, l);
+      // (K6) R[j0:e, :] = A[j0:e, :] - Y[j0:e, :e] WT[:e, :]
+      if (av.row) e.ok(launch_copy_rows_rm(st, av.rows_from(j0), lda, bb, n, w.R + j0, L1));
+      else e.ok(launch_copy_rows(st, A + j0, lda, bb, n, w.R + j0, L1));
+      e.gemm(bb, n, e1, -1.0, w.Y + j0, m, false, w.WT, l, true, 1.0, w.R + j0, L1);
+      e.ok(launch_fix_rrows(st, w.R, L1, j0, (int)bb, w.arr, w.Rb, bb));
+      // sketch update B[:, trailing] -= (B_piv R11^{-1}) R12
+      if (e1 < n) {
+        e.ok(launch_gather_cols(st, w.B, s, s, w.arr + j0, bb, w.Bp, s));
+        e.tri_inverse(w.Rb, bb, bb, w.Rinv, bb);
+        e.gemm(s, bb, bb, 1.0, w.Bp, s, false, w.Rinv, bb, true, 0.0, w.Z, s);
+        e.gemm(s, n, bb, -1.0, w.Z, s, false, w.R + j0, L1, true, 1.0, w.B, s);
+      }
     }
-    // (K5) WT[j0:e, :] = T22^T (Y2^T A - (Y2^T Y1) WT[:j0, :])
-    e.gemm(bb, n, m - j0, 1.0, w.Y + j0 + j0 * m, m, true, A + j0, lda, true, 0.0, w.G1, bb);
-    if (j0 > 0) e.gemm(bb, n, j0, -1.0, w.S1, j0, true, w.WT, l, true, 1.0, w.G1, bb);
-    e.gemm(bb, n, bb, 1.0, w.T + j0 + j0 * l, l, true, w.G1, bb, true, 0.0, w.WT + j0, l);
-    // (K6) R[j0:e, :] = A[j0:e, :] - Y[j0:e, :e] WT[:e, :]
-    e.ok(launch_copy_rows(st, A + j0, lda, bb, n, w.R + j0, L1));
-    e.gemm(bb, n, e1, -1.0, w.Y + j0, m, false, w.WT, l, true, 1.0, w.R + j0, L1);
-    e.ok(launch_fix_rrows(st, w.R, L1, j0, (int)bb, w.arr, w.Rb, bb));
-    // sketch update B[:, trailing] -= (B_piv R11^{-1}) R12
-    if (e1 < n) {
-      e.ok(launch_gather_cols(st, w.B, s, s, w.arr + j0, bb, w.Bp, s));
-      e.tri_inverse(w.Rb, bb, bb, w.Rinv, bb);
-      e.gemm(s, bb, bb, 1.0, w.Bp, s, false, w.Rinv, bb, true, 0.0, w.Z, s);
-      e.gemm(s, n, bb, -1.0, w.Z, s, false, w.R + j0, L1, true, 1.0, w.B, s);
-    }
-  }
+  };
 
   auto outputs_common = [&]() {
     if (out->perm)
@@ -634,6 +799,80 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
     if (out->pivot_gap)
       e.ok(d2d(out->pivot_gap, w.gap, sizeof(double) * l, st));
   };
+
+  // ------------------------------------------------------------------ SRQR
+  auto srqr_init = [&]() {
+    // dense Q[:, :l] = E - Y (T Y[:l, :]^T)   (srqr.py:91-93)
+    e.gemm(l, l, l, 1.0, w.T, l, false, w.Y, m, false, 0.0, w.TYt, l);
+    e.gemm(m, l, l, -1.0, w.Y, m, false, w.TYt, l, true, 0.0, w.Q, m);
+    e.ok(launch_add_identity(st, w.Q, m, m, l, 1.0));
+    e.okm(cudaMemsetAsync(w.Q + m * l, 0, sizeof(double) * m, st));
+    e.ok(launch_rinit(st, w.B, s, (int)s, w.arr, n, l, w.r, w.rinit));
+    e.ok(launch_anorm(st, w.colsq, n, w.sc));
+  };
+  auto extend = [&]() {
+    e.ok(launch_ext_pick(st, l, n, w.arr, w.pos, w.r, w.rinit, w.sc));
+    e.ok(launch_ext_project(st, A, av.rs(), av.cs(), m, l, w.Q, m, w.R, L1, w.arr, w.u, w.ct, w.part,
+                            w.sc, w.r, w.R));
+    const int nparts = (int)((m + 255) / 256);
+    e.ok(launch_ext_finish(st, w.part, nparts, l, n, w.arr, w.R, L1, w.r, w.sc, w.u, m, w.Q + m * l));
+  };
+
+  auto pack = [&]() { e.ok(launch_pack(st, w.R, L1, w.arr, w.colsq, l, n, w.part, 0, w.sc)); };
+  auto pack_outputs = [&]() {
+    outputs_common();
+    if (out->Q) e.ok(launch_copy_rows(st, w.Q, m, m, L1, out->Q, out->ldq));
+    if (out->rtilde) e.ok(launch_r_arranged(st, w.R, L1, w.arr, L1, L1, out->rtilde, L1, L1));
+  };
+
+  // ------------------------------------------------------------ flip-flop
+  auto flipflop_core = [&]() {
+    e.ok(launch_build_rt(st, w.R, L1, w.arr, l, n, w.X, n));
+    e.hh_qr(w.X, n, l, n, w.Yl, n, w.Tl, l, w.Rl, l, false);
+    // Qhat1 = E - Yl (Tl Yl[:l,:]^T) ; Yh = Pi Qhat1 (rows scattered to original order)
+    e.gemm(l, l, l, 1.0, w.Tl, l, false, w.Yl, n, false, 0.0, w.TYt, l);
+    e.gemm(n, l, l, -1.0, w.Yl, n, false, w.TYt, l, true, 0.0, w.Qh, n);
+    e.ok(launch_add_identity(st, w.Qh, n, n, l, 1.0));
+    e.ok(launch_scatter_rows(st, w.Qh, n, n, l, w.arr, w.Yh, n));
+    // (K13) tmp = A * Yh
+    e.gemm(m, l, n, 1.0, A, lda, av.kc_as_a(), w.Yh, n, true, 0.0, w.tmp, m);
+    // (K14) tmp = Qt Rt, SVD(Rt)
+    e.hh_qr(w.tmp, m, l, m, w.Yt, m, w.Tt, l, w.Rt, l, true);
+    // one-sided block Jacobi SVD of Rt (ffb_jacobi.cu): Rt = Us diag(sig) Vo^T
+    e.ok(launch_jacobi_svd(st, ctx->sms, w.Rt, l, (int)l, w.sig, w.Us, l, w.Vo, l, w.jwork, w.jbar,
+                           w.joff, w.jsweeps, w.jorder, kMaxSweeps));
+    e.launches += 5;   // scale, layout, Jacobi, V replay, norms, out kernels
+    // (K15, left half) W2 = Tt (Yt[:l]^T Us[:, :k])
+    e.gemm(l, D.k, l, 1.0, w.Yt, m, true, w.Us, l, true, 0.0, w.W1, l);
+    e.gemm(l, D.k, l, 1.0, w.Tt, l, false, w.W1, l, true, 0.0, w.W2, l);
+  };
+  // the caller's outputs of the flip-flop tail (kept out of the cached graph so
+  // its key does not depend on where the caller's output buffers live)
+  auto flipflop_out = [&]() {
+    const int64_t k = D.k;
+    if (out->diag_L) e.ok(launch_diag(st, w.Rl, l, l, out->diag_L));
+    // (K15) u = Qt[:, :l] Us[:, :k] ; v = Yh Vs[:, :k]
+    e.gemm(m, k, l, -1.0, w.Yt, m, false, w.W2, l, true, 0.0, out->u, out->ldu);
+    e.ok(launch_add_top(st, out->u, out->ldu, w.Us, l, l, k));
+    e.gemm(n, k, l, 1.0, w.Yh, n, false, w.Vo, l, true, 0.0, out->v, out->ldv);
+    e.ok(d2d(out->s, w.sig, sizeof(double) * k, st));
+    if (out->sv_all) e.ok(d2d(out->sv_all, w.sig, sizeof(double) * l, st));
+  };
+
+  // The launch sequence up to the certificate depends only on the shapes, the
+  // parameters and the device buffers (A, Omega, workspace): it is captured once
+  // into a CUDA graph and replayed by later calls with the same key.
+  auto core = [&]() {
+    trqrcp_body();
+    if (mode == FFB_MODE_TRQRCP) return;
+    srqr_init();
+    extend();
+    e.g2();
+    pack();
+    if (mode == FFB_MODE_FLIPFLOP) flipflop_core();
+  };
+  run_core(ctx, e, st, graph_key(mode, A, lda, av.row, m, n, D, omega, workspace, workspace_bytes, out),
+           core);
 
   if (mode == FFB_MODE_TRQRCP) {
     outputs_common();
@@ -652,61 +891,8 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
     return FFB_OK;
   }
 
-  // ------------------------------------------------------------------ SRQR
-  // dense Q[:, :l] = E - Y (T Y[:l, :]^T)   (srqr.py:91-93)
-  e.gemm(l, l, l, 1.0, w.T, l, false, w.Y, m, false, 0.0, w.TYt, l);
-  e.gemm(m, l, l, -1.0, w.Y, m, false, w.TYt, l, true, 0.0, w.Q, m);
-  e.ok(launch_add_identity(st, w.Q, m, m, l, 1.0));
-  e.okm(cudaMemsetAsync(w.Q + m * l, 0, sizeof(double) * m, st));
-  e.ok(launch_rinit(st, w.B, s, (int)s, w.arr, n, l, w.r, w.rinit));
-  e.ok(launch_anorm(st, w.colsq, n, w.sc));
-  auto extend = [&]() {
-    e.ok(launch_ext_pick(st, l, n, w.arr, w.pos, w.r, w.rinit, w.sc));
-    e.ok(launch_ext_project(st, A, lda, m, l, w.Q, m, w.R, L1, w.arr, w.u, w.ct, w.part, w.sc, w.r, w.R));
-    const int nparts = (int)((m + 255) / 256);
-    e.ok(launch_ext_finish(st, w.part, nparts, l, n, w.arr, w.R, L1, w.r, w.sc, w.u, m, w.Q + m * l));
-  };
-  extend();
-  e.g2();
-
-  auto pack_and_outputs = [&]() {
-    e.ok(launch_pack(st, w.R, L1, w.arr, w.colsq, l, n, w.part, 0, w.sc));
-    outputs_common();
-    if (out->Q) e.ok(launch_copy_rows(st, w.Q, m, m, L1, out->Q, out->ldq));
-    if (out->rtilde) e.ok(launch_r_arranged(st, w.R, L1, w.arr, L1, L1, out->rtilde, L1, L1));
-  };
-
-  // ------------------------------------------------------------ flip-flop
-  auto flipflop = [&]() {
-    const int64_t k = D.k;
-    e.ok(launch_build_rt(st, w.R, L1, w.arr, l, n, w.X, n));
-    e.hh_qr(w.X, n, l, n, w.Yl, n, w.Tl, l, w.Rl, l, false);
-    if (out->diag_L) e.ok(launch_diag(st, w.Rl, l, l, out->diag_L));
-    // Qhat1 = E - Yl (Tl Yl[:l,:]^T) ; Yh = Pi Qhat1 (rows scattered to original order)
-    e.gemm(l, l, l, 1.0, w.Tl, l, false, w.Yl, n, false, 0.0, w.TYt, l);
-    e.gemm(n, l, l, -1.0, w.Yl, n, false, w.TYt, l, true, 0.0, w.Qh, n);
-    e.ok(launch_add_identity(st, w.Qh, n, n, l, 1.0));
-    e.ok(launch_scatter_rows(st, w.Qh, n, n, l, w.arr, w.Yh, n));
-    // (K13) tmp = A * Yh
-    e.gemm(m, l, n, 1.0, A, lda, false, w.Yh, n, true, 0.0, w.tmp, m);
-    // (K14) tmp = Qt Rt, SVD(Rt)
-    e.hh_qr(w.tmp, m, l, m, w.Yt, m, w.Tt, l, w.Rt, l, true);
-    // one-sided block Jacobi SVD of Rt (ffb_jacobi.cu): Rt = Us diag(sig) Vo^T
-    e.ok(launch_jacobi_svd(st, ctx->sms, w.Rt, l, (int)l, w.sig, w.Us, l, w.Vo, l, w.jwork, w.jbar,
-                           w.joff, w.jsweeps, w.jorder, kMaxSweeps));
-    e.launches += 5;   // scale, layout, Jacobi, V replay, norms, out kernels
-    // (K15) u = Qt[:, :l] Us[:, :k] ; v = Yh Vs[:, :k]
-    e.gemm(l, k, l, 1.0, w.Yt, m, true, w.Us, l, true, 0.0, w.W1, l);
-    e.gemm(l, k, l, 1.0, w.Tt, l, false, w.W1, l, true, 0.0, w.W2, l);
-    e.gemm(m, k, l, -1.0, w.Yt, m, false, w.W2, l, true, 0.0, out->u, out->ldu);
-    e.ok(launch_add_top(st, out->u, out->ldu, w.Us, l, l, k));
-    e.gemm(n, k, l, 1.0, w.Yh, n, false, w.Vo, l, true, 0.0, out->v, out->ldv);
-    e.ok(d2d(out->s, w.sig, sizeof(double) * k, st));
-    if (out->sv_all) e.ok(d2d(out->sv_all, w.sig, sizeof(double) * l, st));
-  };
-
-  pack_and_outputs();
-  if (mode == FFB_MODE_FLIPFLOP) flipflop();
+  pack_outputs();
+  if (mode == FFB_MODE_FLIPFLOP) flipflop_out();
 
   auto read_sc = [&]() -> cudaError_t {
     if (!t_host.sc) cudaMallocHost(&t_host.sc, sizeof(SrqrScalars));
@@ -731,14 +917,16 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
     // ---- the reference's swap loop (srqr.py:192-206), host-driven
     while (true) {
       if (swaps >= 50 * l) {
-        pack_and_outputs();
+        pack();
+        pack_outputs();
         se = read_sc();
         sc = *t_host.sc;
         out->alpha = sc.alpha; out->g1 = sc.g1; out->g2 = sc.g2; out->r22 = sc.r22;
         out->tau_bound = sc.tau; out->tau_hat_bound = sc.tau_hat; out->swaps = swaps;
         return fail(ctx, FFB_ERR_CERTIFICATION, "swap cap reached");
       }
-      e.ok(launch_ext_row(st, A, lda, m, n, l, w.Q, m, w.R, L1, w.arr, w.colsq, w.r, w.rinit, w.sc));
+      e.ok(launch_ext_row(st, A, av.rs(), av.cs(), m, n, l, w.Q, m, w.R, L1, w.arr, w.colsq, w.r,
+                          w.rinit, w.sc));
       if (swaps < 64) out->i_off_trace[swaps] = sc.i_off;
       ++swaps;
       e.ok(launch_rotate_out(st, w.R, L1, w.Q, m, m, n, l, w.arr, w.pos, w.r, w.rinit, w.sc, w.rot));
@@ -757,8 +945,12 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
       if (sc.status & kStSingular) return fail(ctx, FFB_ERR_SINGULAR_TRAILING, "zero diagonal in leading triangular block");
       if (!sc.need_swap) break;
     }
-    pack_and_outputs();
-    if (mode == FFB_MODE_FLIPFLOP) flipflop();
+    pack();
+    pack_outputs();
+    if (mode == FFB_MODE_FLIPFLOP) {
+      flipflop_core();
+      flipflop_out();
+    }
     se = read_sc();
     if (e.cerr != cudaSuccess) return cuda_fail(ctx, e.cerr, "launch");
     if (se != cudaSuccess) return cuda_fail(ctx, se, "flipflop");
@@ -784,10 +976,10 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
 }
 
 int ffb_flipflop(ffb_ctx* ctx, void* stream, const double* A, int64_t m, int64_t n, int64_t lda,
-                 const ffb_params* prm, const double* omega, ffb_gauss_cb gauss, void* gauss_user,
-                 void* workspace, size_t workspace_bytes, ffb_result* out) {
-  return ffb_run(ctx, stream, FFB_MODE_FLIPFLOP, A, m, n, lda, prm, omega, gauss, gauss_user,
-                 workspace, workspace_bytes, out);
+                 int a_layout, const ffb_params* prm, const double* omega, ffb_gauss_cb gauss,
+                 void* gauss_user, void* workspace, size_t workspace_bytes, ffb_result* out) {
+  return ffb_run(ctx, stream, FFB_MODE_FLIPFLOP, A, m, n, lda, a_layout, prm, omega, gauss,
+                 gauss_user, workspace, workspace_bytes, out);
 }
 
 }  // extern "C"
@@ -803,8 +995,8 @@ extern "C" int ffb_run_batched(ffb_ctx* ctx, ffb_batch_item* items, int64_t coun
   auto worker = [&]() {
     for (int64_t i = next++; i < count; i = next++) {
       ffb_batch_item& it = items[i];
-      it.status = ffb_run(ctx, it.stream, it.mode, it.A, it.m, it.n, it.lda, &it.prm, it.omega,
-                          gauss, gauss_user, it.workspace, it.workspace_bytes, it.out);
+      it.status = ffb_run(ctx, it.stream, it.mode, it.A, it.m, it.n, it.lda, it.a_layout, &it.prm,
+                          it.omega, gauss, gauss_user, it.workspace, it.workspace_bytes, it.out);
       if (it.status != FFB_OK) msgs[(size_t)i] = t_err;
     }
   };
@@ -838,12 +1030,14 @@ extern "C" int ffb_rsisvd_workspace_query(int64_t m, int64_t n, int64_t k, int64
 }
 
 extern "C" int ffb_rsisvd(ffb_ctx* ctx, void* stream, const double* A, int64_t m, int64_t n,
-                          int64_t lda, int64_t k, int64_t r, int64_t q, const double* omega,
+                          int64_t lda, int a_layout, int64_t k, int64_t r, int64_t q, const double* omega,
                           void* workspace, size_t workspace_bytes, double* u, int64_t ldu,
                           double* s, double* v, int64_t ldv, int64_t* flops, int32_t* sweeps_out) {
   if (!ctx || !A || !omega || !workspace || !u || !s || !v) return FFB_ERR_ARGUMENT;
   DeviceGuard dg(ctx->device);
-  if (m < 1 || n < 1 || k < 1 || k > r || r > std::min(m, n) || q < 0 || lda < m ||
+  if (a_layout != FFB_LAYOUT_COL && a_layout != FFB_LAYOUT_ROW) return FFB_ERR_ARGUMENT;
+  const bool arow = a_layout == FFB_LAYOUT_ROW;
+  if (m < 1 || n < 1 || k < 1 || k > r || r > std::min(m, n) || q < 0 || lda < (arow ? n : m) ||
       ldu < m || ldv < n)
     return fail(ctx, FFB_ERR_DIMENSION, "rsisvd needs 1 <= k <= r <= min(m, n), q >= 0");
   Eng e;
@@ -861,19 +1055,19 @@ extern "C" int ffb_rsisvd(ffb_ctx* ctx, void* stream, const double* A, int64_t m
   e.okm(cudaMemsetAsync(w.status, 0, sizeof(uint32_t), st));
   e.okm(cudaMemsetAsync(w.skcnt, 0, sizeof(unsigned) * 65536, st));
   // Y = A Omega (Omega n x r, row-major = numpy C order)
-  e.gemm(m, r, n, 1.0, A, lda, false, omega, r, false, 0.0, w.tmp, m);
+  e.gemm(m, r, n, 1.0, A, lda, arow, omega, r, false, 0.0, w.tmp, m);
   e.hh_qr(w.tmp, m, r, m, w.Yt, m, w.Tt, r, w.Rt, r, false);
   explicit_q(e, w.Yt, m, w.Tt, r, m, r, w.Q, m);
   for (int64_t it = 0; it < q; ++it) {
-    e.gemm(n, r, m, 1.0, A, lda, true, w.Q, m, true, 0.0, w.X, n);          // Z = A^T Q
+    e.gemm(n, r, m, 1.0, A, lda, !arow, w.Q, m, true, 0.0, w.X, n);         // Z = A^T Q
     e.hh_qr(w.X, n, r, n, w.Yl, n, w.Tl, r, w.Rl, r, false);
     explicit_q(e, w.Yl, n, w.Tl, r, n, r, w.Qh, n);
-    e.gemm(m, r, n, 1.0, A, lda, false, w.Qh, n, true, 0.0, w.tmp, m);      // Y = A Q_z
+    e.gemm(m, r, n, 1.0, A, lda, arow, w.Qh, n, true, 0.0, w.tmp, m);       // Y = A Q_z
     e.hh_qr(w.tmp, m, r, m, w.Yt, m, w.Tt, r, w.Rt, r, false);
     explicit_q(e, w.Yt, m, w.Tt, r, m, r, w.Q, m);
   }
   // B^T = A^T Q = Q_b R_b
-  e.gemm(n, r, m, 1.0, A, lda, true, w.Q, m, true, 0.0, w.X, n);
+  e.gemm(n, r, m, 1.0, A, lda, !arow, w.Q, m, true, 0.0, w.X, n);
   e.hh_qr(w.X, n, r, n, w.Yl, n, w.Tl, r, w.Rl, r, true);
   e.ok(launch_jacobi_svd(st, ctx->sms, w.Rl, r, (int)r, w.sig, w.Us, r, w.Vo, r, w.jwork, w.jbar,
                          w.joff, w.jsweeps, w.jorder, kMaxSweeps));

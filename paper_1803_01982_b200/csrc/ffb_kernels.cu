@@ -88,6 +88,44 @@ cudaError_t launch_colsq(cudaStream_t st, const double* A, int64_t lda, int64_t 
   FFB_LAUNCH_CHECK();
 }
 
+// Row-major A (A(i, j) = A[i * lda + j]): thread per column, coalesced along
+// rows; kColsqSplit row slabs write partial sums that a second pass adds in
+// slab order (deterministic).
+constexpr int kColsqSplit = 16;
+__global__ void colsq_rm_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n,
+                                double* __restrict__ part) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int64_t per = (m + kColsqSplit - 1) / kColsqSplit;
+  const int64_t i0 = blockIdx.y * per, i1 = i0 + per < m ? i0 + per : m;
+  double s0 = 0.0, s1 = 0.0;
+  int64_t i = i0;
+  for (; i + 1 < i1; i += 2) {
+    const double x = A[i * lda + j], y = A[(i + 1) * lda + j];
+    s0 = fma(x, x, s0);
+    s1 = fma(y, y, s1);
+  }
+  if (i < i1) s0 = fma(A[i * lda + j], A[i * lda + j], s0);
+  part[blockIdx.y * n + j] = s0 + s1;
+}
+
+__global__ void colsq_rm_sum_kernel(const double* __restrict__ part, int64_t n, double* colsq) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double s = 0.0;
+  for (int q = 0; q < kColsqSplit; ++q) s += part[q * n + j];
+  colsq[j] = s;
+}
+
+size_t colsq_rm_part_doubles(int64_t n) { return (size_t)kColsqSplit * (size_t)n; }
+
+cudaError_t launch_colsq_rm(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n,
+                            double* part, double* colsq) {
+  colsq_rm_kernel<<<dim3(nblk(n, 256), kColsqSplit), 256, 0, st>>>(A, lda, m, n, part);
+  colsq_rm_sum_kernel<<<nblk(n, 256), 256, 0, st>>>(part, n, colsq);
+  FFB_LAUNCH_CHECK();
+}
+
 __global__ void iota2_kernel(int64_t* arr, int64_t* pos, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -660,24 +698,31 @@ cudaError_t launch_pivots(cudaStream_t st, const PivotArgs& a, bool smem_mode, s
 
 // ------------------------------------------------------- gathers / copies
 
-__global__ void gather_cols_kernel(const double* __restrict__ src, int64_t ld_src, int64_t rows,
+// element (i, c) of src at src[i * rs + c * cs] (column-major: rs = 1, cs = ld)
+__global__ void gather_cols_kernel(const double* __restrict__ src, int64_t rs, int64_t cs, int64_t rows,
                                    const int64_t* __restrict__ idx, int64_t ncols,
                                    double* __restrict__ dst, int64_t ld_dst) {
   const int64_t j = blockIdx.y;
   const int64_t c = idx[j];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
        i += (int64_t)gridDim.x * blockDim.x)
-    dst[i + j * ld_dst] = src[i + c * ld_src];
+    dst[i + j * ld_dst] = src[i * rs + c * cs];
+}
+
+cudaError_t launch_gather_cols_strided(cudaStream_t st, const double* src, int64_t rs, int64_t cs,
+                                       int64_t rows, const int64_t* idx, int64_t ncols, double* dst,
+                                       int64_t ld_dst) {
+  if (rows <= 0 || ncols <= 0) return cudaSuccess;
+  unsigned gx = nblk(rows, 256);
+  if (gx > 64) gx = 64;
+  gather_cols_kernel<<<dim3(gx, (unsigned)ncols), 256, 0, st>>>(src, rs, cs, rows, idx, ncols, dst,
+                                                                 ld_dst);
+  FFB_LAUNCH_CHECK();
 }
 
 cudaError_t launch_gather_cols(cudaStream_t st, const double* src, int64_t ld_src, int64_t rows,
                                const int64_t* idx, int64_t ncols, double* dst, int64_t ld_dst) {
-  if (rows <= 0 || ncols <= 0) return cudaSuccess;
-  unsigned gx = nblk(rows, 256);
-  if (gx > 64) gx = 64;
-  gather_cols_kernel<<<dim3(gx, (unsigned)ncols), 256, 0, st>>>(src, ld_src, rows, idx, ncols, dst,
-                                                                 ld_dst);
-  FFB_LAUNCH_CHECK();
+  return launch_gather_cols_strided(st, src, 1, ld_src, rows, idx, ncols, dst, ld_dst);
 }
 
 // dst[idx[c], j] = src[c, j]
@@ -719,6 +764,28 @@ cudaError_t launch_copy_rows(cudaStream_t st, const double* src, int64_t ld_src,
   unsigned g = nblk(total, 256);
   if (g > 8192) g = 8192;
   copy2d_kernel<<<g, 256, 0, st>>>(src, ld_src, rows, cols, dst, ld_dst);
+  FFB_LAUNCH_CHECK();
+}
+
+// rows x cols block of a ROW-major source (src[i * ld_src + j]) into column-major dst
+// (reads coalesced along j, one row per warp-stride)
+__global__ void copy2d_rm_kernel(const double* __restrict__ src, int64_t ld_src, int64_t rows,
+                                 int64_t cols, double* __restrict__ dst, int64_t ld_dst) {
+  const int64_t total = rows * cols;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t % cols, i = t / cols;
+    dst[i + j * ld_dst] = src[i * ld_src + j];
+  }
+}
+
+cudaError_t launch_copy_rows_rm(cudaStream_t st, const double* src, int64_t ld_src, int64_t rows,
+                                int64_t cols, double* dst, int64_t ld_dst) {
+  const int64_t total = rows * cols;
+  if (total <= 0) return cudaSuccess;
+  unsigned g = nblk(total, 256);
+  if (g > 8192) g = 8192;
+  copy2d_rm_kernel<<<g, 256, 0, st>>>(src, ld_src, rows, cols, dst, ld_dst);
   FFB_LAUNCH_CHECK();
 }
 
@@ -1187,7 +1254,7 @@ cudaError_t launch_ext_pick(cudaStream_t st, int64_t l, int64_t n, int64_t* arr,
 }
 
 // u = A[:, c] - Q1 R[:l, c]   (c = arr[l])
-__global__ void ext_u_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t l,
+__global__ void ext_u_kernel(const double* __restrict__ A, int64_t ars, int64_t acs, int64_t m, int64_t l,
                              const double* __restrict__ Q, int64_t ldq, const double* __restrict__ R,
                              int64_t ldr, const int64_t* __restrict__ arr, double* u) {
   extern __shared__ double rc[];
@@ -1203,7 +1270,7 @@ __global__ void ext_u_kernel(const double* __restrict__ A, int64_t lda, int64_t 
     a1 = fma(Q[i + (j + 1) * ldq], rc[j + 1], a1);
   }
   if (j < l) a0 = fma(Q[i + j * ldq], rc[j], a0);
-  u[i] = A[i + c * lda] - (a0 + a1);
+  u[i] = A[i * ars + c * acs] - (a0 + a1);
 }
 
 // ct[j] = Q[:, j]^T u  (one CTA per j, deterministic)
@@ -1271,14 +1338,14 @@ __global__ void ext_q_kernel(const double* __restrict__ u, int64_t m, double* Ql
   if (i < m) Ql[i] = alpha > 0.0 ? u[i] / alpha : 0.0;
 }
 
-cudaError_t launch_ext_project(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t l,
+cudaError_t launch_ext_project(cudaStream_t st, const double* A, int64_t ars, int64_t acs, int64_t m, int64_t l,
                                const double* Q, int64_t ldq, const double* R, int64_t ldr,
                                const int64_t* arr, double* u, double* ct, double* part,
                                SrqrScalars* sc, double* r, double* Rfull) {
   (void)R;
   const unsigned g = nblk(m, 256);
   const size_t sh = sizeof(double) * (size_t)(l > 0 ? l : 1);
-  ext_u_kernel<<<g, 256, sh, st>>>(A, lda, m, l, Q, ldq, Rfull, ldr, arr, u);
+  ext_u_kernel<<<g, 256, sh, st>>>(A, ars, acs, m, l, Q, ldq, Rfull, ldr, arr, u);
   if (l > 0) {
     ext_ct_kernel<<<(unsigned)l, 256, 0, st>>>(Q, ldq, m, u, ct);
   }
@@ -1297,7 +1364,7 @@ cudaError_t launch_ext_finish(cudaStream_t st, const double* part, int nparts, i
 // Extension row R[l, arr[p]] = q^T A[:, arr[p]] for p > l, downdate r and the
 // guard recompute against exact_trailing_sq(i, l+1) (srqr.py:136-149).  Only
 // materialised on the swap path (the row is dead when g2 <= g).
-__global__ void ext_row_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n,
+__global__ void ext_row_kernel(const double* __restrict__ A, int64_t ars, int64_t acs, int64_t m, int64_t n,
                                int64_t l, const double* __restrict__ q, double* R, int64_t ldr,
                                const int64_t* __restrict__ arr, const double* __restrict__ colsq,
                                double* r, const double* __restrict__ rinit,
@@ -1306,9 +1373,9 @@ __global__ void ext_row_kernel(const double* __restrict__ A, int64_t lda, int64_
   const int64_t p = l + 1 + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (p >= n || !(sc->alpha > 0.0)) return;
   const int64_t col = arr[p];
-  const double* a = A + col * lda;
+  const double* a = A + col * acs;
   double acc = 0.0;
-  for (int64_t i = lane; i < m; i += 32) acc = fma(q[i], a[i], acc);
+  for (int64_t i = lane; i < m; i += 32) acc = fma(q[i], a[i * ars], acc);
   acc = warp_sum(acc);
   // exact trailing norm below l+1 rows, needed only by the guard
   double rs = 0.0;
@@ -1325,12 +1392,12 @@ __global__ void ext_row_kernel(const double* __restrict__ A, int64_t lda, int64_
   }
 }
 
-cudaError_t launch_ext_row(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n,
+cudaError_t launch_ext_row(cudaStream_t st, const double* A, int64_t ars, int64_t acs, int64_t m, int64_t n,
                            int64_t l, const double* Q, int64_t ldq, double* R, int64_t ldr,
                            const int64_t* arr, const double* colsq, double* r,
                            const double* rinit, const SrqrScalars* sc) {
   if (n <= l + 1) return cudaSuccess;
-  ext_row_kernel<<<nblk(n - l - 1, 8), 256, 0, st>>>(A, lda, m, n, l, Q + l * ldq, R, ldr, arr,
+  ext_row_kernel<<<nblk(n - l - 1, 8), 256, 0, st>>>(A, ars, acs, m, n, l, Q + l * ldq, R, ldr, arr,
                                                        colsq, r, rinit, sc);
   FFB_LAUNCH_CHECK();
 }

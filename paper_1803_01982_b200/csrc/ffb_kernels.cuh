@@ -51,6 +51,14 @@ struct SrqrScalars {
 
 cudaError_t launch_colsq(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n,
                          double* colsq);
+size_t colsq_rm_part_doubles(int64_t n);
+cudaError_t launch_colsq_rm(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n,
+                            double* part, double* colsq);
+cudaError_t launch_gather_cols_strided(cudaStream_t st, const double* src, int64_t rs, int64_t cs,
+                                       int64_t rows, const int64_t* idx, int64_t ncols, double* dst,
+                                       int64_t ld_dst);
+cudaError_t launch_copy_rows_rm(cudaStream_t st, const double* src, int64_t ld_src, int64_t rows,
+                                int64_t cols, double* dst, int64_t ld_dst);
 cudaError_t launch_iota2(cudaStream_t st, int64_t* arr, int64_t* pos, int64_t n);
 cudaError_t launch_pivots(cudaStream_t st, const PivotArgs& a, bool smem_mode, size_t smem);
 size_t pivots_smem_bytes(int s, int cpc, bool smem_mode);
@@ -91,11 +99,11 @@ cudaError_t launch_rinit(cudaStream_t st, const double* B, int64_t ldb, int s, c
 cudaError_t launch_anorm(cudaStream_t st, const double* colsq, int64_t n, SrqrScalars* sc);
 cudaError_t launch_ext_pick(cudaStream_t st, int64_t l, int64_t n, int64_t* arr, int64_t* pos,
                             double* r, double* rinit, SrqrScalars* sc);
-cudaError_t launch_ext_project(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t l,
+cudaError_t launch_ext_project(cudaStream_t st, const double* A, int64_t ars, int64_t acs, int64_t m, int64_t l,
                                const double* Q, int64_t ldq, const double* R, int64_t ldr,
                                const int64_t* arr, double* u, double* ct, double* part,
                                SrqrScalars* sc, double* r, double* Rfull);
-cudaError_t launch_ext_row(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n,
+cudaError_t launch_ext_row(cudaStream_t st, const double* A, int64_t ars, int64_t acs, int64_t m, int64_t n,
                            int64_t l, const double* Q, int64_t ldq, double* R, int64_t ldr,
                            const int64_t* arr, const double* colsq, double* r,
                            const double* rinit, const SrqrScalars* sc);

@@ -170,26 +170,32 @@ def _download(torch, x):
     return finish(out)
 
 
-def _to_device_colmajor(A, device):
-    """(col-major float64 CUDA tensor, is_numpy_input)."""
+def _to_device(A, device):
+    """(device float64 tensor, is_numpy_input, layout, ld): A in HBM in the
+    caller's storage order.  Column-major (F-ordered numpy, torch views with unit
+    row stride) runs as FFB_LAYOUT_COL, row-major (C-ordered numpy, contiguous
+    torch) as FFB_LAYOUT_ROW — read in place by the engine, never transposed."""
     torch = _torch()
     if isinstance(A, torch.Tensor):
         if A.dim() != 2:
             raise DimensionError("expected a 2-D matrix")
         A = A.to(device=device, dtype=torch.float64)
         m, n = A.shape
-        if not (A.stride(0) == 1 and A.stride(1) >= max(m, 1)):
-            A = A.t().contiguous().t()
-        return A, False
+        if A.stride(0) == 1 and A.stride(1) >= max(m, 1):
+            return A, False, _capi.FFB_LAYOUT_COL, A.stride(1)
+        if A.stride(1) == 1 and A.stride(0) >= max(n, 1):
+            return A, False, _capi.FFB_LAYOUT_ROW, A.stride(0)
+        A = A.contiguous()
+        return A, False, _capi.FFB_LAYOUT_ROW, max(n, 1)
     a = np.asarray(A, dtype=float)
     if a.ndim != 2:
         raise DimensionError("expected a 2-D matrix")
     m, n = a.shape
-    if a.flags.f_contiguous:
+    if a.flags.f_contiguous and not a.flags.c_contiguous:
         t = _upload_bytes(torch, a.T, device).view(n, m)     # (n, m) row-major == A column-major
-    else:
-        t = _upload_bytes(torch, np.ascontiguousarray(a), device).view(m, n).t().contiguous()
-    return t.t(), True
+        return t.t(), True, _capi.FFB_LAYOUT_COL, max(m, 1)
+    t = _upload_bytes(torch, np.ascontiguousarray(a), device).view(m, n)
+    return t, True, _capi.FFB_LAYOUT_ROW, max(n, 1)
 
 
 def _workspace(torch, device, nbytes):
@@ -304,7 +310,7 @@ def run(A, params: SketchParams, mode, device=None, trace_gaps=False):
     torch = _torch()
     dev = _device(device if device is not None else (A.device if isinstance(A, torch.Tensor) and A.is_cuda else None))
     with torch.cuda.device(dev):
-        Ad, is_np = _to_device_colmajor(A, dev)
+        Ad, is_np, layout, lda = _to_device(A, dev)
         m, n = Ad.shape
         prm = params.resolve(m, n)
         if mode != _capi.FFB_MODE_TRQRCP and prm.l + 1 > min(m, n):
@@ -358,7 +364,7 @@ def run(A, params: SketchParams, mode, device=None, trace_gaps=False):
             res.rtilde = out["rtilde"].data_ptr()
         stream = torch.cuda.current_stream(dev).cuda_stream
         rc = lib.ffb_run(ctx, C.c_void_p(stream), mode, C.c_void_p(Ad.data_ptr()), m, n,
-                         Ad.stride(1), C.byref(cp), C.c_void_p(omega.data_ptr()), _gauss_cb, None,
+                         lda, layout, C.byref(cp), C.c_void_p(omega.data_ptr()), _gauss_cb, None,
                          C.c_void_p(ws.data_ptr()), ws.numel(), C.byref(res))
         out.update(alpha=res.alpha, g1=res.g1, g2=res.g2, tau=res.tau_bound,
                    tau_hat=res.tau_hat_bound, r22=res.r22, swaps=int(res.swaps),
@@ -476,7 +482,7 @@ def rsisvd(A, k, p=5, q=2, seed=0, device=None):
     r = min(k + p, min(m, n))
     dev = _device(device if device is not None else (A.device if isinstance(A, torch.Tensor) and A.is_cuda else None))
     with torch.cuda.device(dev):
-        Ad, is_np = _to_device_colmajor(A, dev)
+        Ad, is_np, layout, lda = _to_device(A, dev)
         lib = _capi.load()
         ctx = _capi.context(dev.index)
         nbytes = C.c_size_t()
@@ -499,7 +505,7 @@ def rsisvd(A, k, p=5, q=2, seed=0, device=None):
         fl = C.c_int64(0)
         sw = C.c_int32(0)
         stream = torch.cuda.current_stream(dev).cuda_stream
-        rc = lib.ffb_rsisvd(ctx, C.c_void_p(stream), C.c_void_p(Ad.data_ptr()), m, n, Ad.stride(1),
+        rc = lib.ffb_rsisvd(ctx, C.c_void_p(stream), C.c_void_p(Ad.data_ptr()), m, n, lda, layout,
                             k, r, q, C.c_void_p(om.data_ptr()), C.c_void_p(ws.data_ptr()), ws.numel(),
                             C.c_void_p(u.data_ptr()), m, C.c_void_p(s.data_ptr()),
                             C.c_void_p(v.data_ptr()), n, C.byref(fl), C.byref(sw))

@@ -97,6 +97,7 @@ def test_c_abi_run_batched(ffb):
         res.s, res.u, res.ldu, res.v, res.ldv, res.perm = s.data_ptr(), u.data_ptr(), m, v.data_ptr(), n, perm.data_ptr()
         it = items[i]
         it.stream, it.mode, it.A, it.m, it.n, it.lda = streams[i].cuda_stream, _capi.FFB_MODE_FLIPFLOP, Ad.data_ptr(), m, n, m
+        it.a_layout = _capi.FFB_LAYOUT_COL
         it.prm, it.omega, it.workspace, it.workspace_bytes = prm, om.data_ptr(), ws.data_ptr(), ws.numel()
         it.out = C.pointer(res)
         keep.append((Ad, ws, om, s, u, v, perm, res))

@@ -275,3 +275,15 @@ def test_flop_count_band_1000(ffb):
     assert abs(ap.flop_count - formula) <= 0.15 * formula
     rs = ffb.rsisvd(A, 30, p=5, q=1, seed=0)
     assert abs(rs.flop_count - ffb.rsisvd_flop_formula(1000, 1000, 30, 5, 1)) <= 0.15 * rs.flop_count
+
+
+def test_graph_replay_is_bitwise_repeatable(ffb):
+    # the second and third calls replay the CUDA graph captured by the first
+    # (same A, Omega and workspace); results must not change by a bit
+    c = load("cfg1")
+    A = torch.from_numpy(np.asfortranarray(c["A"]).T).cuda().t()
+    runs = [ffb.flip_flop_srqr(A, c["k"], l=c["l"], b=c["b"], p=c["p"], seed=c["seed"]) for _ in range(3)]
+    for r in runs[1:]:
+        assert torch.equal(r.s, runs[0].s) and torch.equal(r.u, runs[0].u) and torch.equal(r.v, runs[0].v)
+        assert torch.equal(r.meta["srqr"].fact.perm, runs[0].meta["srqr"].fact.perm)
+    assert runs[2].meta["kernels"] == runs[0].meta["kernels"]

@@ -21,7 +21,9 @@ def test_staged_upload_matches_device_input(order):
     A = rs.standard_normal((m, n))
     A = np.asfortranarray(A) if order == "F" else np.ascontiguousarray(A)
     ap_np = ffb.flip_flop_srqr(A, 20, l=40, b=16, p=4, seed=3)
-    Ad = torch.from_numpy(np.asfortranarray(A).T).cuda().t()
+    # the same storage order on the device: F -> column-major view, C -> row-major
+    # (FFB_LAYOUT_ROW, read in place)
+    Ad = torch.from_numpy(np.asfortranarray(A).T).cuda().t() if order == "F" else torch.from_numpy(A).cuda()
     ap_dev = ffb.flip_flop_srqr(Ad, 20, l=40, b=16, p=4, seed=3)
     assert np.array_equal(np.asarray(ap_np.s), ap_dev.s.cpu().numpy())
     assert np.array_equal(np.asarray(ap_np.u), ap_dev.u.cpu().numpy())
@@ -64,3 +66,32 @@ def test_host_pipeline_matches_direct_calls():
     for i, h in enumerate(hosts):
         ref = ffb.flip_flop_srqr(h.cuda(), 10, l=24, b=8, p=4, seed=i).s.cpu().numpy()
         assert np.array_equal(got[i], ref)
+
+
+@pytest.mark.parametrize("shape", [(700, 500), (500, 700)])
+def test_row_major_layout_matches_column_major(shape):
+    """FFB_LAYOUT_ROW (a C-ordered matrix read in place: row-major sketch / WT /
+    A*Qhat GEMM operands, row-major column norms, gathers and row copies) gives
+    the column-major factorization: same pivots, sigma and certificate to
+    rounding, for flip_flop_srqr, srqr and rsisvd."""
+    import paper_1803_01982_b200 as ffb
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    m, n = shape
+    rs = np.random.default_rng(m)
+    U, _ = np.linalg.qr(rs.standard_normal((m, 200)))
+    V, _ = np.linalg.qr(rs.standard_normal((n, 200)))
+    A = (U * np.geomspace(1, 1e-5, 200)) @ V.T + 1e-9 * rs.standard_normal((m, n))
+    Ac = torch.from_numpy(np.ascontiguousarray(A)).cuda()            # row-major
+    Af = torch.from_numpy(np.asfortranarray(A).T).cuda().t()         # column-major
+    assert Ac.stride(1) == 1 and Af.stride(0) == 1
+    a_r = ffb.flip_flop_srqr(Ac, 40, l=60, b=32, p=8, g=1.2, seed=5)
+    a_c = ffb.flip_flop_srqr(Af, 40, l=60, b=32, p=8, g=1.2, seed=5)
+    assert torch.equal(a_r.meta["srqr"].fact.perm, a_c.meta["srqr"].fact.perm)
+    assert a_r.meta["srqr"].cert.swaps == a_c.meta["srqr"].cert.swaps
+    torch.testing.assert_close(a_r.s, a_c.s, rtol=1e-12, atol=0)
+    assert abs(a_r.meta["srqr"].cert.g2 - a_c.meta["srqr"].cert.g2) <= 1e-12 * a_c.meta["srqr"].cert.g2
+    r_r = ffb.rsisvd(Ac, 30, p=10, q=1, seed=2)
+    r_c = ffb.rsisvd(Af, 30, p=10, q=1, seed=2)
+    torch.testing.assert_close(r_r.s, r_c.s, rtol=1e-12, atol=0)
