@@ -12,6 +12,8 @@ from __future__ import annotations
 import threading
 from concurrent.futures import ThreadPoolExecutor
 
+from . import _capi
+
 
 def partition(n_problems, world, rank):
     """Contiguous share of rank `rank`: range(lo, hi)."""
@@ -41,10 +43,22 @@ def _pool(dev, n_streams):
         return ent
 
 
-def run_streams(problems, solve, n_streams=4, device=None):
+def sm_budget(dev, n_streams):
+    """SMs per in-flight problem when `n_streams` problems share the device."""
+    import torch
+
+    if n_streams <= 1:
+        return 0
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    return max(8, sms // n_streams)
+
+
+def run_streams(problems, solve, n_streams=4, device=None, budget="auto"):
     """Run `solve(problem)` for every problem on `n_streams` CUDA streams.
 
     `solve` is called inside `torch.cuda.stream(s)`; results keep input order.
+    budget: SMs each problem's grid-synchronised kernels may use
+    (ffb_set_thread_sm_budget); "auto" = SMs / n_streams, 0 = the whole device.
     """
     import torch
 
@@ -52,10 +66,13 @@ def run_streams(problems, solve, n_streams=4, device=None):
     if dev.index is None:
         dev = torch.device("cuda", torch.cuda.current_device())
     streams, ex, lock, free = _pool(dev, max(1, n_streams))
+    nb = sm_budget(dev, n_streams) if budget == "auto" else int(budget)
+    lib = _capi.load()
 
     def _one(p):
         with lock:
             sid = free.pop()
+        lib.ffb_set_thread_sm_budget(nb)
         try:
             with torch.cuda.device(dev), torch.cuda.stream(streams[sid]):
                 out = solve(p)
@@ -68,7 +85,7 @@ def run_streams(problems, solve, n_streams=4, device=None):
     return list(ex.map(_one, problems))
 
 
-def run_host_pipeline(host_inputs, solve, n_streams=3, prefetch=2, device=None):
+def run_host_pipeline(host_inputs, solve, n_streams=3, prefetch=2, device=None, budget="auto"):
     """Host-resident inputs -> `solve(i, device_tensor)` on `n_streams` compute streams,
     with every upload issued ahead by one copy thread on its own stream.
 
@@ -77,7 +94,7 @@ def run_host_pipeline(host_inputs, solve, n_streams=3, prefetch=2, device=None):
     compute.  Here the copy engine runs back to back, at most
     ``n_streams + prefetch`` inputs resident on the device at a time.  Inputs
     should be pinned CPU tensors (any strides; the device copy keeps them).
-    Results keep input order.
+    Results keep input order.  budget: as in run_streams.
     """
     import queue
 
@@ -87,6 +104,8 @@ def run_host_pipeline(host_inputs, solve, n_streams=3, prefetch=2, device=None):
     if dev.index is None:
         dev = torch.device("cuda", torch.cuda.current_device())
     streams, ex, lock, free = _pool(dev, max(1, n_streams))
+    nb = sm_budget(dev, n_streams) if budget == "auto" else int(budget)
+    lib = _capi.load()
     key = (dev.index, "copy")
     with _pools_lock:
         if key not in _pools:
@@ -119,6 +138,7 @@ def run_host_pipeline(host_inputs, solve, n_streams=3, prefetch=2, device=None):
         i, d, ev = item
         with lock:
             sid = free.pop()
+        lib.ffb_set_thread_sm_budget(nb)
         try:
             s_ = streams[sid]
             with torch.cuda.device(dev), torch.cuda.stream(s_):

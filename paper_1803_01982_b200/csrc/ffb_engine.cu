@@ -70,6 +70,16 @@ struct HostStage {
 };
 thread_local HostStage t_host;
 
+// SMs one problem may spread its cooperative kernels over (0 = the whole
+// device): batch drivers with S problems in flight give each ~SMs / S, so the
+// problems' grid-synchronised kernels are co-resident instead of queueing.
+thread_local int t_sm_budget = 0;
+
+int effective_sms(const ffb_ctx* ctx) {
+  const int all = ctx ? ctx->sms : 148;
+  return t_sm_budget > 0 ? std::min(t_sm_budget, all) : all;
+}
+
 // small stream-ordered read-back (<= 256 B).  An SM kernel writes the pinned
 // staging word (UVA) instead of a D2H memcpy: the copy engines' queues, where
 // another stream's large transfer may be in flight, stay off the critical path.
@@ -90,6 +100,18 @@ inline cudaError_t d2d(void* dst, const void* src, size_t bytes, cudaStream_t st
 }
 
 constexpr int kPanelW = 64;
+
+// column width of the Householder panels hh_qr factors in one fused kernel
+// (<= kPanelW; FFB_PANEL_W tunes it): narrower panels shorten the serial
+// Cholesky / sign-LU chains at the cost of more trailing-update GEMMs
+int panel_step() {
+  static int w = -1;
+  if (w < 0) {
+    const char* e = getenv("FFB_PANEL_W");
+    w = e ? std::max(8, std::min(kPanelW, atoi(e))) : kPanelW;
+  }
+  return w;
+}
 constexpr size_t kAlign = 256;
 
 struct Bump {
@@ -149,7 +171,7 @@ int64_t max_i(int64_t a, int64_t b) { return a > b ? a : b; }
 // Pivot-kernel geometry: G CTAs (<= #SMs, ~64 columns each), columns in
 // shared memory when they fit.
 void pivot_geometry(const ffb_ctx* ctx, int64_t n, int64_t s, Work& w) {
-  int gmax = std::min(ctx ? ctx->sms : 148, 160);   // kPivMaxK * 32
+  int gmax = std::min(effective_sms(ctx), 160);   // kPivMaxK * 32
   if (const char* ev = getenv("FFB_PIV_G")) gmax = std::max(1, std::min(gmax, atoi(ev)));
   // 64 columns per CTA (the register-resident maximum) when the grid allows:
   // fewer CTAs shorten the per-step all-CTA exchange
@@ -199,10 +221,11 @@ size_t carve(const ffb_ctx* ctx, const Dims& D, void* base, size_t cap, Work& w)
   w.hhW = b.take<double>(kPanelW * max_i(l, 1));
   w.hhW2 = b.take<double>(kPanelW * max_i(l, 1));
   pivot_geometry(ctx, n, s, w);
-  w.prec = b.take<unsigned long long>(2 * (size_t)w.G * pivots_recw((int)s));
+  // sized for any grid the SM budget may pick (G <= 160, G * cpc < n + G)
+  w.prec = b.take<unsigned long long>(2 * (size_t)160 * pivots_recw((int)s));
   w.hist = b.take<int64_t>(max_i(D.b, 1));
   w.gap = b.take<double>(max_i(l, 1));
-  w.pwork = w.piv_smem ? nullptr : b.take<double>((size_t)w.G * pivots_stride((int)s) * w.cpc);
+  w.pwork = w.piv_smem ? nullptr : b.take<double>((size_t)(n + 160) * pivots_stride((int)s));
   w.r = b.take<double>(n);
   w.rinit = b.take<double>(n);
   w.u = b.take<double>(m);
@@ -303,6 +326,7 @@ struct AView {
 
 struct Eng {
   ffb_ctx* ctx;
+  int sms = 148;                   // SM budget of this problem (effective_sms)
   cudaStream_t st;
   Dims D;
   Work w;
@@ -378,7 +402,7 @@ struct Eng {
   void recon(const double* Xp, int64_t Mp, int wb, int64_t ldx, double* Yp, int64_t ldy,
              double* Tp, int64_t ldt, double* Rp, int64_t ldr) {
     if (cerr != cudaSuccess) return;
-    ok(launch_panel_qr(st, ctx->sms, Xp, ldx, Mp, wb, Yp, ldy, Tp, ldt, Rp, ldr, w.Xa, w.Xb,
+    ok(launch_panel_qr(st, sms, Xp, ldx, Mp, wb, Yp, ldy, Tp, ldt, Rp, ldr, w.Xa, w.Xb,
                        w.ppart, w.Gm, w.pbar, w.status));
     gc.flops += 3 * 4 * Mp * (int64_t)wb * wb + 2 * Mp * (int64_t)wb * wb;
   }
@@ -391,8 +415,9 @@ struct Eng {
     memset2d(Y, ldy, Mx, Nx);
     memset2d(T, ldt, Nx, Nx);
     memset2d(R, ldr, Nx, Nx);
-    for (int64_t c0 = 0; c0 < Nx; c0 += kPanelW) {
-      const int64_t c1 = std::min<int64_t>(Nx, c0 + kPanelW);
+    const int pw = panel_step();
+    for (int64_t c0 = 0; c0 < Nx; c0 += pw) {
+      const int64_t c1 = std::min<int64_t>(Nx, c0 + pw);
       const int wb = (int)(c1 - c0);
       const int64_t Mp = Mx - c0;
       double* Yp = Y + c0 + c0 * ldy;
@@ -501,6 +526,7 @@ std::string graph_key(int mode, const double* A, int64_t lda, bool arow, int64_t
   key_put(k, ws);
   key_put(k, wsb);
   key_put(k, out->pivot_gap != nullptr);
+  key_put(k, t_sm_budget);
   return k;
 }
 
@@ -509,7 +535,10 @@ std::string graph_key(int mode, const double* A, int64_t lda, bool arow, int64_t
 // instantiate, cache and launch it; anything not capturable runs eagerly.
 template <class Eng_, class F>
 void run_core(ffb_ctx* ctx, Eng_& e, cudaStream_t& st, const std::string& key, F&& core) {
-  if (!graphs_enabled()) {
+  // graphs serve the one-problem-at-a-time path; batch worker threads (an SM
+  // budget is set) launch eagerly: their launch latency is hidden by the other
+  // problems in flight, and concurrent captures on many threads measured fragile
+  if (!graphs_enabled() || t_sm_budget > 0) {
     core();
     return;
   }
@@ -538,7 +567,13 @@ void run_core(ffb_ctx* ctx, Eng_& e, cudaStream_t& st, const std::string& key, F
   const int64_t l0 = e.launches, gl0 = e.gc.launches, f0 = e.gc.flops;
   st = e.st = cap;
   cudaGraph_t graph = nullptr;
-  bool ok = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  static const cudaStreamCaptureMode cmode = [] {
+    const char* e = getenv("FFB_GRAPH_CAPTURE_MODE");   // 0 global, 1 thread-local, 2 relaxed
+    const int v = e ? atoi(e) : 1;
+    return v == 0 ? cudaStreamCaptureModeGlobal
+                  : (v == 1 ? cudaStreamCaptureModeThreadLocal : cudaStreamCaptureModeRelaxed);
+  }();
+  bool ok = cudaStreamBeginCapture(cap, cmode) == cudaSuccess;
   if (ok) {
     core();
     const cudaError_t ce = cudaStreamEndCapture(cap, &graph);
@@ -549,6 +584,9 @@ void run_core(ffb_ctx* ctx, Eng_& e, cudaStream_t& st, const std::string& key, F
   if (ok) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
   if (graph) cudaGraphDestroy(graph);
   if (!ok) {   // not capturable here: run the sequence eagerly
+    if (getenv("FFB_GRAPH_DEBUG"))
+      fprintf(stderr, "[ffb graph] capture failed (%s), running eagerly\n",
+              cudaGetErrorString(e.cerr != cudaSuccess ? e.cerr : cudaGetLastError()));
     (void)cudaGetLastError();
     e.cerr = cudaSuccess;
     e.launches = l0;
@@ -706,7 +744,8 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
   Work& w = e.w;
   const size_t need = carve(ctx, D, workspace, workspace_bytes, w);
   if (need > workspace_bytes) return fail(ctx, FFB_ERR_ARGUMENT, "workspace too small");
-  e.gc.sms = ctx->sms;
+  e.sms = effective_sms(ctx);
+  e.gc.sms = e.sms;
   e.gc.partial = w.gpart;
   e.gc.partial_cap = w.gpart_cap;
   e.gc.counters = w.skcnt;
@@ -839,7 +878,7 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
     // (K14) tmp = Qt Rt, SVD(Rt)
     e.hh_qr(w.tmp, m, l, m, w.Yt, m, w.Tt, l, w.Rt, l, true);
     // one-sided block Jacobi SVD of Rt (ffb_jacobi.cu): Rt = Us diag(sig) Vo^T
-    e.ok(launch_jacobi_svd(st, ctx->sms, w.Rt, l, (int)l, w.sig, w.Us, l, w.Vo, l, w.jwork, w.jbar,
+    e.ok(launch_jacobi_svd(st, e.sms, w.Rt, l, (int)l, w.sig, w.Us, l, w.Vo, l, w.jwork, w.jbar,
                            w.joff, w.jsweeps, w.jorder, kMaxSweeps));
     e.launches += 5;   // scale, layout, Jacobi, V replay, norms, out kernels
     // (K15, left half) W2 = Tt (Yt[:l]^T Us[:, :k])
@@ -984,6 +1023,11 @@ int ffb_flipflop(ffb_ctx* ctx, void* stream, const double* A, int64_t m, int64_t
 
 }  // extern "C"
 
+extern "C" int ffb_set_thread_sm_budget(int sms) {
+  t_sm_budget = sms > 0 ? sms : 0;
+  return FFB_OK;
+}
+
 extern "C" int ffb_run_batched(ffb_ctx* ctx, ffb_batch_item* items, int64_t count, int max_threads,
                                ffb_gauss_cb gauss, void* gauss_user) {
   if (!ctx || (count > 0 && !items)) return FFB_ERR_ARGUMENT;
@@ -992,13 +1036,17 @@ extern "C" int ffb_run_batched(ffb_ctx* ctx, ffb_batch_item* items, int64_t coun
   if (nt > count) nt = (int)count;
   std::atomic<int64_t> next{0};
   std::vector<std::string> msgs((size_t)count);
+  const int budget = nt > 1 ? std::max(8, ctx->sms / nt) : 0;
   auto worker = [&]() {
+    const int saved = t_sm_budget;
+    if (budget) t_sm_budget = budget;
     for (int64_t i = next++; i < count; i = next++) {
       ffb_batch_item& it = items[i];
       it.status = ffb_run(ctx, it.stream, it.mode, it.A, it.m, it.n, it.lda, it.a_layout, &it.prm,
                           it.omega, gauss, gauss_user, it.workspace, it.workspace_bytes, it.out);
       if (it.status != FFB_OK) msgs[(size_t)i] = t_err;
     }
+    t_sm_budget = saved;
   };
   std::vector<std::thread> pool;
   for (int t = 1; t < nt; ++t) pool.emplace_back(worker);
@@ -1046,7 +1094,8 @@ extern "C" int ffb_rsisvd(ffb_ctx* ctx, void* stream, const double* A, int64_t m
   Work& w = e.w;
   const size_t need = carve_rsisvd(ctx, m, n, k, r, workspace, workspace_bytes, w);
   if (need > workspace_bytes) return fail(ctx, FFB_ERR_ARGUMENT, "workspace too small");
-  e.gc.sms = ctx->sms;
+  e.sms = effective_sms(ctx);
+  e.gc.sms = e.sms;
   e.gc.partial = w.gpart;
   e.gc.partial_cap = w.gpart_cap;
   e.gc.counters = w.skcnt;
@@ -1069,7 +1118,7 @@ extern "C" int ffb_rsisvd(ffb_ctx* ctx, void* stream, const double* A, int64_t m
   // B^T = A^T Q = Q_b R_b
   e.gemm(n, r, m, 1.0, A, lda, !arow, w.Q, m, true, 0.0, w.X, n);
   e.hh_qr(w.X, n, r, n, w.Yl, n, w.Tl, r, w.Rl, r, true);
-  e.ok(launch_jacobi_svd(st, ctx->sms, w.Rl, r, (int)r, w.sig, w.Us, r, w.Vo, r, w.jwork, w.jbar,
+  e.ok(launch_jacobi_svd(st, e.sms, w.Rl, r, (int)r, w.sig, w.Us, r, w.Vo, r, w.jwork, w.jbar,
                          w.joff, w.jsweeps, w.jorder, kMaxSweeps));
   e.launches += 5;
   // u = Q V_r[:, :k] ; v = Q_b [U_r[:, :k]; 0] ; s = sigma[:k]
@@ -1126,7 +1175,7 @@ extern "C" int ffb_small_svd(ffb_ctx* ctx, void* stream, const double* M, int64_
   if (carve_small_svd(l, workspace, workspace_bytes, w) > workspace_bytes)
     return fail(ctx, FFB_ERR_ARGUMENT, "workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = launch_jacobi_svd(st, ctx->sms, M, ldm, (int)l, sig, U, ldu, V, ldv, w.jwork, w.jbar,
+  cudaError_t e = launch_jacobi_svd(st, effective_sms(ctx), M, ldm, (int)l, sig, U, ldu, V, ldv, w.jwork, w.jbar,
                                     w.joff, w.jsweeps, w.jorder, kMaxSweeps);
   int sw = 0;
   if (e == cudaSuccess) e = d2h(&sw, w.jsweeps, sizeof(int), st);
