@@ -528,6 +528,17 @@ def run_batched(args):
                 i = sum(shares[:r]) + j
                 row = gathered[r, j]
                 ok &= bool(row[0].item() == float(i)) if dry else bool(row[m * cfg.k].item() > 0)
+    stages = None
+    if rank == 0 and not dry:
+        # CUPTI shares of one problem run alone (what a problem costs without
+        # the other streams' contention)
+        try:
+            one = mine[0]
+            ktimes, kcounts = profile_kernels(lambda: ffb.flip_flop_srqr(
+                probs[one], cfg.k, l=cfg.l, b=cfg.b, p=cfg.p, seed=seed_of(one)))
+            stages = stage_table(cfg, ktimes, kcounts, sum(ktimes.values()), hbm_peak()[0])
+        except Exception as e:   # pragma: no cover - profiler unavailable
+            stages = [{"error": f"profiler unavailable: {e!r}"}]
     if rank == 0:
         flop_alg = ffb.flip_flop_flop_formula(m, n, cfg.l, cfg.b, cfg.p) * cfg.batch
         achieved = flop_alg / (ms * 1e-3) / 1e12
@@ -551,6 +562,7 @@ def run_batched(args):
                        "bytes_per_step": slot_bytes * cfg.batch if ws > 1 else 0,
                        "collective": "NCCL all_gather per chunk of %d problems on a dedicated stream" % chunk
                        if ws > 1 else "none (1 GPU)", "complete": ok},
+            "stages_one_problem": stages,
             "clocks": clk,
         }
         if dry:

@@ -267,7 +267,7 @@ def prefetch_omega_async(keys, device=None, threads=8):
 
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     with _omega_lock:
-        if _prefetch_pool is None or _prefetch_pool._max_workers != threads:
+        if _prefetch_pool is None or _prefetch_pool._max_workers < threads:
             _prefetch_pool = ThreadPoolExecutor(max_workers=max(1, threads), thread_name_prefix="ffb-omega")
         pool = _prefetch_pool
 
@@ -310,6 +310,11 @@ def run(A, params: SketchParams, mode, device=None, trace_gaps=False):
     torch = _torch()
     dev = _device(device if device is not None else (A.device if isinstance(A, torch.Tensor) and A.is_cuda else None))
     with torch.cuda.device(dev):
+        if not (isinstance(A, torch.Tensor) and A.is_cuda) and len(getattr(A, "shape", ())) == 2:
+            # host input: generate Omega on a host thread while A uploads
+            m0, n0 = A.shape
+            p0 = params.resolve(m0, n0)
+            prefetch_omega_async([(p0.b + p0.p, m0, p0.seed)], device=dev, threads=2)
         Ad, is_np, layout, lda = _to_device(A, dev)
         m, n = Ad.shape
         prm = params.resolve(m, n)
