@@ -39,8 +39,29 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-FP64_PEAK_TFLOPS = 37.0   # measured DMMA peak on this pool's B200 (profiles/r01_fp64_peak.md)
-FP64_PEAK_SOURCE = "measured DMMA peak, profiles/r01_fp64_peak.md (MEASURED_PEAKS.json has no FP64 entry)"
+FP64_PEAK_TFLOPS = 37.0   # fallback: DMMA peak measured in round 1 (profiles/r01_fp64_peak.md)
+FP64_PEAK_SOURCE = "DMMA peak measured in round 1, profiles/r01_fp64_peak.md (MEASURED_PEAKS.json has no FP64 entry)"
+
+
+def measure_fp64_peak():
+    """The FP64 tensor-core denominator measured live on this GPU
+    (ffb_fp64_peak_probe: register-only DMMA loop on every SM, CUDA events).
+    Sets the module-level peak used by every roofline in the line."""
+    global FP64_PEAK_TFLOPS, FP64_PEAK_SOURCE
+    import ctypes as C
+
+    import torch
+
+    from paper_1803_01982_b200 import _capi
+
+    t = C.c_double(0.0)
+    rc = _capi.load().ffb_fp64_peak_probe(C.c_void_p(torch.cuda.current_stream().cuda_stream), 100000,
+                                          C.byref(t))
+    if rc == 0 and t.value > 1.0:
+        FP64_PEAK_TFLOPS = float(t.value)
+        FP64_PEAK_SOURCE = ("measured live in this run: register-only DMMA loop (mma.sync m8n8k4 f64) "
+                            "on every SM, ffb_fp64_peak_probe; MEASURED_PEAKS.json has no FP64 entry")
+    return FP64_PEAK_TFLOPS
 METRIC = "flip_flop_srqr_factorizations_per_s"
 L2_BYTES = 126 * 2 ** 20
 L2_LABEL = "126 MiB"
@@ -530,6 +551,7 @@ def run_batched(args):
                 ok &= bool(row[0].item() == float(i)) if dry else bool(row[m * cfg.k].item() > 0)
     stages = None
     if rank == 0 and not dry:
+        measure_fp64_peak()
         # CUPTI shares of one problem run alone (what a problem costs without
         # the other streams' contention)
         try:
@@ -660,6 +682,8 @@ def run_single(args):
     def step():
         return ffb.flip_flop_srqr(A, k, l=l, b=b, p=p, seed=0)
 
+    if rank == 0:
+        measure_fp64_peak()
     # host generation of Omega = gaussian(b+p, m, 0, 0) (reported; cached per (seed, s, m))
     t0 = time.perf_counter()
     rng.gaussian(b + p, m, 0, rng.STREAM_SKETCH)

@@ -28,7 +28,7 @@ EXPORTS = ("ffb_ctx_create", "ffb_ctx_destroy", "ffb_last_error", "ffb_version",
            "ffb_workspace_query", "ffb_run", "ffb_flipflop", "ffb_gemm", "ffb_block_pivots",
            "ffb_run_batched", "ffb_rsisvd_workspace_query", "ffb_rsisvd", "ffb_svt_partials",
            "ffb_ialm_update", "ffb_sumsq", "ffb_shrink_cols", "ffb_small_svd_workspace_query",
-           "ffb_small_svd", "ffb_set_thread_sm_budget")
+           "ffb_small_svd", "ffb_set_thread_sm_budget", "ffb_fp64_peak_probe")
 
 
 class Params(C.Structure):
@@ -147,6 +147,8 @@ def load(path=LIB_PATH):
                                       C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                                       C.c_void_p, C.c_size_t, C.POINTER(C.c_int32)]
         lib.ffb_small_svd.restype = C.c_int
+        lib.ffb_fp64_peak_probe.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_double)]
+        lib.ffb_fp64_peak_probe.restype = C.c_int
         lib.ffb_set_thread_sm_budget.argtypes = [C.c_int]
         lib.ffb_set_thread_sm_budget.restype = C.c_int
         _lib = lib

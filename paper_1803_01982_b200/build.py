@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libffb200.so")
 SOURCES = ["ffb_engine.cu", "ffb_gemm.cu", "ffb_kernels.cu", "ffb_jacobi.cu", "ffb_panel.cu",
-           "ffb_svt.cu"]
+           "ffb_svt.cu", "ffb_probe.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-diag-suppress", "177"]

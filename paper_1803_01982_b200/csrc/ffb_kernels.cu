@@ -231,8 +231,11 @@ FFB_DEV void warp_best(double& r, int64_t& p) {
 // (sub + 4q, q < RQ) in registers; shared memory gets a write-through copy that
 // the publish step reads.  RQ == 0: generic shared/global-memory loop with the
 // rows of a column loaded to registers (s <= 128).  RQ == -1: generic loop
-// straight on shared/global memory (any s).  XQ: winner-column rows per lane
-// of the reflector warp (s <= 32 XQ).
+// straight on shared/global memory (any s).  RQ == -2 (global memory, s <= 48,
+// many columns per CTA, e.g. a 400 x 160000 unfolding's sketch): one THREAD per
+// column, W stored row-major ([s][cpc]) so a warp's loads of one sketch row are
+// coalesced and every column's s loads are in flight at once.  XQ: winner-column
+// rows per lane of the reflector warp (s <= 32 XQ).
 template <bool SMEM, int RQ, int XQ>
 __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
   extern __shared__ __align__(16) double sm[];
@@ -245,7 +248,11 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
   if (ncl > cpc) ncl = cpc;
   if (ncl < 0) ncl = 0;
   const int nc = (int)ncl;
-  double* W = SMEM ? sm : a.work + (size_t)blockIdx.x * sP * cpc;   // [cpc][sP]
+  double* W = SMEM ? sm : a.work + (size_t)blockIdx.x * sP * cpc;   // [cpc][sP] ([s][cpc] for RQ == -2)
+  constexpr bool kRowMajor = RQ == -2;
+  constexpr int kS2 = 48;   // RQ == -2: max sketch rows (registers)
+  // element (i, c) of the CTA's column slab
+  auto widx = [&](int c, int i) -> size_t { return kRowMajor ? (size_t)i * cpc + c : (size_t)c * sP + i; };
   double* base = SMEM ? sm + (size_t)sP * cpc : sm;
   double* r = base;
   double* r0 = r + cpc;
@@ -257,7 +264,7 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
 
   for (int idx = tid; idx < s * nc; idx += kPivThreads) {
     const int c = idx / s, i = idx - c * s;
-    W[c * sP + i] = a.B[i + (c0 + c) * a.ldb];
+    W[widx(c, i)] = a.B[i + (c0 + c) * a.ldb];
   }
   for (int c = tid; c < nc; c += kPivThreads) pp[c] = a.pos[c0 + c];
   __syncthreads();
@@ -271,7 +278,25 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
     }
   }
   // initial norms and local top-2 over positions >= j0
-  {
+  if constexpr (kRowMajor) {
+    Cand2 cd{-1.0, -1, -1.0, -1};
+    for (int c = tid; c < nc; c += kPivThreads) {
+      double t0 = 0.0, t1 = 0.0;
+      int i = 0;
+      for (; i + 1 < s; i += 2) {
+        const double u = W[widx(c, i)], v = W[widx(c, i + 1)];
+        t0 = fma(u, u, t0);
+        t1 = fma(v, v, t1);
+      }
+      if (i < s) t0 = fma(W[widx(c, i)], W[widx(c, i)], t0);
+      const double t = t0 + t1;
+      r[c] = t;
+      r0[c] = t;
+      if (pp[c] >= a.j0) cand_push(cd, t, pp[c]);
+    }
+    cd = warp_top2(cd);
+    if (lane == 0) wc[warp] = cd;
+  } else {
     Cand2 cd{-1.0, -1, -1.0, -1};
     for (int c = grp; c < nc; c += kPivGroups) {
       const double* col = W + (size_t)c * sP;
@@ -322,9 +347,8 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
           for (int c = lane; c < nc; c += 32)
             if (pp[c] == cd.p1) cl = c;
           cl = (int)__reduce_max_sync(0xffffffffu, (unsigned)(cl + 1)) - 1;
-          const double* col = W + (size_t)cl * sP;
           for (int i = j + lane; i < s; i += 32) {
-            const double x = col[i];
+            const double x = W[widx(cl, i)];
             st_ll2(rec + 8 + 2 * i, ll_pack((uint32_t)__double2loint(x), tag),
                    ll_pack((uint32_t)__double2hiint(x), tag));
           }
@@ -517,6 +541,46 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
           cand_push(cd, rr, p);
         }
       }
+    } else if constexpr (kRowMajor) {
+      for (int c = tid; c < nc; c += kPivThreads) {
+        int64_t p = pp[c];
+        if (p == wpos) p = P;
+        else if (p == P) p = wpos;
+        pp[c] = p;
+        if (p <= P) continue;
+        double xr[kS2];
+#pragma unroll
+        for (int i = 0; i < kS2; ++i) xr[i] = (i >= j && i < s) ? W[widx(c, i)] : 0.0;
+        if (tau != 0.0) {
+          double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+          for (int i = 0; i < kS2; ++i)
+            if (i >= j && i < s) {
+              if (i & 1) w1 = fma(vv[i], xr[i], w1);
+              else w0 = fma(vv[i], xr[i], w0);
+            }
+          const double wt = (w0 + w1) * tau;
+#pragma unroll
+          for (int i = 0; i < kS2; ++i)
+            if (i >= j && i < s) {
+              xr[i] = fma(-vv[i], wt, xr[i]);
+              W[widx(c, i)] = xr[i];
+            }
+        }
+        double rj = 0.0;
+#pragma unroll
+        for (int i = 0; i < kS2; ++i) rj = sel_f64(i == j, xr[i], rj);
+        double rr = r[c] - rj * rj;
+        if (rr < 1e-8 * r0[c] || rr < 0.0) {
+          double t = 0.0;
+#pragma unroll
+          for (int i = 0; i < kS2; ++i)
+            if (i > j && i < s) t = fma(xr[i], xr[i], t);
+          rr = t > 0.0 ? t : 0.0;
+        }
+        r[c] = rr;
+        cand_push(cd, rr, p);
+      }
     } else if constexpr (RQ < 0) {
       for (int c = grp; c < nc; c += kPivGroups) {
         int64_t p = pp[c];
@@ -646,6 +710,7 @@ int pivots_stride(int s) {
 }
 
 int pivots_rq(int s, int cpc, bool smem_mode) {
+  if (!smem_mode && s <= 48) return -2;
   if (s > 128) return -1;
   if (!smem_mode || cpc > kPivGroups) return 0;
   return s <= 32 ? 8 : s <= 64 ? 16 : s <= 96 ? 24 : 32;
@@ -654,7 +719,7 @@ int pivots_rq(int s, int cpc, bool smem_mode) {
 void* pivots_kernel_ptr(bool smem_mode, int rq, int s) {
   if (s > 256) return smem_mode ? (void*)pivots_kernel<true, -1, 16> : (void*)pivots_kernel<false, -1, 16>;
   if (s > 128) return smem_mode ? (void*)pivots_kernel<true, -1, 8> : (void*)pivots_kernel<false, -1, 8>;
-  if (!smem_mode) return (void*)pivots_kernel<false, 0, 4>;
+  if (!smem_mode) return rq == -2 ? (void*)pivots_kernel<false, -2, 4> : (void*)pivots_kernel<false, 0, 4>;
   switch (rq) {
     case 8: return (void*)pivots_kernel<true, 8, 4>;
     case 16: return (void*)pivots_kernel<true, 16, 4>;
@@ -678,9 +743,9 @@ cudaError_t launch_pivots(cudaStream_t st, const PivotArgs& a, bool smem_mode, s
   const int rq = pivots_rq(a.s, a.cpc, smem_mode);
   void* kern = pivots_kernel_ptr(smem_mode, rq, a.s);
   // one per-device opt-in mask per kernel instance of pivots_kernel_ptr
-  static std::atomic<unsigned long long> attr_done[10];
+  static std::atomic<unsigned long long> attr_done[11];
   const int ki = a.s > 256 ? 6 + smem_mode : a.s > 128 ? 8 + smem_mode
-               : !smem_mode ? 0 : rq == 8 ? 1 : rq == 16 ? 2 : rq == 24 ? 3 : rq == 32 ? 4 : 5;
+               : !smem_mode ? (rq == -2 ? 10 : 0) : rq == 8 ? 1 : rq == 16 ? 2 : rq == 24 ? 3 : rq == 32 ? 4 : 5;
   ensure_smem_optin(kern, 210 * 1024, attr_done[ki]);
   cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3(a.G),
                                               dim3(kPivThreads), kargs, smem, st);

@@ -71,3 +71,20 @@ def test_no_cpu_fallback_without_device():
 
     with pytest.raises(ffb.EngineUnavailable):
         ffb.flip_flop_srqr(np.eye(8), 3)
+
+
+def test_sass_stages_tiles_with_tma():
+    # the sketch / WT products load their tiles with cp.async.bulk.tensor (TMA)
+    import subprocess
+
+    lib = os.path.join(ROOT, "paper_1803_01982_b200", "libffb200.so")
+    out = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
+    assert "UTMALDG" in out
+
+
+def test_batch_item_layout_matches_header():
+    from paper_1803_01982_b200 import _capi
+
+    # stream, mode(+pad), A, m, n, lda, a_layout(+pad), prm, omega, workspace, bytes, out, status
+    assert _capi.BatchItem.a_layout.offset == 48
+    assert _capi.BatchItem.prm.offset == 56

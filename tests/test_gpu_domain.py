@@ -153,3 +153,10 @@ def test_small_svd_against_lapack(ffb, l):
     assert np.abs(Vh.T @ Vh - np.eye(l)).max() < 1e-12 * l
     assert np.abs((Uh * sig.cpu().numpy()) @ Vh.T - R).max() < 1e-13 * l
     assert 0 < sweeps < 30
+
+
+def test_wide_unfolding_global_pivots(ffb):
+    # a sketch too wide for shared memory (s x n = 42 x 90000 over <= 148 CTAs):
+    # the global-memory pivot kernel, one thread per column (cfg4's shape class)
+    A = _matrix(300, 90000, 8)
+    _compare(ffb, A, 30, 40, 32, 10, seed=8)
