@@ -47,8 +47,13 @@ def sm_budget(dev, n_streams):
     """SMs per in-flight problem when `n_streams` problems share the device."""
     import torch
 
+    import os
+
     if n_streams <= 1:
         return 0
+    env = os.environ.get("FFB_SM_BUDGET")
+    if env is not None:            # explicit per-problem SM budget (0 = whole device)
+        return max(0, int(env))
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     return max(8, sms // n_streams)
 

@@ -17,6 +17,7 @@
 #include <cstring>
 #include <string>
 #include <atomic>
+#include <condition_variable>
 #include <mutex>
 #include <thread>
 #include <unordered_map>
@@ -482,6 +483,48 @@ int cuda_fail(ffb_ctx* ctx, cudaError_t e, const char* where) {
   return fail(ctx, FFB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
+// ---- concurrent-call tracking for graph capture.  A capture must not overlap
+// another thread's launches: with lazy module loading, a kernel loaded for the
+// first time during another thread's capture fails with "operation not
+// permitted when stream is capturing" (seen with 8 batch threads).  So a
+// capture only starts when this is the only call in flight, new calls wait
+// until it ends, and once calls have overlapped the process stops capturing
+// (cached graphs still replay).
+std::atomic<int> g_inflight{0};
+std::atomic<bool> g_capturing{false};
+std::atomic<bool> g_ever_concurrent{false};
+std::mutex g_cap_mu;
+std::condition_variable g_cap_cv;
+
+struct CallGuard {
+  CallGuard() {
+    if (g_inflight.fetch_add(1) + 1 > 1) g_ever_concurrent.store(true);
+    if (g_capturing.load()) {
+      std::unique_lock<std::mutex> lk(g_cap_mu);
+      g_cap_cv.wait(lk, [] { return !g_capturing.load(); });
+    }
+  }
+  ~CallGuard() { g_inflight.fetch_sub(1); }
+};
+
+bool begin_exclusive_capture() {
+  if (g_ever_concurrent.load()) return false;
+  g_capturing.store(true);
+  if (g_inflight.load() != 1) {
+    g_capturing.store(false);
+    std::lock_guard<std::mutex> lk(g_cap_mu);
+    g_cap_cv.notify_all();
+    return false;
+  }
+  return true;
+}
+
+void end_exclusive_capture() {
+  g_capturing.store(false);
+  std::lock_guard<std::mutex> lk(g_cap_mu);
+  g_cap_cv.notify_all();
+}
+
 // ---- CUDA graph cache of ffb_run's core (FFB_GRAPHS=0 disables it)
 constexpr size_t kMaxGraphs = 256;
 
@@ -545,7 +588,7 @@ void run_core(ffb_ctx* ctx, Eng_& e, cudaStream_t& st, const std::string& key, F
   {
     std::lock_guard<std::mutex> g(ctx->gmu);
     auto it = ctx->graphs.find(key);
-    if (it != ctx->graphs.end()) {
+    if (it != ctx->graphs.end() && it->second.exec) {
       GraphEnt& ge = it->second;
       ge.stamp = ++ctx->gstamp;
       e.okm(cudaGraphLaunch(ge.exec, st));
@@ -554,6 +597,18 @@ void run_core(ffb_ctx* ctx, Eng_& e, cudaStream_t& st, const std::string& key, F
       e.gc.flops += ge.flops;
       return;
     }
+    if (it == ctx->graphs.end()) {
+      // first sighting: run eagerly (loads every kernel the sequence uses);
+      // the second call with this key captures
+      if (ctx->graphs.size() < kMaxGraphs) ctx->graphs.emplace(key, GraphEnt{});
+      it = ctx->graphs.end();
+      core();
+      return;
+    }
+  }
+  if (!begin_exclusive_capture()) {
+    core();
+    return;
   }
   int dev = 0;
   cudaGetDevice(&dev);
@@ -567,6 +622,9 @@ void run_core(ffb_ctx* ctx, Eng_& e, cudaStream_t& st, const std::string& key, F
   const int64_t l0 = e.launches, gl0 = e.gc.launches, f0 = e.gc.flops;
   st = e.st = cap;
   cudaGraph_t graph = nullptr;
+  struct EndCap {
+    ~EndCap() { end_exclusive_capture(); }
+  } end_cap;
   static const cudaStreamCaptureMode cmode = [] {
     const char* e = getenv("FFB_GRAPH_CAPTURE_MODE");   // 0 global, 1 thread-local, 2 relaxed
     const int v = e ? atoi(e) : 1;
@@ -602,20 +660,23 @@ void run_core(ffb_ctx* ctx, Eng_& e, cudaStream_t& st, const std::string& key, F
   ge.flops = e.gc.flops - f0;
   e.okm(cudaGraphLaunch(exec, st));
   std::lock_guard<std::mutex> g(ctx->gmu);
-  if (ctx->graphs.count(key)) {   // another thread captured the same key meanwhile
+  auto found = ctx->graphs.find(key);
+  if (found != ctx->graphs.end() && found->second.exec) {   // captured meanwhile elsewhere
     ctx->retired.push_back(exec);
     return;
   }
-  if (ctx->graphs.size() >= kMaxGraphs) {
+  if (found == ctx->graphs.end() && ctx->graphs.size() >= kMaxGraphs) {
     auto old = ctx->graphs.begin();
     for (auto it = ctx->graphs.begin(); it != ctx->graphs.end(); ++it)
       if (it->second.stamp < old->second.stamp) old = it;
-    cudaDeviceSynchronize();   // the evicted graph may still run on another stream
-    cudaGraphExecDestroy(old->second.exec);
+    if (old->second.exec) {
+      cudaDeviceSynchronize();   // the evicted graph may still run on another stream
+      cudaGraphExecDestroy(old->second.exec);
+    }
     ctx->graphs.erase(old);
   }
   ge.stamp = ++ctx->gstamp;
-  ctx->graphs.emplace(key, ge);
+  ctx->graphs[key] = ge;
 }
 
 bool validate(const Dims& D) {
@@ -653,7 +714,8 @@ int ffb_ctx_destroy(ffb_ctx* c) {
   {
     DeviceGuard dg(c->device);
     cudaDeviceSynchronize();
-    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second.exec);
+    for (auto& kv : c->graphs)
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     for (auto ex : c->retired) cudaGraphExecDestroy(ex);
   }
   if (c->pinned) cudaFreeHost(c->pinned);
@@ -682,6 +744,7 @@ int ffb_gemm(ffb_ctx* ctx, void* stream, int64_t M, int64_t N, int64_t K, double
   if (!ctx) return FFB_ERR_ARGUMENT;
   DeviceGuard dg(ctx->device);
   GemmCtx gc;
+  CallGuard call_guard;
   gc.sms = ctx->sms;
   // workspace: [stream-K counters (64Ki u32, zeroed here) | split-K / stream-K partials]
   const size_t cnt_bytes = 65536 * sizeof(unsigned);
@@ -703,7 +766,8 @@ int ffb_block_pivots(ffb_ctx* ctx, void* stream, const double* B, int64_t s, int
                      void* workspace, size_t workspace_bytes) {
   if (!ctx) return FFB_ERR_ARGUMENT;
   DeviceGuard dg(ctx->device);
-  if (bb < 1 || j0 < 0 || j0 + bb > n || n >= 2147483647LL || s < 1 || s > 128)
+  CallGuard call_guard;
+  if (bb < 1 || j0 < 0 || j0 + bb > n || n >= 2147483647LL || s < 1 || s > 512)
     return fail(ctx, FFB_ERR_DIMENSION, "bad pivot block");
   Work w;
   pivot_geometry(ctx, n, s, w);
@@ -729,6 +793,7 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
             ffb_gauss_cb gauss, void* gauss_user, void* workspace, size_t workspace_bytes,
             ffb_result* out) {
   if (!ctx || !prm || !out || !A || !omega || !workspace) return FFB_ERR_ARGUMENT;
+  CallGuard call_guard;
   if (a_layout != FFB_LAYOUT_COL && a_layout != FFB_LAYOUT_ROW) return FFB_ERR_ARGUMENT;
   const AView av{A, lda, a_layout == FFB_LAYOUT_ROW};
   DeviceGuard dg(ctx->device);
@@ -745,7 +810,9 @@ int ffb_run(ffb_ctx* ctx, void* stream, int mode, const double* A, int64_t m, in
   const size_t need = carve(ctx, D, workspace, workspace_bytes, w);
   if (need > workspace_bytes) return fail(ctx, FFB_ERR_ARGUMENT, "workspace too small");
   e.sms = effective_sms(ctx);
-  e.gc.sms = e.sms;
+  // GEMMs are not grid-synchronised: their split / stream-K choices stay those of
+  // the whole device, so results do not depend on the caller's SM budget
+  e.gc.sms = ctx->sms;
   e.gc.partial = w.gpart;
   e.gc.partial_cap = w.gpart_cap;
   e.gc.counters = w.skcnt;
@@ -1082,6 +1149,7 @@ extern "C" int ffb_rsisvd(ffb_ctx* ctx, void* stream, const double* A, int64_t m
                           void* workspace, size_t workspace_bytes, double* u, int64_t ldu,
                           double* s, double* v, int64_t ldv, int64_t* flops, int32_t* sweeps_out) {
   if (!ctx || !A || !omega || !workspace || !u || !s || !v) return FFB_ERR_ARGUMENT;
+  CallGuard call_guard;
   DeviceGuard dg(ctx->device);
   if (a_layout != FFB_LAYOUT_COL && a_layout != FFB_LAYOUT_ROW) return FFB_ERR_ARGUMENT;
   const bool arow = a_layout == FFB_LAYOUT_ROW;
@@ -1095,7 +1163,9 @@ extern "C" int ffb_rsisvd(ffb_ctx* ctx, void* stream, const double* A, int64_t m
   const size_t need = carve_rsisvd(ctx, m, n, k, r, workspace, workspace_bytes, w);
   if (need > workspace_bytes) return fail(ctx, FFB_ERR_ARGUMENT, "workspace too small");
   e.sms = effective_sms(ctx);
-  e.gc.sms = e.sms;
+  // GEMMs are not grid-synchronised: their split / stream-K choices stay those of
+  // the whole device, so results do not depend on the caller's SM budget
+  e.gc.sms = ctx->sms;
   e.gc.partial = w.gpart;
   e.gc.partial_cap = w.gpart_cap;
   e.gc.counters = w.skcnt;
@@ -1169,6 +1239,7 @@ extern "C" int ffb_small_svd(ffb_ctx* ctx, void* stream, const double* M, int64_
                              double* sig, double* U, int64_t ldu, double* V, int64_t ldv,
                              void* workspace, size_t workspace_bytes, int32_t* sweeps) {
   if (!ctx || !M || !sig || !U || !V || !workspace) return FFB_ERR_ARGUMENT;
+  CallGuard call_guard;
   DeviceGuard dg(ctx->device);
   if (l < 1 || ldm < l || ldu < l || ldv < l) return fail(ctx, FFB_ERR_DIMENSION, "small svd needs l >= 1, ld >= l");
   Work w;

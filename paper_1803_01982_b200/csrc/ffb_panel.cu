@@ -17,6 +17,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
+
 #include "ffb_common.cuh"
 #include "ffb_panel.cuh"
 #include "ffb_tile64.cuh"
@@ -294,17 +296,22 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
     const int64_t lds = pass == 0 ? a.ldx : Mp;
     double* dst = pass == 1 ? a.Qb : a.Qa;
     qfin = dst;
-    // (a) local Gram of rows [r0, r1) on DMMA (Cs^T Cs per staged chunk)
-    Acc64 gacc;
-    acc_zero(gacc);
-    for (int64_t c0 = r0; c0 < r1; c0 += kCH) {
-      const int rows = (int)(r1 - c0 < kCH ? r1 - c0 : kCH);
-      __syncthreads();
-      load_chunk(Cs, src, lds, c0, rows, w);
-      __syncthreads();
-      dmma64(gacc, Cs, true, Cs, (rows + 3) & ~3);
+    // (a) Gram of each row group this CTA owns (groups grp = blockIdx.x, + G, ..;
+    // the partition into a.vg groups depends on Mp only, so the fixed-order
+    // reduction below gives the same bits for any grid / SM budget)
+    for (int grp = blockIdx.x; grp < a.vg; grp += G) {
+      const int64_t g0 = (int64_t)grp * a.gpr, g1 = g0 + a.gpr < Mp ? g0 + a.gpr : Mp;
+      Acc64 gacc;
+      acc_zero(gacc);
+      for (int64_t c0 = g0; c0 < g1; c0 += kCH) {
+        const int rows = (int)(g1 - c0 < kCH ? g1 - c0 : kCH);
+        __syncthreads();
+        load_chunk(Cs, src, lds, c0, rows, w);
+        __syncthreads();
+        dmma64(gacc, Cs, true, Cs, (rows + 3) & ~3);
+      }
+      acc_store_global(gacc, a.part + (size_t)grp * ww, w, 0, w, w);
     }
-    acc_store_global(gacc, a.part + (size_t)blockIdx.x * ww, w, 0, w, w);
     QPROF(0)
     grid_sync(a.bar, G);
     // (b) distributed fixed-order reduction
@@ -320,11 +327,12 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
         if (e < e1) {
           double v[4] = {0.0, 0.0, 0.0, 0.0};
           int c = k8;
-          for (; c + 24 < G; c += 32) {
+          const int ng = a.vg;
+          for (; c + 24 < ng; c += 32) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) v[u] += a.part[(size_t)(c + 8 * u) * ww + e];
           }
-          for (; c < G; c += 8) v[0] += a.part[(size_t)c * ww + e];
+          for (; c < ng; c += 8) v[0] += a.part[(size_t)c * ww + e];
           s = (v[0] + v[1]) + (v[2] + v[3]);
         }
         s += __shfl_xor_sync(0xffffffffu, s, 1);
@@ -449,14 +457,18 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
       __syncthreads();
       for (int t = tid; t < kW * kW; t += nt) Ra[(t >> 6) * kL + (t & 63)] = Ws[(t >> 6) * kL + (t & 63)];
     }
-    // (d) own rows <- rows * R^-1 (a single-chunk CTA still holds its rows in Cs)
-    const bool one_chunk = r1 - r0 <= kCH;
-    for (int64_t c0 = r0; c0 < r1; c0 += kCH) {
-      const int rows = (int)(r1 - c0 < kCH ? r1 - c0 : kCH);
-      __syncthreads();
-      if (!one_chunk) load_chunk(Cs, src, lds, c0, rows, w);
-      __syncthreads();
-      apply_upper(Cs, rows, w, Xs, dst, Mp, c0);
+    // (d) own rows <- rows * R^-1 (a CTA with one group of <= kCH rows still
+    // holds them in Cs)
+    const bool one_chunk = a.vg <= G && a.gpr <= kCH;
+    for (int grp = blockIdx.x; grp < a.vg; grp += G) {
+      const int64_t g0 = (int64_t)grp * a.gpr, g1 = g0 + a.gpr < Mp ? g0 + a.gpr : Mp;
+      for (int64_t c0 = g0; c0 < g1; c0 += kCH) {
+        const int rows = (int)(g1 - c0 < kCH ? g1 - c0 : kCH);
+        __syncthreads();
+        if (!one_chunk) load_chunk(Cs, src, lds, c0, rows, w);
+        __syncthreads();
+        apply_upper(Cs, rows, w, Xs, dst, Mp, c0);
+      }
     }
     QPROF(3)
   }
@@ -523,14 +535,17 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
   __syncthreads();
   // (f) Y rows >= w: Y = Q * (D U^-1)  (Ui is upper triangular)
   {
-    const int64_t y0 = r0 > w ? r0 : w;
     double* Ys = Ws;
-    for (int64_t c0 = y0; c0 < r1; c0 += kCH) {
-      const int rows = (int)(r1 - c0 < kCH ? r1 - c0 : kCH);
-      __syncthreads();
-      load_chunk(Ys, qfin, Mp, c0, rows, w);
-      __syncthreads();
-      apply_upper(Ys, rows, w, Ui, a.Y, a.ldy, c0);
+    for (int grp = blockIdx.x; grp < a.vg; grp += G) {
+      const int64_t g0 = (int64_t)grp * a.gpr, g1 = g0 + a.gpr < Mp ? g0 + a.gpr : Mp;
+      const int64_t y0 = g0 > w ? g0 : w;
+      for (int64_t c0 = y0; c0 < g1; c0 += kCH) {
+        const int rows = (int)(g1 - c0 < kCH ? g1 - c0 : kCH);
+        __syncthreads();
+        load_chunk(Ys, qfin, Mp, c0, rows, w);
+        __syncthreads();
+        apply_upper(Ys, rows, w, Ui, a.Y, a.ldy, c0);
+      }
     }
   }
   QPROF(6)
@@ -566,9 +581,14 @@ cudaError_t launch_panel_qr(cudaStream_t st, int sms, const double* X, int64_t l
   static std::atomic<unsigned long long> attr{0};
   const size_t smem = panel_smem_bytes();
   ensure_smem_optin((const void*)panel_qr_kernel, (int)smem, attr);
-  const int G = panel_grid(sms, Mp);
+  int dev = 0, all_sms = sms;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&all_sms, cudaDevAttrMultiProcessorCount, dev);
+  const int VG = panel_grid(std::max(all_sms, sms), Mp);   // row groups: Mp and the device only
+  const int G = std::min(VG, std::max(1, sms));           // CTAs: the caller's SM budget
+  const int64_t gpr = (Mp + VG - 1) / VG;
   PanelArgs a{X, ldx, Mp, w, Y, ldy, T, ldt, R, ldr, Qa, Qb, part, Gg, bar, status,
-              (int)((Mp + G - 1) / G), nullptr};
+              (int)((Mp + G - 1) / G), VG, gpr, nullptr};
   static long long* prof = nullptr;
   if (getenv("FFB_PANEL_PROF") && !prof) cudaMallocManaged(&prof, 16 * sizeof(long long));
   a.prof = prof;

@@ -22,7 +22,9 @@ struct PanelArgs {
   double* Gg;      // w*w reduced Gram
   uint32_t* bar;   // [2] grid barrier
   uint32_t* status;
-  int rpc;         // rows per CTA
+  int rpc;         // rows per CTA (Householder fallback)
+  int vg;          // row groups of the CholeskyQR passes (fixed by Mp, not by the grid)
+  int64_t gpr;     // rows per group
   long long* prof; // optional [8] phase cycles of CTA 0 (FFB_PANEL_PROF)
 };
 

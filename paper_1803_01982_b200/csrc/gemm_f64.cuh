@@ -500,48 +500,25 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
   }  // segment loop
 }
 
-// Stream-K fixup: C(tile) = alpha * sum over covering CTAs (ascending) + beta * C.
-template <int BM, int BN>
-__global__ void __launch_bounds__(256) gemm_streamk_fixup(GemmArgs g, int64_t ntiles) {
-  const int64_t tile = blockIdx.x;
-  if (tile >= ntiles) return;
-  __shared__ const double* seg[16];
-  __shared__ int nseg;
-  const int64_t i0 = (tile / g.sk_tiles_n) * BM, j0 = (tile % g.sk_tiles_n) * BN;
-  if (threadIdx.x == 0) {
-    const int64_t t0 = tile * g.sk_kiters, t1 = t0 + g.sk_kiters - 1;
-    const int64_t b0 = t0 / g.sk_per, b1 = t1 / g.sk_per;
-    int n = 0;
-    for (int64_t b = b0; b <= b1 && n < 16; ++b, ++n) {
-      const int64_t ft = (b * g.sk_per) / g.sk_kiters;
-      seg[n] = g.partial + (size_t)(b * g.sk_maxseg + (tile - ft)) * (BM * BN);
-    }
-    nseg = n;
-  }
-  __syncthreads();
-  const int ns = nseg;
-  const int64_t rows = g.M - i0 < BM ? g.M - i0 : BM;
-  const int64_t cols = g.N - j0 < BN ? g.N - j0 : BN;
-  for (int c = 0; c < cols; ++c) {
-    for (int r = threadIdx.x; r < rows; r += blockDim.x) {
-      const int e = r + c * BM;
-      double sum = 0.0;
-      for (int q = 0; q < ns; ++q) sum += seg[q][e];
-      double* cp = g.C + (i0 + r) + (j0 + c) * g.ldc;
-      const double v = g.alpha * sum;
-      *cp = g.beta == 0.0 ? v : v + g.beta * (*cp);
-    }
-  }
-}
-
-// Fixed-order reduction of split-K partials into C.
+// Fixed-order reduction of split-K partials into C.  The partial loads are
+// issued 8 at a time (independent, in flight together) and summed in split
+// order: a serial chain of L2 round trips made this kernel ~10 us for the
+// small-output, long-K products of the panel updates.
 __global__ void gemm_splitk_reduce(const double* __restrict__ part, int splits, int64_t M, int64_t N,
                                    double alpha, double beta, double* C, int64_t ldc) {
   const int64_t total = M * N;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (int q = 0; q < splits; ++q) s += part[(size_t)q * total + t];
+    int q = 0;
+    for (; q + 8 <= splits; q += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(part + (size_t)(q + u) * total + t);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; q < splits; ++q) s += __ldcg(part + (size_t)q * total + t);
     const int64_t i = t % M, j = t / M;
     double* cp = C + i + j * ldc;
     const double v = alpha * s;
