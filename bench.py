@@ -393,25 +393,24 @@ def slot_layout(cfg, workload):
     return parts
 
 
-def pack_slot(res, parts, out):
-    """Flatten one ApproxSvd into its slot row (device copies on the current stream)."""
+def pack_slot(o, parts, out):
+    """Flatten one problem's outputs (batch.NativeBatch dict: device u, s, v, perm
+    and the certificate scalars) into its slot row (device copies, current stream)."""
     import torch
 
     off = 0
     for name, cnt in parts:
         dst = out[off:off + cnt]
-        if name == "u":
-            dst.view(res.u.shape[1], res.u.shape[0]).copy_(res.u.t())
-        elif name == "v":
-            dst.view(res.v.shape[1], res.v.shape[0]).copy_(res.v.t())
+        if name in ("u", "v"):
+            x = o[name]
+            dst.view(x.shape[1], x.shape[0]).copy_(x.t())
         elif name == "s":
-            dst.copy_(res.s)
+            dst.copy_(o["s"])
         elif name == "perm":
-            dst.copy_(res.meta["srqr"].fact.perm.view(torch.float64))
+            dst.copy_(o["perm"].view(torch.float64))
         else:
-            c = res.meta["srqr"].cert
-            dst.copy_(torch.tensor([c.alpha, c.g1, c.g2, c.swaps, c.tau_bound, c.tau_hat_bound,
-                                    res.meta["srqr"].r22_norm_estimate, 0.0], dtype=torch.float64))
+            dst.copy_(torch.tensor([o["alpha"], o["g1"], o["g2"], o["swaps"], o["tau"], o["tau_hat"],
+                                    o["r22"], 0.0], dtype=torch.float64))
         off += cnt
 
 
@@ -444,8 +443,8 @@ def run_batched(args):
     parts = slot_layout(cfg, args.workload)
     slot_len = sum(c for _, c in parts)
     if args.streams <= 0:
-        args.streams = 8 if args.workload == "cfg5" else 1
-    chunk = max(1, args.streams)
+        args.streams = 8 if args.workload == "cfg5" else 3
+    chunk = int(os.environ.get("FFB_BENCH_CHUNK", "16"))   # problems per ffb_run_batched call
     if dry:
         probs = {i: None for i in mine}
         seed_of = lambda i: i
@@ -461,43 +460,44 @@ def run_batched(args):
     gathered = torch.zeros((ws, pad, slot_len), dtype=torch.float64, device=dev) if ws > 1 else None
     comm = None if dry else torch.cuda.Stream(device=dev)
 
-    def solve(i):
-        if dry:
-            return None
-        r = ffb.flip_flop_srqr(probs[i], cfg.k, l=cfg.l, b=cfg.b, p=cfg.p, seed=seed_of(i))
-        if ws > 1:
-            pack_slot(r, parts, local_slots[i - mine[0]])
-        return r
+    # one ffb_run_batched call per chunk of problems: C++ worker threads, each with
+    # an SM budget of SMs / threads, per-problem streams, workspaces and outputs
+    nbatch = None if dry else batch.NativeBatch([probs[i] for i in mine], cfg.k, cfg.l, cfg.b, cfg.p,
+                                                seeds=[seed_of(i) for i in mine], device=dev,
+                                                threads=args.streams)
 
     def step(fresh_omega=True):
-        if fresh_omega and not dry:
-            # every step generates its sketches on the host, on background
-            # threads ahead of the problems that need them
-            engine.clear_omega_cache()
-            engine.prefetch_omega_async([(cfg.b + cfg.p, m, seed_of(i)) for i in mine], device=dev,
-                                        threads=max(1, min(8, len(os.sched_getaffinity(0)) // 2)))
         works = []
-        for c0 in range(0, pad, chunk):
-            ids = [mine[j] for j in range(c0, min(c0 + chunk, len(mine)))]
+        done = set()
+
+        def gather_chunk(lo, hi):
+            if ws == 1 or lo in done:
+                return
+            done.add(lo)
+            hi = min(pad, lo + chunk)            # padded rows: every rank issues the same collectives
+            seg = local_slots[lo:hi]
+            outs = [gathered[r, lo:hi] for r in range(ws)]
             if dry:
-                for i in ids:
-                    local_slots[i - mine[0]].fill_(float(i))
-            elif len(ids) > 1:
-                batch.run_streams(ids, solve, n_streams=args.streams, device=dev)
-            else:
-                for i in ids:
-                    solve(i)
-            if ws > 1:
-                seg = local_slots[c0:c0 + chunk]
-                outs = [gathered[r, c0:c0 + chunk] for r in range(ws)]
-                if dry:
-                    dist.all_gather(outs, seg.contiguous())
-                else:
-                    ev = torch.cuda.Event()
-                    ev.record(torch.cuda.current_stream(dev))
-                    comm.wait_event(ev)
-                    with torch.cuda.stream(comm):
-                        works.append(dist.all_gather(outs, seg, async_op=True))
+                dist.all_gather(outs, seg.contiguous())
+                return
+            for j in range(lo, min(hi, len(mine))):
+                pack_slot(nbatch.out[j], parts, local_slots[j])
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(dev))
+            comm.wait_event(ev)
+            with torch.cuda.stream(comm):
+                works.append(dist.all_gather(outs, seg, async_op=True))
+
+        if dry:
+            for lo in range(0, pad, chunk):
+                for j in range(lo, min(lo + chunk, len(mine))):
+                    local_slots[j].fill_(float(mine[j]))
+                gather_chunk(lo, lo + chunk)
+        else:
+            nbatch.run(fresh_omega=fresh_omega, chunk=chunk, on_chunk=gather_chunk,
+                       omega_threads=max(1, min(8, len(os.sched_getaffinity(0)) // 2)))
+            for lo in range(0, pad, chunk):       # a short share still joins every collective
+                gather_chunk(lo, lo + chunk)
         for w in works:
             w.wait()
         if not dry:
@@ -574,15 +574,18 @@ def run_batched(args):
             "step_roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                               "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
                               "flop_alg": flop_alg, "peak_source": FP64_PEAK_SOURCE},
-            "streams_per_gpu": args.streams,
+            "driver": {"path": "batch.NativeBatch -> ffb_run_batched (C++ worker threads, GIL released)",
+                       "threads_per_gpu": args.streams, "problems_per_call": chunk,
+                       "sm_budget_per_problem": "SMs / threads (ffb_set_thread_sm_budget)"},
             "omega": {"inside_timed_region": True,
                       "host_ms_per_step_rank0": om_ms,
                       "note": "engine Omega cache cleared every step: each problem's gaussian(b+p, m, seed, 0) "
                               "is generated again on host threads (engine.prefetch_omega_async, "
-                              "in problem order) while the earlier problems compute"},
+                              "in problem order) while the earlier chunks compute"},
             "gather": {"slot": [nm for nm, _ in parts], "bytes_per_problem": slot_bytes,
                        "bytes_per_step": slot_bytes * cfg.batch if ws > 1 else 0,
-                       "collective": "NCCL all_gather per chunk of %d problems on a dedicated stream" % chunk
+                       "collective": "NCCL all_gather per chunk of %d problems on a dedicated stream, "
+                                     "overlapping the next chunk's factorizations" % chunk
                        if ws > 1 else "none (1 GPU)", "complete": ok},
             "stages_one_problem": stages,
             "clocks": clk,
@@ -942,8 +945,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=120.0)
     ap.add_argument("--streams", type=int, default=0,
-                    help="batched workloads: problems in flight per GPU (CUDA streams); "
-                         "0 = default (cfg5: 8, cfg4: 1)")
+                    help="batched workloads: problems in flight per GPU (C++ worker threads); "
+                         "0 = default (cfg5: 8, cfg4: 3)")
     ap.add_argument("--dry", action="store_true",
                     help="CPU/gloo run of the batched partition + gather logic (tests)")
     args = ap.parse_args()

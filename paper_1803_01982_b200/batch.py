@@ -220,3 +220,110 @@ def flip_flop_batch(make_problem, n_problems, k, l, b, p, seed_of=lambda i: i, n
         shape = tuple(local.shape[1:])
         gathered[name] = gather_slots(local, n_problems, shape, rank, world, dev)
     return results, gathered
+
+
+class NativeBatch:
+    """Many independent flip-flop factorizations through one ``ffb_run_batched``
+    call: C++ worker threads (the GIL is released for the whole batch), one
+    stream, workspace and set of output buffers per problem, allocated once and
+    reused by every ``run``.  Replaces the reference's Python loop over
+    independent problems (ffsrqr/tensor.py:112-115) without per-problem host work.
+
+    problems: list of CUDA float64 matrices (column- or row-major), all with the
+    same k, l, b, p.  seeds: per-problem seed (Omega and g2 streams).
+    """
+
+    def __init__(self, problems, k, l, b, p, seeds, d=None, g=2.0, device=None, threads=8):
+        import ctypes as C
+
+        import torch
+
+        from . import engine
+        from .results import SketchParams
+
+        self.torch = torch
+        self.lib = _capi.load()
+        dev = torch.device(device) if device is not None else problems[0].device
+        self.dev = dev
+        self.ctx = _capi.context(dev.index)
+        self.threads = max(1, int(threads))
+        self.seeds = [int(s) for s in seeds]
+        n_prob = len(problems)
+        self.items = (_capi.BatchItem * n_prob)()
+        self.results = [_capi.Result() for _ in range(n_prob)]
+        self.out = []
+        self.keep = []
+        self.streams = [torch.cuda.Stream(device=dev) for _ in range(n_prob)]
+        self.prm = []
+        for i, A in enumerate(problems):
+            Ad, _, layout, lda = engine._to_device(A, dev)
+            m, n = Ad.shape
+            sp = SketchParams(k=k, l=l, b=b, p=p, d=d, g=g, seed=self.seeds[i]).resolve(m, n)
+            prm = _capi.Params(sp.k, sp.l, sp.b, sp.p, sp.d, sp.epsilon, sp.g,
+                               int(sp.seed) & 0xFFFFFFFFFFFFFFFF)
+            nb = C.c_size_t()
+            rc = self.lib.ffb_workspace_query(m, n, C.byref(prm), _capi.FFB_MODE_FLIPFLOP, C.byref(nb))
+            if rc != _capi.FFB_OK:
+                from .errors import DimensionError
+
+                raise DimensionError("invalid dimensions for the engine")
+            ws = torch.empty(nb.value, dtype=torch.uint8, device=dev)
+            o = {"u": torch.empty((sp.k, m), dtype=torch.float64, device=dev).t(),
+                 "s": torch.empty(sp.k, dtype=torch.float64, device=dev),
+                 "v": torch.empty((sp.k, n), dtype=torch.float64, device=dev).t(),
+                 "perm": torch.empty(n, dtype=torch.int64, device=dev)}
+            res = self.results[i]
+            res.u, res.ldu = o["u"].data_ptr(), m
+            res.s = o["s"].data_ptr()
+            res.v, res.ldv = o["v"].data_ptr(), n
+            res.perm = o["perm"].data_ptr()
+            it = self.items[i]
+            it.stream, it.mode, it.A, it.m, it.n, it.lda = (self.streams[i].cuda_stream, _capi.FFB_MODE_FLIPFLOP,
+                                                            Ad.data_ptr(), m, n, lda)
+            it.a_layout = layout
+            it.prm, it.workspace, it.workspace_bytes = prm, ws.data_ptr(), ws.numel()
+            it.out = C.pointer(res)
+            self.out.append(o)
+            self.keep.append((Ad, ws))
+            self.prm.append(sp)
+
+    def run(self, fresh_omega=False, chunk=16, on_chunk=None, omega_threads=8):
+        """Factorize every problem; returns the list of output dicts (device
+        tensors u, s, v, perm, plus the certificate scalars).
+
+        fresh_omega: regenerate every problem's Omega on host threads (as each
+        reference call does) — in problem order, overlapped with the device
+        work of the earlier chunks.  The problems run in chunks of `chunk`
+        through ffb_run_batched; on_chunk(lo, hi) is called after each chunk
+        (e.g. to start gathering its results while the next chunk computes)."""
+        import ctypes as C
+
+        from . import engine
+
+        torch = self.torch
+        n = len(self.items)
+        keys = [(sp.b + sp.p, self.items[i].m, sp.seed) for i, sp in enumerate(self.prm)]
+        if fresh_omega:
+            engine.clear_omega_cache()
+        futs = engine.prefetch_omega_async(keys, device=self.dev, threads=omega_threads)
+        torch.cuda.current_stream(self.dev).synchronize()
+        size = C.sizeof(_capi.BatchItem)
+        base = C.addressof(self.items)
+        self._oms = []
+        for lo in range(0, n, max(1, chunk)):
+            hi = min(n, lo + max(1, chunk))
+            for i in range(lo, hi):
+                om = futs[i].result()
+                self.items[i].omega = om.data_ptr()
+                self._oms.append(om)
+            part = (_capi.BatchItem * (hi - lo)).from_address(base + lo * size)
+            rc = self.lib.ffb_run_batched(self.ctx, part, hi - lo, self.threads, engine._gauss_cb, None)
+            if rc != _capi.FFB_OK:
+                raise RuntimeError(f"ffb_run_batched failed ({rc}): {_capi.last_error(self.ctx)}")
+            for i in range(lo, hi):
+                r = self.results[i]
+                self.out[i].update(alpha=r.alpha, g1=r.g1, g2=r.g2, swaps=int(r.swaps), tau=r.tau_bound,
+                                   tau_hat=r.tau_hat_bound, r22=r.r22)
+            if on_chunk is not None:
+                on_chunk(lo, hi)
+        return self.out

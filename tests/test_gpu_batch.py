@@ -110,3 +110,23 @@ def test_c_abi_run_batched(ffb):
         s = keep[i][3]
         assert torch.equal(s, want[i].s)
         assert torch.equal(keep[i][6], want[i].meta["srqr"].fact.perm if isinstance(want[i].meta["srqr"].fact.perm, torch.Tensor) else torch.as_tensor(want[i].meta["srqr"].fact.perm, device="cuda"))
+
+
+def test_native_batch_matches_single_calls(ffb):
+    """batch.NativeBatch (ffb_run_batched on C++ threads with an SM budget per
+    problem, Omega regenerated on host threads, chunks of 3) gives every problem
+    bitwise the single-call result: the budget changes grids, not arithmetic."""
+    from paper_1803_01982_b200 import batch
+
+    n_prob, k, l, b, p = 7, 30, 40, 16, 8
+    As = [_mat(i) for i in range(n_prob)]
+    want = [ffb.flip_flop_srqr(A, k, l=l, b=b, p=p, seed=10 + i) for i, A in enumerate(As)]
+    nb = batch.NativeBatch(As, k, l, b, p, seeds=[10 + i for i in range(n_prob)], threads=3)
+    for rep in range(2):
+        out = nb.run(fresh_omega=True, chunk=3)
+        torch.cuda.synchronize()
+        for i in range(n_prob):
+            assert torch.equal(out[i]["s"], want[i].s)
+            assert torch.equal(out[i]["u"], want[i].u) and torch.equal(out[i]["v"], want[i].v)
+            assert torch.equal(out[i]["perm"], want[i].meta["srqr"].fact.perm)
+            assert out[i]["g2"] == want[i].meta["srqr"].cert.g2
