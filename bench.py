@@ -258,14 +258,14 @@ def pivot_bytes(n, l, b, p):
 
 
 def stage_table(cfg, kern_times, counts, step_ms, hbm_gbps):
-    """Top kernel families of one factorization: share of the step, algorithmic
-    work, achieved rate and roofline fraction."""
+    """Top kernels of one factorization, grouped like an ncu launch list (one row
+    per kernel family, GEMMs per tile configuration): share of the step,
+    algorithmic work, achieved rate and roofline fraction; plus one summary row
+    for all GEMM launches against the paper's flop formula."""
     from paper_1803_01982_b200 import flip_flop_flop_formula
 
     m, n, l, b, p = cfg.m, cfg.n, cfg.l, cfg.b, cfg.p
     algo = {
-        "gemm_f64_kernel": ("tensor", flip_flop_flop_formula(m, n, l, b, p), "flop",
-                            "sketch + WT + A*Qhat GEMMs: 4mnl + 2(b+p)mn (svd.py:258-260)"),
         "jacobi_kernel": ("tensor", 6 * l ** 3, "flop",
                           "count_svd(l, l) = 6 l^3 (flops.py:49-52) of the l x l SVD"),
         "jacobi_general_kernel": ("tensor", 6 * l ** 3, "flop", "count_svd(l, l) = 6 l^3"),
@@ -274,53 +274,51 @@ def stage_table(cfg, kern_times, counts, step_ms, hbm_gbps):
         "pivots_kernel": ("hbm", pivot_bytes(n, l, b, p), "byte",
                           "SURVEY 8(d) K2: sum_blocks bb * 8 s (n - j0)"),
     }
+
+    def rate(ent, bound, work, unit, note, t_ms):
+        if unit == "flop":
+            ach = work / (t_ms * 1e-3) / 1e12
+            ent.update(bound=bound, algorithmic_flop=work, achieved=ach, unit="TFLOP/s",
+                       peak=FP64_PEAK_TFLOPS, frac=ach / FP64_PEAK_TFLOPS, algorithm=note)
+        else:
+            ach = work / (t_ms * 1e-3) / 1e9
+            ent.update(bound=bound, algorithmic_bytes=work, achieved=ach, unit="GB/s",
+                       peak=hbm_gbps, frac=ach / hbm_gbps, algorithm=note)
+
     tot = sum(kern_times.values())
     rows = []
-    for fam, t_ms in sorted(kern_times.items(), key=lambda kv: -kv[1])[:6]:
-        ent = {"kernel": fam, "launches": counts[fam], "ms": round(t_ms, 4),
+    for key, t_ms in sorted(kern_times.items(), key=lambda kv: -kv[1])[:6]:
+        ent = {"kernel": key, "launches": counts[key], "ms": round(t_ms, 4),
                "share_of_kernel_time": round(t_ms / tot, 4) if tot else None,
                "share_of_step": round(t_ms / step_ms, 4)}
-        if fam in algo:
-            bound, work, unit, note = algo[fam]
-            if unit == "flop":
-                ach = work / (t_ms * 1e-3) / 1e12
-                ent.update(bound=bound, algorithmic_flop=work, achieved=ach, unit="TFLOP/s",
-                           peak=FP64_PEAK_TFLOPS, frac=ach / FP64_PEAK_TFLOPS, algorithm=note)
-            else:
-                ach = work / (t_ms * 1e-3) / 1e9
-                ent.update(bound=bound, algorithmic_bytes=work, achieved=ach, unit="GB/s",
-                           peak=hbm_gbps, frac=ach / hbm_gbps, algorithm=note)
+        if key in algo:
+            rate(ent, *algo[key], t_ms)
+        elif key.startswith("gemm_f64_kernel<"):
+            ent.update(bound="tensor", note="FP64 DMMA GEMM, one tile configuration "
+                                            "(template: BM, BN, BK, WM, WN, A k-contig, B k-contig, "
+                                            "stages, 16-byte loads, stream-K, TMA)")
         else:
             ent.update(bound="latency", note="small kernels: launch/latency bound")
+        rows.append(ent)
+    g_ms = sum(t for k, t in kern_times.items() if k.startswith("gemm_f64_kernel"))
+    if g_ms > 0:
+        ent = {"kernel": "gemm_f64_kernel (all launches)",
+               "launches": sum(c for k, c in counts.items() if k.startswith("gemm_f64_kernel")),
+               "ms": round(g_ms, 4), "share_of_kernel_time": round(g_ms / tot, 4) if tot else None,
+               "share_of_step": round(g_ms / step_ms, 4)}
+        rate(ent, "tensor", flip_flop_flop_formula(m, n, l, b, p), "flop",
+             "sketch + WT + A*Qhat GEMMs: 4mnl + 2(b+p)mn (svd.py:258-260) over every GEMM launch", g_ms)
         rows.append(ent)
     return rows
 
 
-def profile_kernels(step):
-    """Per-family device time of one step from CUPTI activity records
-    (torch.profiler) — the share table; the headline numbers are CUDA events."""
-    from collections import defaultdict
-
-    import torch
-    from torch.profiler import ProfilerActivity, profile
-
-    times, counts = defaultdict(float), defaultdict(int)
-    with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        step()
-        torch.cuda.synchronize()
-    for ev in prof.events():
-        dt = getattr(ev, "device_type", None)
-        if dt is None or "CUDA" not in str(dt):
-            continue
-        us = getattr(ev, "device_time", None)
-        if us is None:
-            us = getattr(ev, "cuda_time", 0.0)
-        fam = kernel_family(ev.name)
-        if fam.startswith("Memset") or fam.startswith("Memcpy") or "memset" in fam.lower():
-            continue
-        times[fam] += us / 1e3
-        counts[fam] += 1
-    return dict(times), dict(counts)
+def top_kernel(stages):
+    """The time-dominant launch-list entry (first row; the GEMM summary row is
+    not a launch-list entry)."""
+    for ent in stages:
+        if "kernel" in ent and "(all launches)" not in ent["kernel"]:
+            return ent
+    return None
 
 
 def time_top_kernel(fam, cfg, A, st, dev, ctx, lib):
@@ -414,12 +412,14 @@ def pack_slot(o, parts, out):
         off += cnt
 
 
-def run_batched(args):
+def batched_record(args, profile=True):
     """cfg4 / cfg5: independent problems partitioned contiguously over the ranks
-    (batch.partition); each rank factorizes its share on several streams, with
-    Omega generated on the host inside the timed region (every matrix of cfg5
-    has its own seed), and each finished chunk of result slots is all-gathered
-    to rank 0 on a dedicated NCCL stream while the next chunk computes."""
+    (batch.partition); each rank factorizes its share through batch.NativeBatch,
+    with Omega generated on the host inside the timed region (every matrix of
+    cfg5 has its own seed), and each finished chunk of result slots is
+    all-gathered to rank 0 on a dedicated NCCL stream while the next chunk
+    computes.  The process group (if any) is already initialised.  Returns
+    (line dict on rank 0 else None, every slot arrived)."""
     import torch
     import torch.distributed as dist
 
@@ -429,13 +429,6 @@ def run_batched(args):
     ws, rank, local = dist_init()
     dry = args.dry
     dev = torch.device("cpu") if dry else torch.device("cuda", local)
-    if not dry:
-        torch.cuda.set_device(local)
-    if ws > 1:
-        if dry:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=dev)
     cfg = workloads.CONFIGS[args.workload]
     mine = list(batch.partition(cfg.batch, ws, rank))
     shares = [len(batch.partition(cfg.batch, ws, r)) for r in range(ws)]
@@ -550,7 +543,7 @@ def run_batched(args):
                 row = gathered[r, j]
                 ok &= bool(row[0].item() == float(i)) if dry else bool(row[m * cfg.k].item() > 0)
     stages = None
-    if rank == 0 and not dry:
+    if rank == 0 and not dry and profile:
         measure_fp64_peak()
         # CUPTI shares of one problem run alone (what a problem costs without
         # the other streams' contention)
@@ -592,6 +585,26 @@ def run_batched(args):
         }
         if dry:
             line["dry"] = True
+        del nbatch
+        return line, ok
+    del nbatch
+    return None, ok
+
+
+def run_batched(args):
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_init()
+    if not args.dry:
+        torch.cuda.set_device(local)
+    if ws > 1:
+        if args.dry:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    line, ok = batched_record(args)
+    if line is not None:
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()
@@ -743,14 +756,16 @@ def run_single(args):
             stages = stage_table(cfg, ktimes, kcounts, ms, hbm_gbps)
         except Exception as e:   # pragma: no cover - profiler unavailable
             stages = [{"error": f"profiler unavailable: {e!r}"}]
-        top = stages[0]["kernel"] if stages and "kernel" in stages[0] else "gemm_f64_kernel"
-        timed = time_top_kernel(top, cfg, A, st, dev, ctx, lib)
+        top_ent = top_kernel(stages) or {"kernel": "gemm_f64_kernel"}
+        top = top_ent["kernel"]
+        fam = "gemm_f64_kernel" if top.startswith("gemm_f64_kernel") else top
+        timed = time_top_kernel(fam, cfg, A, st, dev, ctx, lib)
         if timed is None:          # no standalone launcher: the profiler's average
-            ent = stages[0]
+            ent = top_ent
             timed = (ent["ms"] / ent["launches"], ent.get("algorithmic_bytes", 0) / ent["launches"],
                      "byte", ent.get("algorithm", ""))
         kms, work, unit, note = timed
-        traffic, tsrc = ncu_traffic(top)
+        traffic, tsrc = ncu_traffic(fam)
         if unit == "flop":
             ach = work / (kms * 1e-3) / 1e12
             roof = {"bound": "tensor", "kernel": top, "achieved": ach, "peak": FP64_PEAK_TFLOPS,
@@ -904,6 +919,24 @@ def run_single(args):
                          f"(oracle/ffsrqr_oracle.py) on the same matrix, {t_cpu:.2f} s; calibration "
                          "against the numba reference: profiles/r04_cpu_calibration.json"}
 
+    # the batched configs at this N (north_star: cfg4 / cfg5 at 1, 2, 4, 8 GPUs):
+    # strong-scaling sub-records measured by the same ranks after the headline
+    batched = None
+    if not args.no_batched:
+        import argparse as _ap
+
+        batched = {}
+        del A
+        torch.cuda.empty_cache()
+        for wl in ("cfg5", "cfg4"):
+            sub = _ap.Namespace(workload=wl, streams=0, steps=3, warmup=3, dry=False)
+            rec, ok_b = batched_record(sub, profile=False)
+            if rec is not None:
+                batched[wl] = {k: rec[k] for k in ("value", "unit", "n_gpus", "ms_per_step", "scaling",
+                                                   "steps", "warmup", "config", "step_roofline", "gather",
+                                                   "driver", "omega")}
+            torch.cuda.empty_cache()
+
     if rank == 0:
         achieved = flop_alg / (ms * 1e-3) / 1e12
         line = {
@@ -927,6 +960,7 @@ def run_single(args):
             "concurrent": conc,
             "certificate": {"swaps": ap_.meta["srqr"].cert.swaps, "g2": ap_.meta["srqr"].cert.g2,
                             "svd_sweeps": ap_.meta["svd_sweeps"]},
+            "batched": batched,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -943,6 +977,8 @@ def main():
     ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-batched", action="store_true",
+                    help="skip the cfg5 / cfg4 strong-scaling sub-records of the single-matrix line")
     ap.add_argument("--ref-budget-s", type=float, default=120.0)
     ap.add_argument("--streams", type=int, default=0,
                     help="batched workloads: problems in flight per GPU (C++ worker threads); "
