@@ -230,6 +230,46 @@ def kernel_family(name):
     return n.split("::")[-1]
 
 
+def launch_key(name):
+    """Launch-list key of a kernel name: the family, except GEMMs, which keep
+    their tile-configuration template arguments (one row per configuration)."""
+    import re
+
+    fam = kernel_family(name)
+    if fam == "gemm_f64_kernel":
+        mt = re.search(r"gemm_f64_kernel<([^>]*)>", name)
+        if mt:
+            return "gemm_f64_kernel<" + mt.group(1).replace(" ", "") + ">"
+    return fam
+
+
+def profile_kernels(step):
+    """Per-key device time of one step from CUPTI activity records
+    (torch.profiler) — the share table; the headline numbers are CUDA events."""
+    from collections import defaultdict
+
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    times, counts = defaultdict(float), defaultdict(int)
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        step()
+        torch.cuda.synchronize()
+    for ev in prof.events():
+        dt = getattr(ev, "device_type", None)
+        if dt is None or "CUDA" not in str(dt):
+            continue
+        us = getattr(ev, "device_time", None)
+        if us is None:
+            us = getattr(ev, "cuda_time", 0.0)
+        key = launch_key(ev.name)
+        if key.startswith("Memset") or key.startswith("Memcpy") or "memset" in key.lower():
+            continue
+        times[key] += us / 1e3
+        counts[key] += 1
+    return dict(times), dict(counts)
+
+
 def panel_bytes(m, n, l, b):
     """Algorithmic bytes of every panel_qr launch of one factorization: each
     Mp x wb panel read once and its reflectors written once (2 * 8 Mp wb)."""
