@@ -13,14 +13,14 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libffb200.so")
-SOURCES = ["ffb_engine.cu", "ffb_gemm.cu", "ffb_kernels.cu", "ffb_jacobi.cu", "ffb_panel.cu",
+SOURCES = ["ffb_engine.cu", "ffb_gemm.cu", "ffb_kernels.cu", "ffb_jacobi.cu", "ffb_jacobi_ring.cu", "ffb_panel.cu",
            "ffb_svt.cu", "ffb_probe.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-diag-suppress", "177"]
 # Jacobi: fp32 is used only for the rotation angle (refined to fp64 afterwards),
 # so flushing fp32 denormals removes the slow-path branches from the inner loop.
-EXTRA = {"ffb_jacobi.cu": ["-ftz=true"]}
+EXTRA = {"ffb_jacobi.cu": ["-ftz=true"], "ffb_jacobi_ring.cu": ["-ftz=true"]}
 
 
 def nvcc():

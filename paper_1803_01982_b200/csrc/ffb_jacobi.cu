@@ -93,7 +93,7 @@ FFB_DEV void inner_pair(int t, int k, int n_within, int& p, int& q) {
 // is orthogonal to working precision.  Returns (cc^2, aa*bb) for the caller's
 // off-diagonal measure; c = 1, s = 0 when the pair is already orthogonal.
 FFB_DEV bool rotation(const double* G, int p, int q, double tol2, double& c, double& s,
-                      double& c2, double& den) {
+                      double& c2, double& den, bool kLeanRotation) {
   c = 1.0;
   s = 0.0;
   c2 = 0.0;
@@ -103,6 +103,27 @@ FFB_DEV bool rotation(const double* G, int p, int q, double tol2, double& c, dou
   c2 = cc * cc;
   den = aa * bb;
   if (!(c2 > tol2 * den)) return false;
+  if (kLeanRotation) {
+    // tan(theta) = sign(d) g / (|d| + h), d = bb - aa, g = 2 cc, h = hypot(d, g):
+    //   c = sqrt((h + |d|) / 2h),  s = sign(d) g / (2 h c)
+    // in fp32 from power-of-two-normalised (d, g) (two MUFU.RSQ), then (c, s)
+    // renormalised in fp64 by the second-order series of 1/sqrt(c^2 + s^2)
+    const double d = bb - aa, g = cc + cc;
+    const int ex = (__double2hiint(fabs(d) + fabs(g)) >> 20) & 0x7ff;
+    const double scale = __hiloint2double((2046 - ex) << 20, 0);
+    const float df = (float)(d * scale), gf = (float)(g * scale);
+    const float rh = rsqrtf(fmaf(df, df, gf * gf));
+    const float h2 = fmaf(0.5f * fabsf(df), rh, 0.5f);
+    const float rc = rsqrtf(h2);
+    const float cf = h2 * rc;
+    const float sf = copysignf(0.5f * rh * rc, df) * gf;
+    const double cd = (double)cf, sd = (double)sf;
+    const double e = fma(sd, sd, fma(cd, cd, -1.0));   // c^2 in [0.5, 1]: c^2 - 1 is exact
+    const double r = fma(e, fma(e, 0.375, -0.5), 1.0);
+    c = cd * r;
+    s = sd * r;
+    return true;
+  }
   const float zf = __fdividef((float)(bb - aa), 2.0f * (float)cc);
   double t;
   if (fabsf(zf) < 1e15f) {
@@ -434,7 +455,7 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
         const double j00 = Jc[ra + pb2], j01 = Jc[ra + qb2];
         const double j10 = Jc[rq + pb2], j11 = Jc[rq + qb2];
         double cb, sb, c2b, denb;
-        const bool rot = rotation(Gc, pb2, qb2, tol2, cb, sb, c2b, denb);
+        const bool rot = rotation(Gc, pb2, qb2, tol2, cb, sb, c2b, denb, a.lean != 0);
         // lane ba of this warp has bb2 == ba: its rotation is pair ba's
         const double ca = __shfl_sync(0xffffffffu, cb, ba);
         const double sa = __shfl_sync(0xffffffffu, sb, ba);
@@ -666,7 +687,7 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_general_kernel(JacobiArgs
           const double j00 = Jc[ra + pb2], j01 = Jc[ra + qb2];
           const double j10 = Jc[rq + pb2], j11 = Jc[rq + qb2];
           double cb, sb, c2b, denb;
-          const bool rot = rotation(Gc, pb2, qb2, tol2, cb, sb, c2b, denb);
+          const bool rot = rotation(Gc, pb2, qb2, tol2, cb, sb, c2b, denb, a.lean != 0);
           const double ca = __shfl_sync(0xffffffffu, cb, ba);
           const double sa = __shfl_sync(0xffffffffu, sb, ba);
           if (rot && ba == bb2 && c2b * offd > offn * denb) {
@@ -948,10 +969,23 @@ size_t jacobi_work_doubles(int l, int max_sweeps) {
   return w;
 }
 
+cudaError_t launch_jacobi_scale(cudaStream_t st, const double* M, int64_t ldm, int l, int* sweeps) {
+  jacobi_scale_kernel<<<1, 1024, 0, st>>>(M, ldm, l, sweeps);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, const double* M, int64_t ldm, int l,
                               double* sig, double* U, int64_t ldu, double* Vo, int64_t ldvo,
                               double* work, uint32_t* bar, double* offmax, int* sweeps, int* order,
                               int max_sweeps) {
+  {
+    // small l: one lane group per column pair, iterate resident in one cluster's
+    // shared memory (ffb_jacobi_ring.cu); FFB_JACOBI_BLOCK=1 keeps the block kernels
+    if (getenv("FFB_JACOBI_BLOCK") == nullptr && getenv("FFB_JACOBI_GENERAL") == nullptr &&
+        jacobi_ring_supported(l, sms))
+      return launch_jacobi_ring(st, sms, M, ldm, l, sig, U, ldu, Vo, ldvo, work, offmax, sweeps, order,
+                                max_sweeps);
+  }
   int nb, lpad, ncp;
   jacobi_geometry(l, nb, lpad, ncp);
   const int P = nb / 2;
@@ -970,7 +1004,7 @@ cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, const double* M, int64_t
   const size_t smem = general ? sizeof(double) * ((size_t)kRC * kMW + 4 * 32 * kMW + 4 * 32 * 33)
                               : sizeof(double) * ((size_t)lpad * kMW + 4 * 32 * kMW + 4 * 32 * 33);
   JacobiArgs a{Mrm, jhist, ncp, l, lpad, nb, 1e-15 * sqrt((double)l), max_sweeps, bar, offmax,
-               sweeps, inner, prof, P, Vrm, bar + 2, 0, gdiag};
+               sweeps, inner, prof, P, Vrm, bar + 2, 0, gdiag, getenv("FFB_JACOBI_ROT_OLD") ? 0 : 1};
   if (general) {
     cudaError_t e = cudaFuncSetAttribute(jacobi_general_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess) e = cudaMemsetAsync(bar, 0, 4 * sizeof(uint32_t), st);

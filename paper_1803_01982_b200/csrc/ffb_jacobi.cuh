@@ -22,6 +22,7 @@ struct JacobiArgs {
   uint32_t* progress;  // [0] rounds published, [1] total rounds + 1 when done
   int fused;
   double* gdiag;     // [nb][kBS x kBS] diagonal Gram blocks carried between rounds
+  int lean;          // rotation formula: 1 = two-MUFU hypot form, 0 = zeta / Newton form
 };
 
 int jacobi_block_size(int l);
@@ -33,5 +34,16 @@ cudaError_t launch_jacobi_svd(cudaStream_t st, int sms, const double* M, int64_t
                               double* sig, double* U, int64_t ldu, double* Vo, int64_t ldvo,
                               double* work, uint32_t* bar, double* offmax, int* sweeps, int* order,
                               int max_sweeps);
+
+// Column-ring variant (ffb_jacobi_ring.cu) for small l: whole iterate in one
+// cluster's distributed shared memory.  Same contract as launch_jacobi_svd;
+// work needs jacobi_work_doubles(l) (it uses less).
+bool jacobi_ring_supported(int l, int sms);
+cudaError_t launch_jacobi_ring(cudaStream_t st, int sms, const double* M, int64_t ldm, int l,
+                               double* sig, double* U, int64_t ldu, double* Vo, int64_t ldvo,
+                               double* work, double* offmax, int* sweeps, int* order,
+                               int max_sweeps);
+// sweeps[1] <- exponent e with 2^e ~ max |M| (the power-of-two prescale)
+cudaError_t launch_jacobi_scale(cudaStream_t st, const double* M, int64_t ldm, int l, int* sweeps);
 
 }  // namespace ffb
