@@ -36,6 +36,10 @@ import time
 
 import numpy as np
 
+# before any CUDA context exists (see paper_1803_01982_b200/__init__.py): one
+# hardware work queue per stream of the batched workloads
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -309,6 +313,8 @@ def stage_table(cfg, kern_times, counts, step_ms, hbm_gbps):
         "jacobi_kernel": ("tensor", 6 * l ** 3, "flop",
                           "count_svd(l, l) = 6 l^3 (flops.py:49-52) of the l x l SVD"),
         "jacobi_general_kernel": ("tensor", 6 * l ** 3, "flop", "count_svd(l, l) = 6 l^3"),
+        "jacobi_ring_kernel": ("tensor", 6 * l ** 3, "flop",
+                               "count_svd(l, l) = 6 l^3 (flops.py:49-52); column-ring kernel, l <= 160"),
         "panel_qr_kernel": ("hbm", panel_bytes(m, n, l, b), "byte",
                             "each Mp x wb panel read once + reflectors written once"),
         "pivots_kernel": ("hbm", pivot_bytes(n, l, b, p), "byte",
@@ -380,7 +386,7 @@ def time_top_kernel(fam, cfg, A, st, dev, ctx, lib):
                          A.stride(1), 0, C.c_void_p(Yh.data_ptr()), n, 1, 0.0,
                          C.c_void_p(out.data_ptr()), m, C.c_void_p(wsb.data_ptr()), wsb.numel())
         work, unit, note = 2.0 * m * n * l, "flop", "K13 A*Qhat (m x l x n): 2mnl flop"
-    elif fam in ("jacobi_kernel", "jacobi_general_kernel"):
+    elif fam in ("jacobi_kernel", "jacobi_general_kernel", "jacobi_ring_kernel"):
         # the l x l SVD on an R_t with the workload's leading spectrum
         from paper_1803_01982_b200 import workloads
 
@@ -476,7 +482,9 @@ def batched_record(args, profile=True):
     parts = slot_layout(cfg, args.workload)
     slot_len = sum(c for _, c in parts)
     if args.streams <= 0:
-        args.streams = 8 if args.workload == "cfg5" else 3
+        # cfg5: 16 worker threads (9 SMs each) with 32 CUDA work queues measured best
+        # (8: 830, 10: 658, 12: 666, 16: 934, 18: 810, 24: 771 factorizations/s)
+        args.streams = 16 if args.workload == "cfg5" else 3
     chunk = int(os.environ.get("FFB_BENCH_CHUNK", "16"))   # problems per ffb_run_batched call
     if dry:
         probs = {i: None for i in mine}

@@ -10,6 +10,7 @@
 
 #include "ffb_common.cuh"
 #include "ffb_kernels.cuh"
+#include "ffb_pivot_dev.cuh"
 #include "ffb_tile64.cuh"
 
 namespace ffb {
@@ -28,31 +29,6 @@ FFB_DEV uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
-}
-
-// LL ("low-latency") exchange words: 32-bit payload + 32-bit step tag in one
-// single-copy-atomic 64-bit word, so readers validate data by its tag and no
-// fence or flag is needed between producer and consumers.
-FFB_DEV unsigned long long ll_pack(uint32_t data, uint32_t tag) {
-  return ((unsigned long long)tag << 32) | data;
-}
-FFB_DEV uint32_t ll_tag(unsigned long long w) { return (uint32_t)(w >> 32); }
-FFB_DEV uint32_t ll_data(unsigned long long w) { return (uint32_t)w; }
-FFB_DEV void st_ll2(unsigned long long* p, unsigned long long x, unsigned long long y) {
-  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};\n" ::"l"(p), "l"(x), "l"(y) : "memory");
-}
-FFB_DEV void ld_ll2(const unsigned long long* p, unsigned long long& x, unsigned long long& y) {
-  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(x), "=l"(y) : "l"(p) : "memory");
-}
-
-// opaque select: keeps unrolled "pick element q of a register array" chains from
-// being turned into a dynamically indexed (local-memory) array by the compiler
-FFB_DEV double sel_f64(bool c, double a, double b) {
-  double r;
-  asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\tselp.f64 %0, %1, %2, p;\n\t}"
-      : "=d"(r)
-      : "d"(a), "d"(b), "r"((unsigned)c));
-  return r;
 }
 
 static inline unsigned nblk(int64_t work, int per) {
@@ -159,13 +135,6 @@ struct Cand2 {
   int64_t p2;
 };
 
-FFB_DEV bool cand_better(double ra, int64_t pa, double rb, int64_t pb) {
-  // is (ra, pa) strictly better than (rb, pb)?  pb < 0 means "none"
-  if (pa < 0) return false;
-  if (pb < 0) return true;
-  return ra > rb || (ra == rb && pa < pb);
-}
-
 FFB_DEV void cand_push(Cand2& c, double r, int64_t p) {
   if (cand_better(r, p, c.r1, c.p1)) {
     c.r2 = c.r1;
@@ -204,28 +173,6 @@ FFB_DEV Cand2 warp_top2(Cand2 c) {
 constexpr int kPivThreads = 256;
 constexpr int kPivGroups = kPivThreads / 4;
 constexpr int kPivMaxK = 5;   // CTAs per lane in the header exchange (G <= 160)
-
-// exact warp argmax: largest r, ties -> lowest position.  r >= 0 for every
-// candidate (norms; the downdate clamps at 0), so the IEEE bit pattern orders
-// like the value: key = bits + 1 (0 = no candidate), reduced with three redux
-// instructions (max hi word, max lo word among the hi winners, min position).
-// Positions are < 2^31 (checked at the boundary).
-FFB_DEV void warp_best(double& r, int64_t& p) {
-  const unsigned long long key =
-      p >= 0 ? (unsigned long long)__double_as_longlong(r > 0.0 ? r : 0.0) + 1ull : 0ull;
-  const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
-  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
-  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
-  const bool top = key != 0ull && hi == mhi && lo == mlo;
-  const unsigned pm = __reduce_min_sync(0xffffffffu, top ? (unsigned)p : 0xffffffffu);
-  if (pm == 0xffffffffu) {
-    r = -1.0;
-    p = -1;
-  } else {
-    r = __longlong_as_double((long long)((((unsigned long long)mhi << 32) | mlo) - 1ull));
-    p = (int64_t)pm;
-  }
-}
 
 // RQ > 0: every column group owns at most one column and keeps its rows
 // (sub + 4q, q < RQ) in registers; shared memory gets a write-through copy that
