@@ -208,6 +208,8 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
   Cand2* wc = reinterpret_cast<Cand2*>(vv + ((s + 1) & ~1));   // per-warp top-2 [8]
   __shared__ double s_tau;
   __shared__ int64_t s_wpos;
+  __shared__ double s_hr[kPivThreads / 32];    // spread exchange: the warps' local winners
+  __shared__ int64_t s_hp[kPivThreads / 32];
 
   for (int idx = tid; idx < s * nc; idx += kPivThreads) {
     const int c = idx / s, i = idx - c * s;
@@ -273,7 +275,137 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
   for (int j = 0; j < a.bb; ++j) {
     const int64_t P = a.j0 + j;
     const int par = j & 1;
-    if (warp == 0) {
+    // Register-resident columns without gap tracing: the exchange is spread over
+    // the CTA instead of running in warp 0 alone.  Every warp derives the CTA's
+    // candidate, the owning thread group publishes the column from its
+    // registers (no scan, no shared-memory copy), warp w polls the headers of
+    // CTAs w, w + 8, .. (one per lane) and fetches ITS best CTA's column right
+    // away, so the column load no longer waits for the global pick; the warp
+    // that holds the global winner builds the reflector.
+    bool spread = false;
+    if constexpr (RQ > 0) spread = a.gap == nullptr;
+    if (spread) {
+      const uint32_t tag = (uint32_t)(j + 1);
+      unsigned long long* base = a.rec + (size_t)par * a.G * a.recw;
+      Cand2 cd = lane < (kPivThreads / 32) ? wc[lane] : Cand2{-1.0, -1, -1.0, -1};
+      warp_best(cd.r1, cd.p1);
+      {
+        unsigned long long* rec = base + (size_t)blockIdx.x * a.recw;
+        if (cd.p1 >= 0 && grp < nc && pp[grp] == cd.p1) {
+          if constexpr (RQ > 0) {
+#pragma unroll
+            for (int q = 0; q < RQ; ++q) {
+              const int i = sub + 4 * q;
+              if (i >= j && i < s)
+                st_ll2(rec + 8 + 2 * i, ll_pack((uint32_t)__double2loint(x[q]), tag),
+                       ll_pack((uint32_t)__double2hiint(x[q]), tag));
+            }
+          }
+        }
+        if (warp == 0) {
+          if (lane == 0)
+            st_ll2(rec, ll_pack((uint32_t)__double2loint(cd.r1), tag),
+                   ll_pack((uint32_t)__double2hiint(cd.r1), tag));
+          if (lane == 1) st_ll2(rec + 2, ll_pack((uint32_t)(int32_t)cd.p1, tag), ll_pack(0u, tag));
+        }
+      }
+      PPROF(0)
+      // this warp's share of the headers: lane k polls CTA warp + 8 k
+      const int myc = warp + (kPivThreads / 32) * lane;
+      unsigned long long h0 = 0, h1 = 0, h2 = 0, h3 = 0;
+      bool need = myc < a.G;
+      do {
+        if (need) {
+          const unsigned long long* rc = base + (size_t)myc * a.recw;
+          ld_ll2(rc, h0, h1);
+          ld_ll2(rc + 2, h2, h3);
+          if (ll_tag(h0) == tag && ll_tag(h1) == tag && ll_tag(h2) == tag && ll_tag(h3) == tag) need = false;
+        }
+      } while (__any_sync(0xffffffffu, need));
+      PPROF(1)
+      double lr = -1.0;
+      int64_t lp = -1;
+      if (myc < a.G) {
+        lr = __hiloint2double((int)ll_data(h1), (int)ll_data(h0));
+        lp = (int64_t)(int32_t)ll_data(h2);
+      }
+      const int64_t mine = lp;
+      warp_best(lr, lp);
+      const int wcta = (int)__reduce_max_sync(0xffffffffu, (lp >= 0 && mine == lp) ? (unsigned)(myc + 1) : 0u) - 1;
+      // rows j.. of the local winner's column (all loads in flight, validated by tag)
+      double xv[XQ];
+      {
+        const unsigned long long* wrec = base + (size_t)(wcta >= 0 ? wcta : 0) * a.recw + 8;
+        unsigned long long xw[XQ][2];
+        unsigned xneed = 0;
+#pragma unroll
+        for (int q = 0; q < XQ; ++q) {
+          const int i = lane + 32 * q;
+          if (i >= j && i < s && wcta >= 0) xneed |= 1u << q;
+          xw[q][0] = xw[q][1] = 0ull;
+        }
+        do {
+#pragma unroll
+          for (int q = 0; q < XQ; ++q)
+            if (xneed & (1u << q)) ld_ll2(wrec + 2 * (lane + 32 * q), xw[q][0], xw[q][1]);
+#pragma unroll
+          for (int q = 0; q < XQ; ++q)
+            if ((xneed & (1u << q)) && ll_tag(xw[q][0]) == tag && ll_tag(xw[q][1]) == tag)
+              xneed &= ~(1u << q);
+        } while (__any_sync(0xffffffffu, xneed != 0));
+#pragma unroll
+        for (int q = 0; q < XQ; ++q) {
+          const int i = lane + 32 * q;
+          xv[q] = (i >= j && i < s && wcta >= 0)
+                      ? __hiloint2double((int)ll_data(xw[q][1]), (int)ll_data(xw[q][0]))
+                      : 0.0;
+        }
+      }
+      if (lane == 0) {
+        s_hr[warp] = lr;
+        s_hp[warp] = lp;
+      }
+      __syncthreads();
+      PPROF(2)
+      // global pick over the 8 local winners (every warp, identical)
+      double rg = lane < (kPivThreads / 32) ? s_hr[lane] : -1.0;
+      int64_t pg = lane < (kPivThreads / 32) ? s_hp[lane] : -1;
+      warp_best(rg, pg);
+      if (pg >= 0 ? (lp == pg) : (warp == 0)) {
+        // winner column rows j..s-1 -> reflector (ffsrqr/qr.py:21-43)
+        const int64_t wpos = pg >= 0 ? pg : P;
+        double tsq = 0.0;
+#pragma unroll
+        for (int q = 0; q < XQ; ++q) {
+          const int i = lane + 32 * q;
+          if (pg < 0) xv[q] = 0.0;
+          if (i > j && i < s) tsq = fma(xv[q], xv[q], tsq);
+        }
+        tsq = warp_sum(tsq);
+        double xsel = 0.0;
+#pragma unroll
+        for (int q = 0; q < XQ; ++q) xsel = sel_f64(q == (j >> 5), xv[q], xsel);
+        const double x0 = __shfl_sync(0xffffffffu, xsel, j & 31);
+        double tau = 0.0, div = 1.0;
+        if (tsq != 0.0) {
+          const double nrm = sqrt(x0 * x0 + tsq);
+          const double alpha = x0 == 0.0 ? nrm : -copysign(nrm, x0);
+          div = x0 - alpha;
+          tau = (alpha - x0) / alpha;
+        }
+#pragma unroll
+        for (int q = 0; q < XQ; ++q) {
+          const int i = lane + 32 * q;
+          if (i < s) vv[i] = (i == j) ? 1.0 : (i > j && tau != 0.0 ? xv[q] / div : 0.0);
+        }
+        if (lane == 0) {
+          s_tau = tau;
+          s_wpos = wpos;
+          if (blockIdx.x == 0) a.hist[j] = wpos;
+        }
+      }
+      PPROF(3)
+    } else if (warp == 0) {
       // ---- local candidate -> publish (tagged LL words, no fences) -> global
       // pick -> reflector, all in warp 0
       const uint32_t tag = (uint32_t)(j + 1);
@@ -464,13 +596,13 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
               const int i = sub + 4 * q;
               if (i >= j && i < s) {
                 x[q] = fma(-vv[i], wt, x[q]);
-                col[i] = x[q];
+                if (!spread) col[i] = x[q];   // the warp-0 publish reads the column from shared memory
               }
             }
           }
           double xj = 0.0;
 #pragma unroll
-          for (int q = 0; q < RQ; ++q) xj = sel_f64(q == (j >> 2), x[q], xj);
+          for (int q = 0; q < RQ; ++q) mov_if_f64(xj, q == (j >> 2), x[q]);
           const double rj = __shfl_sync(gmask, xj, (lane & ~3) | (j & 3));
           double rr = r[c] - rj * rj;
           if (rr < 1e-8 * r0[c] || rr < 0.0) {

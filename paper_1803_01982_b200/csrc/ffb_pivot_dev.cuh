@@ -30,6 +30,14 @@ FFB_DEV double sel_f64(bool c, double a, double b) {
   return r;
 }
 
+// dst = src when c: a predicated move, so an unrolled "pick element q of a
+// register array" costs one issue slot per element and no dependent select chain
+FFB_DEV void mov_if_f64(double& dst, bool c, double src) {
+  asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p mov.f64 %0, %1;\n\t}"
+      : "+d"(dst)
+      : "d"(src), "r"((unsigned)c));
+}
+
 FFB_DEV bool cand_better(double ra, int64_t pa, double rb, int64_t pb) {
   // is (ra, pa) strictly better than (rb, pb)?  pb < 0 means "none"
   if (pa < 0) return false;
