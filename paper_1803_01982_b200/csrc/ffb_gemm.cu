@@ -164,6 +164,10 @@ int pick_cfg(int64_t M, int64_t N, int64_t K) {
   // HBM once -- and 128 x 144 / 64 x 128 tiles measured slower than 64 x 144)
   if (M >= 1024 && N > 192) return 9;   // tall, wide N (A*Yhat at l = 272 / 420): 64 x 144
                                        // tiles + stream-K: 28.4 / 30.1 TF vs 25.5 / 23.7 (128 x 96)
+  // N just under one 144-column tile (cfg5's A*Yhat, l = 144): 64 x 144 tiles with
+  // no padding columns, 20.8 TF against 16.7 on 128 x 64 (a quarter of the third
+  // N tile empty)
+  if (M >= 1024 && N > 128 && N <= 144 && K >= 1024) return 9;
   if (M >= 1024) {
     // tall products (N = l): pick the N tile with less padding waste
     const int64_t w64 = (N + 63) / 64 * 64 - N, w96 = (N + 95) / 96 * 96 - N;

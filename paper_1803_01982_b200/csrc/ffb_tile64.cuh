@@ -197,48 +197,57 @@ FFB_DEV void sign_lu(Tile& q, int w, double* Ls, double* Us, double* Dd, double*
     Us[r * kTL + c] = 0.0;
   }
   __syncthreads();
-  for (int c = 0; c < w; ++c) {
-    double* col = buf + (c & 1) * 128;      // column c of the working matrix
-    double* rowc = col + 64;                // row c of the working matrix
+  // Steps run four at a time with the in-tile index jj a compile-time constant
+  // (c = c4 + jj): the owners of column / row c are the threads with bj == c4 /
+  // bi == c4, so publishing a column costs one comparison and four stores
+  // instead of a four-way predicated search through the register tile.
+  for (int c4 = 0; c4 < w; c4 += 4) {
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj)
-      if (c == bj + jj) {
+    for (int jj = 0; jj < 4; ++jj) {
+      const int c = c4 + jj;
+      if (c >= w) break;
+      double* col = buf + (jj & 1) * 128;     // column c of the working matrix
+      double* rowc = col + 64;                // row c of the working matrix
+      if (bj == c4) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) col[bi + i] = q.v[i][jj];
       }
+      if (bi == c4) {
 #pragma unroll
-    for (int ii = 0; ii < 4; ++ii)
-      if (c == bi + ii) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) rowc[bj + j] = q.v[ii][j];
+        for (int j = 0; j < 4; ++j) rowc[bj + j] = q.v[jj][j];
       }
-    __syncthreads();
-    const double z = col[c];
-    double d;
-    if (fabs(z) == 1.0) d = z > 0.0 ? 1.0 : -1.0;   // identity reflector (tail == 0)
-    else d = z > 0.0 ? -1.0 : 1.0;                  // pivot -(1+|z|) = -tau
-    const double ucc = d * z - 1.0;
-    const double sc = ucc != 0.0 ? d * fast_rcp(ucc) : 0.0;
-    if (tid < 64) {
-      const int r = tid;
-      if (r < c) Us[r * kTL + c] = d * col[r];
-      else if (r == c) {
-        Us[c * kTL + c] = ucc;
-        Dd[c] = d;
-      } else if (r < w) {
-        Ls[r * kTL + c] = sc * col[r];
+      __syncthreads();
+      const double z = col[c];
+      double d;
+      if (fabs(z) == 1.0) d = z > 0.0 ? 1.0 : -1.0;   // identity reflector (tail == 0)
+      else d = z > 0.0 ? -1.0 : 1.0;                  // pivot -(1+|z|) = -tau
+      const double ucc = d * z - 1.0;
+      const double sc = ucc != 0.0 ? d * fast_rcp(ucc) : 0.0;
+      if (tid < 64) {
+        const int r = tid;
+        if (r < c) Us[r * kTL + c] = d * col[r];
+        else if (r == c) {
+          Us[c * kTL + c] = ucc;
+          Dd[c] = d;
+        } else if (r < w) {
+          Ls[r * kTL + c] = sc * col[r];
+        }
+      }
+      // tiles above or left of block c4 are finished; inside block row / column c4
+      // only the rows / columns past c still change
+      if (bi >= c4 && bj >= c4) {
+        double li[4], rj[4];
+#pragma unroll
+        for (int q2 = 0; q2 < 4; ++q2) {
+          li[q2] = (bi + q2 > c && bi + q2 < w) ? sc * col[bi + q2] : 0.0;
+          rj[q2] = (bj + q2 > c && bj + q2 < w) ? rowc[bj + q2] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) q.v[i][j] = fma(-li[i], rj[j], q.v[i][j]);
       }
     }
-    double li[4], rj[4];
-#pragma unroll
-    for (int q2 = 0; q2 < 4; ++q2) {
-      li[q2] = (bi + q2 > c && bi + q2 < w) ? sc * col[bi + q2] : 0.0;
-      rj[q2] = (bj + q2 > c && bj + q2 < w) ? rowc[bj + q2] : 0.0;
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) q.v[i][j] = fma(-li[i], rj[j], q.v[i][j]);
   }
   __syncthreads();
 }
