@@ -43,22 +43,19 @@ FFB_DEV void st_rel(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 
-// Sense/generation grid barrier; bar[0] = arrivals, bar[1] = generation.
-FFB_DEV void grid_barrier(uint32_t* bar, uint32_t nblocks) {
+// Grid barrier on one monotone counter (bar[0], zero at launch): the k-th
+// barrier completes when the counter reaches k * nblocks.  Arrival is a
+// fire-and-forget red.release, the wait polls with ld.acquire — one L2 round
+// trip on the critical path (ffb_panel.cu has the same barrier).  `passed`
+// counts the barriers this thread has been through.
+FFB_DEV void grid_barrier(uint32_t* bar, uint32_t nblocks, uint32_t& passed) {
+  ++passed;
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint32_t gen = ld_acq(bar + 1);
-    __threadfence();
-    const uint32_t arrived = atomicAdd(bar, 1u) + 1u;
-    if (arrived == nblocks) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      st_rel(bar + 1, gen + 1u);
-    } else {
-      while (ld_acq(bar + 1) == gen) {
-      }
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar) : "memory");
+    const uint32_t target = passed * nblocks;
+    while (ld_acq(bar) < target) {
     }
-    __threadfence();
   }
   __syncthreads();
 }
@@ -148,12 +145,12 @@ FFB_DEV bool rotation(const double* G, int p, int q, double tol2, double& c, dou
 // the hardware cluster barrier (release/acquire at cluster scope covers the
 // global M, V); otherwise a cooperative grid barrier.
 template <bool CLUSTER>
-FFB_DEV void round_barrier(uint32_t* bar, uint32_t P) {
+FFB_DEV void round_barrier(uint32_t* bar, uint32_t P, uint32_t& passed) {
   if (CLUSTER) {
     __syncthreads();
     cg::this_cluster().sync();
   } else {
-    grid_barrier(bar, P);
+    grid_barrier(bar, P, passed);
   }
 }
 
@@ -321,6 +318,7 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
   const double tol2 = a.tol * a.tol;
   const int64_t ld = a.ld;
 
+  uint32_t gbn = 0;   // grid barriers passed (non-cluster launch)
   long long tp[6] = {0, 0, 0, 0, 0, 0};
   long long tc = clock64();
 #define JPROF(i)                              \
@@ -523,7 +521,7 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(JacobiArgs a) {
         atomicMax(reinterpret_cast<unsigned long long*>(a.offmax + sweep),
                   (unsigned long long)__double_as_longlong(s_off));
       JPROF(4)
-      round_barrier<CLUSTER>(a.bar, P);
+      round_barrier<CLUSTER>(a.bar, P, gbn);
       // publish progress to the V replay CTAs: J of every finished round is visible
       if (a.fused && tid == 0 && blockIdx.x == 0) {
         __threadfence();
@@ -586,6 +584,7 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_general_kernel(JacobiArgs
   const int lpad = a.lpad, nb = a.nb, P = a.P;
   const int lrows = ((a.l + 31) & ~31) < lpad ? ((a.l + 31) & ~31) : lpad;
   const bool resident = lrows <= kRC;   // one chunk: staged once, reused by the apply
+  uint32_t gbn = 0;                     // grid barriers passed
   double* Ms = sm;                      // kRC x kMW
   double* Gs = Ms + (size_t)kRC * kMW;
   double* Js = Gs + 32 * kMW;
@@ -760,7 +759,7 @@ __global__ void __launch_bounds__(kJThreads, 1) jacobi_general_kernel(JacobiArgs
       if (tid == 0 && s_off > 0.0)
         atomicMax(reinterpret_cast<unsigned long long*>(a.offmax + sweep),
                   (unsigned long long)__double_as_longlong(s_off));
-      grid_barrier(a.bar, gridDim.x);
+      grid_barrier(a.bar, gridDim.x, gbn);
     }
     const double om = *((volatile double*)(a.offmax + sweep));
     if (tid == 0 && blockIdx.x == 0) *a.sweeps = sweep + 1;

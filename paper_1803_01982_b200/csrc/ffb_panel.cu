@@ -40,21 +40,21 @@ FFB_DEV void st_rel32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 
-FFB_DEV void grid_sync(uint32_t* bar, uint32_t nblocks) {
+// Grid barrier on one monotone counter (bar[0], zero at launch): the k-th
+// barrier is complete when the counter reaches k * nblocks.  Arrival is a
+// fire-and-forget red.release (cumulative over the CTA's writes ordered by the
+// __syncthreads before it), the wait polls with ld.acquire: one L2 round trip
+// on the critical path, where the sense / generation version paid four (read
+// the generation, atomicAdd and wait for its value, reset, publish).  `passed`
+// counts the barriers this thread has been through (same in every thread).
+FFB_DEV void grid_sync(uint32_t* bar, uint32_t nblocks, uint32_t& passed) {
+  ++passed;
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint32_t gen = ld_acq32(bar + 1);
-    __threadfence();
-    const uint32_t arrived = atomicAdd(bar, 1u) + 1u;
-    if (arrived == nblocks) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      st_rel32(bar + 1, gen + 1u);
-    } else {
-      while (ld_acq32(bar + 1) == gen) {
-      }
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar) : "memory");
+    const uint32_t target = passed * nblocks;
+    while (ld_acq32(bar) < target) {
     }
-    __threadfence();
   }
   __syncthreads();
 }
@@ -169,7 +169,7 @@ FFB_DEV void apply_upper(const double* Cs, int rows, int w, const double* Xs, do
 // projections v^T X[:, j > c] and Y[:, k < c]^T v (for T), all reduced in fixed
 // order so every CTA derives identical reflectors.  Writes Y, T, R with the
 // panel kernel's contract; X is read only (copied to Qa first).
-FFB_DEV void panel_householder(const PanelArgs& a, int64_t r0, int64_t r1, double* red) {
+FFB_DEV void panel_householder(const PanelArgs& a, int64_t r0, int64_t r1, double* red, uint32_t& gsn) {
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, G = gridDim.x;
   const int w = a.w;
   const int64_t Mp = a.Mp;
@@ -184,14 +184,14 @@ FFB_DEV void panel_householder(const PanelArgs& a, int64_t r0, int64_t r1, doubl
       a.T[r + (int64_t)c * a.ldt] = 0.0;
       a.R[r + (int64_t)c * a.ldr] = 0.0;
     }
-  grid_sync(a.bar, G);
+  grid_sync(a.bar, G, gsn);
   for (int c = 0; c < w; ++c) {
     // (A) tail norm of column c over this CTA's rows i > c
     double t = 0.0;
     for (int64_t i = (r0 > c + 1 ? r0 : c + 1) + tid; i < r1; i += nt) t = fma(W[i + c * Mp], W[i + c * Mp], t);
     t = block_sum(t, red);
     if (tid == 0) partA[blockIdx.x] = t;
-    grid_sync(a.bar, G);
+    grid_sync(a.bar, G, gsn);
     double tsq = 0.0;
     for (int b = 0; b < G; ++b) tsq += partA[b];
     const double x0 = W[c + c * Mp];
@@ -220,7 +220,7 @@ FFB_DEV void panel_householder(const PanelArgs& a, int64_t r0, int64_t r1, doubl
       d = warp_sum(d);
       if (lane == 0) partB[(size_t)blockIdx.x * 64 + q] = d;
     }
-    grid_sync(a.bar, G);
+    grid_sync(a.bar, G, gsn);
     // every CTA: reduced projections (fixed order) -> rank-1 update of its rows
     double* proj = red + 32;   // [64] in shared memory
     for (int q = tid; q < nproj; q += nt) {
@@ -275,6 +275,7 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
   const int ww = w * w;
   const int bi = bi_of(tid), bj = bj_of(tid);
   bool zero = false;
+  uint32_t gsn = 0;   // grid barriers passed
   long long tp[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long tlast = clock64();
 #define QPROF(i)                                    \
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
       acc_store_global(gacc, a.part + (size_t)grp * ww, w, 0, w, w);
     }
     QPROF(0)
-    grid_sync(a.bar, G);
+    grid_sync(a.bar, G, gsn);
     // (b) distributed fixed-order reduction
     {
       // 8 threads per element: thread k sums partials k, k+8, .. (independent
@@ -341,7 +342,7 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
         if (e < e1 && k8 == 0) a.Gg[e] = s;
       }
     }
-    grid_sync(a.bar, G);
+    grid_sync(a.bar, G, gsn);
     QPROF(1)
     // (c) every CTA: shifted Cholesky + inverse (redundant, no broadcast step)
     Tile g;
@@ -473,11 +474,11 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
     QPROF(3)
   }
   if (fallback) {
-    grid_sync(a.bar, G);   // every CTA is done with the CholeskyQR work buffers
-    panel_householder(a, r0, r1, buf);
+    grid_sync(a.bar, G, gsn);   // every CTA is done with the CholeskyQR work buffers
+    panel_householder(a, r0, r1, buf, gsn);
     return;
   }
-  grid_sync(a.bar, G);   // Q = Qa complete (top w rows visible to every CTA)
+  grid_sync(a.bar, G, gsn);   // Q = Qa complete (top w rows visible to every CTA)
   QPROF(4)
 
   // (e) Householder reconstruction (redundant in every CTA)
