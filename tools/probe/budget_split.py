@@ -36,5 +36,5 @@ for b in (0, budget):
         f = bench.kernel_family(k)
         fam[f] = fam.get(f, 0.0) + v
     print(f"{name} budget={b}: {e0.elapsed_time(e1) / 5:.3f} ms/factorization, kernel sum {sum(times.values()):.3f} ms")
-    for f, v in sorted(fam.items(), key=lambda kv: -kv[1])[:8]:
+    for f, v in sorted(fam.items(), key=lambda kv: -kv[1])[:int(os.environ.get("TOPN", "8"))]:
         print(f"   {v:7.3f} ms  {f}")
