@@ -88,3 +88,30 @@ def test_batch_item_layout_matches_header():
     # stream, mode(+pad), A, m, n, lda, a_layout(+pad), prm, omega, workspace, bytes, out, status
     assert _capi.BatchItem.a_layout.offset == 48
     assert _capi.BatchItem.prm.offset == 56
+
+
+def test_import_requests_work_queues_without_overriding_the_caller():
+    # batches run up to 16 problem streams: the package asks for 32 CUDA work
+    # queues at import but never replaces a caller's setting
+    import subprocess
+    import sys
+
+    code = "import os; import paper_1803_01982_b200; print(os.environ['CUDA_DEVICE_MAX_CONNECTIONS'])"
+    env = {k: v for k, v in os.environ.items() if k != "CUDA_DEVICE_MAX_CONNECTIONS"}
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=ROOT, capture_output=True, text=True)
+    assert out.stdout.strip() == "32", out.stderr[-300:]
+    env["CUDA_DEVICE_MAX_CONNECTIONS"] = "4"
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=ROOT, capture_output=True, text=True)
+    assert out.stdout.strip() == "4"
+
+
+def test_sass_has_cluster_async_stores_for_the_ring_jacobi():
+    # the column-ring Jacobi hands boundary columns over with st.async + mbarrier
+    # (SASS: STAS / SYNCS), no fence inside a sweep
+    import subprocess
+
+    lib = os.path.join(ROOT, "paper_1803_01982_b200", "libffb200.so")
+    obj = os.path.join(ROOT, "paper_1803_01982_b200", "build", "ffb_jacobi_ring.o")
+    sass = subprocess.run(["cuobjdump", "-sass", obj if os.path.exists(obj) else lib], capture_output=True, text=True).stdout
+    assert "jacobi_ring_kernel" in sass
+    assert "STAS" in sass and "SYNCS" in sass
