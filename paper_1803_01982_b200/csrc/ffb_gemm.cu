@@ -243,6 +243,7 @@ cudaError_t gemm_f64(GemmCtx& c, cudaStream_t st, int64_t M, int64_t N, int64_t 
   g.sk_per = 0;
   g.sk_maxseg = 0;
   g.sk_tiles_n = (int)gx;
+  g.sk_lock = 0;
   g.sk_kiters = (K + sh.bk - 1) / sh.bk;
   g.sk_cnt = nullptr;
   int64_t kper = (K + splits - 1) / splits;
@@ -277,21 +278,35 @@ cudaError_t gemm_f64(GemmCtx& c, cudaStream_t st, int64_t M, int64_t N, int64_t 
     const double eff = (double)tiles / (double)(waves * slots);
     // short K: the fixup would cost more than the tail it removes
     if (eff < 0.9 && kit >= 32 && tiles >= 32) {
-      const int64_t total = tiles * kit;
+      // Lockstep over N: a row operand larger than L2 with 2-4 N tiles (A*Yhat at
+      // l = 272 / 420) was streamed from HBM once per N tile, because the CTAs on
+      // the N tiles of one row block worked at different k offsets; here the tn
+      // CTAs of a range owner walk the same (row block, k) range together
+      // (FFB_GEMM_LOCK=0 disables)
+      static int lock_mode = -2;
+      if (lock_mode == -2) {
+        const char* e = getenv("FFB_GEMM_LOCK");
+        lock_mode = e ? atoi(e) : 1;
+      }
+      const bool lock = lock_mode != 0 && gx >= 2 && gx <= 4 && (double)M * (double)K * 8.0 > 96e6;
+      const int64_t tn = lock ? gx : 1;
+      const int64_t rtiles = tiles / tn;          // tiles of the range space
+      const int64_t total = rtiles * kit;
       // <= 8 CTAs cover any tile (bounded fixup work), >= 4 k-tiles per CTA
-      int64_t G = std::min<int64_t>(std::min<int64_t>(slots, tiles * 8), std::max<int64_t>(1, total / 4));
+      int64_t G = std::min<int64_t>(std::min<int64_t>(slots / tn, rtiles * 8), std::max<int64_t>(1, total / 4));
+      G = std::max<int64_t>(G, 1);
       int64_t per = (total + G - 1) / G;
       G = (total + per - 1) / per;
       const int64_t maxseg = (per + kit - 1) / kit + 1;
-      const int64_t maxcover = per / kit + 2;   // CTAs covering one tile
-      if ((size_t)G * maxseg * sh.bm * sh.bn <= c.partial_cap && c.counters &&
+      if ((size_t)(G * tn) * maxseg * sh.bm * sh.bn <= c.partial_cap && c.counters &&
           tiles <= (int64_t)c.counter_cap && kit / per + 2 <= 16) {
         use_sk = true;
         g.sk_per = per;
         g.sk_cnt = c.counters;
         g.sk_maxseg = (int)maxseg;
+        g.sk_lock = lock ? 1 : 0;
         g.splits = 1;
-        gx = G;
+        gx = G * tn;
         gy = 1;
       }
     }

@@ -44,6 +44,9 @@ struct GemmArgs {
   int64_t sk_per;
   int sk_maxseg;
   int sk_tiles_n;    // tiles along N (tile = ty * sk_tiles_n + tx)
+  int sk_lock;       // 1: the sk_tiles_n CTAs b*tn .. b*tn + tn - 1 walk the SAME (row block, k) range, one
+                     // N tile each, in lockstep: the big row operand is read from HBM once and hits L2
+                     // for the other N tiles (0: one linear range over all tiles per CTA)
   int64_t sk_kiters; // k-tiles per tile
   unsigned* sk_cnt;  // per-tile arrival counters (zero; reset by the last arriver)
   CUtensorMap tmA;   // LOAD_TMA: A as (K inner, M rows), box (16, BM), 128B swizzle
@@ -234,10 +237,13 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
   // segment loop: classic grid = one segment; stream-K = this CTA's iteration range
   int64_t it = 0, it_end = 1;
   constexpr bool sk = SK;
+  // stream-K range owner and (lockstep mode) this CTA's N tile
+  const int64_t sk_rng = sk && g.sk_lock ? (int64_t)blockIdx.x / g.sk_tiles_n : (int64_t)blockIdx.x;
+  const int sk_nt = sk && g.sk_lock ? (int)(blockIdx.x % g.sk_tiles_n) : 0;
   if (sk) {
-    it = (int64_t)blockIdx.x * g.sk_per;
+    it = sk_rng * g.sk_per;
     it_end = it + g.sk_per;
-    const int64_t total = g.sk_kiters * ((g.M + BM - 1) / BM) * g.sk_tiles_n;
+    const int64_t total = g.sk_kiters * ((g.M + BM - 1) / BM) * (g.sk_lock ? 1 : g.sk_tiles_n);
     if (it_end > total) it_end = total;
   }
   int local_seg = 0;
@@ -245,19 +251,26 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
   for (; it < it_end; ++local_seg) {
   int64_t i0, j0, kbeg, kend;
   int split;
-  int64_t sk_tile = 0;
+  int64_t sk_tile = 0, sk_lin = 0;   // output tile (counter index), tile index in the range space
   bool sk_whole = false;
   if (sk) {
     const int64_t tile = it / g.sk_kiters;
     const int64_t kb = it - tile * g.sk_kiters;
     int64_t ke = g.sk_kiters;
     if (ke - kb > it_end - it) ke = kb + (it_end - it);
-    i0 = (tile / g.sk_tiles_n) * BM;
-    j0 = (tile % g.sk_tiles_n) * BN;
+    if (g.sk_lock) {
+      i0 = tile * BM;
+      j0 = (int64_t)sk_nt * BN;
+      sk_tile = tile * g.sk_tiles_n + sk_nt;
+    } else {
+      i0 = (tile / g.sk_tiles_n) * BM;
+      j0 = (tile % g.sk_tiles_n) * BN;
+      sk_tile = tile;
+    }
+    sk_lin = tile;
     kbeg = kb * BK;
     kend = ke * BK < g.K ? ke * BK : g.K;
     split = (int)(blockIdx.x * g.sk_maxseg + (tile - first_tile));
-    sk_tile = tile;
     sk_whole = (kb == 0 && ke == g.sk_kiters);
     it += ke - kb;
   } else {
@@ -447,7 +460,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
     // last CTA to finish this tile reduces every segment in CTA order -> C
     __shared__ int s_last;
     __syncthreads();
-    const int64_t t0 = sk_tile * g.sk_kiters, t1 = t0 + g.sk_kiters - 1;
+    const int64_t t0 = sk_lin * g.sk_kiters, t1 = t0 + g.sk_kiters - 1;
     const int64_t b0 = t0 / g.sk_per, b1 = t1 / g.sk_per;
     if (tid == 0) {
       __threadfence();
@@ -459,9 +472,10 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, A_KC, B_KC, STAGES
       __threadfence();
       __shared__ const double* segp[16];
       if (tid <= (int)(b1 - b0) && tid < 16) {
-        const int64_t bq = b0 + tid;
+        const int64_t bq = b0 + tid;   // range owner; its CTA for this N tile in lockstep mode
         const int64_t ft = (bq * g.sk_per) / g.sk_kiters;
-        segp[tid] = g.partial + (size_t)(bq * g.sk_maxseg + (sk_tile - ft)) * (BM * BN);
+        const int64_t blk = g.sk_lock ? bq * g.sk_tiles_n + sk_nt : bq;
+        segp[tid] = g.partial + (size_t)(blk * g.sk_maxseg + (sk_lin - ft)) * (BM * BN);
       }
       __syncthreads();
       const int ns = (int)(b1 - b0 + 1);
