@@ -61,8 +61,8 @@ FFB_DEV void grid_sync(uint32_t* bar, uint32_t nblocks, uint32_t& passed) {
 
 // Stage rows [c0, c0+rows) of src (ld lds) into Cs (kCH x kL), zero padding for
 // rows >= rows and columns >= w, so DMMA tiles see zeros.  All 16 copies of a
-// thread are in flight at once (cp.async, zero-fill); waits before returning.
-FFB_DEV void load_chunk(double* Cs, const double* src, int64_t lds, int64_t c0, int rows, int w) {
+// thread are in flight at once (cp.async, zero-fill); the caller waits.
+FFB_DEV void issue_chunk(double* Cs, const double* src, int64_t lds, int64_t c0, int rows, int w) {
   // thread -> (row = t & 63, col = t >> 6): consecutive threads read consecutive
   // rows of one column (coalesced)
 #pragma unroll
@@ -73,7 +73,31 @@ FFB_DEV void load_chunk(double* Cs, const double* src, int64_t lds, int64_t c0, 
     cp_async8(Cs + rr * kL + cc, ok ? src + (c0 + rr) + (int64_t)cc * lds : src, ok);
   }
   cp_async_commit();
-  cp_async_wait<0>();
+}
+
+// A CTA's row chunks [g0, g1) of src streamed through two shared-memory stages:
+// chunk i + 1 is in flight while `body(stage, c0, rows)` works on chunk i, so a
+// CTA with several chunks (tall panels on few CTAs: batches under an SM budget,
+// 160000-row unfoldings) no longer exposes one L2 / HBM latency per chunk.
+template <class Body>
+FFB_DEV void stream_chunks(double* s0, double* s1, const double* src, int64_t lds, int64_t g0, int64_t g1,
+                           int w, Body body) {
+  if (g0 >= g1) return;
+  const int nch = (int)((g1 - g0 + kCH - 1) / kCH);
+  __syncthreads();   // earlier readers of the stages are done
+  issue_chunk(s0, src, lds, g0, (int)(g1 - g0 < kCH ? g1 - g0 : kCH), w);
+  for (int ci = 0; ci < nch; ++ci) {
+    const int64_t c0 = g0 + (int64_t)ci * kCH;
+    const int rows = (int)(g1 - c0 < kCH ? g1 - c0 : kCH);
+    double* cur = (ci & 1) ? s1 : s0;
+    cp_async_wait<0>();
+    __syncthreads();   // chunk ci landed; everyone is done with the other stage
+    if (ci + 1 < nch) {
+      const int64_t n0 = c0 + kCH;
+      issue_chunk((ci & 1) ? s0 : s1, src, lds, n0, (int)(g1 - n0 < kCH ? g1 - n0 : kCH), w);
+    }
+    body(cur, c0, rows);
+  }
 }
 
 // Warp tile of a 64 x 64 product: warp -> rows 16*(warp/2)..+16, cols 32*(warp%2)..+32.
@@ -266,6 +290,7 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
   double* Ws = Cs + kCH * kL;         // Linv / row stage
   double* buf = Ws + kW * kL;         // 256 doubles of broadcast scratch
   double* Sx = buf + 256;             // 1024 doubles: blocked-inverse scratch
+  double* Cs2 = Sx + 1024;            // second row-chunk stage (stream_chunks)
   __shared__ double Dd[kW];
   __shared__ double red[8];
   const int tid = threadIdx.x, nt = blockDim.x, G = gridDim.x, w = a.w;
@@ -304,13 +329,9 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
       const int64_t g0 = (int64_t)grp * a.gpr, g1 = g0 + a.gpr < Mp ? g0 + a.gpr : Mp;
       Acc64 gacc;
       acc_zero(gacc);
-      for (int64_t c0 = g0; c0 < g1; c0 += kCH) {
-        const int rows = (int)(g1 - c0 < kCH ? g1 - c0 : kCH);
-        __syncthreads();
-        load_chunk(Cs, src, lds, c0, rows, w);
-        __syncthreads();
-        dmma64(gacc, Cs, true, Cs, (rows + 3) & ~3);
-      }
+      stream_chunks(Cs, Cs2, src, lds, g0, g1, w, [&](const double* cur, int64_t, int rows) {
+        dmma64(gacc, cur, true, cur, (rows + 3) & ~3);
+      });
       acc_store_global(gacc, a.part + (size_t)grp * ww, w, 0, w, w);
     }
     QPROF(0)
@@ -463,12 +484,13 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
     const bool one_chunk = a.vg <= G && a.gpr <= kCH;
     for (int grp = blockIdx.x; grp < a.vg; grp += G) {
       const int64_t g0 = (int64_t)grp * a.gpr, g1 = g0 + a.gpr < Mp ? g0 + a.gpr : Mp;
-      for (int64_t c0 = g0; c0 < g1; c0 += kCH) {
-        const int rows = (int)(g1 - c0 < kCH ? g1 - c0 : kCH);
-        __syncthreads();
-        if (!one_chunk) load_chunk(Cs, src, lds, c0, rows, w);
-        __syncthreads();
-        apply_upper(Cs, rows, w, Xs, dst, Mp, c0);
+      if (one_chunk) {
+        __syncthreads();   // Xs complete; the chunk is still in Cs from the Gram
+        if (g0 < g1) apply_upper(Cs, (int)(g1 - g0), w, Xs, dst, Mp, g0);
+      } else {
+        stream_chunks(Cs, Cs2, src, lds, g0, g1, w, [&](const double* cur, int64_t c0, int rows) {
+          apply_upper(cur, rows, w, Xs, dst, Mp, c0);
+        });
       }
     }
     QPROF(3)
@@ -536,17 +558,13 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
   __syncthreads();
   // (f) Y rows >= w: Y = Q * (D U^-1)  (Ui is upper triangular)
   {
-    double* Ys = Ws;
+    double* Ys = Ws;   // Cs holds Ui: the stages are Ws and Cs2
     for (int grp = blockIdx.x; grp < a.vg; grp += G) {
       const int64_t g0 = (int64_t)grp * a.gpr, g1 = g0 + a.gpr < Mp ? g0 + a.gpr : Mp;
       const int64_t y0 = g0 > w ? g0 : w;
-      for (int64_t c0 = y0; c0 < g1; c0 += kCH) {
-        const int rows = (int)(g1 - c0 < kCH ? g1 - c0 : kCH);
-        __syncthreads();
-        load_chunk(Ys, qfin, Mp, c0, rows, w);
-        __syncthreads();
-        apply_upper(Ys, rows, w, Ui, a.Y, a.ldy, c0);
-      }
+      stream_chunks(Ys, Cs2, qfin, Mp, y0, g1, w, [&](const double* cur, int64_t c0, int rows) {
+        apply_upper(cur, rows, w, Ui, a.Y, a.ldy, c0);
+      });
     }
   }
   QPROF(6)
@@ -555,7 +573,7 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
     for (int i = 0; i < 12; ++i) a.prof[i] = tp[i];
 }
 
-size_t panel_smem_bytes() { return sizeof(double) * (size_t)(4 * kW * kL + kCH * kL + 256 + 1024); }
+size_t panel_smem_bytes() { return sizeof(double) * (size_t)(4 * kW * kL + 2 * kCH * kL + 256 + 1024); }
 
 int panel_grid(int sms, int64_t Mp) {
   static int rpc = -1;   // rows per CTA (FFB_PANEL_RPC tuning knob)
