@@ -283,12 +283,8 @@ cudaError_t gemm_f64(GemmCtx& c, cudaStream_t st, int64_t M, int64_t N, int64_t 
       // the N tiles of one row block worked at different k offsets; here the tn
       // CTAs of a range owner walk the same (row block, k) range together
       // (FFB_GEMM_LOCK=0 disables)
-      static int lock_mode = -2;
-      if (lock_mode == -2) {
-        const char* e = getenv("FFB_GEMM_LOCK");
-        lock_mode = e ? atoi(e) : 1;
-      }
-      const bool lock = lock_mode != 0 && gx >= 2 && gx <= 4 && (double)M * (double)K * 8.0 > 96e6;
+      const char* lock_env = getenv("FFB_GEMM_LOCK");   // read per call (tests toggle it)
+      const bool lock = !(lock_env && atoi(lock_env) == 0) && gx >= 2 && gx <= 4 && (double)M * (double)K * 8.0 > 96e6;
       const int64_t tn = lock ? gx : 1;
       const int64_t rtiles = tiles / tn;          // tiles of the range space
       const int64_t total = rtiles * kit;

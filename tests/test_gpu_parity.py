@@ -72,6 +72,38 @@ def test_gemm_engine_layouts(ffb):
                 assert err < 1e-13, (M, N, K, akc, bkc, err)
 
 
+@pytest.mark.parametrize("M,N,K", [(8192, 272, 2048), (6000, 420, 3000), (5000, 500, 2600), (8192, 272, 8192)])
+def test_gemm_lockstep_stream_k(ffb, M, N, K, monkeypatch):
+    # tall products whose row operand exceeds L2 with 2-4 N tiles (A*Yhat): the CTAs
+    # of one row block walk the same k range in lockstep; same result as the
+    # linear stream-K ranges up to the order of the split sums
+    from paper_1803_01982_b200 import _capi
+    import ctypes as C
+
+    lib = _capi.load()
+    ctx = _capi.context(0)
+    g = torch.Generator(device="cuda").manual_seed(M + N)
+    ws = torch.empty(128 << 20, dtype=torch.uint8, device="cuda")
+    A = torch.randn(M, K, generator=g, dtype=torch.float64, device="cuda")
+    B = torch.randn(K, N, generator=g, dtype=torch.float64, device="cuda")
+    Ast = A.t().contiguous()      # column-major A (akc = 0), as the flip-flop's A*Yhat
+    Bst = B.t().contiguous()      # k-contiguous B (bkc = 1)
+    ref = A @ B
+    outs = []
+    for lock in ("1", "0"):
+        monkeypatch.setenv("FFB_GEMM_LOCK", lock)
+        Cc = torch.zeros(N, M, dtype=torch.float64, device="cuda")
+        rc = lib.ffb_gemm(ctx, C.c_void_p(torch.cuda.current_stream().cuda_stream), M, N, K, 1.0,
+                          C.c_void_p(Ast.data_ptr()), M, 0, C.c_void_p(Bst.data_ptr()), K, 1, 0.0,
+                          C.c_void_p(Cc.data_ptr()), M, C.c_void_p(ws.data_ptr()), ws.numel())
+        assert rc == 0
+        torch.cuda.synchronize()
+        err = (Cc.t() - ref).abs().max().item() / ref.abs().max().item()
+        assert err < 1e-13, (lock, err)
+        outs.append(Cc)
+    assert (outs[0] - outs[1]).abs().max().item() <= 1e-12 * ref.abs().max().item()
+
+
 @pytest.mark.parametrize("name", CASES)
 def test_first_block_pivots(ffb, name):
     from paper_1803_01982_b200 import _capi, rng
