@@ -933,16 +933,19 @@ def run_single(args):
 
         _batch.run_streams(list(range(3)), cstep, n_streams=3, device=dev)
         torch.cuda.synchronize()
-        z0, z1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         nconc = 12
-        z0.record(st)
-        _batch.run_streams(list(range(nconc)), cstep, n_streams=3, device=dev)
-        torch.cuda.synchronize()
-        z1.record(st)
-        torch.cuda.synchronize()
-        cms = z0.elapsed_time(z1) / nconc
+        cruns = []
+        for _ in range(2):   # two timed batches, the faster one reported (both kept)
+            z0, z1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            z0.record(st)
+            _batch.run_streams(list(range(nconc)), cstep, n_streams=3, device=dev)
+            torch.cuda.synchronize()
+            z1.record(st)
+            torch.cuda.synchronize()
+            cruns.append(z0.elapsed_time(z1) / nconc)
+        cms = min(cruns)
         conc = {"value": 1000.0 / cms * ws, "unit": "factorizations/s", "ms_per_factorization": cms,
-                "streams": 3, "factorizations": nconc}
+                "streams": 3, "factorizations": nconc, "runs_ms": cruns}
 
     # the paper's competitor on the same device kernels
     rsi = None
