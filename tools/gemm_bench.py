@@ -22,6 +22,9 @@ SHAPES = {  # name: (M, N, K, a_kc, b_kc)
     "cfg3_K13": (20000, 420, 5000, 0, 1),
     "cfg5_WT": (32, 2048, 4096, 1, 1),
     "cfg5_K13": (4096, 144, 2048, 0, 1),
+    "cfg4_K13": (400, 50, 160000, 0, 1),
+    "cfg4_WT": (32, 160000, 400, 1, 1),
+    "cfg4_sketch": (42, 160000, 400, 1, 1),
 }
 
 
