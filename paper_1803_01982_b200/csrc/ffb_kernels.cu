@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
   __shared__ int64_t s_wpos;
   __shared__ double s_hr[kPivThreads / 32];    // spread exchange: the warps' local winners
   __shared__ int64_t s_hp[kPivThreads / 32];
+  __shared__ double s_xst[128];                // owner warp: the candidate column, rows by lane
 
   for (int idx = tid; idx < s * nc; idx += kPivThreads) {
     const int c = idx / s, i = idx - c * s;
@@ -277,88 +278,138 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
     const int par = j & 1;
     // Register-resident columns without gap tracing: the exchange is spread over
     // the CTA instead of running in warp 0 alone.  Every warp derives the CTA's
-    // candidate, the owning thread group publishes the column from its
-    // registers (no scan, no shared-memory copy), warp w polls the headers of
-    // CTAs w, w + 8, .. (one per lane) and fetches ITS best CTA's column right
-    // away, so the column load no longer waits for the global pick; the warp
-    // that holds the global winner builds the reflector.
+    // candidate; the warp that owns the candidate column publishes the header
+    // and builds the column's reflector (ffsrqr/qr.py:21-43) straight from the
+    // owning threads' registers, publishing (tau, v) while the other seven warps
+    // poll the headers of the G CTAs (one per lane) and fetch THEIR best CTA's
+    // reflector right away; the warp that holds the global winner's hands it to
+    // the CTA.  The reflector arithmetic is off the path between the global pick
+    // and the update, and the winner's load no longer waits for the pick.
     bool spread = false;
     if constexpr (RQ > 0) spread = a.gap == nullptr;
     if (spread) {
       const uint32_t tag = (uint32_t)(j + 1);
       unsigned long long* base = a.rec + (size_t)par * a.G * a.recw;
       Cand2 cd = lane < (kPivThreads / 32) ? wc[lane] : Cand2{-1.0, -1, -1.0, -1};
+      const int64_t wp = cd.p1;              // this lane's warp candidate (lane < 8)
       warp_best(cd.r1, cd.p1);
-      {
-        unsigned long long* rec = base + (size_t)blockIdx.x * a.recw;
-        if (cd.p1 >= 0 && grp < nc && pp[grp] == cd.p1) {
-          if constexpr (RQ > 0) {
-#pragma unroll
-            for (int q = 0; q < RQ; ++q) {
-              const int i = sub + 4 * q;
-              if (i >= j && i < s)
-                st_ll2(rec + 8 + 2 * i, ll_pack((uint32_t)__double2loint(x[q]), tag),
-                       ll_pack((uint32_t)__double2hiint(x[q]), tag));
-            }
-          }
-        }
-        if (warp == 0) {
-          if (lane == 0)
-            st_ll2(rec, ll_pack((uint32_t)__double2loint(cd.r1), tag),
-                   ll_pack((uint32_t)__double2hiint(cd.r1), tag));
-          if (lane == 1) st_ll2(rec + 2, ll_pack((uint32_t)(int32_t)cd.p1, tag), ll_pack(0u, tag));
-        }
-      }
-      PPROF(0)
-      // this warp's share of the headers: lane k polls CTA warp + 8 k
-      const int myc = warp + (kPivThreads / 32) * lane;
-      unsigned long long h0 = 0, h1 = 0, h2 = 0, h3 = 0;
-      bool need = myc < a.G;
-      do {
-        if (need) {
-          const unsigned long long* rc = base + (size_t)myc * a.recw;
-          ld_ll2(rc, h0, h1);
-          ld_ll2(rc + 2, h2, h3);
-          if (ll_tag(h0) == tag && ll_tag(h1) == tag && ll_tag(h2) == tag && ll_tag(h3) == tag) need = false;
-        }
-      } while (__any_sync(0xffffffffu, need));
-      PPROF(1)
+      // the warp that owns the CTA's candidate column builds that column's
+      // reflector while the other warps poll: if the candidate wins globally its
+      // v is already on its way to L2 when the pollers ask for it
+      const int ow = (int)__ffs(__ballot_sync(0xffffffffu, lane < (kPivThreads / 32) && cd.p1 >= 0 && wp == cd.p1)) - 1;
+      unsigned long long* rec = base + (size_t)blockIdx.x * a.recw;
       double lr = -1.0;
       int64_t lp = -1;
-      if (myc < a.G) {
-        lr = __hiloint2double((int)ll_data(h1), (int)ll_data(h0));
-        lp = (int64_t)(int32_t)ll_data(h2);
-      }
-      const int64_t mine = lp;
-      warp_best(lr, lp);
-      const int wcta = (int)__reduce_max_sync(0xffffffffu, (lp >= 0 && mine == lp) ? (unsigned)(myc + 1) : 0u) - 1;
-      // rows j.. of the local winner's column (all loads in flight, validated by tag)
       double xv[XQ];
-      {
-        const unsigned long long* wrec = base + (size_t)(wcta >= 0 ? wcta : 0) * a.recw + 8;
-        unsigned long long xw[XQ][2];
-        unsigned xneed = 0;
+      double ltau = 0.0;
 #pragma unroll
-        for (int q = 0; q < XQ; ++q) {
-          const int i = lane + 32 * q;
-          if (i >= j && i < s && wcta >= 0) xneed |= 1u << q;
-          xw[q][0] = xw[q][1] = 0ull;
+      for (int q = 0; q < XQ; ++q) xv[q] = 0.0;
+      if (warp == (ow >= 0 ? ow : 0)) {
+        // ---- candidate header first, then (owner warp) the reflector of the column
+        if (lane == 0)
+          st_ll2(rec, ll_pack((uint32_t)__double2loint(cd.r1), tag), ll_pack((uint32_t)__double2hiint(cd.r1), tag));
+        if (lane == 1) st_ll2(rec + 2, ll_pack((uint32_t)(int32_t)cd.p1, tag), ll_pack(0u, tag));
+        if (ow >= 0) {
+          if constexpr (RQ > 0) {
+            if (grp < nc && pp[grp] == cd.p1) {
+#pragma unroll
+              for (int q = 0; q < RQ; ++q) {
+                const int i = sub + 4 * q;
+                if (i < s) s_xst[i] = x[q];
+              }
+            }
+          }
+          __syncwarp();
+          double xr[XQ];
+#pragma unroll
+          for (int q = 0; q < XQ; ++q) {
+            const int i = lane + 32 * q;
+            xr[q] = (i >= j && i < s) ? s_xst[i] : 0.0;
+          }
+          __syncwarp();
+          double tsq = 0.0;
+#pragma unroll
+          for (int q = 0; q < XQ; ++q) {
+            const int i = lane + 32 * q;
+            if (i > j && i < s) tsq = fma(xr[q], xr[q], tsq);
+          }
+          tsq = warp_sum(tsq);
+          double xsel = 0.0;
+#pragma unroll
+          for (int q = 0; q < XQ; ++q) xsel = sel_f64(q == (j >> 5), xr[q], xsel);
+          const double x0 = __shfl_sync(0xffffffffu, xsel, j & 31);
+          double tau = 0.0, div = 1.0;
+          if (tsq != 0.0) {
+            const double nrm = sqrt(x0 * x0 + tsq);
+            const double alpha = x0 == 0.0 ? nrm : -copysign(nrm, x0);
+            div = x0 - alpha;
+            tau = (alpha - x0) / alpha;
+          }
+#pragma unroll
+          for (int q = 0; q < XQ; ++q) {
+            const int i = lane + 32 * q;
+            if (i >= j && i < s) {
+              const double v = (i == j) ? 1.0 : (tau != 0.0 ? xr[q] / div : 0.0);
+              st_ll2(rec + 8 + 2 * i, ll_pack((uint32_t)__double2loint(v), tag),
+                     ll_pack((uint32_t)__double2hiint(v), tag));
+            }
+          }
+          if (lane == 2)
+            st_ll2(rec + 4, ll_pack((uint32_t)__double2loint(tau), tag), ll_pack((uint32_t)__double2hiint(tau), tag));
         }
+        PPROF(0)
+      }
+      if (ow < 0 || warp != ow) {
+        // ---- pollers: warp index among the np polling warps; lane k polls CTA idx + np k
+        const int np = ow >= 0 ? kPivThreads / 32 - 1 : kPivThreads / 32;
+        const int idx = (ow >= 0 && warp > ow) ? warp - 1 : warp;
+        const int myc = idx + np * lane;
+        unsigned long long h0 = 0, h1 = 0, h2 = 0, h3 = 0;
+        bool need = myc < a.G;
         do {
+          if (need) {
+            const unsigned long long* rc = base + (size_t)myc * a.recw;
+            ld_ll2(rc, h0, h1);
+            ld_ll2(rc + 2, h2, h3);
+            if (ll_tag(h0) == tag && ll_tag(h1) == tag && ll_tag(h2) == tag && ll_tag(h3) == tag) need = false;
+          }
+        } while (__any_sync(0xffffffffu, need));
+        PPROF(1)
+        if (myc < a.G) {
+          lr = __hiloint2double((int)ll_data(h1), (int)ll_data(h0));
+          lp = (int64_t)(int32_t)ll_data(h2);
+        }
+        const int64_t mine = lp;
+        warp_best(lr, lp);
+        const int wcta = (int)__reduce_max_sync(0xffffffffu, (lp >= 0 && mine == lp) ? (unsigned)(myc + 1) : 0u) - 1;
+        // v rows j.. and tau of the local winner (its owner warp may still be at work)
+        if (wcta >= 0) {
+          const unsigned long long* wrec = base + (size_t)wcta * a.recw;
+          unsigned long long xw[XQ][2], t0 = 0, t1 = 0;
+          unsigned xneed = 1u << XQ;
 #pragma unroll
-          for (int q = 0; q < XQ; ++q)
-            if (xneed & (1u << q)) ld_ll2(wrec + 2 * (lane + 32 * q), xw[q][0], xw[q][1]);
+          for (int q = 0; q < XQ; ++q) {
+            const int i = lane + 32 * q;
+            if (i >= j && i < s) xneed |= 1u << q;
+            xw[q][0] = xw[q][1] = 0ull;
+          }
+          do {
+            if (xneed & (1u << XQ)) ld_ll2(wrec + 4, t0, t1);
 #pragma unroll
-          for (int q = 0; q < XQ; ++q)
-            if ((xneed & (1u << q)) && ll_tag(xw[q][0]) == tag && ll_tag(xw[q][1]) == tag)
-              xneed &= ~(1u << q);
-        } while (__any_sync(0xffffffffu, xneed != 0));
+            for (int q = 0; q < XQ; ++q)
+              if (xneed & (1u << q)) ld_ll2(wrec + 8 + 2 * (lane + 32 * q), xw[q][0], xw[q][1]);
+            if ((xneed & (1u << XQ)) && ll_tag(t0) == tag && ll_tag(t1) == tag) xneed &= ~(1u << XQ);
 #pragma unroll
-        for (int q = 0; q < XQ; ++q) {
-          const int i = lane + 32 * q;
-          xv[q] = (i >= j && i < s && wcta >= 0)
-                      ? __hiloint2double((int)ll_data(xw[q][1]), (int)ll_data(xw[q][0]))
-                      : 0.0;
+            for (int q = 0; q < XQ; ++q)
+              if ((xneed & (1u << q)) && ll_tag(xw[q][0]) == tag && ll_tag(xw[q][1]) == tag)
+                xneed &= ~(1u << q);
+          } while (__any_sync(0xffffffffu, xneed != 0));
+          ltau = __hiloint2double((int)ll_data(t1), (int)ll_data(t0));
+#pragma unroll
+          for (int q = 0; q < XQ; ++q) {
+            const int i = lane + 32 * q;
+            xv[q] = (i >= j && i < s) ? __hiloint2double((int)ll_data(xw[q][1]), (int)ll_data(xw[q][0])) : 0.0;
+          }
         }
       }
       if (lane == 0) {
@@ -367,41 +418,22 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
       }
       __syncthreads();
       PPROF(2)
-      // global pick over the 8 local winners (every warp, identical)
+      // global pick over the polling warps' local winners (every warp, identical)
       double rg = lane < (kPivThreads / 32) ? s_hr[lane] : -1.0;
       int64_t pg = lane < (kPivThreads / 32) ? s_hp[lane] : -1;
       warp_best(rg, pg);
       if (pg >= 0 ? (lp == pg) : (warp == 0)) {
-        // winner column rows j..s-1 -> reflector (ffsrqr/qr.py:21-43)
-        const int64_t wpos = pg >= 0 ? pg : P;
-        double tsq = 0.0;
+        // the warp holding the winner's reflector hands it to the CTA
+        const double tau = pg >= 0 ? ltau : 0.0;
 #pragma unroll
         for (int q = 0; q < XQ; ++q) {
           const int i = lane + 32 * q;
-          if (pg < 0) xv[q] = 0.0;
-          if (i > j && i < s) tsq = fma(xv[q], xv[q], tsq);
-        }
-        tsq = warp_sum(tsq);
-        double xsel = 0.0;
-#pragma unroll
-        for (int q = 0; q < XQ; ++q) xsel = sel_f64(q == (j >> 5), xv[q], xsel);
-        const double x0 = __shfl_sync(0xffffffffu, xsel, j & 31);
-        double tau = 0.0, div = 1.0;
-        if (tsq != 0.0) {
-          const double nrm = sqrt(x0 * x0 + tsq);
-          const double alpha = x0 == 0.0 ? nrm : -copysign(nrm, x0);
-          div = x0 - alpha;
-          tau = (alpha - x0) / alpha;
-        }
-#pragma unroll
-        for (int q = 0; q < XQ; ++q) {
-          const int i = lane + 32 * q;
-          if (i < s) vv[i] = (i == j) ? 1.0 : (i > j && tau != 0.0 ? xv[q] / div : 0.0);
+          if (i < s) vv[i] = pg >= 0 ? xv[q] : (i == j ? 1.0 : 0.0);
         }
         if (lane == 0) {
           s_tau = tau;
-          s_wpos = wpos;
-          if (blockIdx.x == 0) a.hist[j] = wpos;
+          s_wpos = pg >= 0 ? pg : P;
+          if (blockIdx.x == 0) a.hist[j] = pg >= 0 ? pg : P;
         }
       }
       PPROF(3)
