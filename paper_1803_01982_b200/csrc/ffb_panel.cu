@@ -105,6 +105,16 @@ struct Acc64 {
   double c[2][4][2];
 };
 
+// How the 8 warps tile an output: warp -> rows rs * (warp / 2) .. + rs, columns
+// cs * (warp % 2) .. + cs (rs in {8, 16}, cs in {16, 32}).  {16, 32} covers
+// 64 x 64; panels of width <= 32 use {8, 16} for their 32 x 32 Gram and
+// {16, 16} for rows x 32 products, a quarter / half of the DMMA work of the
+// zero-padded 64-wide tiles.
+struct Tiling {
+  int rs, cs;
+};
+constexpr Tiling kTile64{16, 32};
+
 FFB_DEV void acc_zero(Acc64& a) {
 #pragma unroll
   for (int i = 0; i < 2; ++i)
@@ -114,32 +124,36 @@ FFB_DEV void acc_zero(Acc64& a) {
 
 // acc += A(64 x K) * B(K x 64); A(i,k) = at ? A[k*kL + i] : A[i*kL + k];
 // B(k,j) = bt ? B[j*kL + k] : B[k*kL + j].
-FFB_DEV void dmma64(Acc64& acc, const double* A, bool at, const double* B, int K, bool bt = false) {
+FFB_DEV void dmma64(Acc64& acc, const double* A, bool at, const double* B, int K, bool bt = false,
+                    Tiling tl = kTile64) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;
+  const int r0 = (warp >> 1) * tl.rs, c0 = (warp & 1) * tl.cs;
+  const int nti = tl.rs >> 3, ntj = tl.cs >> 3;
   const int fr = lane >> 2, fk = lane & 3;
   for (int k0 = 0; k0 < K; k0 += 4) {
     double af[2], bf[4];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int r = r0 + 8 * i + fr, k = k0 + fk;
-      af[i] = at ? A[k * kL + r] : A[r * kL + k];
+      af[i] = i < nti ? (at ? A[k * kL + r] : A[r * kL + k]) : 0.0;
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      bf[j] = bt ? B[(c0 + 8 * j + fr) * kL + k0 + fk] : B[(k0 + fk) * kL + c0 + 8 * j + fr];
+      bf[j] = j < ntj ? (bt ? B[(c0 + 8 * j + fr) * kL + k0 + fk] : B[(k0 + fk) * kL + c0 + 8 * j + fr]) : 0.0;
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) dmma_884(acc.c[i][j][0], acc.c[i][j][1], af[i], bf[j]);
+      for (int j = 0; j < 4; ++j)
+        if (i < nti && j < ntj) dmma_884(acc.c[i][j][0], acc.c[i][j][1], af[i], bf[j]);
   }
 }
 
 // Write rows < rows, cols < w of the accumulator to global dst (row offset row0).
 FFB_DEV void acc_store_global(const Acc64& acc, double* dst, int64_t ldd, int64_t row0, int rows,
-                              int w) {
+                              int w, Tiling tl = kTile64) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;
+  const int r0 = (warp >> 1) * tl.rs, c0 = (warp & 1) * tl.cs;
+  const int nti = tl.rs >> 3, ntj = tl.cs >> 3;
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -147,7 +161,7 @@ FFB_DEV void acc_store_global(const Acc64& acc, double* dst, int64_t ldd, int64_
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int r = r0 + 8 * i + (lane >> 2), c = c0 + 8 * j + 2 * (lane & 3) + h;
-        if (r < rows && c < w) dst[(row0 + r) + (int64_t)c * ldd] = acc.c[i][j][h];
+        if (i < nti && j < ntj && r < rows && c < w) dst[(row0 + r) + (int64_t)c * ldd] = acc.c[i][j][h];
       }
 }
 
@@ -178,10 +192,11 @@ FFB_DEV void mm_smem(const double* A, bool at, const double* B, bool bt, int K, 
 // rows x w chunk in Cs times upper-triangular Xs (w x w) -> global dst
 FFB_DEV void apply_upper(const double* Cs, int rows, int w, const double* Xs, double* dst,
                          int64_t ldd, int64_t row0) {
+  const Tiling tl = w <= 32 ? Tiling{16, 16} : kTile64;   // rows x 32 output for narrow panels
   Acc64 acc;
   acc_zero(acc);
-  dmma64(acc, Cs, false, Xs, (w + 3) & ~3);
-  acc_store_global(acc, dst, ldd, row0, rows, w);
+  dmma64(acc, Cs, false, Xs, (w + 3) & ~3, false, tl);
+  acc_store_global(acc, dst, ldd, row0, rows, w, tl);
 }
 
 }  // namespace
@@ -327,12 +342,13 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
     // reduction below gives the same bits for any grid / SM budget)
     for (int grp = blockIdx.x; grp < a.vg; grp += G) {
       const int64_t g0 = (int64_t)grp * a.gpr, g1 = g0 + a.gpr < Mp ? g0 + a.gpr : Mp;
+      const Tiling tg = w <= 32 ? Tiling{8, 16} : kTile64;   // 32 x 32 Gram for narrow panels
       Acc64 gacc;
       acc_zero(gacc);
       stream_chunks(Cs, Cs2, src, lds, g0, g1, w, [&](const double* cur, int64_t, int rows) {
-        dmma64(gacc, cur, true, cur, (rows + 3) & ~3);
+        dmma64(gacc, cur, true, cur, (rows + 3) & ~3, false, tg);
       });
-      acc_store_global(gacc, a.part + (size_t)grp * ww, w, 0, w, w);
+      acc_store_global(gacc, a.part + (size_t)grp * ww, w, 0, w, w, tg);
     }
     QPROF(0)
     grid_sync(a.bar, G, gsn);
