@@ -263,7 +263,7 @@ FFB_DEV void sign_lu(Tile& q, int w, double* Ls, double* Us, double* Dd, double*
 
 // Off-diagonal blocks of X = U^{-1} from inverted 16x16 diagonal blocks already in
 // Xs (strictly lower blocks zero): X12 = -X11 U12 X22, 16 -> 32 -> 64.
-FFB_DEV void inv_upper_levels(const double* Us, double* Xs, double* S) {
+FFB_DEV void inv_upper_levels(const double* Us, double* Xs, double* S, int w = 64) {
   const int tid = threadIdx.x;
   // level 1: blocks (0,1) and (2,3): T = U12 X22 (S), X12 = -X11 T; thread -> (k, r, c, c+8)
   // (entries of Us beyond w are zero off the diagonal: callers zero-fill)
@@ -291,7 +291,13 @@ FFB_DEV void inv_upper_levels(const double* Us, double* Xs, double* S) {
     __syncthreads();
   }
   // level 2: T = U12 X22 (32x32, S), X12 = -X11 T; thread -> (r, c + 8 m), m < 4
-  {
+  // (w <= 32: U12 is identity padding's zero block, so X12 = 0 without the products)
+  if (w <= 32) {
+    const int r = tid >> 3, c = tid & 7;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) Xs[r * kTL + 32 + c + 8 * m] = 0.0;
+    __syncthreads();
+  } else {
     const int r = tid >> 3, c = tid & 7;
     double a[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll 8
@@ -319,7 +325,7 @@ FFB_DEV void inv_upper_levels(const double* Us, double* Xs, double* S) {
 
 // Off-diagonal blocks of X = L^{-1} from inverted 16x16 diagonal blocks already in
 // Xs (strictly upper blocks zero): X21 = -X22 L21 X11, 16 -> 32 -> 64.
-FFB_DEV void inv_unit_lower_levels(const double* Ls, double* Xs, double* S) {
+FFB_DEV void inv_unit_lower_levels(const double* Ls, double* Xs, double* S, int w = 64) {
   const int tid = threadIdx.x;
   // level 1: X21 = -X22 (L21 X11); thread -> (k, r, c, c+8)  (Ls off-diagonal
   // entries beyond w are zero: callers zero-fill)
@@ -346,8 +352,13 @@ FFB_DEV void inv_unit_lower_levels(const double* Ls, double* Xs, double* S) {
     Xs[(oo + 16 + r) * kTL + oo + c + 8] = -a1;
     __syncthreads();
   }
-  // level 2: X21 = -X22 (L21 X11) with 32x32 blocks
-  {
+  // level 2: X21 = -X22 (L21 X11) with 32x32 blocks (w <= 32: L21 = 0, X21 = 0)
+  if (w <= 32) {
+    const int r = tid >> 3, c = tid & 7;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) Xs[(32 + r) * kTL + c + 8 * m] = 0.0;
+    __syncthreads();
+  } else {
     const int r = tid >> 3, c = tid & 7;
     double a[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll 8
@@ -619,7 +630,7 @@ FFB_DEV bool chol_inv_blk(Tile& g, int w, double* Rs, double* Xs, double* S) {
     if (t >= w) Rs[t * kTL + t] = 0.0;
   const bool ok = s_ok != 0;
   __syncthreads();
-  inv_upper_levels(Rs, Xs, S);
+  inv_upper_levels(Rs, Xs, S, w);
   return ok;
 }
 
@@ -683,8 +694,8 @@ FFB_DEV void inv_upper_lower_blk(const double* Us, const double* Ls, int w, doub
     }
   }
   __syncthreads();
-  inv_upper_levels(Us, Ui, S);
-  inv_unit_lower_levels(Ls, Li, S);
+  inv_upper_levels(Us, Ui, S, w);
+  inv_unit_lower_levels(Ls, Li, S, w);
 }
 
 }  // namespace tile64
