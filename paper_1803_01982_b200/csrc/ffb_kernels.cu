@@ -1583,15 +1583,18 @@ cudaError_t launch_ext_row(cudaStream_t st, const double* A, int64_t ars, int64_
 // Thread k owns row k of Z (its d right-hand sides live in registers).  Step i:
 // the owner of row i (already final) divides by Rtilde_ii and publishes z_i;
 // one barrier; every row k < i does z_k -= Rtilde_ki z_i.  Column values
-// Rtilde_ki = R[k, arr[i]] are prefetched four steps ahead (register ring with
-// static roles).  Omega is d x (l+1) row-major (numpy C order).
+// Rtilde_ki = R[k, arr[i]] are prefetched RING steps ahead with cp.async into a
+// per-thread ring in shared memory (each thread only ever reads its own row, so
+// the ring needs no barrier): the columns sit 2 KB apart in R, mostly out of L2
+// by the time this kernel runs, and a four-deep register ring left 47 % of the
+// stall samples on those loads.  Omega is d x (l+1) row-major (numpy C order).
 constexpr int kG2MaxD = 16;
-template <int MAXT>
+template <int MAXT, int RING>
 __global__ void __launch_bounds__(MAXT) g2_kernel(const double* __restrict__ R, int64_t ldr,
                                                   const int64_t* __restrict__ arr, int64_t l,
                                                   const double* __restrict__ omega, int d, double g,
                                                   double* Z, SrqrScalars* sc) {
-  extern __shared__ int64_t g2cols[];   // [l+1] arrangement (column of Rtilde -> R column)
+  extern __shared__ int64_t g2cols[];   // [l+1] arrangement (column of Rtilde -> R column), then the ring
   __shared__ double zb[2][kG2MaxD];
   __shared__ double red_v[32];
   __shared__ int64_t red_i[32];
@@ -1626,9 +1629,13 @@ __global__ void __launch_bounds__(MAXT) g2_kernel(const double* __restrict__ R, 
   const int k = tid;   // this thread's row (L1 <= 1024)
   const double dkk = k < L1 ? (k == (int)l ? alpha : R[k + g2cols[k] * ldr]) : 1.0;
   const double rdkk = 1.0 / dkk;   // the solve multiplies by the inverted diagonal
-  // Rtilde_{k,col}: column l is (R[:l, arr[l]]; alpha); rows above the column only
-  auto colval = [&](int col) -> double {
-    return (col >= 0 && k < col) ? R[k + g2cols[col] * ldr] : 0.0;
+  // Rtilde_{k,col}: column l is (R[:l, arr[l]]; alpha); rows above the column only.
+  // ring[slot][thread]: slot col % RING holds this row's entry of column col
+  double* ring = reinterpret_cast<double*>(g2cols + ((L1 + 1) & ~1));
+  auto prefetch = [&](int col) {
+    const bool live = col >= 0 && k < col;
+    cp_async8(ring + (size_t)((col % RING + RING) % RING) * nt + tid, live ? R + k + g2cols[col] * ldr : R, live);
+    cp_async_commit();
   };
   double nrm2 = 0.0;
   for (int r0 = 0; r0 < d; r0 += kG2MaxD) {   // right-hand sides in chunks of 16
@@ -1637,8 +1644,8 @@ __global__ void __launch_bounds__(MAXT) g2_kernel(const double* __restrict__ R, 
 #pragma unroll
     for (int r = 0; r < kG2MaxD; ++r)
       z[r] = (r < dc && k < L1) ? omega[(int64_t)(r0 + r) * L1 + k] : 0.0;
-    double c0 = colval(L1 - 1), c1 = colval(L1 - 2), c2 = colval(L1 - 3), c3 = colval(L1 - 4);
-    auto step = [&](int i, double& cslot) {
+    for (int q = 0; q < RING; ++q) prefetch(L1 - 1 - q);
+    auto step = [&](int i) {
       const int par = i & 1;
       if (k == i) {
 #pragma unroll
@@ -1648,21 +1655,18 @@ __global__ void __launch_bounds__(MAXT) g2_kernel(const double* __restrict__ R, 
             zb[par][r] = z[r];
           }
       }
+      cp_async_wait<RING - 1>();   // this thread's copy for step i has landed
+      const double c = ring[(size_t)(i % RING) * nt + tid];
       __syncthreads();
-      const double c = cslot;
-      cslot = colval(i - 4);   // ring slot now serves step i - 4
+      prefetch(i - RING);          // the slot now serves step i - RING
       if (k < i) {
 #pragma unroll
         for (int r = 0; r < kG2MaxD; ++r)
           if (r < dc) z[r] = fma(-c, zb[par][r], z[r]);
       }
     };
-    for (int i = L1 - 1; i >= 0; i -= 4) {
-      step(i, c0);
-      if (i - 1 >= 0) step(i - 1, c1);
-      if (i - 2 >= 0) step(i - 2, c2);
-      if (i - 3 >= 0) step(i - 3, c3);
-    }
+    for (int i = L1 - 1; i >= 0; --i) step(i);
+    cp_async_wait<0>();
 #pragma unroll
     for (int r = 0; r < kG2MaxD; ++r)
       if (r < dc) nrm2 = fma(z[r], z[r], nrm2);
@@ -1683,10 +1687,17 @@ __global__ void __launch_bounds__(MAXT) g2_kernel(const double* __restrict__ R, 
 cudaError_t launch_g2(cudaStream_t st, const double* R, int64_t ldr, const int64_t* arr, int64_t l,
                       const double* omega, int d, double g, double* Z, SrqrScalars* sc) {
   if (l + 1 > 1024) return cudaErrorInvalidValue;
-  const size_t smem = sizeof(int64_t) * (size_t)(l + 1);
   const int threads = (int)((l + 1 + 31) / 32 * 32);
-  if (threads <= 512) g2_kernel<512><<<1, threads, smem, st>>>(R, ldr, arr, l, omega, d, g, Z, sc);
-  else g2_kernel<1024><<<1, threads, smem, st>>>(R, ldr, arr, l, omega, d, g, Z, sc);
+  const int ring = threads <= 512 ? 32 : 16;
+  const size_t smem = sizeof(int64_t) * (size_t)((l + 2) & ~1) + sizeof(double) * (size_t)ring * threads;
+  static std::atomic<unsigned long long> attr_done[2];
+  if (threads <= 512) {
+    ensure_smem_optin((const void*)g2_kernel<512, 32>, 200 * 1024, attr_done[0]);
+    g2_kernel<512, 32><<<1, threads, smem, st>>>(R, ldr, arr, l, omega, d, g, Z, sc);
+  } else {
+    ensure_smem_optin((const void*)g2_kernel<1024, 16>, 200 * 1024, attr_done[1]);
+    g2_kernel<1024, 16><<<1, threads, smem, st>>>(R, ldr, arr, l, omega, d, g, Z, sc);
+  }
   FFB_LAUNCH_CHECK();
 }
 
