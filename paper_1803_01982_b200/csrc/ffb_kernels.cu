@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
     // the CTA.  The reflector arithmetic is off the path between the global pick
     // and the update, and the winner's load no longer waits for the pick.
     bool spread = false;
-    if constexpr (RQ >= 0 && SMEM) spread = a.gap == nullptr && s <= 32 * XQ;
+    if constexpr ((RQ >= 0 && SMEM) || RQ == -2) spread = a.gap == nullptr && s <= 32 * XQ;
     if (spread) {
       const uint32_t tag = (uint32_t)(j + 1);
       unsigned long long* base = a.rec + (size_t)par * a.G * a.recw;
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
           st_ll2(rec, ll_pack((uint32_t)__double2loint(cd.r1), tag), ll_pack((uint32_t)__double2hiint(cd.r1), tag));
         if (lane == 1) st_ll2(rec + 2, ll_pack((uint32_t)(int32_t)cd.p1, tag), ll_pack(0u, tag));
         if (ow >= 0) {
-          const double* xsrc = s_xst;
+          int cl = 0;   // RQ <= 0: the candidate column, read in place through widx
           if constexpr (RQ > 0) {
             if (grp < nc && pp[grp] == cd.p1) {
 #pragma unroll
@@ -320,20 +320,22 @@ __global__ void __launch_bounds__(kPivThreads, 1) pivots_kernel(PivotArgs a) {
               }
             }
           } else {
-            // shared-memory columns (more than 64 per CTA): the candidate is one of
-            // this warp's columns grp, grp + 64, ..; read it in place
-            int cl = -1;
-            for (int c = grp; c < nc; c += kPivGroups)
-              if (pp[c] == cd.p1) cl = c;
-            cl = (int)__reduce_max_sync(0xffffffffu, (unsigned)(cl + 1)) - 1;
-            xsrc = W + (size_t)(cl >= 0 ? cl : 0) * sP;
+            // columns in shared / global memory (more than 64 per CTA): the candidate
+            // is one of this warp's columns (grp, grp + 64, .. or, one thread per
+            // column, tid, tid + 256, ..)
+            int c1 = -1;
+            for (int c = kRowMajor ? tid : grp; c < nc; c += kRowMajor ? kPivThreads : kPivGroups)
+              if (pp[c] == cd.p1) c1 = c;
+            c1 = (int)__reduce_max_sync(0xffffffffu, (unsigned)(c1 + 1)) - 1;
+            cl = c1 >= 0 ? c1 : 0;
           }
           __syncwarp();
           double xr[XQ];
 #pragma unroll
           for (int q = 0; q < XQ; ++q) {
             const int i = lane + 32 * q;
-            xr[q] = (i >= j && i < s) ? xsrc[i] : 0.0;
+            if constexpr (RQ > 0) xr[q] = (i >= j && i < s) ? s_xst[i] : 0.0;
+            else xr[q] = (i >= j && i < s) ? W[widx(cl, i)] : 0.0;
           }
           __syncwarp();
           double tsq = 0.0;
