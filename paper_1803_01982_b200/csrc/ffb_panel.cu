@@ -75,28 +75,54 @@ FFB_DEV void issue_chunk(double* Cs, const double* src, int64_t lds, int64_t c0,
   cp_async_commit();
 }
 
-// A CTA's row chunks [g0, g1) of src streamed through two shared-memory stages:
-// chunk i + 1 is in flight while `body(stage, c0, rows)` works on chunk i, so a
-// CTA with several chunks (tall panels on few CTAs: batches under an SM budget,
-// 160000-row unfoldings) no longer exposes one L2 / HBM latency per chunk.
+// Every row chunk of the CTA's row groups (grp = blockIdx.x, + G, .. of vg groups
+// of gpr rows; rows below `lo` are skipped) streamed through two shared-memory
+// stages: the next chunk — of this group or the next — is in flight while
+// `body(stage, grp, c0, rows, first, last)` works on the current one, so a CTA
+// with several chunks (tall panels on few CTAs: batches under an SM budget,
+// 160000-row unfoldings) exposes one L2 / HBM latency per pass, not one per
+// chunk.  first / last: the chunk opens / closes its group.
 template <class Body>
-FFB_DEV void stream_chunks(double* s0, double* s1, const double* src, int64_t lds, int64_t g0, int64_t g1,
-                           int w, Body body) {
-  if (g0 >= g1) return;
-  const int nch = (int)((g1 - g0 + kCH - 1) / kCH);
+FFB_DEV void stream_groups(double* s0, double* s1, const double* src, int64_t lds, int G, int vg,
+                           int64_t gpr, int64_t Mp, int64_t lo, int w, Body body) {
+  // chunk cursor: (grp, c0) with c0 in [max(g0, lo), g1)
+  auto range = [&](int grp, int64_t& b0, int64_t& b1) {
+    b0 = (int64_t)grp * gpr;
+    b1 = b0 + gpr < Mp ? b0 + gpr : Mp;
+    if (b0 < lo) b0 = lo;
+  };
+  int grp = blockIdx.x;
+  int64_t b0 = 0, b1 = 0, c0 = 0;
+  auto seek = [&]() {   // first group from `grp` on with rows; false when none is left
+    for (; grp < vg; grp += G) {
+      range(grp, b0, b1);
+      if (b0 < b1) {
+        c0 = b0;
+        return true;
+      }
+    }
+    return false;
+  };
+  if (!seek()) return;
   __syncthreads();   // earlier readers of the stages are done
-  issue_chunk(s0, src, lds, g0, (int)(g1 - g0 < kCH ? g1 - g0 : kCH), w);
-  for (int ci = 0; ci < nch; ++ci) {
-    const int64_t c0 = g0 + (int64_t)ci * kCH;
-    const int rows = (int)(g1 - c0 < kCH ? g1 - c0 : kCH);
+  issue_chunk(s0, src, lds, c0, (int)(b1 - c0 < kCH ? b1 - c0 : kCH), w);
+  for (int ci = 0;; ++ci) {
+    const int cgrp = grp;
+    const int64_t cc0 = c0, cb0 = b0, cb1 = b1;
+    const int rows = (int)(cb1 - cc0 < kCH ? cb1 - cc0 : kCH);
+    // advance the cursor to the next chunk
+    bool more = true;
+    c0 += kCH;
+    if (c0 >= b1) {
+      grp += G;
+      more = seek();
+    }
     double* cur = (ci & 1) ? s1 : s0;
     cp_async_wait<0>();
     __syncthreads();   // chunk ci landed; everyone is done with the other stage
-    if (ci + 1 < nch) {
-      const int64_t n0 = c0 + kCH;
-      issue_chunk((ci & 1) ? s0 : s1, src, lds, n0, (int)(g1 - n0 < kCH ? g1 - n0 : kCH), w);
-    }
-    body(cur, c0, rows);
+    if (more) issue_chunk((ci & 1) ? s0 : s1, src, lds, c0, (int)(b1 - c0 < kCH ? b1 - c0 : kCH), w);
+    body(cur, cgrp, cc0, rows, cc0 == cb0, cc0 + kCH >= cb1);
+    if (!more) break;
   }
 }
 
@@ -305,7 +331,7 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
   double* Ws = Cs + kCH * kL;         // Linv / row stage
   double* buf = Ws + kW * kL;         // 256 doubles of broadcast scratch
   double* Sx = buf + 256;             // 1024 doubles: blocked-inverse scratch
-  double* Cs2 = Sx + 1024;            // second row-chunk stage (stream_chunks)
+  double* Cs2 = Sx + 1024;            // second row-chunk stage (stream_groups)
   __shared__ double Dd[kW];
   __shared__ double red[8];
   const int tid = threadIdx.x, nt = blockDim.x, G = gridDim.x, w = a.w;
@@ -340,15 +366,15 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
     // (a) Gram of each row group this CTA owns (groups grp = blockIdx.x, + G, ..;
     // the partition into a.vg groups depends on Mp only, so the fixed-order
     // reduction below gives the same bits for any grid / SM budget)
-    for (int grp = blockIdx.x; grp < a.vg; grp += G) {
-      const int64_t g0 = (int64_t)grp * a.gpr, g1 = g0 + a.gpr < Mp ? g0 + a.gpr : Mp;
+    {
       const Tiling tg = w <= 32 ? Tiling{8, 16} : kTile64;   // 32 x 32 Gram for narrow panels
       Acc64 gacc;
-      acc_zero(gacc);
-      stream_chunks(Cs, Cs2, src, lds, g0, g1, w, [&](const double* cur, int64_t, int rows) {
-        dmma64(gacc, cur, true, cur, (rows + 3) & ~3, false, tg);
-      });
-      acc_store_global(gacc, a.part + (size_t)grp * ww, w, 0, w, w, tg);
+      stream_groups(Cs, Cs2, src, lds, G, a.vg, a.gpr, Mp, 0, w,
+                    [&](const double* cur, int grp, int64_t, int rows, bool first, bool last) {
+                      if (first) acc_zero(gacc);
+                      dmma64(gacc, cur, true, cur, (rows + 3) & ~3, false, tg);
+                      if (last) acc_store_global(gacc, a.part + (size_t)grp * ww, w, 0, w, w, tg);
+                    });
     }
     QPROF(0)
     grid_sync(a.bar, G, gsn);
@@ -498,16 +524,15 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
     // (d) own rows <- rows * R^-1 (a CTA with one group of <= kCH rows still
     // holds them in Cs)
     const bool one_chunk = a.vg <= G && a.gpr <= kCH;
-    for (int grp = blockIdx.x; grp < a.vg; grp += G) {
-      const int64_t g0 = (int64_t)grp * a.gpr, g1 = g0 + a.gpr < Mp ? g0 + a.gpr : Mp;
-      if (one_chunk) {
-        __syncthreads();   // Xs complete; the chunk is still in Cs from the Gram
-        if (g0 < g1) apply_upper(Cs, (int)(g1 - g0), w, Xs, dst, Mp, g0);
-      } else {
-        stream_chunks(Cs, Cs2, src, lds, g0, g1, w, [&](const double* cur, int64_t c0, int rows) {
-          apply_upper(cur, rows, w, Xs, dst, Mp, c0);
-        });
-      }
+    if (one_chunk) {
+      const int64_t g0 = (int64_t)blockIdx.x * a.gpr, g1 = g0 + a.gpr < Mp ? g0 + a.gpr : Mp;
+      __syncthreads();   // Xs complete; the chunk is still in Cs from the Gram
+      if ((int)blockIdx.x < a.vg && g0 < g1) apply_upper(Cs, (int)(g1 - g0), w, Xs, dst, Mp, g0);
+    } else {
+      stream_groups(Cs, Cs2, src, lds, G, a.vg, a.gpr, Mp, 0, w,
+                    [&](const double* cur, int, int64_t c0, int rows, bool, bool) {
+                      apply_upper(cur, rows, w, Xs, dst, Mp, c0);
+                    });
     }
     QPROF(3)
   }
@@ -575,13 +600,10 @@ __global__ void __launch_bounds__(256, 1) panel_qr_kernel(PanelArgs a) {
   // (f) Y rows >= w: Y = Q * (D U^-1)  (Ui is upper triangular)
   {
     double* Ys = Ws;   // Cs holds Ui: the stages are Ws and Cs2
-    for (int grp = blockIdx.x; grp < a.vg; grp += G) {
-      const int64_t g0 = (int64_t)grp * a.gpr, g1 = g0 + a.gpr < Mp ? g0 + a.gpr : Mp;
-      const int64_t y0 = g0 > w ? g0 : w;
-      stream_chunks(Ys, Cs2, qfin, Mp, y0, g1, w, [&](const double* cur, int64_t c0, int rows) {
-        apply_upper(cur, rows, w, Ui, a.Y, a.ldy, c0);
-      });
-    }
+    stream_groups(Ys, Cs2, qfin, Mp, G, a.vg, a.gpr, Mp, w, w,
+                  [&](const double* cur, int, int64_t c0, int rows, bool, bool) {
+                    apply_upper(cur, rows, w, Ui, a.Y, a.ldy, c0);
+                  });
   }
   QPROF(6)
 #undef QPROF
